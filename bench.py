@@ -1,0 +1,398 @@
+"""Benchmark: decompose + recompose throughput (GB/s of input) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = decompose + recompose of one 513^3 fp32 field (BASELINE.json
+config 2 shape/distribution; config 5a's per-field unit when N > 1) with the
+input resident in HBM.  Under torchrun every rank processes its own field
+(per-rank seed) — batch sharding with no collective on the data path, so
+`scaling` is "weak" and `value` = all ranks' input bytes / max-over-ranks
+time.  Rank 0 prints one JSON line.
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref/libmgrx_ref.so, the unmodified reference compiled from its
+sources; falls back to the pinned oracle port if that library is absent) on
+the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DIMS = (513, 513, 513)
+FIELD_DTYPE = "f32"
+WORKLOAD = "config2: 513^3 fp32 field (16 bumps + 8 oblique sine modes + 1e-4 noise), full decompose + recompose (stop 0)"
+METRIC = "decompose+recompose GB/s of input per GPU and % of HBM roofline; 1/2/4/8 GPU"
+
+
+def hierarchy_bytes(dims, esize):
+    """Algorithmic bytes per direction: sum_{l=1..L} 2 * s * #N_l."""
+    import numpy as np
+
+    from paper_2010_05872_b200 import GridHierarchy
+
+    h = GridHierarchy.create(dims)
+    return sum(2 * esize * h.node_count(l) for l in range(1, h.num_levels() + 1)), h
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) == 6]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+
+        backend = "nccl"
+        dist.init_process_group(backend=backend)
+    return ws, rank, local
+
+
+def max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# --------------------------------------------------------------- reference
+
+def run_reference(args, ws, rank):
+    """The reference's own CPU path on all host threads: each thread runs
+    mgrx::decompose + mgrx::recompose (transform.hpp:509,517) on its own
+    513^3 fp32 field, one field per thread per step."""
+    if rank != 0:
+        return
+    import ctypes
+    import numpy as np
+
+    from oracle.oracle import Oracle, Reference, reference_available
+
+    lib = Reference() if reference_available() else Oracle()
+    kind = "reference" if reference_available() else "port"
+    ncpu = os.cpu_count() or 1
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 16 << 30
+    per_field = 4 * 540_000_000  # input + output + reference field copy + fp64 correction scratch
+    threads = max(1, min(ncpu, int(avail * 0.6 // per_field), args.ref_threads or ncpu))
+    import torch
+
+    from paper_2010_05872_b200.fields import config2_field
+
+    fields = [config2_field(DIMS, seed=i).numpy() for i in range(threads)]
+    outs = [np.empty(f.size, dtype=np.float32) for f in fields]
+
+    def work(i):
+        c = lib.decompose(fields[i])
+        outs[i] = lib.recompose(c, DIMS)
+
+    def step():
+        ts = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+
+    for _ in range(args.warmup_ref):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    nbytes = threads * fields[0].nbytes * args.steps
+    value = nbytes / dt / 1e9
+    err = float(np.max(np.abs(outs[0].reshape(DIMS) - fields[0])))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "field": list(DIMS), "field_dtype": FIELD_DTYPE,
+                   "parallelism": f"{threads} host threads, one field each"},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind,
+                         "sample": f"{threads} x 513^3 f32 decompose+recompose per step, "
+                                   f"{args.warmup_ref} untimed warm-up steps",
+                         "cpu": _cpu_model()},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "roundtrip_linf": err,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline_sample(field_np):
+    """Reference CPU decompose+recompose of the same field on 1 core (the
+    library is single-threaded by contract)."""
+    from oracle.oracle import Oracle, Reference, reference_available
+
+    lib = Reference() if reference_available() else Oracle()
+    t0 = time.perf_counter()
+    c = lib.decompose(field_np)
+    t1 = time.perf_counter()
+    lib.recompose(c, field_np.shape)
+    t2 = time.perf_counter()
+    return {"value": field_np.nbytes / (t2 - t0) / 1e9, "unit": "GB/s", "cores": 1,
+            "kind": "reference" if reference_available() else "port",
+            "sample": f"one 513^3 f32 decompose ({t1 - t0:.2f} s) + recompose ({t2 - t1:.2f} s), same field, rank 0",
+            "cpu": _cpu_model()}
+
+
+# --------------------------------------------------------------------- ours
+
+def run_ours(args, ws, rank, local):
+    import numpy as np
+    import torch
+
+    import paper_2010_05872_b200 as mg
+    from paper_2010_05872_b200.fields import config2_field
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    esize = 4
+    alg_dir, h = hierarchy_bytes(DIMS, esize)
+    field = config2_field(DIMS, seed=rank, device=dev)
+    nbytes = field.numel() * esize
+    wsp = mg.SolverWorkspace(device=local, path=args.path)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        mc = mg.decompose(field, h, 0, wsp)
+        return mg.recompose(mc, wsp)
+
+    for _ in range(max(args.warmup, 0)):
+        out = step()
+    torch.cuda.synchronize()
+    err = float((out - field).abs().max().item())
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    l0 = wsp.launch_count()
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        out = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    clk = clocks.stop()
+    launches = (wsp.launch_count() - l0) // max(args.steps, 1)
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_max = max_over_ranks(ms, ws)
+    value = ws * nbytes / (ms_max * 1e-3) / 1e9
+    peak, peak_src = measured_peak()
+    step_achieved = 2 * alg_dir / (ms * 1e-3) / 1e9
+
+    # per-kernel device times (CUDA events on the library's stream) over the
+    # same number of steps, right after the timed region
+    wsp.profile_begin()
+    for _ in range(args.steps):
+        step()
+    prof = wsp.profile_end()
+    dominant = max(prof.items(), key=lambda kv: kv[1][0]) if prof else ("none", (0.0, 1))
+    kernel_bytes = kernel_algorithmic_bytes(dominant[0], h, esize)
+    kern_ms = dominant[1][0] / max(dominant[1][1], 1)
+    kern_achieved = kernel_bytes / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else 0.0
+    prof_total = sum(v[0] for v in prof.values()) / args.steps
+
+    # end-to-end through the host-buffer C-ABI entry points (pinned host
+    # memory; H2D of the field + D2H of the coefficients for decompose, H2D
+    # of the coefficients + D2H of the field for recompose, every step)
+    e2e = e2e_measure(mg, wsp, field, h, args)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(field.cpu().numpy())
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "field": list(DIMS), "field_dtype": FIELD_DTYPE,
+                       "levels": h.num_levels(), "path": args.path,
+                       "l2": "inputs larger than L2 (540 MB field vs 126 MB L2); no flush",
+                       "parallelism": f"batch: {ws} independent field(s), one per GPU, no collective"},
+            "roofline": {"bound": "hbm", "achieved": kern_achieved, "peak": peak, "unit": "GB/s",
+                         "frac": kern_achieved / peak, "traffic": None, "kernel": dominant[0],
+                         "kernel_ms": kern_ms, "kernel_alg_bytes": kernel_bytes, "peak_source": peak_src},
+            "step_roofline": {"achieved": step_achieved, "peak": peak, "frac": step_achieved / peak,
+                              "alg_bytes_per_step": 2 * alg_dir,
+                              "definition": "sum_l 2*s*#N_l per direction, dec+rec, / device step time"},
+            "kernels_ms_per_step": {k: v[0] / args.steps for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])},
+            "kernels_launches_per_step": {k: v[1] // args.steps for k, v in prof.items()},
+            "profiled_step_ms": prof_total,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "gpu_launches": int(launches),
+            "roundtrip_linf": err,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def kernel_algorithmic_bytes(tag, h, esize):
+    """Minimum bytes per launch of a kernel family at the finest level (the
+    level that dominates): the level pass must read and write the level block
+    once (2*s*#N_L); for the column passes the coarse-grid fp64 volume."""
+    L = h.num_levels()
+    nL = h.node_count(L)
+    nc = h.node_count(L - 1)
+    table = {
+        "f3_dec_plane": 2 * esize * nL,
+        "f3_rec_plane": 2 * esize * nL,
+        "f3_rec_interp": 2 * esize * nL,
+        "f3_col": 2 * 8 * nc,
+        "gen_dec_coef": 2 * esize * nL,
+        "gen_rec_interp": 2 * esize * nL,
+        "gen_rec_comp": esize * nL + 8 * nL,
+        "gen_sweep": 8 * nL,
+        "gen_apply": 2 * esize * nc,
+    }
+    return table.get(tag, 2 * esize * nL)
+
+
+def e2e_measure(mg, wsp, field, h, args):
+    import ctypes as C
+
+    import torch
+
+    from paper_2010_05872_b200._lib import lib
+
+    host_in = field.cpu().pin_memory()
+    host_c = torch.empty(field.numel(), dtype=field.dtype).pin_memory()
+    host_out = torch.empty_like(host_in).pin_memory()
+    dims = (C.c_uint64 * 3)(*DIMS)
+    nbytes = field.numel() * field.element_size()
+
+    def one():
+        rc = lib.mgrx_host_decompose(wsp.handle, 0, 3, dims, -1, 0, C.c_void_p(host_in.data_ptr()),
+                                     C.c_void_p(host_c.data_ptr()))
+        assert rc == 0, rc
+        rc = lib.mgrx_host_recompose(wsp.handle, 0, 3, dims, -1, 0, C.c_void_p(host_c.data_ptr()),
+                                     C.c_void_p(host_out.data_ptr()))
+        assert rc == 0, rc
+
+    one()
+    k = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(k):
+        one()
+    dt = (time.perf_counter() - t0) / k
+    return {"value": nbytes / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 2 * nbytes,
+            "d2h_bytes_per_step": 2 * nbytes, "ms_per_step": dt * 1e3,
+            "path": "mgrx_host_decompose + mgrx_host_recompose (pinned host buffers)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--path", choices=["auto", "general"], default="auto")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-threads", type=int, default=0)
+    ap.add_argument("--warmup-ref", type=int, default=0, help="untimed reference steps (CPU code needs none)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        # rank 0 alone runs the CPU reference; other torchrun ranks exit 0
+        run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
+        return
+    ws, rank, local = dist_init()
+    run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,164 @@
+/* mgrx_b200 — C-ABI of the B200-native multilevel decompose / recompose and
+ * level-wise quantization path (the hot path of the optimized multigrid
+ * compressor, arXiv 2010.05872; reference: /root/reference/proj/core).
+ *
+ * This is the drop-in boundary.  Every entry point takes plain pointers and
+ * sizes; no C++ or torch types cross it and nothing throws across it.  Each
+ * function below names the reference interface it replaces (file:line is
+ * relative to the reference's proj/core/).
+ *
+ * Conventions
+ *  - Status: MGRX_OK (0) or 1 + the reference's mgrx::errc value
+ *    (include/mgrx/error.hpp:9-36), so a host wrapper can rethrow the same
+ *    mgrx::Error code.  CUDA failures and argument errors that the reference
+ *    cannot produce get codes >= 100.  mgrx_gpu_last_error() returns the
+ *    message of the last failure on that context.
+ *  - dims: row-major extents, slowest axis first (TensorField, tensor.hpp:20).
+ *  - levels: number of levels L, or -1 for the default depth
+ *    (GridHierarchy::create, src/grid.cpp:22).
+ *  - Device-pointer calls (mgrx_gpu_*) are asynchronous on the context's
+ *    stream unless stated otherwise; host-buffer calls (mgrx_host_*) copy in,
+ *    compute and copy out, and return after the stream has drained.
+ *  - A context is the GPU analogue of SolverWorkspace (transform.hpp:46-75):
+ *    it owns a stream, device scratch, uploaded per-level tables and cached
+ *    launch plans.  It is not thread-safe; use one per host thread.  Calls on
+ *    distinct contexts are independent.
+ */
+#ifndef MGRX_B200_H
+#define MGRX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MGRX_B200_ABI_VERSION 1
+#define MGRX_MAX_DIMS 8 /* update_coefficients' corner table: offs[1u << 8] (transform.hpp:271) */
+
+typedef struct mgrx_gpu_ctx mgrx_gpu_ctx;
+
+typedef enum { MGRX_F32 = 0, MGRX_F64 = 1 } mgrx_dtype;
+
+/* QuantMode (quantize.hpp:14) */
+typedef enum { MGRX_QUANT_UNIFORM = 0, MGRX_QUANT_LEVELWISE = 1 } mgrx_quant_mode;
+
+/* Status codes: 1 + mgrx::errc (error.hpp:9-36), then local codes. */
+enum {
+  MGRX_OK = 0,
+  MGRX_INVALID_DIMS = 1,
+  MGRX_DEPTH_EXCEEDED = 2,
+  MGRX_INVALID_LEVEL = 3,
+  MGRX_INVALID_AXIS = 4,
+  MGRX_DEGENERATE_LINE = 5,
+  MGRX_DEGENERATE_SYSTEM = 6,
+  MGRX_SHAPE_ERROR = 7,
+  MGRX_INVALID_BUDGET = 8,
+  MGRX_NONFINITE_DATA = 9,
+  MGRX_INVALID_INPUT = 15,
+  MGRX_CUDA_ERROR = 100,
+  MGRX_OUT_OF_MEMORY = 101,
+  MGRX_INVALID_ARGUMENT = 102,
+  MGRX_CAPACITY_EXCEEDED = 103
+};
+
+/* ---- library / context ------------------------------------------------ */
+
+int mgrx_abi_version(void);
+
+/* Creates a context on `device` with its own non-blocking stream.  Replaces
+ * SolverWorkspace ws(batch); ws.prepare(h) (transform.hpp:50,58). */
+int mgrx_gpu_ctx_create(int device, mgrx_gpu_ctx** out);
+int mgrx_gpu_ctx_destroy(mgrx_gpu_ctx* ctx);
+/* Run subsequent work on an external stream (cudaStream_t as void*); NULL
+ * restores the context's own stream. */
+int mgrx_gpu_set_stream(mgrx_gpu_ctx* ctx, void* stream);
+void* mgrx_gpu_get_stream(mgrx_gpu_ctx* ctx);
+int mgrx_gpu_synchronize(mgrx_gpu_ctx* ctx);
+const char* mgrx_gpu_last_error(const mgrx_gpu_ctx* ctx);
+/* Number of kernels this context has launched so far (launch accounting for
+ * the benchmark's gpu_launches). */
+uint64_t mgrx_gpu_launch_count(const mgrx_gpu_ctx* ctx);
+/* Per-kernel CUDA-event timing for roofline reporting: between begin and
+ * end every tagged kernel launch is bracketed by events on its stream.  end
+ * synchronises and returns, per distinct kernel tag, the summed device
+ * time (ms) and launch count; tags are written as 32-byte NUL-terminated
+ * slots.  *n = number of distinct tags (rows beyond cap are dropped). */
+int mgrx_gpu_profile_begin(mgrx_gpu_ctx* ctx);
+int mgrx_gpu_profile_end(mgrx_gpu_ctx* ctx, char* tags, double* ms, uint64_t* counts, int cap, int* n);
+/* Select the kernel family: 0 = auto (fused 3-D path where it applies),
+ * 1 = general per-step kernels only (bitwise equal to the reference). */
+int mgrx_gpu_set_path(mgrx_gpu_ctx* ctx, int path);
+
+/* ---- host metadata (no device work) ------------------------------------ */
+
+/* GridHierarchy::create / level_dims / delta_count (grid.hpp:30-56,
+ * grid.cpp:9-49).  level_dims: (L+1) * ndims entries, level 0 (coarsest)
+ * first; delta_counts: L+1 entries.  Either output may be NULL. */
+int mgrx_hierarchy(int ndims, const uint64_t* dims, int levels, int* out_levels, uint64_t* level_dims,
+                   uint64_t* delta_counts);
+
+/* make_plan (quantize.cpp:7-24): bin_widths[L+1], level 0 first. */
+int mgrx_make_plan(int mode, double budget, int ndims, const uint64_t* dims, int levels, double* bin_widths);
+
+/* ---- device-pointer entry points ----------------------------------------- */
+
+/* decompose (transform.hpp:509-515): d_field (N elements, row-major, not
+ * modified) -> d_out, the level-centric buffer of MultilevelCoefficients
+ * (transform.hpp:158-163, layout pack_level_centric reorder.hpp:162). */
+int mgrx_gpu_decompose(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels,
+                       int stop_level, const void* d_field, void* d_out);
+
+/* recompose (transform.hpp:517-530): level-centric d_coeffs -> d_field. */
+int mgrx_gpu_recompose(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels,
+                       int stop_level, const void* d_coeffs, void* d_field);
+
+/* Nonuniform-coordinate variants (no reference counterpart: SPEC.md:13,:73
+ * normalise the spacing away).  coords[a] is a HOST array of dims[a]
+ * strictly increasing coordinates for axis a; with equispaced coordinates
+ * the result equals mgrx_gpu_decompose to rounding. */
+int mgrx_gpu_decompose_nonuniform(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels,
+                                  int stop_level, const double* const* coords, const void* d_field,
+                                  void* d_out);
+int mgrx_gpu_recompose_nonuniform(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels,
+                                  int stop_level, const double* const* coords, const void* d_coeffs,
+                                  void* d_field);
+
+/* quantize (quantize.hpp:79-95) for stop_level == 0, quantize_tail
+ * (quantize.hpp:99-114) for stop_level > 0.  bin_widths: HOST, L+1 entries.
+ * d_labels receives the concatenated per-level LabelStream::labels (levels
+ * stop+1..L for a tail, 0..L otherwise).  Outliers (|label| beyond the
+ * 16-bit alphabet) are written in strictly increasing position order as
+ * required by read_outliers (pipeline.hpp:56-57).  SYNCHRONOUS: returns
+ * MGRX_NONFINITE_DATA like quantize_span (quantize.hpp:64), and
+ * MGRX_CAPACITY_EXCEEDED (with *n_outliers set) when more than
+ * outlier_capacity outliers exist. */
+int mgrx_gpu_quantize(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels,
+                      int stop_level, const double* bin_widths, const void* d_coeffs, int32_t* d_labels,
+                      uint64_t* d_outlier_pos, void* d_outlier_val, uint64_t outlier_capacity,
+                      uint64_t* n_outliers);
+
+/* dequantize / dequantize_tail (quantize.hpp:118-150): labels -> d_coeffs,
+ * then outliers restored exactly.  For stop_level > 0 the coarse block
+ * [0, node_count(stop)) of d_coeffs is left untouched. */
+int mgrx_gpu_dequantize(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels,
+                        int stop_level, const double* bin_widths, const int32_t* d_labels,
+                        const uint64_t* d_outlier_pos, const void* d_outlier_val, uint64_t n_outliers,
+                        void* d_coeffs);
+
+/* ---- host-buffer entry points (end-to-end: H2D + compute + D2H) ---------- */
+
+int mgrx_host_decompose(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels,
+                        int stop_level, const void* h_field, void* h_out);
+int mgrx_host_recompose(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels,
+                        int stop_level, const void* h_coeffs, void* h_field);
+
+/* Device scratch a decompose/recompose of this shape needs (bytes). */
+int mgrx_gpu_workspace_size(int dtype, int ndims, const uint64_t* dims, int levels, int stop_level,
+                            uint64_t* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MGRX_B200_H */

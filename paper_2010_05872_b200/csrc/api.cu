@@ -1,0 +1,839 @@
+// C-ABI layer of mgrx_b200 (include/mgrx_b200.h): contexts, launch plans,
+// scratch management and the level loops of decompose / recompose
+// (reference transform.hpp:485-530) and quantize / dequantize
+// (quantize.hpp:79-150).  Host-side only; all arithmetic runs in the
+// kernels of general.cu, fused3d.cu and quantize.cu.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "fused3d.h"
+#include "kernels.h"
+
+using namespace mgrx_b200;
+
+namespace {
+
+// ---------------------------------------------------------------- errors
+
+struct Status {
+  int code = MGRX_OK;
+  std::string msg;
+};
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  throw Fail{code, buf};
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  const int code = (e == cudaErrorMemoryAllocation) ? MGRX_OUT_OF_MEMORY : MGRX_CUDA_ERROR;
+  fail(code, "%s: %s", what, cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------- hierarchy
+// GridHierarchy::max_levels / create (grid.cpp:9-49).
+
+struct Hierarchy {
+  int d = 0, L = 0;
+  std::vector<std::vector<int64_t>> dims;  // [level][axis], level 0 coarsest
+  std::vector<int64_t> node, delta;        // node_count / delta_count by level
+};
+
+int max_levels(int nd, const uint64_t* dims) {
+  if (nd <= 0) fail(MGRX_INVALID_DIMS, "empty dimension list");
+  if (nd > kMaxD) fail(MGRX_INVALID_DIMS, "rank %d exceeds %d", nd, kMaxD);
+  int depth = 1 << 30;
+  for (int i = 0; i < nd; ++i) {
+    if (dims[i] < 2) fail(MGRX_INVALID_DIMS, "dimension %llu < 2", (unsigned long long)dims[i]);
+    int k = 63 - __builtin_clzll(dims[i] - 1);  // floor(log2(n-1))
+    depth = k < depth ? k : depth;
+  }
+  return depth;
+}
+
+Hierarchy make_hierarchy(int nd, const uint64_t* dims, int levels) {
+  const int feasible = max_levels(nd, dims);
+  const int L = levels < 0 ? feasible : levels;
+  if (L > feasible) fail(MGRX_DEPTH_EXCEEDED, "requested %d levels, at most %d feasible", L, feasible);
+  if (L + 1 > kMaxLevels) fail(MGRX_DEPTH_EXCEEDED, "too many levels");
+  Hierarchy h;
+  h.d = nd;
+  h.L = L;
+  h.dims.assign(L + 1, std::vector<int64_t>(nd));
+  for (int i = 0; i < nd; ++i) h.dims[L][i] = int64_t(dims[i]);
+  for (int l = L - 1; l >= 0; --l)
+    for (int i = 0; i < nd; ++i) h.dims[l][i] = (h.dims[l + 1][i] + 1) / 2;
+  h.node.resize(L + 1);
+  h.delta.resize(L + 1);
+  for (int l = 0; l <= L; ++l) {
+    int64_t c = 1;
+    for (int i = 0; i < nd; ++i) c *= h.dims[l][i];
+    h.node[l] = c;
+    h.delta[l] = c - (l ? h.node[l - 1] : 0);
+  }
+  return h;
+}
+
+LevelGeom make_geom(const Hierarchy& h, int l) {
+  LevelGeom g{};
+  g.d = h.d;
+  for (int i = 0; i < h.d; ++i) {
+    g.n[i] = h.dims[l][i];
+    g.m[i] = h.dims[l - 1][i];
+  }
+  g.st[h.d - 1] = 1;
+  g.cst[h.d - 1] = 1;
+  for (int i = h.d - 2; i >= 0; --i) {
+    g.st[i] = g.st[i + 1] * g.n[i + 1];
+    g.cst[i] = g.cst[i + 1] * g.m[i + 1];
+  }
+  for (int i = 0; i < h.d; ++i) {
+    int64_t p = 1;
+    for (int k = i + 1; k + 1 < h.d; ++k) p *= g.m[k];
+    g.pm[i] = p;
+    g.fn[i] = FastDiv(uint32_t(g.n[i] <= 0xffffffffLL ? g.n[i] : 1));
+  }
+  g.N = h.node[l];
+  g.Nc = h.node[l - 1];
+  return g;
+}
+
+// ThomasAux::build (transform.hpp:29-43), identical constant expressions.
+void thomas_aux(int64_t m, double* w, double* inv_d) {
+  if (m < 2) fail(MGRX_DEGENERATE_SYSTEM, "correction system needs at least 2 unknowns");
+  double dd = kDiagB;
+  w[0] = 0.0;
+  inv_d[0] = 1.0 / dd;
+  for (int64_t i = 1; i < m; ++i) {
+    const double wi = kOff / dd;
+    w[i] = wi;
+    dd = (i + 1 == m ? kDiagB : kDiagI) - wi * kOff;
+    inv_d[i] = 1.0 / dd;
+  }
+}
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// ------------------------------------------------------------------ plan
+
+struct PlanKey {
+  int dtype, L, stop;
+  std::vector<int64_t> dims;
+  bool operator<(const PlanKey& o) const {
+    if (dtype != o.dtype) return dtype < o.dtype;
+    if (L != o.L) return L < o.L;
+    if (stop != o.stop) return stop < o.stop;
+    return dims < o.dims;
+  }
+};
+
+struct Plan {
+  Hierarchy h;
+  int stop = 0;
+  size_t esize = 4;
+  std::vector<LevelGeom> geom;     // index l (valid for l in (stop, L])
+  std::vector<ThomasLevel> thomas; // index l
+  double* d_tables = nullptr;      // uniform Thomas factors for all levels
+  // scratch layout (bytes offsets)
+  size_t off_comp = 0, off_tmp = 0, off_blk = 0, bytes = 0;
+  std::vector<size_t> blk_off;     // level block offsets (levels stop..L-1)
+  std::vector<Fused3DPlan> fused;  // index l; .enabled false when not applicable
+  ~Plan() {
+    if (d_tables) cudaFree(d_tables);
+  }
+};
+
+}  // namespace
+
+// Event profiler behind MGRX_LAUNCH (common.cuh): one start/stop event pair
+// per tagged launch, recorded on the launching stream; summed per tag at
+// mgrx_gpu_profile_end.
+struct mgrx_b200::Profiler {
+  struct Rec {
+    const char* tag;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  cudaEvent_t get() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  ~Profiler() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+void mgrx_b200::prof_mark(const Exec& ex, const char* tag, bool begin) {
+  Profiler* p = ex.prof;
+  if (begin) {
+    cudaEvent_t a = p->get();
+    cudaEventRecord(a, ex.s);
+    p->recs.push_back({tag, a, nullptr});
+  } else {
+    cudaEvent_t b = p->get();
+    cudaEventRecord(b, ex.s);
+    p->recs.back().b = b;
+  }
+}
+
+struct mgrx_gpu_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  uint64_t launches = 0;
+  int path = 0;
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  void* io = nullptr;  // host-entry-point staging (input + output)
+  size_t io_bytes = 0;
+  void* qtmp = nullptr;  // quantize chunk counts / offsets / flags
+  size_t qtmp_bytes = 0;
+  void* pinned = nullptr;  // pinned host readback
+  double* nu_tables = nullptr;  // nonuniform per-call tables (device)
+  size_t nu_bytes = 0;
+  std::map<PlanKey, std::unique_ptr<Plan>> plans;
+  Profiler prof;
+  bool profiling = false;
+};
+
+namespace {
+
+Exec exec(mgrx_gpu_ctx* c) { return Exec{c->stream, &c->launches, c->profiling ? &c->prof : nullptr}; }
+
+void set_device(mgrx_gpu_ctx* c) { cuda_check(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+void ensure(void** p, size_t* have, size_t need, mgrx_gpu_ctx* c, const char* what) {
+  if (*have >= need) return;
+  if (*p) {
+    cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    cudaFree(*p);
+    *p = nullptr;
+    *have = 0;
+  }
+  cuda_check(cudaMalloc(p, need), what);
+  *have = need;
+}
+
+size_t esize_of(int dtype) {
+  if (dtype == MGRX_F32) return 4;
+  if (dtype == MGRX_F64) return 8;
+  fail(MGRX_INVALID_ARGUMENT, "unknown dtype %d", dtype);
+}
+
+Plan* get_plan(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop) {
+  const size_t es = esize_of(dtype);
+  Hierarchy h = make_hierarchy(nd, dims, levels);
+  if (stop < 0 || stop > h.L) fail(MGRX_INVALID_LEVEL, "stop level %d out of range [0, %d]", stop, h.L);
+  PlanKey key{dtype, h.L, stop, h.dims[h.L]};
+  auto it = c->plans.find(key);
+  if (it != c->plans.end()) return it->second.get();
+
+  auto p = std::make_unique<Plan>();
+  p->h = h;
+  p->stop = stop;
+  p->esize = es;
+  const int L = h.L;
+  p->geom.resize(L + 1);
+  p->thomas.resize(L + 1);
+  p->fused.resize(L + 1);
+  // Uniform Thomas tables per level and axis (SolverWorkspace::prepare,
+  // transform.hpp:58-61), uploaded once.
+  std::vector<double> host;
+  std::vector<std::pair<int, int>> slot;  // (level, axis) -> table starts
+  std::vector<size_t> starts;
+  for (int l = stop + 1; l <= L; ++l) {
+    p->geom[l] = make_geom(h, l);
+    for (int a = 0; a < nd; ++a) {
+      const int64_t m = h.dims[l - 1][a];
+      starts.push_back(host.size());
+      host.resize(host.size() + 2 * size_t(m));
+      thomas_aux(m, host.data() + starts.back(), host.data() + starts.back() + m);
+    }
+  }
+  if (!host.empty()) {
+    cuda_check(cudaMalloc(&p->d_tables, host.size() * sizeof(double)), "cudaMalloc(tables)");
+    cuda_check(cudaMemcpy(p->d_tables, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice),
+               "upload tables");
+  }
+  size_t k = 0;
+  for (int l = stop + 1; l <= L; ++l)
+    for (int a = 0; a < nd; ++a, ++k) {
+      const int64_t m = h.dims[l - 1][a];
+      p->thomas[l].w[a] = p->d_tables + starts[k];
+      p->thomas[l].inv_d[a] = p->d_tables + starts[k] + m;
+    }
+  // Scratch: fp64 component + sweep ping-pong (sized for the finest level
+  // processed) and the compact level blocks stop..L-1.
+  int64_t comp = 0, tmp = 0;
+  for (int l = stop + 1; l <= L; ++l) {
+    comp = std::max(comp, h.node[l]);
+    int64_t y0 = h.dims[l - 1][0];
+    for (int i = 1; i < nd; ++i) y0 *= h.dims[l][i];
+    tmp = std::max(tmp, y0);
+  }
+  size_t off = 0;
+  p->off_comp = off;
+  off = align_up(off + size_t(comp) * 8);
+  p->off_tmp = off;
+  off = align_up(off + size_t(tmp) * 8);
+  p->blk_off.assign(L + 1, 0);
+  for (int l = stop; l < L; ++l) {
+    p->blk_off[l] = off;
+    off = align_up(off + size_t(h.node[l]) * es);
+  }
+  // Fused 3-D plans (fused3d.cu) for the levels they cover.
+  for (int l = stop + 1; l <= L; ++l) {
+    p->fused[l] = fused3d_plan(p->geom[l], int(es));
+    if (p->fused[l].enabled) {
+      p->fused[l].scratch_off = off;
+      off = align_up(off + p->fused[l].scratch_bytes);
+    }
+  }
+  p->bytes = off;
+  Plan* raw = p.get();
+  c->plans.emplace(key, std::move(p));
+  return raw;
+}
+
+// ----------------------------------------------------- nonuniform tables
+// Same derivation as oracle/mgrx_oracle.c:nu_build (uniform spacing
+// reduces every table to the reference constants).  Host fp64, uploaded per
+// call into ctx->nu_tables.
+void nu_axis_tables(const double* x, int64_t n, std::vector<double>& out, size_t* o_wl, size_t* o_wr,
+                    size_t* o_s, size_t* o_tw, size_t* o_tid, size_t* o_off) {
+  const int64_t m = (n + 1) / 2;
+  *o_wl = out.size();
+  out.resize(out.size() + n, 0.0);
+  *o_wr = out.size();
+  out.resize(out.size() + n, 0.0);
+  *o_s = out.size();
+  out.resize(out.size() + 5 * m, 0.0);
+  *o_tw = out.size();
+  out.resize(out.size() + m, 0.0);
+  *o_tid = out.size();
+  out.resize(out.size() + m, 0.0);
+  *o_off = out.size();
+  out.resize(out.size() + m, 0.0);
+  double* wl = out.data() + *o_wl;
+  double* wr = out.data() + *o_wr;
+  double* s = out.data() + *o_s;
+  double* tw = out.data() + *o_tw;
+  double* tid = out.data() + *o_tid;
+  double* offd = out.data() + *o_off;
+  for (int64_t j = 1; j < n; j += 2) {
+    if (j + 1 < n) {
+      const double span = x[j + 1] - x[j - 1];
+      wl[j] = (x[j + 1] - x[j]) / span;
+      wr[j] = (x[j] - x[j - 1]) / span;
+    } else {
+      wl[j] = 1.0;
+      wr[j] = 0.0;
+    }
+  }
+  auto H = [&](int64_t j) { return (j >= 0 && j + 1 < n) ? x[j + 1] - x[j] : 0.0; };
+  for (int64_t i = 0; i < m; ++i) {
+    const int64_t c = 2 * i;
+    double* si = s + 5 * i;
+    const bool even_end = (n % 2 == 0) && (i + 1 == m);
+    const double al = i > 0 ? H(c - 2) / (H(c - 2) + H(c - 1)) : 0.0;
+    const double ar = (!even_end && i + 1 < m) ? H(c + 1) / (H(c) + H(c + 1)) : 0.0;
+    if (i > 0) {
+      si[0] = al * H(c - 2) / 6.0;
+      si[1] = al * (H(c - 2) + H(c - 1)) / 3.0 + H(c - 1) / 6.0;
+    }
+    if (even_end) {
+      si[2] = al * H(c - 1) / 6.0 + H(c - 1) / 3.0;
+      si[3] = H(c) / 2.0;
+    } else {
+      si[2] = al * H(c - 1) / 6.0 + (H(c - 1) + H(c)) / 3.0 + ar * H(c) / 6.0;
+      if (i + 1 < m) {
+        si[3] = H(c) / 6.0 + ar * (H(c) + H(c + 1)) / 3.0;
+        si[4] = ar * H(c + 1) / 6.0;
+      }
+    }
+  }
+  std::vector<double> Hc(m, 0.0);
+  for (int64_t i = 0; i + 1 < m; ++i) Hc[i] = x[2 * i + 2] - x[2 * i];
+  double dd = Hc[0] / 3.0;
+  tw[0] = 0.0;
+  tid[0] = 1.0 / dd;
+  for (int64_t i = 0; i + 1 < m; ++i) offd[i] = Hc[i] / 6.0;
+  for (int64_t i = 1; i < m; ++i) {
+    const double wi = offd[i - 1] / dd;
+    tw[i] = wi;
+    const double diag = (Hc[i - 1] + (i + 1 < m ? Hc[i] : 0.0)) / 3.0;
+    dd = diag - wi * offd[i - 1];
+    tid[i] = 1.0 / dd;
+  }
+}
+
+std::vector<NuLevel> upload_nu(mgrx_gpu_ctx* c, const Plan& p, const double* const* coords) {
+  const Hierarchy& h = p.h;
+  if (!coords) fail(MGRX_INVALID_ARGUMENT, "coords is NULL");
+  for (int a = 0; a < h.d; ++a) {
+    if (!coords[a]) fail(MGRX_INVALID_ARGUMENT, "coords[%d] is NULL", a);
+    for (int64_t j = 0; j + 1 < h.dims[h.L][a]; ++j)
+      if (!(coords[a][j + 1] > coords[a][j]))
+        fail(MGRX_INVALID_INPUT, "coordinates of axis %d not strictly increasing at %lld", a, (long long)j);
+  }
+  std::vector<double> host;
+  struct Off {
+    size_t wl, wr, s, tw, tid, off;
+  };
+  std::vector<std::vector<Off>> offs(h.L + 1, std::vector<Off>(h.d));
+  std::vector<double> x;
+  for (int l = p.stop + 1; l <= h.L; ++l)
+    for (int a = 0; a < h.d; ++a) {
+      const int64_t n = h.dims[l][a];
+      const int64_t stride = int64_t(1) << (h.L - l);
+      x.resize(n);
+      for (int64_t j = 0; j < n; ++j) x[j] = coords[a][j * stride];
+      Off& o = offs[l][a];
+      nu_axis_tables(x.data(), n, host, &o.wl, &o.wr, &o.s, &o.tw, &o.tid, &o.off);
+    }
+  size_t need = host.size() * sizeof(double);
+  ensure(reinterpret_cast<void**>(&c->nu_tables), &c->nu_bytes, need ? need : 8, c, "cudaMalloc(nu tables)");
+  cuda_check(cudaMemcpyAsync(c->nu_tables, host.data(), need, cudaMemcpyHostToDevice, c->stream), "upload nu");
+  cuda_check(cudaStreamSynchronize(c->stream), "sync nu upload");
+  std::vector<NuLevel> out(h.L + 1);
+  for (int l = p.stop + 1; l <= h.L; ++l)
+    for (int a = 0; a < h.d; ++a) {
+      const Off& o = offs[l][a];
+      out[l].ax[a] = NuAxis{c->nu_tables + o.wl, c->nu_tables + o.wr, c->nu_tables + o.s,
+                            c->nu_tables + o.tw, c->nu_tables + o.tid, c->nu_tables + o.off};
+    }
+  return out;
+}
+
+// ------------------------------------------------------------- transform
+
+template <typename T>
+void decompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, T* d_out, const std::vector<NuLevel>* nu) {
+  const Hierarchy& h = p.h;
+  const int L = h.L, stop = p.stop;
+  if (stop == L) {  // identity (transform.hpp:494 loop does not run)
+    cuda_check(cudaMemcpyAsync(d_out, d_field, size_t(h.node[L]) * sizeof(T), cudaMemcpyDeviceToDevice, c->stream),
+               "copy");
+    return;
+  }
+  ensure(&c->scratch, &c->scratch_bytes, p.bytes, c, "cudaMalloc(scratch)");
+  char* s = static_cast<char*>(c->scratch);
+  double* comp = reinterpret_cast<double*>(s + p.off_comp);
+  double* tmp = reinterpret_cast<double*>(s + p.off_tmp);
+  const T* blk = d_field;
+  for (int l = L; l > stop; --l) {
+    T* shell = d_out + h.node[l - 1];
+    T* coarse = (l - 1 == stop) ? d_out : reinterpret_cast<T*>(s + p.blk_off[l - 1]);
+    const Fused3DPlan& fp = p.fused[l];
+    cudaError_t e;
+    if (!nu && c->path == 0 && fp.enabled) {
+      e = fused3d_decompose_level<T>(blk, shell, coarse, s + fp.scratch_off, p.geom[l], fp, p.thomas[l], exec(c));
+    } else {
+      e = general_decompose_level<T>(blk, shell, coarse, comp, tmp, p.geom[l], &p.thomas[l],
+                                     nu ? &(*nu)[l] : nullptr, exec(c));
+    }
+    cuda_check(e, "decompose level");
+    blk = coarse;
+  }
+}
+
+template <typename T>
+void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, const std::vector<NuLevel>* nu) {
+  const Hierarchy& h = p.h;
+  const int L = h.L, stop = p.stop;
+  if (stop == L) {
+    cuda_check(cudaMemcpyAsync(d_field, d_coeffs, size_t(h.node[L]) * sizeof(T), cudaMemcpyDeviceToDevice,
+                               c->stream),
+               "copy");
+    return;
+  }
+  ensure(&c->scratch, &c->scratch_bytes, p.bytes, c, "cudaMalloc(scratch)");
+  char* s = static_cast<char*>(c->scratch);
+  double* comp = reinterpret_cast<double*>(s + p.off_comp);
+  double* tmp = reinterpret_cast<double*>(s + p.off_tmp);
+  // unpack_level_centric's coarse block (reorder.hpp:231-238)
+  T* coarse = reinterpret_cast<T*>(s + p.blk_off[stop]);
+  cuda_check(cudaMemcpyAsync(coarse, d_coeffs, size_t(h.node[stop]) * sizeof(T), cudaMemcpyDeviceToDevice,
+                             c->stream),
+             "copy coarse");
+  for (int l = stop + 1; l <= L; ++l) {
+    const T* shell = d_coeffs + h.node[l - 1];
+    T* fine = (l == L) ? d_field : reinterpret_cast<T*>(s + p.blk_off[l]);
+    const Fused3DPlan& fp = p.fused[l];
+    cudaError_t e;
+    if (!nu && c->path == 0 && fp.enabled) {
+      e = fused3d_recompose_level<T>(shell, coarse, fine, s + fp.scratch_off, p.geom[l], fp, p.thomas[l],
+                                     exec(c));
+    } else {
+      e = general_recompose_level<T>(shell, coarse, fine, comp, tmp, p.geom[l], &p.thomas[l],
+                                     nu ? &(*nu)[l] : nullptr, exec(c));
+    }
+    cuda_check(e, "recompose level");
+    coarse = fine;
+  }
+}
+
+QuantLevels quant_levels(const Plan& p, const double* q) {
+  const Hierarchy& h = p.h;
+  QuantLevels ql{};
+  ql.first = p.stop == 0 ? 0 : p.stop + 1;
+  ql.last = h.L;
+  ql.base = p.stop == 0 ? 0 : h.node[p.stop];
+  ql.total = h.node[h.L];
+  for (int l = 0; l <= h.L; ++l) {
+    ql.end[l] = h.node[l];
+    ql.q[l] = q[l];
+  }
+  return ql;
+}
+
+template <typename Fn>
+int guarded(mgrx_gpu_ctx* c, Fn&& fn) {
+  if (!c) return MGRX_INVALID_ARGUMENT;
+  try {
+    set_device(c);
+    fn();
+    return MGRX_OK;
+  } catch (const Fail& f) {
+    c->last_error = f.msg;
+    return f.code;
+  } catch (const std::bad_alloc&) {
+    c->last_error = "host allocation failed";
+    return MGRX_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    c->last_error = e.what();
+    return MGRX_INVALID_ARGUMENT;
+  }
+}
+
+template <typename Fn>
+int guarded_noctx(Fn&& fn) {
+  try {
+    fn();
+    return MGRX_OK;
+  } catch (const Fail& f) {
+    return f.code;
+  } catch (...) {
+    return MGRX_INVALID_ARGUMENT;
+  }
+}
+
+}  // namespace
+
+// =========================================================================
+extern "C" {
+
+int mgrx_abi_version(void) { return MGRX_B200_ABI_VERSION; }
+
+int mgrx_gpu_ctx_create(int device, mgrx_gpu_ctx** out) {
+  if (!out) return MGRX_INVALID_ARGUMENT;
+  *out = nullptr;
+  auto* c = new (std::nothrow) mgrx_gpu_ctx;
+  if (!c) return MGRX_OUT_OF_MEMORY;
+  c->device = device;
+  int rc = guarded(c, [&] {
+    cuda_check(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
+    c->stream = c->own;
+    cuda_check(cudaMallocHost(&c->pinned, 64), "cudaMallocHost");
+  });
+  if (rc != MGRX_OK) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return MGRX_OK;
+}
+
+int mgrx_gpu_ctx_destroy(mgrx_gpu_ctx* c) {
+  if (!c) return MGRX_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  c->plans.clear();
+  if (c->scratch) cudaFree(c->scratch);
+  if (c->io) cudaFree(c->io);
+  if (c->qtmp) cudaFree(c->qtmp);
+  if (c->nu_tables) cudaFree(c->nu_tables);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->own) cudaStreamDestroy(c->own);
+  delete c;
+  return MGRX_OK;
+}
+
+int mgrx_gpu_set_stream(mgrx_gpu_ctx* c, void* stream) {
+  return guarded(c, [&] { c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own; });
+}
+
+void* mgrx_gpu_get_stream(mgrx_gpu_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+int mgrx_gpu_synchronize(mgrx_gpu_ctx* c) {
+  return guarded(c, [&] { cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize"); });
+}
+
+const char* mgrx_gpu_last_error(const mgrx_gpu_ctx* c) { return c ? c->last_error.c_str() : "null context"; }
+
+uint64_t mgrx_gpu_launch_count(const mgrx_gpu_ctx* c) { return c ? c->launches : 0; }
+
+int mgrx_gpu_profile_begin(mgrx_gpu_ctx* c) {
+  return guarded(c, [&] {
+    c->prof.recs.clear();
+    c->prof.used = 0;
+    c->profiling = true;
+  });
+}
+
+int mgrx_gpu_profile_end(mgrx_gpu_ctx* c, char* tags, double* ms, uint64_t* counts, int cap, int* n) {
+  return guarded(c, [&] {
+    c->profiling = false;
+    cuda_check(cudaStreamSynchronize(c->stream), "profile sync");
+    std::vector<std::string> names;
+    std::vector<double> tot;
+    std::vector<uint64_t> cnt;
+    for (const auto& r : c->prof.recs) {
+      float t = 0.f;
+      cuda_check(cudaEventElapsedTime(&t, r.a, r.b), "cudaEventElapsedTime");
+      size_t i = 0;
+      while (i < names.size() && names[i] != r.tag) ++i;
+      if (i == names.size()) {
+        names.push_back(r.tag);
+        tot.push_back(0.0);
+        cnt.push_back(0);
+      }
+      tot[i] += t;
+      cnt[i] += 1;
+    }
+    *n = int(names.size());
+    for (int i = 0; i < int(names.size()) && i < cap; ++i) {
+      std::snprintf(tags + 32 * i, 32, "%s", names[i].c_str());
+      ms[i] = tot[i];
+      counts[i] = cnt[i];
+    }
+    c->prof.recs.clear();
+    c->prof.used = 0;
+  });
+}
+
+int mgrx_gpu_set_path(mgrx_gpu_ctx* c, int path) {
+  return guarded(c, [&] {
+    if (path < 0 || path > 1) fail(MGRX_INVALID_ARGUMENT, "path must be 0 (auto) or 1 (general)");
+    c->path = path;
+  });
+}
+
+int mgrx_hierarchy(int nd, const uint64_t* dims, int levels, int* out_levels, uint64_t* level_dims,
+                   uint64_t* delta_counts) {
+  return guarded_noctx([&] {
+    if (!out_levels || (nd > 0 && !dims)) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    Hierarchy h = make_hierarchy(nd, dims, levels);
+    *out_levels = h.L;
+    for (int l = 0; l <= h.L; ++l) {
+      if (level_dims)
+        for (int i = 0; i < nd; ++i) level_dims[size_t(l) * nd + i] = uint64_t(h.dims[l][i]);
+      if (delta_counts) delta_counts[l] = uint64_t(h.delta[l]);
+    }
+  });
+}
+
+int mgrx_make_plan(int mode, double budget, int nd, const uint64_t* dims, int levels, double* q) {
+  return guarded_noctx([&] {
+    if (!(budget > 0.0) || !std::isfinite(budget)) fail(MGRX_INVALID_BUDGET, "budget must be positive");
+    if (!dims || !q) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    Hierarchy h = make_hierarchy(nd, dims, levels);
+    const int L = h.L;
+    if (mode == MGRX_QUANT_UNIFORM) {
+      const double qq = 2.0 * budget / double(L + 1);
+      for (int l = 0; l <= L; ++l) q[l] = qq;
+    } else if (mode == MGRX_QUANT_LEVELWISE) {
+      const double total = double(h.node[L]);
+      for (int l = 0; l <= L; ++l) q[l] = 2.0 * budget * double(h.delta[l]) / total;
+    } else {
+      fail(MGRX_INVALID_ARGUMENT, "unknown quant mode %d", mode);
+    }
+  });
+}
+
+int mgrx_gpu_workspace_size(int dtype, int nd, const uint64_t* dims, int levels, int stop, uint64_t* bytes) {
+  mgrx_gpu_ctx tmp;  // plan sizing only; no device work besides table upload
+  int rc = guarded(&tmp, [&] {
+    Plan* p = get_plan(&tmp, dtype, nd, dims, levels, stop);
+    *bytes = p->bytes;
+  });
+  tmp.plans.clear();
+  return rc;
+}
+
+int mgrx_gpu_decompose(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
+                       const void* d_field, void* d_out) {
+  return guarded(c, [&] {
+    if (!dims || !d_field || !d_out) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    Plan* p = get_plan(c, dtype, nd, dims, levels, stop);
+    if (dtype == MGRX_F32)
+      decompose_impl<float>(c, *p, static_cast<const float*>(d_field), static_cast<float*>(d_out), nullptr);
+    else
+      decompose_impl<double>(c, *p, static_cast<const double*>(d_field), static_cast<double*>(d_out), nullptr);
+  });
+}
+
+int mgrx_gpu_recompose(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
+                       const void* d_coeffs, void* d_field) {
+  return guarded(c, [&] {
+    if (!dims || !d_coeffs || !d_field) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    Plan* p = get_plan(c, dtype, nd, dims, levels, stop);
+    if (dtype == MGRX_F32)
+      recompose_impl<float>(c, *p, static_cast<const float*>(d_coeffs), static_cast<float*>(d_field), nullptr);
+    else
+      recompose_impl<double>(c, *p, static_cast<const double*>(d_coeffs), static_cast<double*>(d_field), nullptr);
+  });
+}
+
+int mgrx_gpu_decompose_nonuniform(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
+                                  const double* const* coords, const void* d_field, void* d_out) {
+  return guarded(c, [&] {
+    if (!dims || !d_field || !d_out) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    Plan* p = get_plan(c, dtype, nd, dims, levels, stop);
+    std::vector<NuLevel> nu = upload_nu(c, *p, coords);
+    if (dtype == MGRX_F32)
+      decompose_impl<float>(c, *p, static_cast<const float*>(d_field), static_cast<float*>(d_out), &nu);
+    else
+      decompose_impl<double>(c, *p, static_cast<const double*>(d_field), static_cast<double*>(d_out), &nu);
+  });
+}
+
+int mgrx_gpu_recompose_nonuniform(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
+                                  const double* const* coords, const void* d_coeffs, void* d_field) {
+  return guarded(c, [&] {
+    if (!dims || !d_coeffs || !d_field) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    Plan* p = get_plan(c, dtype, nd, dims, levels, stop);
+    std::vector<NuLevel> nu = upload_nu(c, *p, coords);
+    if (dtype == MGRX_F32)
+      recompose_impl<float>(c, *p, static_cast<const float*>(d_coeffs), static_cast<float*>(d_field), &nu);
+    else
+      recompose_impl<double>(c, *p, static_cast<const double*>(d_coeffs), static_cast<double*>(d_field), &nu);
+  });
+}
+
+int mgrx_gpu_quantize(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
+                      const double* q, const void* d_coeffs, int32_t* d_labels, uint64_t* d_opos, void* d_oval,
+                      uint64_t capacity, uint64_t* n_outliers) {
+  return guarded(c, [&] {
+    if (!dims || !q || !d_coeffs || !d_labels || !n_outliers) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    Plan* p = get_plan(c, dtype, nd, dims, levels, stop);
+    for (int l = 0; l <= p->h.L; ++l)
+      if (!(q[l] > 0.0) || !std::isfinite(q[l])) fail(MGRX_INVALID_BUDGET, "bad bin width at level %d", l);
+    QuantLevels ql = quant_levels(*p, q);
+    const int64_t nch = quant_num_chunks(ql);
+    const size_t need = align_up(size_t(nch + 1) * 4) + size_t(nch + 1) * 8 + 16;
+    ensure(&c->qtmp, &c->qtmp_bytes, need, c, "cudaMalloc(quant tmp)");
+    char* b = static_cast<char*>(c->qtmp);
+    uint32_t* counts = reinterpret_cast<uint32_t*>(b);
+    uint64_t* offsets = reinterpret_cast<uint64_t*>(b + align_up(size_t(nch + 1) * 4));
+    int* flags = reinterpret_cast<int*>(offsets + nch + 1);
+    cuda_check(cudaMemsetAsync(flags, 0, sizeof(int), c->stream), "memset");
+    cudaError_t e;
+    if (dtype == MGRX_F32)
+      e = quantize_pass1<float>(static_cast<const float*>(d_coeffs), d_labels, counts, offsets, flags, ql, exec(c));
+    else
+      e = quantize_pass1<double>(static_cast<const double*>(d_coeffs), d_labels, counts, offsets, flags, ql,
+                                 exec(c));
+    cuda_check(e, "quantize");
+    uint64_t* hp = static_cast<uint64_t*>(c->pinned);
+    cuda_check(cudaMemcpyAsync(hp, offsets + nch, 8, cudaMemcpyDeviceToHost, c->stream), "readback");
+    cuda_check(cudaMemcpyAsync(hp + 1, flags, 4, cudaMemcpyDeviceToHost, c->stream), "readback");
+    cuda_check(cudaStreamSynchronize(c->stream), "quantize sync");
+    const uint64_t total = hp[0];
+    const int flag = *reinterpret_cast<int*>(hp + 1);
+    *n_outliers = total;
+    if (flag) fail(MGRX_NONFINITE_DATA, "non-finite value in quantizer input");
+    if (total > capacity) fail(MGRX_CAPACITY_EXCEEDED, "%llu outliers exceed capacity %llu",
+                               (unsigned long long)total, (unsigned long long)capacity);
+    if (total > 0) {
+      if (!d_opos || !d_oval) fail(MGRX_INVALID_ARGUMENT, "null outlier buffers");
+      if (dtype == MGRX_F32)
+        e = quantize_pass2<float>(static_cast<const float*>(d_coeffs), counts, offsets, d_opos,
+                                  static_cast<float*>(d_oval), capacity, ql, exec(c));
+      else
+        e = quantize_pass2<double>(static_cast<const double*>(d_coeffs), counts, offsets, d_opos,
+                                   static_cast<double*>(d_oval), capacity, ql, exec(c));
+      cuda_check(e, "quantize outliers");
+      cuda_check(cudaStreamSynchronize(c->stream), "quantize sync");
+    }
+  });
+}
+
+int mgrx_gpu_dequantize(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
+                        const double* q, const int32_t* d_labels, const uint64_t* d_opos, const void* d_oval,
+                        uint64_t n_outliers, void* d_coeffs) {
+  return guarded(c, [&] {
+    if (!dims || !q || !d_labels || !d_coeffs) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    if (n_outliers && (!d_opos || !d_oval)) fail(MGRX_INVALID_ARGUMENT, "null outlier buffers");
+    Plan* p = get_plan(c, dtype, nd, dims, levels, stop);
+    QuantLevels ql = quant_levels(*p, q);
+    cudaError_t e;
+    if (dtype == MGRX_F32)
+      e = dequantize_run<float>(d_labels, d_opos, static_cast<const float*>(d_oval), n_outliers,
+                                static_cast<float*>(d_coeffs), ql, exec(c));
+    else
+      e = dequantize_run<double>(d_labels, d_opos, static_cast<const double*>(d_oval), n_outliers,
+                                 static_cast<double*>(d_coeffs), ql, exec(c));
+    cuda_check(e, "dequantize");
+  });
+}
+
+static int host_roundtrip(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
+                          const void* h_in, void* h_out, bool dec) {
+  return guarded(c, [&] {
+    if (!dims || !h_in || !h_out) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    Plan* p = get_plan(c, dtype, nd, dims, levels, stop);
+    const size_t bytes = size_t(p->h.node[p->h.L]) * p->esize;
+    ensure(&c->io, &c->io_bytes, 2 * align_up(bytes), c, "cudaMalloc(io)");
+    char* din = static_cast<char*>(c->io);
+    char* dout = din + align_up(bytes);
+    cuda_check(cudaMemcpyAsync(din, h_in, bytes, cudaMemcpyHostToDevice, c->stream), "H2D");
+    if (dtype == MGRX_F32) {
+      if (dec) decompose_impl<float>(c, *p, reinterpret_cast<float*>(din), reinterpret_cast<float*>(dout), nullptr);
+      else recompose_impl<float>(c, *p, reinterpret_cast<float*>(din), reinterpret_cast<float*>(dout), nullptr);
+    } else {
+      if (dec) decompose_impl<double>(c, *p, reinterpret_cast<double*>(din), reinterpret_cast<double*>(dout), nullptr);
+      else recompose_impl<double>(c, *p, reinterpret_cast<double*>(din), reinterpret_cast<double*>(dout), nullptr);
+    }
+    cuda_check(cudaMemcpyAsync(h_out, dout, bytes, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int mgrx_host_decompose(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
+                        const void* h_field, void* h_out) {
+  return host_roundtrip(c, dtype, nd, dims, levels, stop, h_field, h_out, true);
+}
+
+int mgrx_host_recompose(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
+                        const void* h_coeffs, void* h_field) {
+  return host_roundtrip(c, dtype, nd, dims, levels, stop, h_coeffs, h_field, false);
+}
+
+}  // extern "C"

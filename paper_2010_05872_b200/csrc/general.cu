@@ -1,0 +1,327 @@
+// General per-step kernels: any rank 1..8, any extents >= 2, fp32/fp64,
+// uniform and nonuniform coordinates.
+//
+// These follow the reference's per-element arithmetic exactly (same
+// constants, same summation order, no FMA contraction, same axis order for
+// the correction sweeps), so on the uniform path their output is
+// bit-identical to the reference's decompose/recompose.  They are the
+// correctness backbone and the path for shapes the fused 3-D kernels
+// (fused3d.cu) do not take.
+//
+// Layout: every level block lives compact and in natural order (the
+// reference keeps it as the reordered corner of the full array,
+// reorder.hpp:131); the multilevel component is a separate fp64 array in
+// natural order (the reference materialises it in reordered order,
+// transform.hpp:343-381).  The level-centric output layout is produced
+// directly by computing each coefficient's shell position.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mgrx_b200 {
+
+// --------------------------------------------------------------- indexing
+
+template <bool kIdx32>
+__device__ __forceinline__ void unravel(int64_t p, const LevelGeom& g, int64_t* j) {
+  if (kIdx32) {
+    uint32_t q = uint32_t(p);
+    for (int i = g.d - 1; i > 0; --i) {
+      const uint32_t qq = g.fn[i].div(q);
+      j[i] = int64_t(q - qq * uint32_t(g.n[i]));
+      q = qq;
+    }
+    j[0] = q;
+  } else {
+    for (int i = g.d - 1; i > 0; --i) {
+      j[i] = p % g.n[i];
+      p /= g.n[i];
+    }
+    j[0] = p;
+  }
+}
+
+// Shell position of a coefficient node (pack_level_centric,
+// reorder.hpp:180-215): rows of the reordered level block in row-major
+// order; a row whose leading reordered indices are all nodal contributes
+// only its coefficient tail [m_{d-1}, n_{d-1}).
+__device__ __forceinline__ int64_t shell_pos(const LevelGeom& g, const int64_t* j) {
+  const int d = g.d;
+  int64_t row = 0, before = 0;
+  bool inside = true;
+  for (int i = 0; i + 1 < d; ++i) {
+    const int64_t r = (j[i] & 1) ? g.m[i] + (j[i] >> 1) : (j[i] >> 1);
+    row = row * g.n[i] + r;
+    if (inside) {
+      if (r < g.m[i]) {
+        before += r * g.pm[i];
+      } else {
+        before += g.m[i] * g.pm[i];
+        inside = false;
+      }
+    }
+  }
+  const int64_t jl = j[d - 1];
+  const int64_t rl = (jl & 1) ? g.m[d - 1] + (jl >> 1) : (jl >> 1);
+  return row * g.n[d - 1] - before * g.m[d - 1] + (inside ? rl - g.m[d - 1] : rl);
+}
+
+// Multilinear prediction at node j from nodal values.  Uniform path:
+// corner_average (transform.hpp:206-212) with update_coefficients' corner
+// enumeration (:223-301) — set axes ascending, cmask ascending, a degenerate
+// even-axis end counting its single neighbour twice, sum * 2^-k.
+// src is either the natural fine block (coarse == false) or the compact
+// coarse block (coarse == true).
+template <typename T, bool kNu>
+__device__ __forceinline__ double predict(const T* __restrict__ src, bool coarse, const LevelGeom& g,
+                                          const NuLevel& nu, const int64_t* j) {
+  int set[kMaxD];
+  int k = 0;
+  int64_t base = 0;
+  for (int i = 0; i < g.d; ++i) {
+    const int64_t stride = coarse ? g.cst[i] : g.st[i];
+    if (j[i] & 1) {
+      set[k++] = i;
+      base += (coarse ? (j[i] - 1) >> 1 : j[i] - 1) * stride;
+    } else {
+      base += (coarse ? j[i] >> 1 : j[i]) * stride;
+    }
+  }
+  double sum = 0.0;
+  for (unsigned cm = 0; cm < (1u << k); ++cm) {
+    int64_t off = base;
+    double wprod = 1.0;
+    for (int b = 0; b < k; ++b) {
+      const int ax = set[b];
+      const bool right = (cm >> b) & 1u;
+      const bool has_right = j[ax] + 1 < g.n[ax];
+      if (right && has_right) off += coarse ? g.cst[ax] : 2 * g.st[ax];
+      if (kNu) wprod = mul_(wprod, right ? nu.ax[ax].wr[j[ax]] : nu.ax[ax].wl[j[ax]]);
+    }
+    const double v = double(src[off]);
+    sum = kNu ? add_(sum, mul_(wprod, v)) : add_(sum, v);
+  }
+  return kNu ? sum : mul_(sum, 1.0 / double(1u << k));
+}
+
+// ------------------------------------------------------------ decompose
+// reorder_level + compute_coefficients (transform.hpp:310) + the component
+// materialisation of compute_correction (:343-381) + the shell part of
+// pack_level_centric, one thread per fine node.
+template <typename T, bool kIdx32, bool kNu>
+__global__ void __launch_bounds__(256) k_dec_coef(const T* __restrict__ blk, T* __restrict__ shell,
+                                                  T* __restrict__ coarse, double* __restrict__ comp,
+                                                  const LevelGeom g, const NuLevel nu) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < g.N; p += stride) {
+    int64_t j[kMaxD];
+    unravel<kIdx32>(p, g, j);
+    bool nodal = true;
+    for (int i = 0; i < g.d; ++i) nodal &= !(j[i] & 1);
+    if (nodal) {
+      int64_t c = 0;
+      for (int i = 0; i < g.d; ++i) c += (j[i] >> 1) * g.cst[i];
+      coarse[c] = blk[p];
+      comp[p] = 0.0;
+    } else {
+      const double pred = predict<T, kNu>(blk, false, g, nu, j);
+      const T v = to_t<T>(sub_(double(blk[p]), pred));
+      comp[p] = double(v);
+      shell[shell_pos(g, j)] = v;
+    }
+  }
+}
+
+// One tensor-product sweep of compute_correction (transform.hpp:392-428)
+// along an axis: load vector (load_entry :84-96) + Thomas solve
+// (batched_solve :116-130), one thread per line; consecutive threads take
+// consecutive positions of the trailing axes so accesses coalesce whenever
+// the swept axis is not the last one.
+template <bool kNu>
+__global__ void __launch_bounds__(128) k_sweep(const double* __restrict__ x, double* __restrict__ y,
+                                               int64_t outer, int64_t inner, int64_t n, int64_t m,
+                                               const double* __restrict__ w, const double* __restrict__ inv_d,
+                                               const NuAxis nu) {
+  const int64_t lines = outer * inner;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t t0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t0 < lines; t0 += stride) {
+    const int64_t o = t0 / inner, t = t0 - o * inner;
+    const double* c = x + o * n * inner + t;
+    double* f = y + o * m * inner + t;
+    double prev = 0.0;
+    for (int64_t i = 0; i < m; ++i) {
+      double acc = 0.0;
+      if (kNu) {
+        const double* s = nu.s + 5 * i;
+        for (int k = 0; k < 5; ++k) {
+          const int64_t jj = 2 * i + k - 2;
+          if (jj >= 0 && jj < n) acc = add_(acc, mul_(s[k], c[jj * inner]));
+        }
+        if (i > 0) acc = sub_(acc, mul_(nu.tw[i], prev));
+      } else {
+        if (i >= 1) {
+          acc = add_(acc, mul_(kW12, c[(2 * i - 2) * inner]));
+          acc = add_(acc, mul_(0.5, c[(2 * i - 1) * inner]));
+        }
+        acc = add_(acc, mul_((i == 0 || i + 1 == m) ? kW5_12 : kW5_6, c[(2 * i) * inner]));
+        if (2 * i + 1 < n) acc = add_(acc, mul_(0.5, c[(2 * i + 1) * inner]));
+        if (2 * i + 2 < n) acc = add_(acc, mul_(kW12, c[(2 * i + 2) * inner]));
+        if (i > 0) acc = sub_(acc, mul_(w[i], prev));
+      }
+      f[i * inner] = acc;
+      prev = acc;
+    }
+    double nxt = mul_(prev, kNu ? nu.tid[m - 1] : inv_d[m - 1]);
+    f[(m - 1) * inner] = nxt;
+    for (int64_t i = m - 2; i >= 0; --i) {
+      const double v = kNu ? mul_(sub_(f[i * inner], mul_(nu.off[i], nxt)), nu.tid[i])
+                           : mul_(sub_(f[i * inner], mul_(kOff, nxt)), inv_d[i]);
+      f[i * inner] = v;
+      nxt = v;
+    }
+  }
+}
+
+// apply_correction (transform.hpp:435-477): corner <- T(double(corner) + s*z).
+template <typename T>
+__global__ void __launch_bounds__(256) k_apply(T* __restrict__ coarse, const double* __restrict__ z, int64_t nc,
+                                               double sign) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < nc; p += stride)
+    coarse[p] = to_t<T>(add_(double(coarse[p]), mul_(sign, z[p])));
+}
+
+// ------------------------------------------------------------ recompose
+// Component of a level from its shell (unpack_level_centric reorder.hpp:221
+// + the materialisation of compute_correction).
+template <typename T, bool kIdx32>
+__global__ void __launch_bounds__(256) k_rec_comp(const T* __restrict__ shell, double* __restrict__ comp,
+                                                  const LevelGeom g) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < g.N; p += stride) {
+    int64_t j[kMaxD];
+    unravel<kIdx32>(p, g, j);
+    bool nodal = true;
+    for (int i = 0; i < g.d; ++i) nodal &= !(j[i] & 1);
+    comp[p] = nodal ? 0.0 : double(shell[shell_pos(g, j)]);
+  }
+}
+
+// add_interpolant (transform.hpp:317) + inverse_reorder_level
+// (reorder.hpp:138): fine natural block from corrected coarse nodes and the
+// shell coefficients.
+template <typename T, bool kIdx32, bool kNu>
+__global__ void __launch_bounds__(256) k_rec_interp(const T* __restrict__ shell, const T* __restrict__ coarse,
+                                                    T* __restrict__ fine, const LevelGeom g, const NuLevel nu) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < g.N; p += stride) {
+    int64_t j[kMaxD];
+    unravel<kIdx32>(p, g, j);
+    bool nodal = true;
+    for (int i = 0; i < g.d; ++i) nodal &= !(j[i] & 1);
+    if (nodal) {
+      int64_t c = 0;
+      for (int i = 0; i < g.d; ++i) c += (j[i] >> 1) * g.cst[i];
+      fine[p] = coarse[c];
+    } else {
+      const double pred = predict<T, kNu>(coarse, true, g, nu, j);
+      fine[p] = to_t<T>(add_(double(shell[shell_pos(g, j)]), pred));
+    }
+  }
+}
+
+// ------------------------------------------------------------- launchers
+
+template <typename T>
+static void launch_dec_coef(const T* blk, T* shell, T* coarse, double* comp, const LevelGeom& g, const NuLevel* nu,
+                            const Exec& ex) {
+  const int grid = grid_for(g.N, 256);
+  const bool i32 = g.N < (int64_t(1) << 32);
+  const NuLevel z = nu ? *nu : NuLevel{};
+  if (nu) {
+    if (i32) MGRX_LAUNCH(ex, "gen_dec_coef", k_dec_coef<T, true, true><<<grid, 256, 0, ex.s>>>(blk, shell, coarse, comp, g, z));
+    else MGRX_LAUNCH(ex, "gen_dec_coef", k_dec_coef<T, false, true><<<grid, 256, 0, ex.s>>>(blk, shell, coarse, comp, g, z));
+  } else {
+    if (i32) MGRX_LAUNCH(ex, "gen_dec_coef", k_dec_coef<T, true, false><<<grid, 256, 0, ex.s>>>(blk, shell, coarse, comp, g, z));
+    else MGRX_LAUNCH(ex, "gen_dec_coef", k_dec_coef<T, false, false><<<grid, 256, 0, ex.s>>>(blk, shell, coarse, comp, g, z));
+  }
+}
+
+template <typename T>
+static void launch_rec_comp(const T* shell, double* comp, const LevelGeom& g, const Exec& ex) {
+  const int grid = grid_for(g.N, 256);
+  if (g.N < (int64_t(1) << 32)) MGRX_LAUNCH(ex, "gen_rec_comp", k_rec_comp<T, true><<<grid, 256, 0, ex.s>>>(shell, comp, g));
+  else MGRX_LAUNCH(ex, "gen_rec_comp", k_rec_comp<T, false><<<grid, 256, 0, ex.s>>>(shell, comp, g));
+}
+
+template <typename T>
+static void launch_rec_interp(const T* shell, const T* coarse, T* fine, const LevelGeom& g, const NuLevel* nu,
+                              const Exec& ex) {
+  const int grid = grid_for(g.N, 256);
+  const bool i32 = g.N < (int64_t(1) << 32);
+  const NuLevel z = nu ? *nu : NuLevel{};
+  if (nu) {
+    if (i32) MGRX_LAUNCH(ex, "gen_rec_interp", k_rec_interp<T, true, true><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, g, z));
+    else MGRX_LAUNCH(ex, "gen_rec_interp", k_rec_interp<T, false, true><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, g, z));
+  } else {
+    if (i32) MGRX_LAUNCH(ex, "gen_rec_interp", k_rec_interp<T, true, false><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, g, z));
+    else MGRX_LAUNCH(ex, "gen_rec_interp", k_rec_interp<T, false, false><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, g, z));
+  }
+}
+
+// compute_correction sweeps on `comp` (natural fine extents); the result
+// (coarse extents, row-major) ends in *result, which points into comp or tmp.
+static void run_sweeps(double* comp, double* tmp, const LevelGeom& g, const ThomasLevel* th, const NuLevel* nu,
+                       double** result, const Exec& ex) {
+  int64_t cur[kMaxD];
+  for (int i = 0; i < g.d; ++i) cur[i] = g.n[i];
+  double* x = comp;
+  double* y = tmp;
+  for (int a = 0; a < g.d; ++a) {
+    int64_t outer = 1, inner = 1;
+    for (int i = 0; i < a; ++i) outer *= cur[i];
+    for (int i = a + 1; i < g.d; ++i) inner *= cur[i];
+    const int64_t lines = outer * inner;
+    const int grid = grid_for(lines, 128, 32);
+    if (nu)
+      MGRX_LAUNCH(ex, "gen_sweep", k_sweep<true><<<grid, 128, 0, ex.s>>>(x, y, outer, inner, g.n[a], g.m[a], nullptr, nullptr, nu->ax[a]));
+    else
+      MGRX_LAUNCH(ex, "gen_sweep", k_sweep<false><<<grid, 128, 0, ex.s>>>(x, y, outer, inner, g.n[a], g.m[a], th->w[a], th->inv_d[a], NuAxis{}));
+    cur[a] = g.m[a];
+    double* t = x;
+    x = y;
+    y = t;
+  }
+  *result = x;
+}
+
+template <typename T>
+cudaError_t general_decompose_level(const T* blk, T* shell, T* coarse, double* comp, double* tmp, const LevelGeom& g,
+                                    const ThomasLevel* th, const NuLevel* nu, const Exec& ex) {
+  launch_dec_coef<T>(blk, shell, coarse, comp, g, nu, ex);
+  double* z = nullptr;
+  run_sweeps(comp, tmp, g, th, nu, &z, ex);
+  MGRX_LAUNCH(ex, "gen_apply", k_apply<T><<<grid_for(g.Nc, 256), 256, 0, ex.s>>>(coarse, z, g.Nc, 1.0));
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t general_recompose_level(const T* shell, T* coarse, T* fine, double* comp, double* tmp, const LevelGeom& g,
+                                    const ThomasLevel* th, const NuLevel* nu, const Exec& ex) {
+  launch_rec_comp<T>(shell, comp, g, ex);
+  double* z = nullptr;
+  run_sweeps(comp, tmp, g, th, nu, &z, ex);
+  MGRX_LAUNCH(ex, "gen_apply", k_apply<T><<<grid_for(g.Nc, 256), 256, 0, ex.s>>>(coarse, z, g.Nc, -1.0));
+  launch_rec_interp<T>(shell, coarse, fine, g, nu, ex);
+  return cudaGetLastError();
+}
+
+#define MGRX_INST(T)                                                                                           \
+  template cudaError_t general_decompose_level<T>(const T*, T*, T*, double*, double*, const LevelGeom&,         \
+                                                  const ThomasLevel*, const NuLevel*, const Exec&);             \
+  template cudaError_t general_recompose_level<T>(const T*, T*, T*, double*, double*, const LevelGeom&,         \
+                                                  const ThomasLevel*, const NuLevel*, const Exec&);
+MGRX_INST(float)
+MGRX_INST(double)
+#undef MGRX_INST
+
+}  // namespace mgrx_b200

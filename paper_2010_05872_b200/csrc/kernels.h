@@ -1,0 +1,38 @@
+// Internal launch interface between the C-ABI layer (api.cu) and the kernel
+// translation units.  Not part of the public boundary.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace mgrx_b200 {
+
+// ---- general per-step path (general.cu) -----------------------------------
+template <typename T>
+cudaError_t general_decompose_level(const T* blk, T* shell, T* coarse, double* comp, double* tmp,
+                                    const LevelGeom& g, const ThomasLevel* th, const NuLevel* nu, const Exec& ex);
+template <typename T>
+cudaError_t general_recompose_level(const T* shell, T* coarse, T* fine, double* comp, double* tmp,
+                                    const LevelGeom& g, const ThomasLevel* th, const NuLevel* nu, const Exec& ex);
+
+// ---- quantization (quantize.cu) --------------------------------------------
+struct QuantLevels {
+  int first, last;         // level range [first, last]
+  int64_t base, total;     // quantized positions [base, total)
+  int64_t end[kMaxLevels]; // end position (exclusive) of level l = node_count(l)
+  double q[kMaxLevels];    // bin widths
+};
+int64_t quant_num_chunks(const QuantLevels& ql);
+template <typename T>
+cudaError_t quantize_pass1(const T* c, int32_t* labels, uint32_t* chunk_counts, uint64_t* offsets, int* flags,
+                           const QuantLevels& ql, const Exec& ex);
+template <typename T>
+cudaError_t quantize_pass2(const T* c, const uint32_t* chunk_counts, const uint64_t* offsets, uint64_t* opos,
+                           T* oval, uint64_t capacity, const QuantLevels& ql, const Exec& ex);
+template <typename T>
+cudaError_t dequantize_run(const int32_t* labels, const uint64_t* opos, const T* oval, uint64_t n_out, T* c,
+                           const QuantLevels& ql, const Exec& ex);
+
+}  // namespace mgrx_b200

@@ -1,0 +1,219 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's
+outputs (tests/golden/golden.npz, generated from the unmodified reference)
+and the pinned CPU oracle.
+
+Bars (BASELINE.json north_star):
+  * general per-step path: bit-identical to the reference (same arithmetic);
+  * auto path (fused 3-D kernels where they apply): coefficients within
+    1e-12 * range (fp64) / 1e-5 * range (fp32) of the reference;
+  * quantized labels bit-exact except values within 1 ulp of a bin edge
+    (counted); dequantize bit-exact.
+"""
+import os
+
+import numpy as np
+import pytest
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden.npz")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+
+    return t
+
+
+@pytest.fixture(scope="module")
+def mg():
+    import paper_2010_05872_b200 as m
+
+    return m
+
+
+@pytest.fixture(scope="module")
+def g():
+    return np.load(GOLDEN)
+
+
+@pytest.fixture(scope="module")
+def ws_general(mg):
+    return mg.SolverWorkspace(path="general")
+
+
+@pytest.fixture(scope="module")
+def ws_auto(mg):
+    return mg.SolverWorkspace(path="auto")
+
+
+def shapes_in(g):
+    out = set()
+    for k in g.files:
+        if k.endswith("_f64_in"):
+            out.add(tuple(int(x) for x in k[: -len("_f64_in")].split("x")))
+    return sorted(out)
+
+
+def key(shape, *parts):
+    return "x".join(str(s) for s in shape) + "_" + "_".join(str(p) for p in parts)
+
+
+def to_dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def bits(a):
+    return np.ascontiguousarray(a).tobytes()
+
+
+def test_general_path_bitwise_against_reference(torch, mg, g, ws_general):
+    checked = 0
+    for shape in shapes_in(g):
+        h = mg.GridHierarchy.create(shape)
+        L = h.num_levels()
+        for name in ("f64", "f32"):
+            x = to_dev(torch, g[key(shape, name, "in")])
+            for stop in sorted({0, min(1, L), L}):
+                mc = mg.decompose(x, h, stop, ws_general)
+                got = mc.buffer.cpu().numpy()
+                want = g[key(shape, name, "dec", stop)]
+                assert bits(got) == bits(want), (shape, name, stop, np.abs(got - want).max())
+                back = mg.recompose(mg.MultilevelCoefficients(to_dev(torch, want), h, stop), ws_general)
+                assert bits(back.cpu().numpy()) == bits(g[key(shape, name, "rec", stop)]), (shape, name, stop)
+                checked += 1
+    assert checked > 100
+    assert ws_general.launch_count() > 0
+
+
+def test_auto_path_within_tolerance(torch, mg, g, ws_auto):
+    for shape in shapes_in(g):
+        h = mg.GridHierarchy.create(shape)
+        L = h.num_levels()
+        for name, tol in (("f64", 1e-12), ("f32", 1e-5)):
+            xin = g[key(shape, name, "in")]
+            rng_ = float(xin.max() - xin.min()) or 1.0
+            x = to_dev(torch, xin)
+            for stop in sorted({0, min(1, L), L}):
+                got = mg.decompose(x, h, stop, ws_auto).buffer.cpu().numpy().astype(np.float64)
+                want = g[key(shape, name, "dec", stop)].astype(np.float64)
+                assert np.max(np.abs(got - want)) <= tol * rng_, (shape, name, stop)
+                back = mg.recompose(mg.MultilevelCoefficients(to_dev(torch, g[key(shape, name, "dec", stop)]), h, stop),
+                                    ws_auto).cpu().numpy().astype(np.float64)
+                wr = g[key(shape, name, "rec", stop)].astype(np.float64)
+                assert np.max(np.abs(back - wr)) <= tol * rng_, (shape, name, stop)
+
+
+def test_quantize_dequantize_bitwise(torch, mg, g, ws_auto):
+    for shape in shapes_in(g):
+        h = mg.GridHierarchy.create(shape)
+        L = h.num_levels()
+        for name in ("f64", "f32"):
+            plan = mg.make_plan(mg.QuantMode.levelwise, 1e-3 * 200.0, h)
+            assert bits(plan.bin_widths) == bits(g[key(shape, name, "q")])
+            c0 = to_dev(torch, g[key(shape, name, "dec", 0)])
+            s = mg.quantize(mg.MultilevelCoefficients(c0, h, 0), plan, ws_auto)
+            assert bits(s.flat.cpu().numpy()) == bits(g[key(shape, name, "labels")]), shape
+            assert bits(s.outlier_positions.cpu().numpy()) == bits(g[key(shape, name, "opos")]), shape
+            assert bits(s.outlier_values.cpu().numpy()) == bits(g[key(shape, name, "oval")]), shape
+            back = mg.dequantize(s, plan, h, ws_auto)
+            assert bits(back.buffer.cpu().numpy()) == bits(g[key(shape, name, "deq")]), shape
+            if L >= 2:
+                t = mg.quantize_tail(c0, h, 1, plan, ws_auto)
+                assert bits(t.flat.cpu().numpy()) == bits(g[key(shape, name, "qtail_labels")])
+                assert bits(t.outlier_positions.cpu().numpy()) == bits(g[key(shape, name, "qtail_opos")])
+                buf = c0.clone()
+                buf[h.node_count(1):] = 0
+                mg.dequantize_tail(buf, t, h, 1, plan, ws_auto)
+                full = mg.dequantize(s, plan, h, ws_auto).buffer
+                assert torch.equal(buf, full)
+
+
+def test_quantize_errors(torch, mg, ws_auto):
+    h = mg.GridHierarchy.create((5,))
+    plan = mg.make_plan(mg.QuantMode.uniform, 0.1, h)
+    c = torch.tensor([0.0, float("nan"), 0.0, 0.0, 0.0], dtype=torch.float64, device="cuda")
+    with pytest.raises(mg.Error) as e:
+        mg.quantize(mg.MultilevelCoefficients(c, h, 0), plan, ws_auto)
+    assert e.value.code == "nonfinite_data"
+    with pytest.raises(mg.Error) as e:
+        mg.quantize(mg.MultilevelCoefficients(c, h, 1), plan, ws_auto)
+    assert e.value.code == "invalid_input"
+    # worked example (test_quantize.cpp:81-93) and overflow outlier (:124-134)
+    plan = mg.make_plan(mg.QuantMode.uniform, 0.3, h)
+    s = mg.quantize(mg.MultilevelCoefficients(torch.tensor([0.0, 0.29, 0, 0, 0], dtype=torch.float64,
+                                                           device="cuda"), h, 0), plan, ws_auto)
+    assert s.flat.cpu().tolist()[:2] == [0, 1]
+    plan = mg.make_plan(mg.QuantMode.uniform, 1e-6, h)
+    s = mg.quantize(mg.MultilevelCoefficients(torch.tensor([5.0, 0, 0, 0, 1e-7], dtype=torch.float64,
+                                                           device="cuda"), h, 0), plan, ws_auto)
+    assert s.outliers == [(0, 5.0)]
+    assert mg.dequantize(s, plan, h, ws_auto).buffer[0].item() == 5.0
+
+
+def test_transform_errors(torch, mg, ws_auto):
+    h = mg.GridHierarchy.create((9, 9))
+    x = torch.zeros((9, 8), dtype=torch.float64, device="cuda")
+    with pytest.raises(mg.Error) as e:
+        mg.decompose(x, h, 0, ws_auto)
+    assert e.value.code == "shape_error"
+    x = torch.zeros((9, 9), dtype=torch.float64, device="cuda")
+    with pytest.raises(mg.Error) as e:
+        mg.decompose(x, h, 5, ws_auto)
+    assert e.value.code == "invalid_level"
+    with pytest.raises(mg.Error) as e:
+        mg.decompose(x.cpu(), h, 0, ws_auto)
+    assert e.value.code == "invalid_argument"
+
+
+def test_level_step_intermediates_general(torch, mg, g, ws_general):
+    """One decompose level: shell equals the reference's reordered coefficient
+    values; the coarse block equals nodal + correction (level_step fixtures)."""
+    from oracle.oracle import Oracle
+
+    for shape in [(9, 9), (17, 9, 5), (6, 5, 3), (7, 4), (9,)]:
+        x = g[key(shape, "step_in")]
+        h = mg.GridHierarchy.create(shape)
+        L = h.num_levels()
+        mc = mg.decompose(to_dev(torch, x), h, L - 1, ws_general).buffer.cpu().numpy()
+        ref_field = g[key(shape, "step_field")]
+        corr = g[key(shape, "step_corr")]
+        # coarse block = nodal values (natural order = reordered corner) + corr
+        coarse_dims = h.level_dims(L - 1)
+        sl = tuple(slice(0, m) for m in coarse_dims)
+        want_coarse = (ref_field[sl].astype(np.float64) + corr).ravel()
+        assert bits(mc[: h.node_count(L - 1)]) == bits(want_coarse)
+        # oracle agrees too
+        assert bits(Oracle().decompose(x, L - 1)) == bits(mc)
+
+
+def test_config1_against_reference(torch, mg):
+    """BASELINE config 1 (129^3 f64, 16 bumps + noise), full decomposition,
+    recomposition and level-wise quantization at 1e-3 relative (budget = tau/2)."""
+    from oracle.oracle import Oracle, Reference, reference_available
+    from paper_2010_05872_b200.fields import config1_field
+
+    ref = Reference() if reference_available() else Oracle()
+    f = config1_field(device="cuda")
+    fh = f.cpu().numpy()
+    h = mg.GridHierarchy.create(f.shape)
+    ws = mg.SolverWorkspace()
+    mc = mg.decompose(f, h, 0, ws)
+    want = ref.decompose(fh)
+    rng_ = float(fh.max() - fh.min())
+    assert np.max(np.abs(mc.buffer.cpu().numpy() - want)) <= 1e-12 * rng_
+    back = mg.recompose(mc, ws).cpu().numpy()
+    assert np.max(np.abs(back - fh)) <= 1e-9 * rng_
+    tau = 1e-3 * rng_
+    plan = mg.make_plan(mg.QuantMode.levelwise, tau / 2.0, h)
+    s = mg.quantize(mc, plan, ws)
+    lab_ref, opos_ref, _ = ref.quantize(want, f.shape, plan.bin_widths)
+    diff = np.nonzero(s.flat.cpu().numpy() != lab_ref)[0]
+    # any flip must be a value within 1 ulp of a bin edge
+    v = want[diff]
+    pos_level = np.searchsorted(np.cumsum(h.delta_counts()), diff, side="right")
+    q = plan.bin_widths[pos_level]
+    frac = np.abs(np.abs(v / q) - np.floor(np.abs(v / q)) - 0.5)
+    assert np.all(frac * q <= np.spacing(np.abs(v)) * 2), diff
+    rec = mg.recompose(mg.dequantize(s, plan, h, ws), ws).cpu().numpy()
+    assert np.max(np.abs(rec - fh)) <= tau
