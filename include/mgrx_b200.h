@@ -71,8 +71,10 @@ int mgrx_abi_version(void);
  * SolverWorkspace ws(batch); ws.prepare(h) (transform.hpp:50,58). */
 int mgrx_gpu_ctx_create(int device, mgrx_gpu_ctx** out);
 int mgrx_gpu_ctx_destroy(mgrx_gpu_ctx* ctx);
-/* Run subsequent work on an external stream (cudaStream_t as void*); NULL
- * restores the context's own stream. */
+/* Run subsequent work on an external stream (cudaStream_t as void*), used
+ * as-is: NULL is the legacy default stream (what torch's default stream is).
+ * mgrx_gpu_get_stream right after creation returns the context's own stream,
+ * which can be passed back here to restore it. */
 int mgrx_gpu_set_stream(mgrx_gpu_ctx* ctx, void* stream);
 void* mgrx_gpu_get_stream(mgrx_gpu_ctx* ctx);
 int mgrx_gpu_synchronize(mgrx_gpu_ctx* ctx);

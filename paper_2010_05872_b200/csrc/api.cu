@@ -586,7 +586,7 @@ int mgrx_gpu_ctx_destroy(mgrx_gpu_ctx* c) {
 }
 
 int mgrx_gpu_set_stream(mgrx_gpu_ctx* c, void* stream) {
-  return guarded(c, [&] { c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own; });
+  return guarded(c, [&] { c->stream = static_cast<cudaStream_t>(stream); });
 }
 
 void* mgrx_gpu_get_stream(mgrx_gpu_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }

@@ -9,13 +9,23 @@
 
 namespace mgrx_b200 {
 
+// Geometry and work decomposition of one fused level pass.
+struct F3Geom {
+  int64_t n0 = 0, n1 = 0, n2 = 0;  // fine extents (level l)
+  int64_t m0 = 0, m1 = 0, m2 = 0;  // coarse extents (level l-1)
+  int64_t chunk = 0;               // coarse planes (axis 0) per work unit
+  int tile_rows = 0;               // coarse rows (axis 1) per work unit
+  int ntile1 = 0;                  // tiles along axis 1
+  int units = 0;                   // work units = chunks * ntile1
+  int threads = 0;                 // plane-pass CTA size (one thread per coarse column)
+  int grid = 0;                    // persistent plane-pass CTAs
+};
+
 struct Fused3DPlan {
   bool enabled = false;
-  size_t scratch_bytes = 0;  // fp64 load-vector volume + nodal staging
+  size_t scratch_bytes = 0;  // fp64 load-vector volume G + work counter
   size_t scratch_off = 0;    // filled by the caller's scratch layout
-  int tile_rows = 0;         // coarse rows per plane-pass CTA (axis 1)
-  int chunk_planes = 0;      // coarse planes per plane-pass CTA (axis 0)
-  int grid_plane = 0;        // plane-pass CTAs
+  F3Geom g;
 };
 
 Fused3DPlan fused3d_plan(const LevelGeom& g, int esize);

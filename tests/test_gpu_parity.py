@@ -217,3 +217,36 @@ def test_config1_against_reference(torch, mg):
     assert np.all(frac * q <= np.spacing(np.abs(v)) * 2), diff
     rec = mg.recompose(mg.dequantize(s, plan, h, ws), ws).cpu().numpy()
     assert np.max(np.abs(rec - fh)) <= tau
+
+
+FUSED_SHAPES = [(33, 33, 33), (65, 65, 65), (40, 36, 66), (35, 34, 100), (129, 65, 33), (6, 7, 300), (17, 100, 64),
+                (66, 66, 66), (5, 200, 34)]
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_fused_path_against_oracle(torch, mg, ws_auto, dtype):
+    """Shapes that take the fused 3-D kernels (alone or mixed with general
+    levels), with odd/even extents, partial tiles and partial chunks."""
+    from oracle.oracle import Oracle
+
+    o = Oracle()
+    rng = np.random.default_rng(5)
+    npdt = np.float64 if dtype == "f64" else np.float32
+    tol = 1e-12 if dtype == "f64" else 1e-5
+    for shape in FUSED_SHAPES:
+        x = rng.uniform(-10, 10, shape).astype(npdt)
+        rg = float(x.max() - x.min())
+        h = mg.GridHierarchy.create(shape)
+        L = h.num_levels()
+        for stop in sorted({0, L - 1}):
+            want = o.decompose(x, stop)
+            mc = mg.decompose(to_dev(torch, x), h, stop, ws_auto)
+            got = mc.buffer.cpu().numpy()
+            err = float(np.max(np.abs(got.astype(np.float64) - want)))
+            assert err <= tol * rg, (shape, dtype, stop, err / rg)
+            back = mg.recompose(mg.MultilevelCoefficients(to_dev(torch, want), h, stop), ws_auto).cpu().numpy()
+            wr = o.recompose(want, shape, stop)
+            err = float(np.max(np.abs(back.astype(np.float64) - wr)))
+            assert err <= tol * rg, (shape, dtype, stop, "rec", err / rg)
+            rt = mg.recompose(mc, ws_auto).cpu().numpy()
+            assert float(np.max(np.abs(rt.astype(np.float64) - x))) <= (1e-9 if dtype == "f64" else 1e-4) * rg
