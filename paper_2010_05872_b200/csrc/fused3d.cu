@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "fused3d.h"
 
@@ -42,12 +43,11 @@ namespace mgrx_b200 {
 
 namespace {
 
-constexpr int kF3MaxThreads = 640;  // plane passes: one thread per coarse column (m2 <= 640)
+constexpr int kPlaneMaxThreads = 576;  // plane passes: up to 18 strips of 30 coarse columns (112-register budget)
 constexpr int kColMaxM = 640;       // column passes: register-resident columns up to this length
-// column-pass block: 32 columns x ceil(m / LS) segments of LS registers;
-// LS = 16 for m <= 320 and LS = 32 for m <= 640, so at most 20 segments
-template <int LS>
-constexpr int kColMaxThreads = 640;
+// column-pass block: 16 columns x S segments of up to LS registers, two
+// segments per warp row; LS = 16 for m <= 320, 32 for m <= 640
+constexpr int kColThreads = 16 * 20;
 
 // ------------------------------------------------------------ PTX helpers
 
@@ -113,66 +113,108 @@ __device__ __forceinline__ void bulk_span(const T* base, int64_t start, int64_t 
   *lead = int((a - a0) / sizeof(T));
 }
 
-// ---------------------------------------------- warp-parallel Thomas (row)
-// Solves M z = f in place for one row x[0..m) held in shared memory with the
-// reference's factors (ThomasAux, transform.hpp:25-44): lane segments run the
-// forward / backward recurrences locally, an affine scan across lanes joins
-// them (exact algebra; rounding differs from the sequential sweep).
-__device__ void warp_thomas_row(double* x, int m, const double* __restrict__ w, const double* __restrict__ inv_d) {
-  const int lane = threadIdx.x & 31;
-  const int seg = (m + 31) >> 5;
-  const int s0 = min(m, lane * seg), s1 = min(m, s0 + seg);
-  // forward: y_i = x_i - w_i y_{i-1}
-  double yl = 0.0, mu = 1.0;
-  for (int i = s0; i < s1; ++i) {
-    const double wi = w[i];
-    yl = x[i] - wi * yl;
-    mu = -wi * mu;
-    x[i] = yl;
-  }
-  double A = (s1 > s0) ? yl : 0.0, B = (s1 > s0) ? mu : 1.0;  // y_end = A + B * y_in
+// ------------------------------------------------- block-parallel Thomas
+// Solves M z = f (ThomasAux factors, transform.hpp:25-44; batched_solve
+// :116-130) in place for `rows` rows of length m held in shared memory,
+// using every warp of the CTA: each row is cut into parts (one per warp) and
+// each part into lane segments.  A segment first runs the recurrence from a
+// zero carry to obtain its affine map y_end = A + B y_in; maps are combined
+// with a warp shuffle scan and a fold over the parts of the row, and the
+// segment then reruns the exact recurrence from its true carry.  Exact
+// algebra; rounding differs from the sequential sweep only in the carries.
+struct Aff {
+  double a, b;
+};
+
+__device__ __forceinline__ Aff aff_then(Aff first, Aff second) {  // apply first, then second
+  return Aff{second.a + second.b * first.a, second.b * first.b};
+}
+
+__device__ void block_thomas_rows_pass(double* x, int row0, int rows, int m, int ld, const double* __restrict__ w,
+                                       const double* __restrict__ inv_d, double* scan);
+
+__device__ void block_thomas_rows(double* x, int rows, int m, int ld, const double* __restrict__ w,
+                                  const double* __restrict__ inv_d, double* scan /* [2][32] */) {
+  // one pass when every row gets at least one warp, else one row per warp per pass
+  const int nwarps = blockDim.x >> 5;
+  const int step = rows <= nwarps ? rows : nwarps;
+  for (int r0 = 0; r0 < rows; r0 += step) block_thomas_rows_pass(x, r0, min(step, rows - r0), m, ld, w, inv_d, scan);
+}
+
+__device__ void block_thomas_rows_pass(double* x, int row0, int rows, int m, int ld, const double* __restrict__ w,
+                                       const double* __restrict__ inv_d, double* scan) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int parts = max(1, nwarps / max(rows, 1));
+  const int row = warp / parts, q = warp - row * parts;
+  const bool live = row < rows;
+  x += size_t(row0) * ld;
+  const int P = (m + parts - 1) / parts;
+  const int p0 = min(m, q * P), p1 = min(m, p0 + P);
+  const int seg = (p1 - p0 + 31) >> 5;
+  const int s0 = min(p1, p0 + lane * seg), s1 = min(p1, s0 + seg);
+  double* xr = x + size_t(live ? row : 0) * ld;
+  double* sA = scan;
+  double* sB = scan + 32;
+  // ---- forward: y_i = x_i - w_i y_{i-1}
+  Aff f{0.0, 1.0};
+  if (live)
+    for (int i = s0; i < s1; ++i) {
+      const double wi = w[i];
+      f.a = xr[i] - wi * f.a;
+      f.b = -wi * f.b;
+    }
+  Aff inc = f;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
-    const double a2 = __shfl_up_sync(0xffffffffu, A, off);
-    const double b2 = __shfl_up_sync(0xffffffffu, B, off);
-    if (lane >= off) {
-      A = A + B * a2;
-      B = B * b2;
+    const Aff o{__shfl_up_sync(0xffffffffu, inc.a, off), __shfl_up_sync(0xffffffffu, inc.b, off)};
+    if (lane >= off) inc = aff_then(o, inc);
+  }
+  Aff exc{__shfl_up_sync(0xffffffffu, inc.a, 1), __shfl_up_sync(0xffffffffu, inc.b, 1)};
+  if (lane == 0) exc = Aff{0.0, 1.0};
+  if (lane == 31 && warp < 32) {
+    sA[warp] = inc.a;
+    sB[warp] = inc.b;
+  }
+  __syncthreads();
+  double carry = 0.0;  // y before this part
+  for (int k = 0; k < q; ++k) carry = sA[row * parts + k] + sB[row * parts + k] * carry;
+  double y = exc.a + exc.b * carry;
+  if (live)
+    for (int i = s0; i < s1; ++i) {
+      y = xr[i] - w[i] * y;
+      xr[i] = y;
     }
-  }
-  double cin = __shfl_up_sync(0xffffffffu, A, 1);
-  if (lane == 0) cin = 0.0;
-  mu = 1.0;
-  for (int i = s0; i < s1; ++i) {
-    mu = -w[i] * mu;
-    x[i] = x[i] + mu * cin;
-  }
-  // backward: z_i = (y_i - kOff z_{i+1}) inv_d_i, z_m = 0
-  double xl = 0.0, nu = 1.0;
-  for (int i = s1 - 1; i >= s0; --i) {
-    const double id = inv_d[i];
-    xl = (x[i] - kOff * xl) * id;
-    nu = -kOff * id * nu;
-    x[i] = xl;
-  }
-  A = (s1 > s0) ? xl : 0.0;
-  B = (s1 > s0) ? nu : 1.0;  // z_start = A + B * z_in(right)
+  __syncthreads();
+  // ---- backward: z_i = (y_i - z_{i+1}/3) / d_i, z_m = 0
+  Aff g{0.0, 1.0};  // z_start = a + b z_in
+  if (live)
+    for (int i = s1 - 1; i >= s0; --i) {
+      const double id = inv_d[i];
+      g.a = (xr[i] - kOff * g.a) * id;
+      g.b = -kOff * id * g.b;
+    }
+  Aff rin = g;  // composite of this lane and the lanes to its right
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
-    const double a2 = __shfl_down_sync(0xffffffffu, A, off);
-    const double b2 = __shfl_down_sync(0xffffffffu, B, off);
-    if (lane + off < 32) {
-      A = A + B * a2;
-      B = B * b2;
+    const Aff o{__shfl_down_sync(0xffffffffu, rin.a, off), __shfl_down_sync(0xffffffffu, rin.b, off)};
+    if (lane + off < 32) rin = aff_then(o, rin);
+  }
+  Aff rexc{__shfl_down_sync(0xffffffffu, rin.a, 1), __shfl_down_sync(0xffffffffu, rin.b, 1)};
+  if (lane == 31) rexc = Aff{0.0, 1.0};
+  if (lane == 0 && warp < 32) {
+    sA[warp] = rin.a;
+    sB[warp] = rin.b;
+  }
+  __syncthreads();
+  double rc = 0.0;  // z after this part
+  for (int k = parts - 1; k > q; --k) rc = sA[row * parts + k] + sB[row * parts + k] * rc;
+  double z = rexc.a + rexc.b * rc;
+  if (live)
+    for (int i = s1 - 1; i >= s0; --i) {
+      z = (xr[i] - kOff * z) * inv_d[i];
+      xr[i] = z;
     }
-  }
-  double cr = __shfl_down_sync(0xffffffffu, A, 1);
-  if (lane == 31) cr = 0.0;
-  nu = 1.0;
-  for (int i = s1 - 1; i >= s0; --i) {
-    nu = -kOff * inv_d[i] * nu;
-    x[i] = x[i] + nu * cr;
-  }
+  __syncthreads();
 }
 
 // Shell offset of reordered row (r0, r1) of a 3-D level block
@@ -205,188 +247,129 @@ __device__ __forceinline__ UnitRange unit_range(const F3Geom& g, int u) {
 }
 
 // --------------------------------------------------------- plane kernels
-// Shared-memory layout shared by the decompose and recompose plane passes.
+// Thread layout of the plane and interpolation passes: warp w owns coarse
+// columns c = 30 w .. 30 w + 29 on lanes 1..30; lanes 0 and 31 are halo
+// lanes that recompute the neighbouring columns so every cross-column
+// value (the odd node's right corners, the axis-2 restriction stencil) moves
+// through warp shuffles.  A thread walks all rows of its tile for its column
+// keeping the fp64 nodal values and the axis-1 restriction in registers.
+struct StripLane {
+  int lane, c;
+  bool valid, owned;
+};
+
+__device__ __forceinline__ StripLane strip_lane(int m2) {
+  StripLane s;
+  s.lane = threadIdx.x & 31;
+  s.c = 30 * int(threadIdx.x >> 5) - 1 + s.lane;
+  s.valid = s.c >= 0 && s.c < m2;
+  s.owned = s.valid && s.lane >= 1 && s.lane <= 30;
+  return s;
+}
+
 template <typename T, int TI1>
 struct PlaneSmem {
   static constexpr int kRows = 2 * TI1 + 3;
   static __host__ __device__ size_t raw_bytes(int64_t n2) {
     return (size_t(kRows) * size_t(n2) * sizeof(T) + 256 + 127) / 128 * 128;
   }
-  static __host__ __device__ size_t nsd_elems(int64_t m2) { return size_t(TI1 + 2) * size_t(m2); }
   static __host__ __device__ size_t acc_elems(int64_t m2) { return size_t(TI1) * size_t(m2); }
-  static __host__ __device__ size_t bytes(int64_t n2, int64_t m2, bool dec) {
-    size_t b = 3 * raw_bytes(n2);
-    if (dec) b += 2 * nsd_elems(m2) * 8;
-    b += 3 * acc_elems(m2) * 8;
-    b += 2 * size_t(n2 + 8) * 8;  // crow double buffer
-    b += 2 * size_t(m2) * 8;      // Thomas tables axis 2
-    b += 64;                      // mbarriers + unit slot
+  static __host__ __device__ size_t bytes(int64_t n2, int64_t m2) {
+    size_t b = 3 * raw_bytes(n2);   // TMA ring of fine plane tiles
+    b += 3 * acc_elems(m2) * 8;     // coarse-plane accumulators (L0)
+    b += 2 * size_t(m2) * 8;        // Thomas tables axis 2
+    b += 64 * 8 + 2 * kRows * 8 + 64;  // scan scratch, row offsets, barriers
     return b;
   }
 };
 
-// Component value of fine node (p, j1, j2) in decompose (coefficient of the
-// reordered level block, transform.hpp:216-304, or 0 on a nodal point).
-// Corners come from the fp64 nodal planes `nsA` (plane p-1 or p) and `nsB`
-// (plane p+1); rows of ns* are the even fine rows from rlo, columns the
-// coarse i2.  Returns the T-rounded coefficient (as double) and sets *nodal.
-template <typename T>
-__device__ __forceinline__ double dec_coef(const F3Geom& g, bool p_odd, bool p_has_right, const double* nsP,
-                                           const double* nsN, int64_t m2s, int64_t j1, int64_t rlo, int64_t j2,
-                                           double raw, bool* nodal) {
-  const bool o1 = j1 & 1, o2 = j2 & 1;
-  *nodal = !(p_odd || o1 || o2);
-  if (*nodal) return 0.0;
-  // corner index pieces
-  const int64_t rl = ((o1 ? j1 - 1 : j1) - rlo) >> 1;            // left/own even row
-  const int64_t rr = o1 ? ((j1 + 1 < g.n1) ? rl + 1 : rl) : rl;   // right even row
-  const int64_t cl = o2 ? (j2 - 1) >> 1 : j2 >> 1;                // left/own coarse column
-  const int64_t cr = o2 ? ((j2 + 1 < g.n2) ? cl + 1 : cl) : cl;   // right coarse column
-  const double* pl = nsP;                                         // left plane (or own)
-  const double* pr = p_odd ? (p_has_right ? nsN : nsP) : nsP;     // right plane
-  double sum;
-  // set axes ascending (0,1,2); cmask bit b <-> b-th set axis; cmask ascending
-  if (p_odd) {
-    if (o1) {
-      if (o2) {  // k = 3
-        sum = pl[rl * m2s + cl];
-        sum += pr[rl * m2s + cl];
-        sum += pl[rr * m2s + cl];
-        sum += pr[rr * m2s + cl];
-        sum += pl[rl * m2s + cr];
-        sum += pr[rl * m2s + cr];
-        sum += pl[rr * m2s + cr];
-        sum += pr[rr * m2s + cr];
-        sum *= 0.125;
-      } else {  // axes 0,1
-        sum = pl[rl * m2s + cl];
-        sum += pr[rl * m2s + cl];
-        sum += pl[rr * m2s + cl];
-        sum += pr[rr * m2s + cl];
-        sum *= 0.25;
-      }
-    } else if (o2) {  // axes 0,2
-      sum = pl[rl * m2s + cl];
-      sum += pr[rl * m2s + cl];
-      sum += pl[rl * m2s + cr];
-      sum += pr[rl * m2s + cr];
-      sum *= 0.25;
-    } else {  // axis 0
-      sum = pl[rl * m2s + cl];
-      sum += pr[rl * m2s + cl];
-      sum *= 0.5;
-    }
-  } else {
-    if (o1) {
-      if (o2) {  // axes 1,2
-        sum = pl[rl * m2s + cl];
-        sum += pl[rr * m2s + cl];
-        sum += pl[rl * m2s + cr];
-        sum += pl[rr * m2s + cr];
-        sum *= 0.25;
-      } else {  // axis 1
-        sum = pl[rl * m2s + cl];
-        sum += pl[rr * m2s + cl];
-        sum *= 0.5;
-      }
-    } else {  // axis 2
-      sum = pl[rl * m2s + cl];
-      sum += pl[rl * m2s + cr];
-      sum *= 0.5;
-    }
-  }
-  return double(to_t<T>(raw - sum));
+// Axis-2 load-vector restriction at column c from the pair values of this
+// lane and its neighbours: H(c) = w(c) e(c) + o(c)/2 + [e(c-1)/12 + o(c-1)/2]
+// + e(c+1)/12 (load_entry, transform.hpp:84-96; missing nodes carry 0).
+__device__ __forceinline__ double strip_restrict(double cE, double cO, int c, int m2) {
+  const double x = kW12 * cE + 0.5 * cO;  // this column's share of H(c+1)
+  const double xl = __shfl_up_sync(0xffffffffu, x, 1);
+  const double er = __shfl_down_sync(0xffffffffu, cE, 1);
+  const double wc = (c == 0 || c + 1 == m2) ? kW5_12 : kW5_6;
+  return wc * cE + 0.5 * cO + xl + kW12 * er;
 }
 
-// One fine row's contribution: L2 restriction of the component row in
-// crow[0..n2) at coarse column i2 (load_entry along axis 2).
-__device__ __forceinline__ double restrict_row(const double* crow, int64_t i2, const F3Geom& g) {
-  const int64_t c = 2 * i2;
-  double acc = 0.0;
-  if (i2 >= 1) {
-    acc += kW12 * crow[c - 2];
-    acc += 0.5 * crow[c - 1];
-  }
-  acc += ((i2 == 0 || i2 + 1 == g.m2) ? kW5_12 : kW5_6) * crow[c];
-  if (c + 1 < g.n2) acc += 0.5 * crow[c + 1];
-  if (c + 2 < g.n2) acc += kW12 * crow[c + 2];
-  return acc;
-}
-
-// Adds the plane's restricted rows Q[] into the coarse-plane accumulators
-// (L0 along axis 0, terms in stencil order) and finishes coarse planes:
-// Thomas along axis 2 per row, store to G.
+// L0 accumulation of the plane's restricted rows into the coarse planes
+// i0 with |p - 2 i0| <= 2 (first term initialises), then completion of
+// finished coarse planes: Thomas along axis 2 with all warps, rows to G.
 template <int TI1>
-__device__ __forceinline__ void plane_epilogue(const F3Geom& g, const UnitRange& ur, int64_t p, const double* Q,
-                                               double* acc, const double* tw2, const double* tid2, double* G,
-                                               int64_t i2, bool active) {
-  const int64_t TR = ur.b1 - ur.b0;
-  const size_t accsz = size_t(TI1) * size_t(g.m2);
-  // target coarse planes i0 with |p - 2 i0| <= 2, i0 in [a0, a1)
-  const int64_t ilo = max(ur.a0, (p - 1) >> 1), ihi = min(ur.a1 - 1, (p + 2) >> 1);
-  if (active) {
-    for (int64_t i0 = ilo; i0 <= ihi; ++i0) {
-      const int k = int(p - 2 * i0);
+__device__ __forceinline__ void plane_finish(const F3Geom& g, const UnitRange& ur, const StripLane& S, int64_t p,
+                                             const double* Q, double* acc, const double* tw2, const double* tid2,
+                                             double* scan, double* __restrict__ G) {
+  const int m2 = int(g.m2), c = S.c;
+  const int TR = int(ur.b1 - ur.b0);
+  const int accsz = TI1 * m2;
+  const int pp = int(p), m0 = int(g.m0);
+  const int ilo = int(max(ur.a0, (p - 1) >> 1)), ihi = int(min(ur.a1 - 1, (p + 2) >> 1));
+  if (S.owned)
+    for (int i0 = ilo; i0 <= ihi; ++i0) {
+      const int k = pp - 2 * i0;
       if (k < -2 || k > 2) continue;
-      const double wt = load_w(k, i0, g.m0);
-      double* a = acc + size_t(i0 % 3) * accsz;
-      const bool first = (p == max(int64_t(0), 2 * i0 - 2));
+      const double w0 = load_w(k, i0, m0);
+      double* a = acc + (i0 % 3) * accsz + c;
+      const bool first = pp == max(0, 2 * i0 - 2);
 #pragma unroll
-      for (int r = 0; r < TI1; ++r)
-        if (r < TR) {
-          double* cell = a + size_t(r) * g.m2 + i2;
-          *cell = first ? wt * Q[r] : *cell + wt * Q[r];
-        }
+      for (int ir = 0; ir < TI1; ++ir)
+        if (ir < TR) a[ir * m2] = first ? w0 * Q[ir] : a[ir * m2] + w0 * Q[ir];
     }
-  }
-  // coarse plane i0 = (p-2)/2 completes at p = 2 i0 + 2, or at the last fine plane
-  int64_t done_lo = -1, done_hi = -2;
+  int64_t lo = -1, hi = -2;
   if (p == g.n0 - 1) {
-    done_lo = max(ur.a0, (p - 2 + 1) >> 1);
-    done_hi = ur.a1 - 1;
+    lo = (p - 1) >> 1;
+    hi = ur.a1 - 1;
   } else if (!(p & 1) && p >= 2) {
-    done_lo = done_hi = (p - 2) >> 1;
+    lo = hi = (p - 2) >> 1;
   }
-  done_lo = max(done_lo, ur.a0);
-  done_hi = min(done_hi, ur.a1 - 1);
-  if (done_lo > done_hi) return;
+  lo = max(lo, ur.a0);
+  hi = min(hi, ur.a1 - 1);
+  if (lo > hi) return;
   __syncthreads();
-  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  for (int64_t i0 = done_lo; i0 <= done_hi; ++i0) {
-    double* a = acc + size_t(i0 % 3) * accsz;
-    for (int r = warp; r < TR; r += nwarps) warp_thomas_row(a + size_t(r) * g.m2, int(g.m2), tw2, tid2);
-  }
-  __syncthreads();
-  for (int64_t i0 = done_lo; i0 <= done_hi; ++i0) {
-    const double* a = acc + size_t(i0 % 3) * accsz;
-    if (active)
-      for (int r = 0; r < TR; ++r) G[((i0 * g.m1) + ur.b0 + r) * g.m2 + i2] = a[size_t(r) * g.m2 + i2];
+  for (int64_t i0 = lo; i0 <= hi; ++i0) {
+    double* a = acc + int(i0 % 3) * accsz;
+    block_thomas_rows(a, TR, m2, m2, tw2, tid2, scan);
+    if (S.owned) {
+      double* gp = G + (i0 * g.m1 + ur.b0) * g.m2 + c;
+      for (int ir = 0; ir < TR; ++ir) gp[int64_t(ir) * m2] = a[ir * m2 + c];
+    }
   }
 }
 
-// Decompose plane pass. One thread per coarse column i2 (its fine pair
-// 2 i2, 2 i2 + 1); persistent CTAs take (axis-0 chunk, axis-1 tile) units.
+// Decompose plane pass: persistent CTAs take (axis-0 chunk, axis-1 tile)
+// units and stream the unit's fine planes through a 3-deep TMA ring.  Per
+// fine row and column pair: coefficients (update_coefficients corner sets;
+// the odd node's sum = own column's sum + right column's sum), shell /
+// coarse writes, axis-2 restriction through shuffles, axis-1 restriction in
+// registers.
 template <typename T, int TI1>
-__global__ void __launch_bounds__(kF3MaxThreads, 1)
+__global__ void __launch_bounds__(kPlaneMaxThreads)
     k_f3_dec_plane(const T* __restrict__ blk, T* __restrict__ shell, T* __restrict__ coarse, double* __restrict__ G,
                    const double* __restrict__ w2g, const double* __restrict__ id2g, int* __restrict__ counter,
                    const F3Geom g) {
   using SM = PlaneSmem<T, TI1>;
+  constexpr int RMAX = SM::kRows;
+  constexpr int NE = TI1 + 2;  // even rows of a tile
   extern __shared__ __align__(128) unsigned char smem[];
+  const int m2 = int(g.m2), n2 = int(g.n2), n1 = int(g.n1), m1 = int(g.m1);
   const size_t rawb = SM::raw_bytes(g.n2);
   unsigned char* raw = smem;
-  double* nsd = reinterpret_cast<double*>(smem + 3 * rawb);
-  double* acc = nsd + 2 * SM::nsd_elems(g.m2);
-  double* crow = acc + 3 * SM::acc_elems(g.m2);
-  double* tw2 = crow + 2 * (g.n2 + 8);
-  double* tid2 = tw2 + g.m2;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(tid2 + g.m2);
+  double* acc = reinterpret_cast<double*>(smem + 3 * rawb);
+  double* tw2 = acc + 3 * SM::acc_elems(g.m2);
+  double* tid2 = tw2 + m2;
+  double* scan = tid2 + m2;
+  int64_t* rowoff = reinterpret_cast<int64_t*>(scan + 64);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rowoff + 2 * RMAX);
   int* unit_slot = reinterpret_cast<int*>(bars + 4);
 
-  const int tid = threadIdx.x;
-  const int64_t i2 = tid;
-  const bool active = i2 < g.m2;
-  for (int64_t i = tid; i < g.m2; i += blockDim.x) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const StripLane S = strip_lane(m2);
+  const int c = S.c;
+  const bool has_odd = S.valid && 2 * c + 1 < n2;
+  const bool right_degen = 2 * c + 2 >= n2;  // odd node's right corner column missing
+  for (int i = tid; i < m2; i += nt) {
     tw2[i] = w2g[i];
     tid2[i] = id2g[i];
   }
@@ -396,7 +379,6 @@ __global__ void __launch_bounds__(kF3MaxThreads, 1)
   }
   __syncthreads();
   uint32_t phase[3] = {0, 0, 0};
-  const int64_t m2s = g.m2;
 
   for (;;) {
     if (tid == 0) *unit_slot = atomicAdd(counter, 1);
@@ -404,113 +386,122 @@ __global__ void __launch_bounds__(kF3MaxThreads, 1)
     const int u = *unit_slot;
     if (u >= g.units) break;
     const UnitRange ur = unit_range(g, u);
-    const int64_t R = ur.rhi - ur.rlo + 1;
-    int lead[3] = {0, 0, 0};
-    // issue one plane into ring slot (p % 3)
+    const int R = int(ur.rhi - ur.rlo + 1), rlo = int(ur.rlo), rhi = int(ur.rhi);
+    const int jbase = int(2 * ur.b0) - 2;  // fine row of tile slot jr = 0
+    const int TR = int(ur.b1 - ur.b0), b0 = int(ur.b0);
+    const int jlo_own = int(2 * ur.b0), jhi_own = int(min(2 * ur.b1, g.n1));
+    auto tile_src = [&](int64_t p) { return blk + (p * g.n1 + ur.rlo) * g.n2; };
     auto issue = [&](int64_t p) {
       if (tid == 0) {
         const char* src;
         uint32_t bytes;
         int ld;
-        bulk_span<T>(blk, (p * g.n1 + ur.rlo) * g.n2, R * g.n2, &src, &bytes, &ld);
-        uint64_t* bar = &bars[p % 3];
+        bulk_span<T>(tile_src(p), 0, int64_t(R) * n2, &src, &bytes, &ld);
         fence_proxy_async();
-        mbar_expect_tx(bar, bytes);
-        bulk_g2s(raw + size_t(p % 3) * rawb, src, bytes, bar);
+        mbar_expect_tx(&bars[p % 3], bytes);
+        bulk_g2s(raw + size_t(p % 3) * rawb, src, bytes, &bars[p % 3]);
       }
     };
-    auto lead_of = [&](int64_t p) {
-      const uintptr_t a = reinterpret_cast<uintptr_t>(blk + (p * g.n1 + ur.rlo) * g.n2);
-      return int((a & 15) / sizeof(T));
+    auto tile = [&](int64_t p) {
+      return reinterpret_cast<const T*>(raw + size_t(p % 3) * rawb) +
+             (reinterpret_cast<uintptr_t>(tile_src(p)) & 15) / sizeof(T);
+    };
+    double NSP[NE], NSN[NE];  // fp64 nodal values (own column) of the left / right even plane
+    auto load_ns = [&](int64_t q, double* ns) {
+      const T* rq = tile(q);
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        const int j1 = jbase + 2 * e;
+        ns[e] = (S.valid && j1 >= rlo && j1 <= rhi) ? double(rq[(j1 - rlo) * n2 + 2 * c]) : 0.0;
+      }
     };
     issue(ur.plo);
     if (ur.plo + 1 <= ur.phi) issue(ur.plo + 1);
-    for (int b = 0; b < 3; ++b) lead[b] = 0;
-
-    int64_t ready = ur.plo - 1;  // planes waited for so far (in order)
+    int64_t ready = ur.plo - 1;
     for (int64_t p = ur.plo; p <= ur.phi; ++p) {
       const bool p_odd = p & 1;
       const bool has_right = p_odd && (p + 1 <= g.n0 - 1);
-      // wait for plane p (and p + 1 when p is odd)
       const int64_t need = has_right ? p + 1 : p;
       while (ready < need) {
         ++ready;
         mbar_wait(&bars[ready % 3], phase[ready % 3]);
         phase[ready % 3] ^= 1;
       }
-      const T* rp = reinterpret_cast<const T*>(raw + size_t(p % 3) * rawb) + lead_of(p);
-      // nodal fp64 copies of even planes: slot (plane/2) % 2
-      auto extract = [&](int64_t q) {
-        const T* rq = reinterpret_cast<const T*>(raw + size_t(q % 3) * rawb) + lead_of(q);
-        double* ns = nsd + size_t((q >> 1) & 1) * SM::nsd_elems(g.m2);
-        if (active)
-          for (int64_t j1 = ur.rlo; j1 <= ur.rhi; j1 += 2) ns[((j1 - ur.rlo) >> 1) * m2s + i2] =
-              double(rq[(j1 - ur.rlo) * g.n2 + 2 * i2]);
-      };
-      if (p == ur.plo) extract(p);  // first plane of the unit is even
-      if (has_right) extract(p + 1);
-      __syncthreads();
-      // the slot of plane p-1 (odd) / p-2 is free: prefetch p + 2
-      if (p + 2 <= ur.phi) issue(p + 2);
-      const double* nsP = nsd + size_t(((p_odd ? p - 1 : p) >> 1) & 1) * SM::nsd_elems(g.m2);
-      const double* nsN = nsd + size_t(((p + 1) >> 1) & 1) * SM::nsd_elems(g.m2);
+      if (p == ur.plo) load_ns(p, NSP);
+      if (has_right) load_ns(p + 1, NSN);
       const bool own_p = p >= 2 * ur.a0 && p < 2 * ur.a1;
       const int64_t r0 = reord(p, g.m0);
-
+      if (tid < R) rowoff[tid] = shell_row_start(g, r0, reord(ur.rlo + tid, g.m1));
+      __syncthreads();
+      if (p + 2 <= ur.phi) issue(p + 2);  // slot of plane p-1 is free
+      const T* rp = tile(p);
+      T* cpl = coarse + ((p >> 1) * g.m1) * g.m2 + c;
       double Q[TI1];
 #pragma unroll
-      for (int r = 0; r < TI1; ++r) Q[r] = 0.0;
-      // fine rows relative to 2 b0 - 2 (compile-time unrolled for static Q indexing)
+      for (int ir = 0; ir < TI1; ++ir) Q[ir] = 0.0;
 #pragma unroll
-      for (int jr = 0; jr < 2 * TI1 + 3; ++jr) {
-        const int64_t j1 = 2 * ur.b0 - 2 + jr;
-        if (j1 < ur.rlo || j1 > ur.rhi) continue;  // uniform across the CTA
-        double* cr = crow + (jr & 1) * (g.n2 + 8);
-        const bool own_row = own_p && j1 >= 2 * ur.b0 && j1 < 2 * ur.b1;
-        if (active) {
-          const T* rr = rp + (j1 - ur.rlo) * g.n2;
-          const int64_t r1 = reord(j1, g.m1);
-          const int64_t rs = own_row ? shell_row_start(g, r0, r1) : 0;
-          const bool inside = r0 < g.m0 && r1 < g.m1;
-          // even node 2 i2
-          {
-            const int64_t j2 = 2 * i2;
-            const T rawv = rr[j2];
-            bool nodal;
-            const double c = dec_coef<T>(g, p_odd, has_right, nsP, nsN, m2s, j1, ur.rlo, j2, double(rawv), &nodal);
-            cr[j2] = c;
-            if (own_row) {
-              if (nodal)
-                coarse[((p >> 1) * g.m1 + (j1 >> 1)) * g.m2 + i2] = rawv;
-              else
-                shell[rs + i2] = to_t<T>(c);
-            }
+      for (int jr = 0; jr < RMAX; ++jr) {
+        const int j1 = jbase + jr;
+        if (j1 < rlo || j1 > rhi) continue;  // uniform
+        constexpr int dummy = 0;
+        (void)dummy;
+        const bool o1 = jr & 1;  // jbase is even
+        const int ea = o1 ? (jr - 1) >> 1 : jr >> 1;
+        const int eb = o1 ? ((j1 + 1 < n1) ? ea + 1 : ea) : ea;
+        const T* rr = rp + (j1 - rlo) * n2 + 2 * c;
+        const double rawE = S.valid ? double(rr[0]) : 0.0;
+        const double rawO = has_odd ? double(rr[1]) : 0.0;
+        // own-column corner sum of the even node (corner order as the reference)
+        const double aL = NSP[o1 ? (jr - 1) >> 1 : jr >> 1];
+        const double bL = o1 ? ((j1 + 1 < n1) ? NSP[(jr + 1) >> 1] : aL) : aL;
+        double se;
+        int ke;
+        if (!p_odd) {
+          se = o1 ? aL + bL : aL;
+          ke = o1 ? 1 : 0;
+        } else {
+          const double aR = has_right ? NSN[o1 ? (jr - 1) >> 1 : jr >> 1] : aL;
+          const double bR = o1 ? (has_right ? ((j1 + 1 < n1) ? NSN[(jr + 1) >> 1] : aR) : bL) : aR;
+          se = aL + aR;
+          if (o1) {
+            se += bL;
+            se += bR;
           }
-          if (2 * i2 + 1 < g.n2) {
-            const int64_t j2 = 2 * i2 + 1;
-            bool nodal;
-            const double c = dec_coef<T>(g, p_odd, has_right, nsP, nsN, m2s, j1, ur.rlo, j2, double(rr[j2]), &nodal);
-            cr[j2] = c;
-            if (own_row) shell[rs + (inside ? 0 : g.m2) + i2] = to_t<T>(c);
-          }
+          ke = o1 ? 2 : 1;
         }
-        __syncthreads();
-        if (active) {
-          const double h = restrict_row(cr, i2, g);
-          // rows 2 i1 + k, k in [-2, 2], of coarse rows i1 in [b0, b1)
+        (void)ea;
+        (void)eb;
+        double sn = __shfl_down_sync(0xffffffffu, se, 1);
+        if (right_degen) sn = se;
+        const double so = se + sn;
+        const double sc_e = ke == 0 ? 0.0 : (ke == 1 ? 0.5 : 0.25);
+        const double sc_o = ke == 0 ? 0.5 : (ke == 1 ? 0.25 : 0.125);
+        const double cE = (ke == 0 || !S.valid) ? 0.0 : double(to_t<T>(rawE - se * sc_e));
+        const double cO = has_odd ? double(to_t<T>(rawO - so * sc_o)) : 0.0;
+        if (S.owned && own_p && j1 >= jlo_own && j1 < jhi_own) {
+          T* srow = shell + rowoff[j1 - rlo];
+          const bool inside = ke == 0;
+          if (inside)
+            cpl[int64_t(j1 >> 1) * g.m2] = rr[0];
+          else
+            srow[c] = to_t<T>(cE);
+          if (has_odd) srow[(inside ? 0 : m2) + c] = to_t<T>(cO);
+        }
+        const double h = strip_restrict(cE, cO, c, m2);
+        // axis-1 restriction: fine row j1 = 2 i1 + k feeds coarse rows i1 = b0 + ir
 #pragma unroll
-          for (int k = -2; k <= 2; ++k) {
-            if (((jr - 2 - k) & 1) != 0) continue;
-            const int ir = (jr - 2 - k) / 2;  // i1 - b0
-            if (ir < 0 || ir >= TI1) continue;
-            const int64_t i1 = ur.b0 + ir;
-            if (i1 >= ur.b1) continue;
-            Q[ir] += load_w(k, i1, g.m1) * h;
-          }
+        for (int k = -2; k <= 2; ++k) {
+          if (((jr - 2 - k) & 1) != 0) continue;
+          const int ir = (jr - 2 - k) / 2;
+          if (ir < 0 || ir >= TI1) continue;
+          if (ir < TR) Q[ir] += load_w(k, b0 + ir, m1) * h;
         }
       }
-      plane_epilogue<TI1>(g, ur, p, Q, acc, tw2, tid2, G, i2, active);
-      // make sure every thread is done with slot p before it is refilled
+      if (p_odd && has_right) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) NSP[e] = NSN[e];  // plane p+1 becomes the left even plane
+      }
+      plane_finish<TI1>(g, ur, S, p, Q, acc, tw2, tid2, scan, G);
       __syncthreads();
     }
   }
@@ -519,26 +510,30 @@ __global__ void __launch_bounds__(kF3MaxThreads, 1)
 // Recompose plane pass: the same load-vector accumulation with the
 // component read from the level's shell (coefficients; 0 on nodal points).
 // Per fine plane the tile's shell rows form two contiguous runs (even fine
-// rows, odd fine rows), fetched with two bulk copies.
+// rows, odd fine rows), fetched with two bulk copies into one ring slot.
 template <typename T, int TI1>
-__global__ void __launch_bounds__(kF3MaxThreads, 1)
+__global__ void __launch_bounds__(kPlaneMaxThreads)
     k_f3_rec_plane(const T* __restrict__ shell, double* __restrict__ G, const double* __restrict__ w2g,
                    const double* __restrict__ id2g, int* __restrict__ counter, const F3Geom g) {
   using SM = PlaneSmem<T, TI1>;
+  constexpr int RMAX = SM::kRows;
   extern __shared__ __align__(128) unsigned char smem[];
+  const int m2 = int(g.m2), n2 = int(g.n2), m1 = int(g.m1);
   const size_t rawb = SM::raw_bytes(g.n2);
   unsigned char* raw = smem;
   double* acc = reinterpret_cast<double*>(smem + 3 * rawb);
-  double* crow = acc + 3 * SM::acc_elems(g.m2);
-  double* tw2 = crow + 2 * (g.n2 + 8);
-  double* tid2 = tw2 + g.m2;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(tid2 + g.m2);
+  double* tw2 = acc + 3 * SM::acc_elems(g.m2);
+  double* tid2 = tw2 + m2;
+  double* scan = tid2 + m2;
+  int64_t* rowoff = reinterpret_cast<int64_t*>(scan + 64);  // element offset of each tile row in the slot
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rowoff + 2 * RMAX);
   int* unit_slot = reinterpret_cast<int*>(bars + 4);
 
-  const int tid = threadIdx.x;
-  const int64_t i2 = tid;
-  const bool active = i2 < g.m2;
-  for (int64_t i = tid; i < g.m2; i += blockDim.x) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const StripLane S = strip_lane(m2);
+  const int c = S.c;
+  const bool has_odd = S.valid && 2 * c + 1 < n2;
+  for (int i = tid; i < m2; i += nt) {
     tw2[i] = w2g[i];
     tid2[i] = id2g[i];
   }
@@ -555,173 +550,235 @@ __global__ void __launch_bounds__(kF3MaxThreads, 1)
     const int u = *unit_slot;
     if (u >= g.units) break;
     const UnitRange ur = unit_range(g, u);
-    // even fine rows of the tile: r1 in [rlo/2, rhi/2]; odd: r1 in [m1 + rlo/2, m1 + (rhi-1)/2]
+    const int R = int(ur.rhi - ur.rlo + 1), rlo = int(ur.rlo), rhi = int(ur.rhi);
+    const int jbase = int(2 * ur.b0) - 2;
+    const int TR = int(ur.b1 - ur.b0), b0 = int(ur.b0);
     const int64_t e_lo = ur.rlo >> 1, e_hi = ur.rhi >> 1;
-    const int64_t o_lo = (ur.rlo + 1) >> 1, o_hi = (ur.rhi - 1) >> 1;  // (j1 - 1) / 2 range
-    auto runs = [&](int64_t p, int64_t* s_even, int64_t* l_even, int64_t* s_odd, int64_t* l_odd) {
+    const int64_t o_lo = (ur.rlo + 1) >> 1, o_hi = (ur.rhi - 1) >> 1;
+    struct Runs {
+      int64_t se, le, so, lo;
+    };
+    auto runs = [&](int64_t p) {
       const int64_t r0 = reord(p, g.m0);
-      *s_even = shell_row_start(g, r0, e_lo);
-      *l_even = shell_row_start(g, r0, e_hi + 1) - *s_even;
-      if (o_hi >= o_lo) {
-        *s_odd = shell_row_start(g, r0, g.m1 + o_lo);
-        *l_odd = shell_row_start(g, r0, g.m1 + o_hi + 1) - *s_odd;
-      } else {
-        *s_odd = 0;
-        *l_odd = 0;
-      }
+      Runs x;
+      x.se = shell_row_start(g, r0, e_lo);
+      x.le = shell_row_start(g, r0, e_hi + 1) - x.se;
+      x.so = o_hi >= o_lo ? shell_row_start(g, r0, g.m1 + o_lo) : 0;
+      x.lo = o_hi >= o_lo ? shell_row_start(g, r0, g.m1 + o_hi + 1) - x.so : 0;
+      return x;
+    };
+    auto odd_slot_off = [&](const Runs& x) {
+      const uintptr_t a0 = reinterpret_cast<uintptr_t>(shell + x.se) & ~uintptr_t(15);
+      const uintptr_t a1 = (reinterpret_cast<uintptr_t>(shell + x.se + x.le) + 15) & ~uintptr_t(15);
+      return (uint32_t(a1 - a0) + 127u) & ~127u;
     };
     auto issue = [&](int64_t p) {
       if (tid == 0) {
-        int64_t se, le, so, lo;
-        runs(p, &se, &le, &so, &lo);
-        const char *src0, *src1;
-        uint32_t b0, b1 = 0;
-        int ld0, ld1;
-        bulk_span<T>(shell, se, le, &src0, &b0, &ld0);
-        if (lo > 0) bulk_span<T>(shell, so, lo, &src1, &b1, &ld1);
-        uint64_t* bar = &bars[p % 3];
+        const Runs x = runs(p);
+        const char *src0, *src1 = nullptr;
+        uint32_t b0b, b1b = 0;
+        int ld;
+        bulk_span<T>(shell, x.se, x.le, &src0, &b0b, &ld);
+        if (x.lo > 0) bulk_span<T>(shell, x.so, x.lo, &src1, &b1b, &ld);
         unsigned char* dst = raw + size_t(p % 3) * rawb;
         fence_proxy_async();
-        mbar_expect_tx(bar, b0 + b1);
-        bulk_g2s(dst, src0, b0, bar);
-        if (lo > 0) bulk_g2s(dst + ((b0 + 127) & ~127u), src1, b1, bar);
+        mbar_expect_tx(&bars[p % 3], b0b + b1b);
+        bulk_g2s(dst, src0, b0b, &bars[p % 3]);
+        if (x.lo > 0) bulk_g2s(dst + odd_slot_off(x), src1, b1b, &bars[p % 3]);
       }
     };
     issue(ur.plo);
     if (ur.plo + 1 <= ur.phi) issue(ur.plo + 1);
-
     for (int64_t p = ur.plo; p <= ur.phi; ++p) {
       mbar_wait(&bars[p % 3], phase[p % 3]);
       phase[p % 3] ^= 1;
-      if (p + 2 <= ur.phi) {
-        // slot (p+2)%3 held plane p-1, finished at the end of the previous step
-        issue(p + 2);
-      }
-      int64_t se, le, so, lo;
-      runs(p, &se, &le, &so, &lo);
-      const unsigned char* base = raw + size_t(p % 3) * rawb;
-      const T* ev = reinterpret_cast<const T*>(base) + (reinterpret_cast<uintptr_t>(shell + se) & 15) / sizeof(T);
-      uint32_t b0 = uint32_t(((reinterpret_cast<uintptr_t>(shell + se + le) + 15) & ~uintptr_t(15)) -
-                             (reinterpret_cast<uintptr_t>(shell + se) & ~uintptr_t(15)));
-      const T* od = reinterpret_cast<const T*>(base + ((b0 + 127) & ~127u)) +
-                    (reinterpret_cast<uintptr_t>(shell + so) & 15) / sizeof(T);
-      const bool p_odd = p & 1;
       const int64_t r0 = reord(p, g.m0);
-
+      if (tid < R) {
+        const Runs x = runs(p);
+        const int64_t j1 = ur.rlo + tid;
+        const int64_t rs = shell_row_start(g, r0, reord(j1, g.m1));
+        if (j1 & 1)
+          rowoff[tid] = int64_t(odd_slot_off(x) / sizeof(T)) +
+                        int64_t((reinterpret_cast<uintptr_t>(shell + x.so) & 15) / sizeof(T)) + (rs - x.so);
+        else
+          rowoff[tid] = int64_t((reinterpret_cast<uintptr_t>(shell + x.se) & 15) / sizeof(T)) + (rs - x.se);
+      }
+      __syncthreads();
+      if (p + 2 <= ur.phi) issue(p + 2);
+      const T* slot = reinterpret_cast<const T*>(raw + size_t(p % 3) * rawb);
+      const bool p_odd = p & 1;
       double Q[TI1];
 #pragma unroll
-      for (int r = 0; r < TI1; ++r) Q[r] = 0.0;
+      for (int ir = 0; ir < TI1; ++ir) Q[ir] = 0.0;
 #pragma unroll
-      for (int jr = 0; jr < 2 * TI1 + 3; ++jr) {
-        const int64_t j1 = 2 * ur.b0 - 2 + jr;
-        if (j1 < ur.rlo || j1 > ur.rhi) continue;
-        double* cr = crow + (jr & 1) * (g.n2 + 8);
-        if (active) {
-          const bool o1 = j1 & 1;
-          const int64_t r1 = reord(j1, g.m1);
-          const bool inside = r0 < g.m0 && r1 < g.m1;
-          // offset of this row inside its run
-          const T* row = o1 ? od + (shell_row_start(g, r0, r1) - so) : ev + (shell_row_start(g, r0, r1) - se);
-          const int64_t j2 = 2 * i2;
-          cr[j2] = (p_odd || o1) ? double(row[i2]) : 0.0;  // even node: coefficient unless nodal
-          if (j2 + 1 < g.n2) cr[j2 + 1] = double(row[(inside ? 0 : g.m2) + i2]);
-        }
-        __syncthreads();
-        if (active) {
-          const double h = restrict_row(cr, i2, g);
+      for (int jr = 0; jr < RMAX; ++jr) {
+        const int j1 = jbase + jr;
+        if (j1 < rlo || j1 > rhi) continue;
+        const bool o1 = jr & 1;
+        const bool inside = !p_odd && !o1;
+        const T* row = slot + rowoff[j1 - rlo];
+        const double cE = (S.valid && !inside) ? double(row[c]) : 0.0;
+        const double cO = has_odd ? double(row[(inside ? 0 : m2) + c]) : 0.0;
+        const double h = strip_restrict(cE, cO, c, m2);
 #pragma unroll
-          for (int k = -2; k <= 2; ++k) {
-            if (((jr - 2 - k) & 1) != 0) continue;
-            const int ir = (jr - 2 - k) / 2;
-            if (ir < 0 || ir >= TI1) continue;
-            const int64_t i1 = ur.b0 + ir;
-            if (i1 >= ur.b1) continue;
-            Q[ir] += load_w(k, i1, g.m1) * h;
-          }
+        for (int k = -2; k <= 2; ++k) {
+          if (((jr - 2 - k) & 1) != 0) continue;
+          const int ir = (jr - 2 - k) / 2;
+          if (ir < 0 || ir >= TI1) continue;
+          if (ir < TR) Q[ir] += load_w(k, b0 + ir, m1) * h;
         }
       }
-      plane_epilogue<TI1>(g, ur, p, Q, acc, tw2, tid2, G, i2, active);
+      plane_finish<TI1>(g, ur, S, p, Q, acc, tw2, tid2, scan, G);
       __syncthreads();
     }
   }
 }
 
+// ----------------------------------------------------------- interpolate
+// add_interpolant (transform.hpp:317) + inverse_reorder_level
+// (reorder.hpp:138) + unpack of the shell: fine block of level l from the
+// corrected coarse block and the shell.  blockIdx.y = fine plane, blockIdx.x
+// = group of TRI fine rows; strip lanes as the plane passes, the coarse
+// values of the block's rows kept in registers.
+template <typename T, int TRI>
+__global__ void __launch_bounds__(kPlaneMaxThreads)
+    k_f3_rec_interp(const T* __restrict__ shell, const T* __restrict__ coarse, T* __restrict__ fine, const F3Geom g) {
+  constexpr int NE = TRI / 2 + 1;
+  const int m2 = int(g.m2), n2 = int(g.n2), n1 = int(g.n1), m1 = int(g.m1);
+  const StripLane S = strip_lane(m2);
+  const int c = S.c;
+  const bool has_odd = S.valid && 2 * c + 1 < n2;
+  const bool right_degen = 2 * c + 2 >= n2;
+  const int64_t p = blockIdx.y;
+  const int j1lo = int(blockIdx.x) * TRI;
+  const bool p_odd = p & 1;
+  const int64_t cp = p >> 1;
+  const int64_t cpr = p_odd ? ((p + 1 < g.n0) ? cp + 1 : cp) : cp;
+  double CL[NE], CR[NE];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const int row = j1lo / 2 + e;
+    const bool ok = S.valid && row < m1;
+    CL[e] = ok ? double(__ldg(coarse + (cp * g.m1 + row) * g.m2 + c)) : 0.0;
+    CR[e] = (ok && p_odd) ? double(__ldg(coarse + (cpr * g.m1 + row) * g.m2 + c)) : CL[e];
+  }
+  const int64_t r0 = reord(p, g.m0);
+#pragma unroll
+  for (int jr = 0; jr < TRI; ++jr) {
+    const int j1 = j1lo + jr;
+    if (j1 >= n1) break;  // uniform
+    const bool o1 = jr & 1;
+    const int ea = jr >> 1;
+    const double aL = CL[ea];
+    const double bL = o1 ? ((j1 + 1 < n1) ? CL[ea + 1] : aL) : aL;
+    double se;
+    int ke;
+    if (!p_odd) {
+      se = o1 ? aL + bL : aL;
+      ke = o1 ? 1 : 0;
+    } else {
+      const double aR = CR[ea];
+      const double bR = o1 ? ((j1 + 1 < n1) ? CR[ea + 1] : aR) : aR;
+      se = aL + aR;
+      if (o1) {
+        se += bL;
+        se += bR;
+      }
+      ke = o1 ? 2 : 1;
+    }
+    double sn = __shfl_down_sync(0xffffffffu, se, 1);
+    if (right_degen) sn = se;
+    const double so = se + sn;
+    if (!S.owned) continue;
+    const int64_t rs = shell_row_start(g, r0, reord(j1, g.m1));
+    const bool inside = ke == 0;
+    T* out = fine + (p * g.n1 + j1) * g.n2 + 2 * c;
+    const double sc_e = ke == 1 ? 0.5 : 0.25;
+    const double sc_o = ke == 0 ? 0.5 : (ke == 1 ? 0.25 : 0.125);
+    out[0] = inside ? to_t<T>(aL) : to_t<T>(double(shell[rs + c]) + se * sc_e);
+    if (has_odd) out[1] = to_t<T>(double(shell[rs + (inside ? 0 : m2) + c]) + so * sc_o);
+  }
+}
+
 // ------------------------------------------------------------ column pass
 // Thomas along axis 0 or 1 of the coarse fp64 volume G (m0 x m1 x m2).
-// Columns are consecutive in memory across lanes (32 per block row); each
-// column is split over blockDim.y segments of up to LS elements held in
-// registers, joined by an affine scan through shared memory.  With `coarse`
-// set (axis 0) the result is applied: coarse += sign * z (apply_correction,
-// transform.hpp:435-477); otherwise written back to G.
+// 16 consecutive columns per block; each column is split into S segments
+// (two per warp row) of up to LS values kept in registers.  A segment runs
+// the recurrence from a zero carry to get its affine map, the maps are
+// folded through shared memory, and the segment reruns the exact recurrence
+// from its true carry.  With `coarse` set the result is applied:
+// coarse += sign * z (apply_correction, transform.hpp:435-477); otherwise it
+// is written back to G.
 template <typename T, int LS>
-__global__ void __launch_bounds__(kColMaxThreads<LS>)
-    k_f3_col(double* __restrict__ G, T* __restrict__ coarse, double sign, int64_t ncols, int64_t m, int64_t stride,
+__global__ void __launch_bounds__(kColThreads, 2)
+    k_f3_col(double* __restrict__ G, T* __restrict__ coarse, double sign, int64_t ncols, int m, int64_t stride,
              int64_t outer_stride, int64_t inner, const double* __restrict__ w, const double* __restrict__ inv_d) {
-  // shared: w[m], inv_d[m], then the scan exchange [2][S][32]
   extern __shared__ double sc[];
-  const int lane = threadIdx.x, s = threadIdx.y, S = blockDim.y;
+  const int lane = threadIdx.x, S = 2 * blockDim.y;
+  const int c16 = lane & 15, s = 2 * threadIdx.y + (lane >> 4);
   double* tw = sc;
   double* tid = sc + m;
-  double* A = tid + m;
-  double* B = A + S * 32;
-  for (int64_t i = s * 32 + lane; i < m; i += S * 32) {
+  double* A = tid + m;  // [S][16]
+  double* B = A + S * 16;
+  for (int i = threadIdx.y * 32 + lane; i < m; i += blockDim.y * 32) {
     tw[i] = w[i];
     tid[i] = inv_d[i];
   }
-  const int64_t col = int64_t(blockIdx.x) * 32 + lane;
+  const int64_t col = int64_t(blockIdx.x) * 16 + c16;
   const bool valid = col < ncols;
-  // column col -> base offset: (col / inner) * outer_stride + col % inner
   const int64_t base = valid ? (col / inner) * outer_stride + (col % inner) : 0;
-  const int64_t seg = (m + S - 1) / S;
-  const int s0 = int(min(m, int64_t(s) * seg)), s1 = int(min(m, int64_t(s0) + seg));
+  const int seg = (m + S - 1) / S;
+  const int s0 = min(m, s * seg), s1 = min(m, s0 + seg);
   const int len = s1 - s0;
   double v[LS];
+  T cv[LS];  // coarse values to update (prefetched with G)
   {
     const double* gp = G + base + int64_t(s0) * stride;
+    const T* cp = coarse ? coarse + base + int64_t(s0) * stride : nullptr;
 #pragma unroll
     for (int k = 0; k < LS; ++k) {
       v[k] = (valid && k < len) ? *gp : 0.0;
+      cv[k] = (cp && valid && k < len) ? *cp : T(0);
       gp += stride;
+      if (cp) cp += stride;
     }
   }
   __syncthreads();
-  // Forward elimination y_i = f_i - w_i y_{i-1} (batched_solve,
-  // transform.hpp:117-120): local run from 0 gives the segment's affine map.
-  double yl = 0.0, mu = 1.0;
+  // forward y_i = f_i - w_i y_{i-1} (batched_solve, transform.hpp:117-120)
+  double ya = 0.0, yb = 1.0;
 #pragma unroll
   for (int k = 0; k < LS; ++k)
     if (k < len) {
       const double wi = ld_volatile(tw + s0 + k);
-      yl = v[k] - wi * yl;
-      mu = -wi * mu;
+      ya = v[k] - wi * ya;
+      yb = -wi * yb;
     }
-  A[s * 32 + lane] = len > 0 ? yl : 0.0;
-  B[s * 32 + lane] = len > 0 ? mu : 1.0;
+  A[s * 16 + c16] = ya;
+  B[s * 16 + c16] = yb;
   __syncthreads();
-  double y = 0.0;  // true y_{s0 - 1}
-  for (int q = 0; q < s; ++q) y = A[q * 32 + lane] + B[q * 32 + lane] * y;
+  double y = 0.0;
+  for (int q = 0; q < s; ++q) y = A[q * 16 + c16] + B[q * 16 + c16] * y;
   __syncthreads();
-  // rerun the recurrence from the true carry
 #pragma unroll
   for (int k = 0; k < LS; ++k)
     if (k < len) {
       y = v[k] - ld_volatile(tw + s0 + k) * y;
       v[k] = y;
     }
-  // Back substitution z_i = (y_i - z_{i+1}/3) / d_i (transform.hpp:121-129).
-  double xl = 0.0, nu = 1.0;
+  // back substitution z_i = (y_i - z_{i+1}/3) / d_i (transform.hpp:121-129)
+  double za = 0.0, zb = 1.0;
 #pragma unroll
   for (int k = LS - 1; k >= 0; --k)
     if (k < len) {
       const double id = ld_volatile(tid + s0 + k);
-      xl = (v[k] - kOff * xl) * id;
-      nu = -kOff * id * nu;
+      za = (v[k] - kOff * za) * id;
+      zb = -kOff * id * zb;
     }
-  A[s * 32 + lane] = len > 0 ? xl : 0.0;
-  B[s * 32 + lane] = len > 0 ? nu : 1.0;
+  A[s * 16 + c16] = za;
+  B[s * 16 + c16] = zb;
   __syncthreads();
-  double z = 0.0;  // true z_{s1}
-  for (int q = S - 1; q > s; --q) z = A[q * 32 + lane] + B[q * 32 + lane] * z;
+  double z = 0.0;
+  for (int q = S - 1; q > s; --q) z = A[q * 16 + c16] + B[q * 16 + c16] * z;
 #pragma unroll
   for (int k = LS - 1; k >= 0; --k)
     if (k < len) {
@@ -733,7 +790,7 @@ __global__ void __launch_bounds__(kColMaxThreads<LS>)
     T* c = coarse + base + int64_t(s0) * stride;
 #pragma unroll
     for (int k = 0; k < LS; ++k) {
-      if (k < len) *c = to_t<T>(double(*c) + sign * v[k]);
+      if (k < len) *c = to_t<T>(double(cv[k]) + sign * v[k]);
       c += stride;
     }
   } else {
@@ -746,147 +803,62 @@ __global__ void __launch_bounds__(kColMaxThreads<LS>)
   }
 }
 
-// ----------------------------------------------------------- interpolate
-// add_interpolant + inverse_reorder_level for one fine row tile: one thread
-// per coarse column i2 (fine pair), blockIdx.x = fine plane, blockIdx.y =
-// group of kRowsPerBlock fine rows.  Corner order as update_coefficients.
-template <typename T>
-__global__ void __launch_bounds__(1024)
-    k_f3_rec_interp(const T* __restrict__ shell, const T* __restrict__ coarse, T* __restrict__ fine, const F3Geom g,
-                    int rows_per_block) {
-  const int64_t p = blockIdx.x;
-  const int64_t i2 = threadIdx.x;
-  if (i2 >= g.m2) return;
-  const bool p_odd = p & 1;
-  const int64_t cp = p >> 1;                                   // left/own coarse plane
-  const int64_t cpr = p_odd ? ((p + 1 < g.n0) ? cp + 1 : cp) : cp;  // right coarse plane
-  const int64_t r0 = reord(p, g.m0);
-  const int64_t j1lo = int64_t(blockIdx.y) * rows_per_block;
-  const int64_t j1hi = min(g.n1, j1lo + rows_per_block);
-  const int64_t cl = i2, crc = (2 * i2 + 2 < g.n2) ? i2 + 1 : i2;
-  const int64_t ps = g.m1 * g.m2;
-  for (int64_t j1 = j1lo; j1 < j1hi; ++j1) {
-    const bool o1 = j1 & 1;
-    const int64_t rl = j1 >> 1, rr = o1 ? ((j1 + 1 < g.n1) ? rl + 1 : rl) : rl;
-    const int64_t r1 = reord(j1, g.m1);
-    const int64_t rs = shell_row_start(g, r0, r1);
-    const bool inside = r0 < g.m0 && r1 < g.m1;
-    const T* cL = coarse + cp * ps;
-    const T* cR = coarse + cpr * ps;
-    T* out = fine + (p * g.n1 + j1) * g.n2;
-    // even node 2 i2
-    {
-      double pred;
-      if (p_odd) {
-        if (o1) {
-          pred = double(__ldg(cL + rl * g.m2 + cl));
-          pred += double(__ldg(cR + rl * g.m2 + cl));
-          pred += double(__ldg(cL + rr * g.m2 + cl));
-          pred += double(__ldg(cR + rr * g.m2 + cl));
-          pred *= 0.25;
-        } else {
-          pred = double(__ldg(cL + rl * g.m2 + cl));
-          pred += double(__ldg(cR + rl * g.m2 + cl));
-          pred *= 0.5;
-        }
-        out[2 * i2] = to_t<T>(double(shell[rs + i2]) + pred);
-      } else if (o1) {
-        pred = double(__ldg(cL + rl * g.m2 + cl));
-        pred += double(__ldg(cL + rr * g.m2 + cl));
-        pred *= 0.5;
-        out[2 * i2] = to_t<T>(double(shell[rs + i2]) + pred);
-      } else {
-        out[2 * i2] = __ldg(cL + rl * g.m2 + cl);
-      }
-    }
-    if (2 * i2 + 1 < g.n2) {
-      double pred;
-      if (p_odd) {
-        if (o1) {
-          pred = double(__ldg(cL + rl * g.m2 + cl));
-          pred += double(__ldg(cR + rl * g.m2 + cl));
-          pred += double(__ldg(cL + rr * g.m2 + cl));
-          pred += double(__ldg(cR + rr * g.m2 + cl));
-          pred += double(__ldg(cL + rl * g.m2 + crc));
-          pred += double(__ldg(cR + rl * g.m2 + crc));
-          pred += double(__ldg(cL + rr * g.m2 + crc));
-          pred += double(__ldg(cR + rr * g.m2 + crc));
-          pred *= 0.125;
-        } else {
-          pred = double(__ldg(cL + rl * g.m2 + cl));
-          pred += double(__ldg(cR + rl * g.m2 + cl));
-          pred += double(__ldg(cL + rl * g.m2 + crc));
-          pred += double(__ldg(cR + rl * g.m2 + crc));
-          pred *= 0.25;
-        }
-      } else if (o1) {
-        pred = double(__ldg(cL + rl * g.m2 + cl));
-        pred += double(__ldg(cL + rr * g.m2 + cl));
-        pred += double(__ldg(cL + rl * g.m2 + crc));
-        pred += double(__ldg(cL + rr * g.m2 + crc));
-        pred *= 0.25;
-      } else {
-        pred = double(__ldg(cL + rl * g.m2 + cl));
-        pred += double(__ldg(cL + rl * g.m2 + crc));
-        pred *= 0.5;
-      }
-      out[2 * i2 + 1] = to_t<T>(double(shell[rs + (inside ? 0 : g.m2) + i2]) + pred);
-    }
-  }
-}
-
 // ------------------------------------------------------------ host side
 
 template <typename T, int TI1>
-size_t plane_smem(const F3Geom& g, bool dec) {
-  return PlaneSmem<T, TI1>::bytes(g.n2, g.m2, dec);
+size_t plane_smem(const F3Geom& g) {
+  return PlaneSmem<T, TI1>::bytes(g.n2, g.m2);
 }
 
+// Largest row tile whose plane-pass CTA fits twice per SM (else once).
 template <typename T>
-bool pick_tile(F3Geom& g, size_t limit) {
-  const int cands[3] = {8, 4, 2};
-  for (int c : cands) {
-    size_t need = 0;
-    if (c == 8) need = plane_smem<T, 8>(g, true);
-    if (c == 4) need = plane_smem<T, 4>(g, true);
-    if (c == 2) need = plane_smem<T, 2>(g, true);
-    if (need <= limit) {
-      g.tile_rows = c;
-      return true;
+bool pick_tile(F3Geom& g, size_t optin, size_t per_sm) {
+  const int cands[4] = {8, 6, 4, 2};
+  for (int pass = 0; pass < 2; ++pass) {
+    const size_t limit = pass == 0 ? std::min(optin, per_sm / 2 - 2048) : optin;
+    for (int c : cands) {
+      size_t need = 0;
+      if (c == 8) need = plane_smem<T, 8>(g);
+      if (c == 6) need = plane_smem<T, 6>(g);
+      if (c == 4) need = plane_smem<T, 4>(g);
+      if (c == 2) need = plane_smem<T, 2>(g);
+      if (need <= limit) {
+        g.tile_rows = c;
+        g.ctas_per_sm = pass == 0 ? 2 : 1;
+        return true;
+      }
     }
   }
   return false;
 }
 
-template <int LS>
-int col_segments(int64_t m) { return int((m + LS - 1) / LS); }
-
 template <typename T>
 void launch_col(double* G, T* coarse, double sign, const F3Geom& g, int axis, const double* w, const double* id,
                 const Exec& ex) {
-  int64_t m, stride, outer_stride, inner, ncols;
+  int64_t stride, outer_stride, inner, ncols;
+  int m;
   if (axis == 1) {
-    m = g.m1;
+    m = int(g.m1);
     stride = g.m2;
     inner = g.m2;
     outer_stride = g.m1 * g.m2;
     ncols = g.m0 * g.m2;
   } else {
-    m = g.m0;
+    m = int(g.m0);
     stride = g.m1 * g.m2;
     inner = g.m1 * g.m2;
     outer_stride = 0;
     ncols = g.m1 * g.m2;
   }
-  const unsigned blocks = unsigned((ncols + 31) / 32);
+  const unsigned blocks = unsigned((ncols + 15) / 16);
   const char* tag = axis == 1 ? "f3_col1" : "f3_col0";
   if (m <= 320) {
-    const int S = col_segments<16>(m);
-    MGRX_LAUNCH(ex, tag, k_f3_col<T, 16><<<blocks, dim3(32, S), (2 * S * 32 + 2 * m) * 8, ex.s>>>(
+    const int SY = (m + 2 * 16 - 1) / (2 * 16);
+    MGRX_LAUNCH(ex, tag, k_f3_col<T, 16><<<blocks, dim3(32, SY), (2 * m + 2 * 2 * SY * 16) * 8, ex.s>>>(
                              G, coarse, sign, ncols, m, stride, outer_stride, inner, w, id));
   } else {
-    const int S = col_segments<32>(m);
-    MGRX_LAUNCH(ex, tag, k_f3_col<T, 32><<<blocks, dim3(32, S), (2 * S * 32 + 2 * m) * 8, ex.s>>>(
+    const int SY = (m + 2 * 32 - 1) / (2 * 32);
+    MGRX_LAUNCH(ex, tag, k_f3_col<T, 32><<<blocks, dim3(32, SY), (2 * m + 2 * 2 * SY * 16) * 8, ex.s>>>(
                              G, coarse, sign, ncols, m, stride, outer_stride, inner, w, id));
   }
 }
@@ -903,45 +875,54 @@ Fused3DPlan fused3d_plan(const LevelGeom& lg, int esize) {
   g.m0 = lg.m[0];
   g.m1 = lg.m[1];
   g.m2 = lg.m[2];
-  // worth it only for sizeable rows; one thread per coarse column
-  if (g.n2 < 33 || g.m2 > kF3MaxThreads || g.m1 > kColMaxM || g.m0 > kColMaxM || g.n1 < 5 || g.n0 < 5) return fp;
-  if (int64_t(g.n0) * g.n1 * g.n2 < (int64_t(1) << 15)) return fp;
+  if (g.n2 < 33 || g.m1 > kColMaxM || g.m0 > kColMaxM || g.n1 < 5 || g.n0 < 5) return fp;
+  if ((g.m2 + 29) / 30 * 32 > kPlaneMaxThreads) return fp;
+  // small levels stay on the general kernels (launch-latency bound either way)
+  {
+    int64_t min_elems = int64_t(1) << 20;
+    if (const char* env = std::getenv("MGRX_FUSED_MIN_ELEMS")) min_elems = std::atoll(env);
+    if (int64_t(g.n0) * g.n1 * g.n2 < min_elems) return fp;
+  }
   int dev = 0;
   cudaGetDevice(&dev);
-  int optin = 0, nsm = 0;
+  int optin = 0, nsm = 0, per_sm = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
   if (optin <= 0) optin = 227 * 1024;
+  if (per_sm <= 0) per_sm = 228 * 1024;
   if (nsm <= 0) nsm = kNumSMs;
-  const bool ok = esize == 4 ? pick_tile<float>(g, size_t(optin)) : pick_tile<double>(g, size_t(optin));
+  const bool ok = esize == 4 ? pick_tile<float>(g, size_t(optin), size_t(per_sm))
+                             : pick_tile<double>(g, size_t(optin), size_t(per_sm));
   if (!ok) return fp;
   g.ntile1 = int((g.m1 + g.tile_rows - 1) / g.tile_rows);
-  // axis-0 chunks: about 6 units per SM so dynamic scheduling evens out
-  const int64_t want_units = int64_t(nsm) * 6;
+  g.threads = int((g.m2 + 29) / 30) * 32;
+  const int ctas = nsm * g.ctas_per_sm;
+  // axis-0 chunks: about 4 units per CTA so dynamic scheduling evens out
+  const int64_t want_units = int64_t(ctas) * 4;
   int64_t nchunk = std::max<int64_t>(1, (want_units + g.ntile1 - 1) / g.ntile1);
   int64_t chunk = std::max<int64_t>(4, (g.m0 + nchunk - 1) / nchunk);
   nchunk = (g.m0 + chunk - 1) / chunk;
   g.chunk = chunk;
   g.units = int(nchunk * g.ntile1);
-  g.threads = int((g.m2 + 31) / 32 * 32);
-  g.grid = std::min<int>(g.units, nsm);
+  g.grid = std::min<int>(g.units, ctas);
   fp.enabled = true;
   fp.scratch_bytes = size_t(g.m0) * g.m1 * g.m2 * 8 + 256;
   return fp;
 }
 
 template <typename T>
-static cudaError_t set_attrs(const F3Geom& g, size_t* dec_smem, size_t* rec_smem) {
+static cudaError_t set_attrs(const F3Geom& g, size_t* smem) {
   cudaError_t e = cudaSuccess;
-#define MGRX_ATTR(TI)                                                                                    \
-  if (g.tile_rows == TI) {                                                                              \
-    *dec_smem = plane_smem<T, TI>(g, true);                                                             \
-    *rec_smem = plane_smem<T, TI>(g, false);                                                            \
-    e = cudaFuncSetAttribute(k_f3_dec_plane<T, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(*dec_smem)); \
-    if (e == cudaSuccess)                                                                               \
-      e = cudaFuncSetAttribute(k_f3_rec_plane<T, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(*rec_smem)); \
+#define MGRX_ATTR(TI)                                                                                        \
+  if (g.tile_rows == TI) {                                                                                  \
+    *smem = plane_smem<T, TI>(g);                                                                           \
+    e = cudaFuncSetAttribute(k_f3_dec_plane<T, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(*smem)); \
+    if (e == cudaSuccess)                                                                                   \
+      e = cudaFuncSetAttribute(k_f3_rec_plane<T, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(*smem)); \
   }
   MGRX_ATTR(8)
+  MGRX_ATTR(6)
   MGRX_ATTR(4)
   MGRX_ATTR(2)
 #undef MGRX_ATTR
@@ -954,8 +935,8 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
   const F3Geom& g = fp.g;
   double* G = static_cast<double*>(scratch);
   int* counter = reinterpret_cast<int*>(static_cast<char*>(scratch) + size_t(g.m0) * g.m1 * g.m2 * 8);
-  size_t ds = 0, rs = 0;
-  cudaError_t e = set_attrs<T>(g, &ds, &rs);
+  size_t ds = 0;
+  cudaError_t e = set_attrs<T>(g, &ds);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(counter, 0, sizeof(int), ex.s);
   if (e != cudaSuccess) return e;
@@ -964,6 +945,7 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
     MGRX_LAUNCH(ex, "f3_dec_plane", k_f3_dec_plane<T, TI><<<g.grid, g.threads, ds, ex.s>>>(            \
                                         blk, shell, coarse, G, th.w[2], th.inv_d[2], counter, g));
   MGRX_DEC(8)
+  MGRX_DEC(6)
   MGRX_DEC(4)
   MGRX_DEC(2)
 #undef MGRX_DEC
@@ -978,24 +960,26 @@ cudaError_t fused3d_recompose_level(const T* shell, T* coarse, T* fine, void* sc
   const F3Geom& g = fp.g;
   double* G = static_cast<double*>(scratch);
   int* counter = reinterpret_cast<int*>(static_cast<char*>(scratch) + size_t(g.m0) * g.m1 * g.m2 * 8);
-  size_t ds = 0, rs = 0;
-  cudaError_t e = set_attrs<T>(g, &ds, &rs);
+  size_t ds = 0;
+  cudaError_t e = set_attrs<T>(g, &ds);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(counter, 0, sizeof(int), ex.s);
   if (e != cudaSuccess) return e;
 #define MGRX_REC(TI)                                                                                   \
   if (g.tile_rows == TI)                                                                              \
     MGRX_LAUNCH(ex, "f3_rec_plane",                                                                   \
-                k_f3_rec_plane<T, TI><<<g.grid, g.threads, rs, ex.s>>>(shell, G, th.w[2], th.inv_d[2], counter, g));
+                k_f3_rec_plane<T, TI><<<g.grid, g.threads, ds, ex.s>>>(shell, G, th.w[2], th.inv_d[2], counter, g));
   MGRX_REC(8)
+  MGRX_REC(6)
   MGRX_REC(4)
   MGRX_REC(2)
 #undef MGRX_REC
   launch_col<T>(G, nullptr, 0.0, g, 1, th.w[1], th.inv_d[1], ex);
   launch_col<T>(G, coarse, -1.0, g, 0, th.w[0], th.inv_d[0], ex);
-  const int rows = 4;
-  MGRX_LAUNCH(ex, "f3_rec_interp", k_f3_rec_interp<T><<<dim3(unsigned(g.n0), unsigned((g.n1 + rows - 1) / rows)),
-                                                         g.threads, 0, ex.s>>>(shell, coarse, fine, g, rows));
+  constexpr int kTRI = 16;
+  MGRX_LAUNCH(ex, "f3_rec_interp",
+              k_f3_rec_interp<T, kTRI><<<dim3(unsigned((g.n1 + kTRI - 1) / kTRI), unsigned(g.n0)), g.threads, 0, ex.s>>>(
+                  shell, coarse, fine, g));
   return cudaGetLastError();
 }
 

@@ -17,7 +17,8 @@ struct F3Geom {
   int tile_rows = 0;               // coarse rows (axis 1) per work unit
   int ntile1 = 0;                  // tiles along axis 1
   int units = 0;                   // work units = chunks * ntile1
-  int threads = 0;                 // plane-pass CTA size (one thread per coarse column)
+  int threads = 0;                 // plane-pass CTA size (strips of 30 coarse columns)
+  int ctas_per_sm = 1;             // plane-pass CTAs resident per SM
   int grid = 0;                    // persistent plane-pass CTAs
 };
 
