@@ -157,8 +157,15 @@ struct Plan {
   size_t off_comp = 0, off_tmp = 0, off_blk = 0, bytes = 0;
   std::vector<size_t> blk_off;     // level block offsets (levels stop..L-1)
   std::vector<Fused3DPlan> fused;  // index l; .enabled false when not applicable
+  // tail: levels stop+1..tail_top run in one CTA (uniform coordinates)
+  int tail_top = -1;
+  int64_t tail_nmax = 0;
+  void* d_tail_dec = nullptr;  // TailLevel[] finest first
+  void* d_tail_rec = nullptr;  // TailLevel[] coarsest first
   ~Plan() {
     if (d_tables) cudaFree(d_tables);
+    if (d_tail_dec) cudaFree(d_tail_dec);
+    if (d_tail_rec) cudaFree(d_tail_rec);
   }
 };
 
@@ -288,6 +295,29 @@ Plan* get_plan(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int lev
       p->thomas[l].w[a] = p->d_tables + starts[k];
       p->thomas[l].inv_d[a] = p->d_tables + starts[k] + m;
     }
+  // Tail: the small levels (block fits one CTA's shared memory) in one launch.
+  {
+    const int64_t tail_max = int64_t((220 * 1024) / (16 + 2 * es));
+    int top = -1;
+    for (int l = stop + 1; l <= L; ++l)
+      if (h.node[l] <= tail_max) top = l;
+    if (top > stop) {
+      p->tail_top = top;
+      p->tail_nmax = h.node[top];
+      const int nlev = top - stop;
+      const size_t lb = tail_level_bytes();
+      std::vector<unsigned char> dec(nlev * lb), rec(nlev * lb);
+      for (int k = 0; k < nlev; ++k) {
+        const int ld = top - k, lr = stop + 1 + k;
+        tail_fill_level(dec.data() + k * lb, p->geom[ld], p->thomas[ld], h.node[ld - 1]);
+        tail_fill_level(rec.data() + k * lb, p->geom[lr], p->thomas[lr], h.node[lr - 1]);
+      }
+      cuda_check(cudaMalloc(&p->d_tail_dec, dec.size()), "cudaMalloc(tail)");
+      cuda_check(cudaMalloc(&p->d_tail_rec, rec.size()), "cudaMalloc(tail)");
+      cuda_check(cudaMemcpy(p->d_tail_dec, dec.data(), dec.size(), cudaMemcpyHostToDevice), "upload tail");
+      cuda_check(cudaMemcpy(p->d_tail_rec, rec.data(), rec.size(), cudaMemcpyHostToDevice), "upload tail");
+    }
+  }
   // Scratch: fp64 component + sweep ping-pong (sized for the finest level
   // processed) and the compact level blocks stop..L-1.
   int64_t comp = 0, tmp = 0;
@@ -448,6 +478,10 @@ void decompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, T* d_out, const 
   double* tmp = reinterpret_cast<double*>(s + p.off_tmp);
   const T* blk = d_field;
   for (int l = L; l > stop; --l) {
+    if (!nu && l == p.tail_top) {  // levels l..stop+1 in one CTA
+      cuda_check(tail_decompose<T>(blk, d_out, d_out, p.d_tail_dec, l - stop, p.tail_nmax, exec(c)), "tail");
+      break;
+    }
     T* shell = d_out + h.node[l - 1];
     T* coarse = (l - 1 == stop) ? d_out : reinterpret_cast<T*>(s + p.blk_off[l - 1]);
     const Fused3DPlan& fp = p.fused[l];
@@ -479,10 +513,19 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
   double* tmp = reinterpret_cast<double*>(s + p.off_tmp);
   // unpack_level_centric's coarse block (reorder.hpp:231-238)
   T* coarse = reinterpret_cast<T*>(s + p.blk_off[stop]);
-  cuda_check(cudaMemcpyAsync(coarse, d_coeffs, size_t(h.node[stop]) * sizeof(T), cudaMemcpyDeviceToDevice,
-                             c->stream),
-             "copy coarse");
-  for (int l = stop + 1; l <= L; ++l) {
+  int l0 = stop + 1;
+  if (!nu && p.tail_top > stop) {  // levels stop+1..tail_top in one CTA
+    const int top = p.tail_top;
+    T* fine = (top == L) ? d_field : reinterpret_cast<T*>(s + p.blk_off[top]);
+    cuda_check(tail_recompose<T>(d_coeffs, d_coeffs, fine, p.d_tail_rec, top - stop, p.tail_nmax, exec(c)), "tail");
+    coarse = fine;
+    l0 = top + 1;
+  } else {
+    cuda_check(cudaMemcpyAsync(coarse, d_coeffs, size_t(h.node[stop]) * sizeof(T), cudaMemcpyDeviceToDevice,
+                               c->stream),
+               "copy coarse");
+  }
+  for (int l = l0; l <= L; ++l) {
     const T* shell = d_coeffs + h.node[l - 1];
     T* fine = (l == L) ? d_field : reinterpret_cast<T*>(s + p.blk_off[l]);
     const Fused3DPlan& fp = p.fused[l];

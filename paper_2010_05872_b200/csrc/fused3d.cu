@@ -43,7 +43,7 @@ namespace mgrx_b200 {
 
 namespace {
 
-constexpr int kPlaneMaxThreads = 576;  // plane passes: up to 18 strips of 30 coarse columns (112-register budget)
+constexpr int kPlaneMaxThreads = 288;  // plane passes: up to 9 strips of 30 coarse columns, 2 CTAs per SM
 constexpr int kColMaxM = 640;       // column passes: register-resident columns up to this length
 // column-pass block: 16 columns x S segments of up to LS registers, two
 // segments per warp row; LS = 16 for m <= 320, 32 for m <= 640
@@ -276,7 +276,7 @@ struct PlaneSmem {
   static __host__ __device__ size_t acc_elems(int64_t m2) { return size_t(TI1) * size_t(m2); }
   static __host__ __device__ size_t bytes(int64_t n2, int64_t m2) {
     size_t b = 3 * raw_bytes(n2);   // TMA ring of fine plane tiles
-    b += 3 * acc_elems(m2) * 8;     // coarse-plane accumulators (L0)
+    b += 2 * acc_elems(m2) * 8;     // finished coarse rows staged for the axis-2 solve
     b += 2 * size_t(m2) * 8;        // Thomas tables axis 2
     b += 64 * 8 + 2 * kRows * 8 + 64;  // scan scratch, row offsets, barriers
     return b;
@@ -294,58 +294,214 @@ __device__ __forceinline__ double strip_restrict(double cE, double cO, int c, in
   return wc * cE + 0.5 * cO + xl + kW12 * er;
 }
 
-// L0 accumulation of the plane's restricted rows into the coarse planes
-// i0 with |p - 2 i0| <= 2 (first term initialises), then completion of
-// finished coarse planes: Thomas along axis 2 with all warps, rows to G.
-template <int TI1>
-__device__ __forceinline__ void plane_finish(const F3Geom& g, const UnitRange& ur, const StripLane& S, int64_t p,
-                                             const double* Q, double* acc, const double* tw2, const double* tid2,
-                                             double* scan, double* __restrict__ G) {
-  const int m2 = int(g.m2), c = S.c;
-  const int TR = int(ur.b1 - ur.b0);
-  const int accsz = TI1 * m2;
-  const int pp = int(p), m0 = int(g.m0);
-  const int ilo = int(max(ur.a0, (p - 1) >> 1)), ihi = int(min(ur.a1 - 1, (p + 2) >> 1));
-  if (S.owned)
-    for (int i0 = ilo; i0 <= ihi; ++i0) {
-      const int k = pp - 2 * i0;
-      if (k < -2 || k > 2) continue;
-      const double w0 = load_w(k, i0, m0);
-      double* a = acc + (i0 % 3) * accsz + c;
-      const bool first = pp == max(0, 2 * i0 - 2);
-#pragma unroll
-      for (int ir = 0; ir < TI1; ++ir)
-        if (ir < TR) a[ir * m2] = first ? w0 * Q[ir] : a[ir * m2] + w0 * Q[ir];
-    }
-  int64_t lo = -1, hi = -2;
-  if (p == g.n0 - 1) {
-    lo = (p - 1) >> 1;
-    hi = ur.a1 - 1;
-  } else if (!(p & 1) && p >= 2) {
-    lo = hi = (p - 2) >> 1;
+// Thomas solve of one row x[0..m) in shared memory by one warp: lane
+// segments get their affine maps from a zero carry, a shuffle scan gives
+// each segment its true carry, and the segment reruns the exact recurrence
+// (ThomasAux factors, transform.hpp:25-44; batched_solve :116-130).
+__device__ __forceinline__ void warp_row_thomas(double* x, int m, const double* __restrict__ w,
+                                                const double* __restrict__ inv_d) {
+  const int lane = threadIdx.x & 31;
+  const int seg = (m + 31) >> 5;
+  const int s0 = min(m, lane * seg), s1 = min(m, s0 + seg);
+  Aff f{0.0, 1.0};
+  for (int i = s0; i < s1; ++i) {
+    const double wi = w[i];
+    f.a = x[i] - wi * f.a;
+    f.b = -wi * f.b;
   }
-  lo = max(lo, ur.a0);
-  hi = min(hi, ur.a1 - 1);
-  if (lo > hi) return;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const Aff o{__shfl_up_sync(0xffffffffu, f.a, off), __shfl_up_sync(0xffffffffu, f.b, off)};
+    if (lane >= off) f = aff_then(o, f);
+  }
+  double y = __shfl_up_sync(0xffffffffu, f.a, 1);
+  if (lane == 0) y = 0.0;
+  for (int i = s0; i < s1; ++i) {
+    y = x[i] - w[i] * y;
+    x[i] = y;
+  }
+  Aff g{0.0, 1.0};
+  for (int i = s1 - 1; i >= s0; --i) {
+    const double id = inv_d[i];
+    g.a = (x[i] - kOff * g.a) * id;
+    g.b = -kOff * id * g.b;
+  }
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const Aff o{__shfl_down_sync(0xffffffffu, g.a, off), __shfl_down_sync(0xffffffffu, g.b, off)};
+    if (lane + off < 32) g = aff_then(o, g);
+  }
+  double z = __shfl_down_sync(0xffffffffu, g.a, 1);
+  if (lane == 31) z = 0.0;
+  for (int i = s1 - 1; i >= s0; --i) {
+    z = (x[i] - kOff * z) * inv_d[i];
+    x[i] = z;
+  }
+  __syncwarp();
+}
+
+// L0 (axis-0 load-vector restriction) on registers: the coarse planes
+// k-1, k, k+1 around fine plane p (k = p/2) accumulate the plane's
+// restricted rows Q in stencil order (load_entry, transform.hpp:84-96);
+// a finished coarse plane is staged in shared memory, solved along axis 2
+// (one warp per row) and stored to G.
+template <int TI1>
+struct L0Planes {
+  double prev[TI1], cur[TI1], next[TI1];
+};
+
+template <int TI1>
+__device__ __forceinline__ void l0_complete(const F3Geom& g, const UnitRange& ur, const StripLane& S,
+                                            const double* v, int64_t i0, double* tb, const double* tw2,
+                                            const double* tid2, double* __restrict__ G) {
+  const int m2 = int(g.m2), TR = int(ur.b1 - ur.b0);
+  if (S.owned) {
+#pragma unroll
+    for (int ir = 0; ir < TI1; ++ir)
+      if (ir < TR) tb[ir * m2 + S.c] = v[ir];
+  }
   __syncthreads();
-  for (int64_t i0 = lo; i0 <= hi; ++i0) {
-    double* a = acc + int(i0 % 3) * accsz;
-    block_thomas_rows(a, TR, m2, m2, tw2, tid2, scan);
-    if (S.owned) {
-      double* gp = G + (i0 * g.m1 + ur.b0) * g.m2 + c;
-      for (int ir = 0; ir < TR; ++ir) gp[int64_t(ir) * m2] = a[ir * m2 + c];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  for (int ir = warp; ir < TR; ir += nwarps) {
+    double* row = tb + ir * m2;
+    warp_row_thomas(row, m2, tw2, tid2);
+    double* gp = G + (i0 * g.m1 + ur.b0 + ir) * g.m2;
+    for (int i = lane; i < m2; i += 32) gp[i] = row[i];
+  }
+}
+
+template <int TI1>
+__device__ __forceinline__ void l0_plane(const F3Geom& g, const UnitRange& ur, const StripLane& S, int64_t p,
+                                         const double* Q, L0Planes<TI1>& A, double* tb, const double* tw2,
+                                         const double* tid2, double* __restrict__ G) {
+  const int64_t k = p >> 1;
+  const int m2 = int(g.m2);
+  const bool last = p == g.n0 - 1;
+  if (!(p & 1)) {
+    const double wc = (k == 0 || k + 1 == g.m0) ? kW5_12 : kW5_6;
+#pragma unroll
+    for (int ir = 0; ir < TI1; ++ir) {
+      A.prev[ir] += kW12 * Q[ir];
+      A.cur[ir] += wc * Q[ir];
+      A.next[ir] += kW12 * Q[ir];
+    }
+    if (k - 1 >= ur.a0 && k - 1 < ur.a1) l0_complete<TI1>(g, ur, S, A.prev, k - 1, tb, tw2, tid2, G);
+    if (last && k >= ur.a0 && k < ur.a1) l0_complete<TI1>(g, ur, S, A.cur, k, tb + TI1 * m2, tw2, tid2, G);
+  } else {
+#pragma unroll
+    for (int ir = 0; ir < TI1; ++ir) {
+      A.cur[ir] += 0.5 * Q[ir];
+      A.next[ir] += 0.5 * Q[ir];
+    }
+    if (last && k >= ur.a0 && k < ur.a1) l0_complete<TI1>(g, ur, S, A.cur, k, tb, tw2, tid2, G);
+#pragma unroll
+    for (int ir = 0; ir < TI1; ++ir) {
+      A.prev[ir] = A.cur[ir];
+      A.cur[ir] = A.next[ir];
+      A.next[ir] = 0.0;
     }
   }
 }
 
-// Decompose plane pass: persistent CTAs take (axis-0 chunk, axis-1 tile)
-// units and stream the unit's fine planes through a 3-deep TMA ring.  Per
-// fine row and column pair: coefficients (update_coefficients corner sets;
-// the odd node's sum = own column's sum + right column's sum), shell /
-// coarse writes, axis-2 restriction through shuffles, axis-1 restriction in
-// registers.
+// Per-plane, per-thread context of the decompose row loop.
+template <typename T>
+struct DecRows {
+  const T* rp;        // tile row 0 (= fine row rlo), at column 2c
+  T* se;              // shell slot of even tile row e = 0 (fine row jbase), at column c
+  T* so;              // shell slot of odd tile row e = 0 (fine row jbase + 1), at column c
+  T* cpe;             // coarse row of even tile row e = 0, at column c
+  int64_t st_e;       // shell stride between consecutive even rows
+  int64_t n2l;        // shell stride between consecutive odd rows
+  int n2, m2, n1, m1; // extents
+  int jbase, rlo, rhi, b0, TR, jlo_own, jhi_own;
+  int oofs;           // odd-node offset inside an even row's shell slot
+  bool own;           // owned lane and owned plane
+  bool valid, has_odd, right_degen, has_right;
+  int c;
+};
+
+// Rows of one fine plane (decompose): for every fine row and this lane's
+// column pair, the coefficients (corner sets of update_coefficients,
+// transform.hpp:216-304; the odd node's sum is the own column's sum plus the
+// right column's, shuffled in), the shell / coarse writes, the axis-2
+// restriction (shuffles) and the axis-1 restriction into Q (registers).
+// PODD: plane parity; FULL: interior tile (all rows present, no degenerate
+// row, interior axis-1 weights) — every row test is then compile-time.
+template <typename T, int TI1, bool PODD, bool FULL>
+__device__ __forceinline__ void dec_rows(const DecRows<T>& x, const double* NSP, const double* NSN, double* Q) {
+  constexpr int RMAX = 2 * TI1 + 3;
+  const int n2 = x.n2;
+  const T* rr = x.rp + (x.jbase - x.rlo) * n2;  // tile row of jr = 0 (may precede the tile when not FULL)
+#pragma unroll
+  for (int jr = 0; jr < RMAX; ++jr, rr += n2) {
+    const int j1 = x.jbase + jr;
+    if (!FULL && (j1 < x.rlo || j1 > x.rhi)) continue;  // uniform
+    constexpr int dummy = 0;
+    (void)dummy;
+    const bool o1 = jr & 1;
+    const int ea = jr >> 1;
+    const bool rdeg = !FULL && o1 && (j1 + 1 >= x.n1);
+    const double rawE = double(rr[0]);
+    const double rawO = x.has_odd ? double(rr[1]) : 0.0;
+    const double aL = NSP[ea];
+    const double bL = o1 ? (rdeg ? aL : NSP[ea + 1]) : aL;
+    double se;
+    int ke;
+    if (!PODD) {
+      se = o1 ? aL + bL : aL;
+      ke = o1 ? 1 : 0;
+    } else {
+      const double aR = x.has_right ? NSN[ea] : aL;
+      const double bR = o1 ? (x.has_right ? (rdeg ? aR : NSN[ea + 1]) : bL) : aR;
+      se = aL + aR;
+      if (o1) {
+        se += bL;
+        se += bR;
+      }
+      ke = o1 ? 2 : 1;
+    }
+    double sn = __shfl_down_sync(0xffffffffu, se, 1);
+    if (x.right_degen) sn = se;
+    const double so = se + sn;
+    const double sc_e = ke == 1 ? 0.5 : 0.25;
+    const double sc_o = ke == 0 ? 0.5 : (ke == 1 ? 0.25 : 0.125);
+    const T tE = to_t<T>(rawE - se * sc_e);
+    const T tO = to_t<T>(rawO - so * sc_o);
+    const double cE = (ke == 0 || !x.valid) ? 0.0 : double(tE);
+    const double cO = x.has_odd ? double(tO) : 0.0;
+    const bool own_row = FULL ? (jr >= 2 && jr < 2 * TI1 + 2) : (j1 >= x.jlo_own && j1 < x.jhi_own);
+    if (x.own && own_row) {
+      if (o1) {
+        T* sr = x.so + int64_t(ea) * x.n2l;
+        sr[0] = tE;
+        if (x.has_odd) sr[x.m2] = tO;
+      } else {
+        T* sr = x.se + int64_t(ea) * x.st_e;
+        if (ke == 0)
+          x.cpe[int64_t(ea) * x.m2] = rr[0];
+        else
+          sr[0] = tE;
+        if (x.has_odd) sr[x.oofs] = tO;
+      }
+    }
+    const double h = strip_restrict(cE, cO, x.c, x.m2);
+#pragma unroll
+    for (int k = -2; k <= 2; ++k) {
+      if (((jr - 2 - k) & 1) != 0) continue;
+      const int ir = (jr - 2 - k) / 2;
+      if (ir < 0 || ir >= TI1) continue;
+      if (FULL)
+        Q[ir] += (k == 0 ? kW5_6 : ((k & 1) ? 0.5 : kW12)) * h;
+      else if (ir < x.TR)
+        Q[ir] += load_w(k, x.b0 + ir, x.m1) * h;
+    }
+  }
+}
+
+// Decompose plane pass: one CTA per (axis-0 chunk, axis-1 tile) unit; the
+// unit's fine planes stream through a 3-deep TMA ring.
 template <typename T, int TI1>
-__global__ void __launch_bounds__(kPlaneMaxThreads)
+__global__ void __launch_bounds__(kPlaneMaxThreads, 2)
     k_f3_dec_plane(const T* __restrict__ blk, T* __restrict__ shell, T* __restrict__ coarse, double* __restrict__ G,
                    const double* __restrict__ w2g, const double* __restrict__ id2g, int* __restrict__ counter,
                    const F3Geom g) {
@@ -357,18 +513,16 @@ __global__ void __launch_bounds__(kPlaneMaxThreads)
   const size_t rawb = SM::raw_bytes(g.n2);
   unsigned char* raw = smem;
   double* acc = reinterpret_cast<double*>(smem + 3 * rawb);
-  double* tw2 = acc + 3 * SM::acc_elems(g.m2);
+  double* tw2 = acc + 2 * SM::acc_elems(g.m2);
   double* tid2 = tw2 + m2;
   double* scan = tid2 + m2;
   int64_t* rowoff = reinterpret_cast<int64_t*>(scan + 64);
   uint64_t* bars = reinterpret_cast<uint64_t*>(rowoff + 2 * RMAX);
-  int* unit_slot = reinterpret_cast<int*>(bars + 4);
+  (void)counter;
 
   const int tid = threadIdx.x, nt = blockDim.x;
   const StripLane S = strip_lane(m2);
   const int c = S.c;
-  const bool has_odd = S.valid && 2 * c + 1 < n2;
-  const bool right_degen = 2 * c + 2 >= n2;  // odd node's right corner column missing
   for (int i = tid; i < m2; i += nt) {
     tw2[i] = w2g[i];
     tid2[i] = id2g[i];
@@ -380,139 +534,141 @@ __global__ void __launch_bounds__(kPlaneMaxThreads)
   __syncthreads();
   uint32_t phase[3] = {0, 0, 0};
 
-  for (;;) {
-    if (tid == 0) *unit_slot = atomicAdd(counter, 1);
+  const UnitRange ur = unit_range(g, int(blockIdx.x));
+  const int R = int(ur.rhi - ur.rlo + 1);
+  DecRows<T> x;
+  x.n2 = n2;
+  x.m2 = m2;
+  x.n1 = n1;
+  x.m1 = m1;
+  x.rlo = int(ur.rlo);
+  x.rhi = int(ur.rhi);
+  x.jbase = int(2 * ur.b0) - 2;
+  x.b0 = int(ur.b0);
+  x.TR = int(ur.b1 - ur.b0);
+  x.jlo_own = int(2 * ur.b0);
+  x.jhi_own = int(min(2 * ur.b1, g.n1));
+  x.valid = S.valid;
+  x.has_odd = S.valid && 2 * c + 1 < n2;
+  x.right_degen = 2 * c + 2 >= n2;
+  x.c = c;
+  x.n2l = g.n2;
+  const bool full = ur.b0 >= 1 && 2 * ur.b1 <= g.n1 - 1;
+  const int cc = S.valid ? c : 0;  // clamp halo columns for addressing
+  auto tile_src = [&](int64_t p) { return blk + (p * g.n1 + ur.rlo) * g.n2; };
+  auto issue = [&](int64_t p) {
+    if (tid == 0) {
+      const char* src;
+      uint32_t bytes;
+      int ld;
+      bulk_span<T>(tile_src(p), 0, int64_t(R) * n2, &src, &bytes, &ld);
+      fence_proxy_async();
+      mbar_expect_tx(&bars[p % 3], bytes);
+      bulk_g2s(raw + size_t(p % 3) * rawb, src, bytes, &bars[p % 3]);
+    }
+  };
+  auto tile = [&](int64_t p) {
+    return reinterpret_cast<const T*>(raw + size_t(p % 3) * rawb) +
+           (reinterpret_cast<uintptr_t>(tile_src(p)) & 15) / sizeof(T);
+  };
+  double NSP[NE], NSN[NE];  // fp64 nodal values (own column) of the left / right even plane
+  auto load_ns = [&](int64_t q, double* ns) {
+    const T* rq = tile(q) + 2 * cc;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const int j1 = x.jbase + 2 * e;
+      ns[e] = (S.valid && j1 >= x.rlo && j1 <= x.rhi) ? double(rq[(j1 - x.rlo) * n2]) : 0.0;
+    }
+  };
+  issue(ur.plo);
+  if (ur.plo + 1 <= ur.phi) issue(ur.plo + 1);
+  int64_t ready = ur.plo - 1;
+  L0Planes<TI1> A;
+#pragma unroll
+  for (int ir = 0; ir < TI1; ++ir) A.prev[ir] = A.cur[ir] = A.next[ir] = 0.0;
+  for (int64_t p = ur.plo; p <= ur.phi; ++p) {
+    const bool p_odd = p & 1;
+    x.has_right = p_odd && (p + 1 <= g.n0 - 1);
+    const int64_t need = x.has_right ? p + 1 : p;
+    while (ready < need) {
+      ++ready;
+      mbar_wait(&bars[ready % 3], phase[ready % 3]);
+      phase[ready % 3] ^= 1;
+    }
+    if (p == ur.plo) load_ns(p, NSP);
+    if (x.has_right) load_ns(p + 1, NSN);
     __syncthreads();
-    const int u = *unit_slot;
-    if (u >= g.units) break;
-    const UnitRange ur = unit_range(g, u);
-    const int R = int(ur.rhi - ur.rlo + 1), rlo = int(ur.rlo), rhi = int(ur.rhi);
-    const int jbase = int(2 * ur.b0) - 2;  // fine row of tile slot jr = 0
-    const int TR = int(ur.b1 - ur.b0), b0 = int(ur.b0);
-    const int jlo_own = int(2 * ur.b0), jhi_own = int(min(2 * ur.b1, g.n1));
-    auto tile_src = [&](int64_t p) { return blk + (p * g.n1 + ur.rlo) * g.n2; };
-    auto issue = [&](int64_t p) {
-      if (tid == 0) {
-        const char* src;
-        uint32_t bytes;
-        int ld;
-        bulk_span<T>(tile_src(p), 0, int64_t(R) * n2, &src, &bytes, &ld);
-        fence_proxy_async();
-        mbar_expect_tx(&bars[p % 3], bytes);
-        bulk_g2s(raw + size_t(p % 3) * rawb, src, bytes, &bars[p % 3]);
-      }
-    };
-    auto tile = [&](int64_t p) {
-      return reinterpret_cast<const T*>(raw + size_t(p % 3) * rawb) +
-             (reinterpret_cast<uintptr_t>(tile_src(p)) & 15) / sizeof(T);
-    };
-    double NSP[NE], NSN[NE];  // fp64 nodal values (own column) of the left / right even plane
-    auto load_ns = [&](int64_t q, double* ns) {
-      const T* rq = tile(q);
+    if (p + 2 <= ur.phi) issue(p + 2);  // slot of plane p-1 is free
+    const int64_t r0 = reord(p, g.m0);
+    const int e0 = x.jbase >> 1;  // even tile row 0 <-> coarse row e0
+    x.st_e = p_odd ? g.n2 : g.n2 - g.m2;
+    x.oofs = p_odd ? m2 : 0;
+    x.se = shell + (shell_row_start(g, r0, e0 + 1) - x.st_e) + cc;
+    x.so = shell + (shell_row_start(g, r0, g.m1 + e0 + 1) - g.n2) + cc;
+    x.cpe = coarse + ((p >> 1) * g.m1 + e0) * g.m2 + cc;
+    x.own = S.owned && p >= 2 * ur.a0 && p < 2 * ur.a1;
+    x.rp = tile(p) + 2 * cc;
+    double Q[TI1];
 #pragma unroll
-      for (int e = 0; e < NE; ++e) {
-        const int j1 = jbase + 2 * e;
-        ns[e] = (S.valid && j1 >= rlo && j1 <= rhi) ? double(rq[(j1 - rlo) * n2 + 2 * c]) : 0.0;
-      }
-    };
-    issue(ur.plo);
-    if (ur.plo + 1 <= ur.phi) issue(ur.plo + 1);
-    int64_t ready = ur.plo - 1;
-    for (int64_t p = ur.plo; p <= ur.phi; ++p) {
-      const bool p_odd = p & 1;
-      const bool has_right = p_odd && (p + 1 <= g.n0 - 1);
-      const int64_t need = has_right ? p + 1 : p;
-      while (ready < need) {
-        ++ready;
-        mbar_wait(&bars[ready % 3], phase[ready % 3]);
-        phase[ready % 3] ^= 1;
-      }
-      if (p == ur.plo) load_ns(p, NSP);
-      if (has_right) load_ns(p + 1, NSN);
-      const bool own_p = p >= 2 * ur.a0 && p < 2 * ur.a1;
-      const int64_t r0 = reord(p, g.m0);
-      if (tid < R) rowoff[tid] = shell_row_start(g, r0, reord(ur.rlo + tid, g.m1));
-      __syncthreads();
-      if (p + 2 <= ur.phi) issue(p + 2);  // slot of plane p-1 is free
-      const T* rp = tile(p);
-      T* cpl = coarse + ((p >> 1) * g.m1) * g.m2 + c;
-      double Q[TI1];
+    for (int ir = 0; ir < TI1; ++ir) Q[ir] = 0.0;
+    if (p_odd) {
+      if (full) dec_rows<T, TI1, true, true>(x, NSP, NSN, Q);
+      else dec_rows<T, TI1, true, false>(x, NSP, NSN, Q);
+    } else {
+      if (full) dec_rows<T, TI1, false, true>(x, NSP, NSN, Q);
+      else dec_rows<T, TI1, false, false>(x, NSP, NSN, Q);
+    }
+    if (p_odd && x.has_right) {
 #pragma unroll
-      for (int ir = 0; ir < TI1; ++ir) Q[ir] = 0.0;
+      for (int e = 0; e < NE; ++e) NSP[e] = NSN[e];  // plane p+1 becomes the left even plane
+    }
+    l0_plane<TI1>(g, ur, S, p, Q, A, acc, tw2, tid2, G);
+  }
+}
+
+// Rows of one fine plane (recompose plane pass): component from the shell
+// slot (coefficients; 0 on nodal points), axis-2 restriction through
+// shuffles, axis-1 restriction into Q.  FULL as in dec_rows.
+template <typename T, int TI1, bool PODD, bool FULL>
+__device__ __forceinline__ void rec_rows(const T* ev, const T* od, int64_t st_e, int n2, int m2, int jbase, int rlo,
+                                         int rhi, int b0, int TR, int m1, int c, bool valid, bool has_odd, double* Q) {
+  constexpr int RMAX = 2 * TI1 + 3;
 #pragma unroll
-      for (int jr = 0; jr < RMAX; ++jr) {
-        const int j1 = jbase + jr;
-        if (j1 < rlo || j1 > rhi) continue;  // uniform
-        constexpr int dummy = 0;
-        (void)dummy;
-        const bool o1 = jr & 1;  // jbase is even
-        const int ea = o1 ? (jr - 1) >> 1 : jr >> 1;
-        const int eb = o1 ? ((j1 + 1 < n1) ? ea + 1 : ea) : ea;
-        const T* rr = rp + (j1 - rlo) * n2 + 2 * c;
-        const double rawE = S.valid ? double(rr[0]) : 0.0;
-        const double rawO = has_odd ? double(rr[1]) : 0.0;
-        // own-column corner sum of the even node (corner order as the reference)
-        const double aL = NSP[o1 ? (jr - 1) >> 1 : jr >> 1];
-        const double bL = o1 ? ((j1 + 1 < n1) ? NSP[(jr + 1) >> 1] : aL) : aL;
-        double se;
-        int ke;
-        if (!p_odd) {
-          se = o1 ? aL + bL : aL;
-          ke = o1 ? 1 : 0;
-        } else {
-          const double aR = has_right ? NSN[o1 ? (jr - 1) >> 1 : jr >> 1] : aL;
-          const double bR = o1 ? (has_right ? ((j1 + 1 < n1) ? NSN[(jr + 1) >> 1] : aR) : bL) : aR;
-          se = aL + aR;
-          if (o1) {
-            se += bL;
-            se += bR;
-          }
-          ke = o1 ? 2 : 1;
-        }
-        (void)ea;
-        (void)eb;
-        double sn = __shfl_down_sync(0xffffffffu, se, 1);
-        if (right_degen) sn = se;
-        const double so = se + sn;
-        const double sc_e = ke == 0 ? 0.0 : (ke == 1 ? 0.5 : 0.25);
-        const double sc_o = ke == 0 ? 0.5 : (ke == 1 ? 0.25 : 0.125);
-        const double cE = (ke == 0 || !S.valid) ? 0.0 : double(to_t<T>(rawE - se * sc_e));
-        const double cO = has_odd ? double(to_t<T>(rawO - so * sc_o)) : 0.0;
-        if (S.owned && own_p && j1 >= jlo_own && j1 < jhi_own) {
-          T* srow = shell + rowoff[j1 - rlo];
-          const bool inside = ke == 0;
-          if (inside)
-            cpl[int64_t(j1 >> 1) * g.m2] = rr[0];
-          else
-            srow[c] = to_t<T>(cE);
-          if (has_odd) srow[(inside ? 0 : m2) + c] = to_t<T>(cO);
-        }
-        const double h = strip_restrict(cE, cO, c, m2);
-        // axis-1 restriction: fine row j1 = 2 i1 + k feeds coarse rows i1 = b0 + ir
+  for (int jr = 0; jr < RMAX; ++jr) {
+    const int j1 = jbase + jr;
+    if (!FULL && (j1 < rlo || j1 > rhi)) continue;  // uniform
+    const bool o1 = jr & 1;
+    const int ea = jr >> 1;
+    double cE, cO;
+    if (o1) {
+      const T* r = od + int64_t(ea) * n2;
+      cE = valid ? double(r[0]) : 0.0;
+      cO = has_odd ? double(r[m2]) : 0.0;
+    } else {
+      const T* r = ev + int64_t(ea) * st_e;
+      cE = (PODD && valid) ? double(r[0]) : 0.0;
+      cO = has_odd ? double(r[PODD ? m2 : 0]) : 0.0;
+    }
+    const double h = strip_restrict(cE, cO, c, m2);
 #pragma unroll
-        for (int k = -2; k <= 2; ++k) {
-          if (((jr - 2 - k) & 1) != 0) continue;
-          const int ir = (jr - 2 - k) / 2;
-          if (ir < 0 || ir >= TI1) continue;
-          if (ir < TR) Q[ir] += load_w(k, b0 + ir, m1) * h;
-        }
-      }
-      if (p_odd && has_right) {
-#pragma unroll
-        for (int e = 0; e < NE; ++e) NSP[e] = NSN[e];  // plane p+1 becomes the left even plane
-      }
-      plane_finish<TI1>(g, ur, S, p, Q, acc, tw2, tid2, scan, G);
-      __syncthreads();
+    for (int k = -2; k <= 2; ++k) {
+      if (((jr - 2 - k) & 1) != 0) continue;
+      const int ir = (jr - 2 - k) / 2;
+      if (ir < 0 || ir >= TI1) continue;
+      if (FULL)
+        Q[ir] += (k == 0 ? kW5_6 : ((k & 1) ? 0.5 : kW12)) * h;
+      else if (ir < TR)
+        Q[ir] += load_w(k, b0 + ir, m1) * h;
     }
   }
 }
 
 // Recompose plane pass: the same load-vector accumulation with the
-// component read from the level's shell (coefficients; 0 on nodal points).
-// Per fine plane the tile's shell rows form two contiguous runs (even fine
-// rows, odd fine rows), fetched with two bulk copies into one ring slot.
+// component read from the level's shell.  Per fine plane the tile's shell
+// rows form two contiguous runs (even fine rows, odd fine rows), fetched
+// with two bulk copies into one ring slot.
 template <typename T, int TI1>
-__global__ void __launch_bounds__(kPlaneMaxThreads)
+__global__ void __launch_bounds__(kPlaneMaxThreads, 2)
     k_f3_rec_plane(const T* __restrict__ shell, double* __restrict__ G, const double* __restrict__ w2g,
                    const double* __restrict__ id2g, int* __restrict__ counter, const F3Geom g) {
   using SM = PlaneSmem<T, TI1>;
@@ -522,16 +678,17 @@ __global__ void __launch_bounds__(kPlaneMaxThreads)
   const size_t rawb = SM::raw_bytes(g.n2);
   unsigned char* raw = smem;
   double* acc = reinterpret_cast<double*>(smem + 3 * rawb);
-  double* tw2 = acc + 3 * SM::acc_elems(g.m2);
+  double* tw2 = acc + 2 * SM::acc_elems(g.m2);
   double* tid2 = tw2 + m2;
   double* scan = tid2 + m2;
-  int64_t* rowoff = reinterpret_cast<int64_t*>(scan + 64);  // element offset of each tile row in the slot
+  int64_t* rowoff = reinterpret_cast<int64_t*>(scan + 64);
   uint64_t* bars = reinterpret_cast<uint64_t*>(rowoff + 2 * RMAX);
-  int* unit_slot = reinterpret_cast<int*>(bars + 4);
+  (void)counter;
 
   const int tid = threadIdx.x, nt = blockDim.x;
   const StripLane S = strip_lane(m2);
   const int c = S.c;
+  const int cc = S.valid ? c : 0;
   const bool has_odd = S.valid && 2 * c + 1 < n2;
   for (int i = tid; i < m2; i += nt) {
     tw2[i] = w2g[i];
@@ -544,93 +701,79 @@ __global__ void __launch_bounds__(kPlaneMaxThreads)
   __syncthreads();
   uint32_t phase[3] = {0, 0, 0};
 
-  for (;;) {
-    if (tid == 0) *unit_slot = atomicAdd(counter, 1);
-    __syncthreads();
-    const int u = *unit_slot;
-    if (u >= g.units) break;
-    const UnitRange ur = unit_range(g, u);
-    const int R = int(ur.rhi - ur.rlo + 1), rlo = int(ur.rlo), rhi = int(ur.rhi);
-    const int jbase = int(2 * ur.b0) - 2;
-    const int TR = int(ur.b1 - ur.b0), b0 = int(ur.b0);
-    const int64_t e_lo = ur.rlo >> 1, e_hi = ur.rhi >> 1;
-    const int64_t o_lo = (ur.rlo + 1) >> 1, o_hi = (ur.rhi - 1) >> 1;
-    struct Runs {
-      int64_t se, le, so, lo;
-    };
-    auto runs = [&](int64_t p) {
-      const int64_t r0 = reord(p, g.m0);
-      Runs x;
-      x.se = shell_row_start(g, r0, e_lo);
-      x.le = shell_row_start(g, r0, e_hi + 1) - x.se;
-      x.so = o_hi >= o_lo ? shell_row_start(g, r0, g.m1 + o_lo) : 0;
-      x.lo = o_hi >= o_lo ? shell_row_start(g, r0, g.m1 + o_hi + 1) - x.so : 0;
-      return x;
-    };
-    auto odd_slot_off = [&](const Runs& x) {
-      const uintptr_t a0 = reinterpret_cast<uintptr_t>(shell + x.se) & ~uintptr_t(15);
-      const uintptr_t a1 = (reinterpret_cast<uintptr_t>(shell + x.se + x.le) + 15) & ~uintptr_t(15);
-      return (uint32_t(a1 - a0) + 127u) & ~127u;
-    };
-    auto issue = [&](int64_t p) {
-      if (tid == 0) {
-        const Runs x = runs(p);
-        const char *src0, *src1 = nullptr;
-        uint32_t b0b, b1b = 0;
-        int ld;
-        bulk_span<T>(shell, x.se, x.le, &src0, &b0b, &ld);
-        if (x.lo > 0) bulk_span<T>(shell, x.so, x.lo, &src1, &b1b, &ld);
-        unsigned char* dst = raw + size_t(p % 3) * rawb;
-        fence_proxy_async();
-        mbar_expect_tx(&bars[p % 3], b0b + b1b);
-        bulk_g2s(dst, src0, b0b, &bars[p % 3]);
-        if (x.lo > 0) bulk_g2s(dst + odd_slot_off(x), src1, b1b, &bars[p % 3]);
-      }
-    };
-    issue(ur.plo);
-    if (ur.plo + 1 <= ur.phi) issue(ur.plo + 1);
-    for (int64_t p = ur.plo; p <= ur.phi; ++p) {
-      mbar_wait(&bars[p % 3], phase[p % 3]);
-      phase[p % 3] ^= 1;
-      const int64_t r0 = reord(p, g.m0);
-      if (tid < R) {
-        const Runs x = runs(p);
-        const int64_t j1 = ur.rlo + tid;
-        const int64_t rs = shell_row_start(g, r0, reord(j1, g.m1));
-        if (j1 & 1)
-          rowoff[tid] = int64_t(odd_slot_off(x) / sizeof(T)) +
-                        int64_t((reinterpret_cast<uintptr_t>(shell + x.so) & 15) / sizeof(T)) + (rs - x.so);
-        else
-          rowoff[tid] = int64_t((reinterpret_cast<uintptr_t>(shell + x.se) & 15) / sizeof(T)) + (rs - x.se);
-      }
-      __syncthreads();
-      if (p + 2 <= ur.phi) issue(p + 2);
-      const T* slot = reinterpret_cast<const T*>(raw + size_t(p % 3) * rawb);
-      const bool p_odd = p & 1;
-      double Q[TI1];
-#pragma unroll
-      for (int ir = 0; ir < TI1; ++ir) Q[ir] = 0.0;
-#pragma unroll
-      for (int jr = 0; jr < RMAX; ++jr) {
-        const int j1 = jbase + jr;
-        if (j1 < rlo || j1 > rhi) continue;
-        const bool o1 = jr & 1;
-        const bool inside = !p_odd && !o1;
-        const T* row = slot + rowoff[j1 - rlo];
-        const double cE = (S.valid && !inside) ? double(row[c]) : 0.0;
-        const double cO = has_odd ? double(row[(inside ? 0 : m2) + c]) : 0.0;
-        const double h = strip_restrict(cE, cO, c, m2);
-#pragma unroll
-        for (int k = -2; k <= 2; ++k) {
-          if (((jr - 2 - k) & 1) != 0) continue;
-          const int ir = (jr - 2 - k) / 2;
-          if (ir < 0 || ir >= TI1) continue;
-          if (ir < TR) Q[ir] += load_w(k, b0 + ir, m1) * h;
-        }
-      }
-      plane_finish<TI1>(g, ur, S, p, Q, acc, tw2, tid2, scan, G);
-      __syncthreads();
+  const UnitRange ur = unit_range(g, int(blockIdx.x));
+  const int rlo = int(ur.rlo), rhi = int(ur.rhi);
+  const int jbase = int(2 * ur.b0) - 2;
+  const int TR = int(ur.b1 - ur.b0), b0 = int(ur.b0);
+  const bool full = ur.b0 >= 1 && 2 * ur.b1 <= g.n1 - 1;
+  // even fine rows: r1 in [rlo/2, rhi/2]; odd: r1 = m1 + [(rlo+1)/2, (rhi-1)/2]
+  const int64_t e_lo = ur.rlo >> 1, e_hi = ur.rhi >> 1;
+  const int64_t o_lo = (ur.rlo + 1) >> 1, o_hi = (ur.rhi - 1) >> 1;
+  struct Runs {
+    int64_t se, le, so, lo;
+  };
+  auto runs = [&](int64_t p) {
+    const int64_t r0 = reord(p, g.m0);
+    Runs x;
+    x.se = shell_row_start(g, r0, e_lo);
+    x.le = shell_row_start(g, r0, e_hi + 1) - x.se;
+    x.so = o_hi >= o_lo ? shell_row_start(g, r0, g.m1 + o_lo) : 0;
+    x.lo = o_hi >= o_lo ? shell_row_start(g, r0, g.m1 + o_hi + 1) - x.so : 0;
+    return x;
+  };
+  auto odd_slot_off = [&](const Runs& x) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(shell + x.se) & ~uintptr_t(15);
+    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(shell + x.se + x.le) + 15) & ~uintptr_t(15);
+    return (uint32_t(a1 - a0) + 127u) & ~127u;
+  };
+  auto issue = [&](int64_t p) {
+    if (tid == 0) {
+      const Runs x = runs(p);
+      const char *src0, *src1 = nullptr;
+      uint32_t b0b, b1b = 0;
+      int ld;
+      bulk_span<T>(shell, x.se, x.le, &src0, &b0b, &ld);
+      if (x.lo > 0) bulk_span<T>(shell, x.so, x.lo, &src1, &b1b, &ld);
+      unsigned char* dst = raw + size_t(p % 3) * rawb;
+      fence_proxy_async();
+      mbar_expect_tx(&bars[p % 3], b0b + b1b);
+      bulk_g2s(dst, src0, b0b, &bars[p % 3]);
+      if (x.lo > 0) bulk_g2s(dst + odd_slot_off(x), src1, b1b, &bars[p % 3]);
     }
+  };
+  issue(ur.plo);
+  if (ur.plo + 1 <= ur.phi) issue(ur.plo + 1);
+  L0Planes<TI1> A;
+#pragma unroll
+  for (int ir = 0; ir < TI1; ++ir) A.prev[ir] = A.cur[ir] = A.next[ir] = 0.0;
+  for (int64_t p = ur.plo; p <= ur.phi; ++p) {
+    mbar_wait(&bars[p % 3], phase[p % 3]);
+    phase[p % 3] ^= 1;
+    __syncthreads();
+    if (p + 2 <= ur.phi) issue(p + 2);
+    const bool p_odd = p & 1;
+    const Runs x = runs(p);
+    const unsigned char* slot = raw + size_t(p % 3) * rawb;
+    // slot positions of even tile row e = 0 (fine row jbase) and odd e = 0 (jbase + 1)
+    const int64_t st_e = p_odd ? g.n2 : g.n2 - g.m2;
+    const T* evrun = reinterpret_cast<const T*>(slot) + (reinterpret_cast<uintptr_t>(shell + x.se) & 15) / sizeof(T);
+    const T* odrun = reinterpret_cast<const T*>(slot + odd_slot_off(x)) +
+                     (reinterpret_cast<uintptr_t>(shell + x.so) & 15) / sizeof(T);
+    // even run starts at fine row 2 e_lo = rlo (rlo is even); jbase may be rlo - 2
+    const T* ev = evrun + (int64_t((jbase - rlo) >> 1)) * st_e + cc;
+    // odd run starts at fine row 2 o_lo + 1; tile odd row e = 0 is fine row jbase + 1
+    const T* od = odrun + (int64_t(((jbase + 1) - (2 * o_lo + 1)) >> 1)) * g.n2 + cc;
+    double Q[TI1];
+#pragma unroll
+    for (int ir = 0; ir < TI1; ++ir) Q[ir] = 0.0;
+    if (p_odd) {
+      if (full) rec_rows<T, TI1, true, true>(ev, od, st_e, n2, m2, jbase, rlo, rhi, b0, TR, m1, c, S.valid, has_odd, Q);
+      else rec_rows<T, TI1, true, false>(ev, od, st_e, n2, m2, jbase, rlo, rhi, b0, TR, m1, c, S.valid, has_odd, Q);
+    } else {
+      if (full) rec_rows<T, TI1, false, true>(ev, od, st_e, n2, m2, jbase, rlo, rhi, b0, TR, m1, c, S.valid, has_odd, Q);
+      else rec_rows<T, TI1, false, false>(ev, od, st_e, n2, m2, jbase, rlo, rhi, b0, TR, m1, c, S.valid, has_odd, Q);
+    }
+    l0_plane<TI1>(g, ur, S, p, Q, A, acc, tw2, tid2, G);
   }
 }
 
@@ -640,45 +783,27 @@ __global__ void __launch_bounds__(kPlaneMaxThreads)
 // corrected coarse block and the shell.  blockIdx.y = fine plane, blockIdx.x
 // = group of TRI fine rows; strip lanes as the plane passes, the coarse
 // values of the block's rows kept in registers.
-template <typename T, int TRI>
-__global__ void __launch_bounds__(kPlaneMaxThreads)
-    k_f3_rec_interp(const T* __restrict__ shell, const T* __restrict__ coarse, T* __restrict__ fine, const F3Geom g) {
-  constexpr int NE = TRI / 2 + 1;
-  const int m2 = int(g.m2), n2 = int(g.n2), n1 = int(g.n1), m1 = int(g.m1);
-  const StripLane S = strip_lane(m2);
-  const int c = S.c;
-  const bool has_odd = S.valid && 2 * c + 1 < n2;
-  const bool right_degen = 2 * c + 2 >= n2;
-  const int64_t p = blockIdx.y;
-  const int j1lo = int(blockIdx.x) * TRI;
-  const bool p_odd = p & 1;
-  const int64_t cp = p >> 1;
-  const int64_t cpr = p_odd ? ((p + 1 < g.n0) ? cp + 1 : cp) : cp;
-  double CL[NE], CR[NE];
-#pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    const int row = j1lo / 2 + e;
-    const bool ok = S.valid && row < m1;
-    CL[e] = ok ? double(__ldg(coarse + (cp * g.m1 + row) * g.m2 + c)) : 0.0;
-    CR[e] = (ok && p_odd) ? double(__ldg(coarse + (cpr * g.m1 + row) * g.m2 + c)) : CL[e];
-  }
-  const int64_t r0 = reord(p, g.m0);
+template <typename T, int TRI, bool PODD, bool FULL>
+__device__ __forceinline__ void interp_rows(const T* __restrict__ se_p, const T* __restrict__ so_p, int64_t st_e,
+                                            int oofs, T* __restrict__ out, const double* CL, const double* CR, int j1lo,
+                                            int n1, int64_t n2l, int m2, bool owned, bool has_odd, bool right_degen) {
 #pragma unroll
   for (int jr = 0; jr < TRI; ++jr) {
     const int j1 = j1lo + jr;
-    if (j1 >= n1) break;  // uniform
+    if (!FULL && j1 >= n1) break;  // uniform
     const bool o1 = jr & 1;
     const int ea = jr >> 1;
+    const bool rdeg = !FULL && o1 && (j1 + 1 >= n1);
     const double aL = CL[ea];
-    const double bL = o1 ? ((j1 + 1 < n1) ? CL[ea + 1] : aL) : aL;
+    const double bL = o1 ? (rdeg ? aL : CL[ea + 1]) : aL;
     double se;
     int ke;
-    if (!p_odd) {
+    if (!PODD) {
       se = o1 ? aL + bL : aL;
       ke = o1 ? 1 : 0;
     } else {
       const double aR = CR[ea];
-      const double bR = o1 ? ((j1 + 1 < n1) ? CR[ea + 1] : aR) : aR;
+      const double bR = o1 ? (rdeg ? aR : CR[ea + 1]) : aR;
       se = aL + aR;
       if (o1) {
         se += bL;
@@ -689,14 +814,56 @@ __global__ void __launch_bounds__(kPlaneMaxThreads)
     double sn = __shfl_down_sync(0xffffffffu, se, 1);
     if (right_degen) sn = se;
     const double so = se + sn;
-    if (!S.owned) continue;
-    const int64_t rs = shell_row_start(g, r0, reord(j1, g.m1));
-    const bool inside = ke == 0;
-    T* out = fine + (p * g.n1 + j1) * g.n2 + 2 * c;
-    const double sc_e = ke == 1 ? 0.5 : 0.25;
-    const double sc_o = ke == 0 ? 0.5 : (ke == 1 ? 0.25 : 0.125);
-    out[0] = inside ? to_t<T>(aL) : to_t<T>(double(shell[rs + c]) + se * sc_e);
-    if (has_odd) out[1] = to_t<T>(double(shell[rs + (inside ? 0 : m2) + c]) + so * sc_o);
+    if (owned) {
+      const double sc_e = ke == 1 ? 0.5 : 0.25;
+      const double sc_o = ke == 0 ? 0.5 : (ke == 1 ? 0.25 : 0.125);
+      const T* sr = o1 ? so_p + int64_t(ea) * n2l : se_p + int64_t(ea) * st_e;
+      T* o = out + int64_t(jr) * n2l;
+      o[0] = ke == 0 ? to_t<T>(aL) : to_t<T>(double(sr[0]) + se * sc_e);
+      if (has_odd) o[1] = to_t<T>(double(sr[o1 ? m2 : oofs]) + so * sc_o);
+    }
+  }
+}
+
+template <typename T, int TRI>
+__global__ void __launch_bounds__(kPlaneMaxThreads)
+    k_f3_rec_interp(const T* __restrict__ shell, const T* __restrict__ coarse, T* __restrict__ fine, const F3Geom g) {
+  constexpr int NE = TRI / 2 + 1;
+  const int m2 = int(g.m2), n2 = int(g.n2), n1 = int(g.n1), m1 = int(g.m1);
+  const StripLane S = strip_lane(m2);
+  const int c = S.c;
+  const int cc = S.valid ? c : 0;
+  const bool has_odd = S.valid && 2 * c + 1 < n2;
+  const bool right_degen = 2 * c + 2 >= n2;
+  const int p = int(blockIdx.y);
+  const int j1lo = int(blockIdx.x) * TRI;  // even
+  const bool p_odd = p & 1;
+  const int cp = p >> 1;
+  const int cpr = p_odd ? ((p + 1 < g.n0) ? cp + 1 : cp) : cp;
+  const int64_t r0 = reord(p, g.m0);
+  const int e0 = j1lo >> 1;
+  const int64_t st_e = p_odd ? g.n2 : g.n2 - g.m2;
+  // shell slots of even tile row 0 (fine row j1lo) and odd tile row 0 (j1lo + 1)
+  const T* se_p = shell + shell_row_start(g, r0, e0) + cc;
+  const T* so_p = shell + shell_row_start(g, r0, g.m1 + e0) + cc;
+  double CL[NE], CR[NE];
+  const T* cLp = coarse + (int64_t(cp) * g.m1 + e0) * g.m2 + cc;
+  const T* cRp = coarse + (int64_t(cpr) * g.m1 + e0) * g.m2 + cc;
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const bool ok = S.valid && e0 + e < m1;
+    CL[e] = ok ? double(__ldg(cLp + int64_t(e) * m2)) : 0.0;
+    CR[e] = p_odd ? (ok ? double(__ldg(cRp + int64_t(e) * m2)) : 0.0) : CL[e];
+  }
+  T* out = fine + (int64_t(p) * g.n1 + j1lo) * g.n2 + 2 * cc;
+  const bool full = j1lo + TRI + 1 <= n1 - 1;
+  const int oofs = p_odd ? m2 : 0;
+  if (p_odd) {
+    if (full) interp_rows<T, TRI, true, true>(se_p, so_p, st_e, oofs, out, CL, CR, j1lo, n1, g.n2, m2, S.owned, has_odd, right_degen);
+    else interp_rows<T, TRI, true, false>(se_p, so_p, st_e, oofs, out, CL, CR, j1lo, n1, g.n2, m2, S.owned, has_odd, right_degen);
+  } else {
+    if (full) interp_rows<T, TRI, false, true>(se_p, so_p, st_e, oofs, out, CL, CR, j1lo, n1, g.n2, m2, S.owned, has_odd, right_degen);
+    else interp_rows<T, TRI, false, false>(se_p, so_p, st_e, oofs, out, CL, CR, j1lo, n1, g.n2, m2, S.owned, has_odd, right_degen);
   }
 }
 
@@ -879,7 +1046,7 @@ Fused3DPlan fused3d_plan(const LevelGeom& lg, int esize) {
   if ((g.m2 + 29) / 30 * 32 > kPlaneMaxThreads) return fp;
   // small levels stay on the general kernels (launch-latency bound either way)
   {
-    int64_t min_elems = int64_t(1) << 20;
+    int64_t min_elems = int64_t(1) << 15;
     if (const char* env = std::getenv("MGRX_FUSED_MIN_ELEMS")) min_elems = std::atoll(env);
     if (int64_t(g.n0) * g.n1 * g.n2 < min_elems) return fp;
   }
@@ -895,17 +1062,20 @@ Fused3DPlan fused3d_plan(const LevelGeom& lg, int esize) {
   const bool ok = esize == 4 ? pick_tile<float>(g, size_t(optin), size_t(per_sm))
                              : pick_tile<double>(g, size_t(optin), size_t(per_sm));
   if (!ok) return fp;
-  g.ntile1 = int((g.m1 + g.tile_rows - 1) / g.tile_rows);
   g.threads = int((g.m2 + 29) / 30) * 32;
   const int ctas = nsm * g.ctas_per_sm;
-  // axis-0 chunks: about 4 units per CTA so dynamic scheduling evens out
-  const int64_t want_units = int64_t(ctas) * 4;
-  int64_t nchunk = std::max<int64_t>(1, (want_units + g.ntile1 - 1) / g.ntile1);
-  int64_t chunk = std::max<int64_t>(4, (g.m0 + nchunk - 1) / nchunk);
-  nchunk = (g.m0 + chunk - 1) / chunk;
+  // Small levels are latency bound (a unit streams its planes serially):
+  // shrink the row tile until single-plane-pair units give two waves.
+  while (g.tile_rows > 2 && ((g.m1 + g.tile_rows - 1) / g.tile_rows) * g.m0 < 2 * int64_t(ctas))
+    g.tile_rows = g.tile_rows == 8 ? 6 : (g.tile_rows == 6 ? 4 : 2);
+  g.ntile1 = int((g.m1 + g.tile_rows - 1) / g.tile_rows);
+  // axis-0 chunks: the largest chunk that still gives about four waves
+  int64_t chunk = std::max<int64_t>(1, (int64_t(g.ntile1) * g.m0) / (4 * int64_t(ctas)));
+  chunk = std::min<int64_t>(chunk, 32);
+  const int64_t nchunk = (g.m0 + chunk - 1) / chunk;
   g.chunk = chunk;
   g.units = int(nchunk * g.ntile1);
-  g.grid = std::min<int>(g.units, ctas);
+  g.grid = g.units;  // one CTA per unit; the hardware scheduler balances
   fp.enabled = true;
   fp.scratch_bytes = size_t(g.m0) * g.m1 * g.m2 * 8 + 256;
   return fp;
@@ -938,8 +1108,6 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
   size_t ds = 0;
   cudaError_t e = set_attrs<T>(g, &ds);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(counter, 0, sizeof(int), ex.s);
-  if (e != cudaSuccess) return e;
 #define MGRX_DEC(TI)                                                                                   \
   if (g.tile_rows == TI)                                                                              \
     MGRX_LAUNCH(ex, "f3_dec_plane", k_f3_dec_plane<T, TI><<<g.grid, g.threads, ds, ex.s>>>(            \
@@ -963,8 +1131,6 @@ cudaError_t fused3d_recompose_level(const T* shell, T* coarse, T* fine, void* sc
   size_t ds = 0;
   cudaError_t e = set_attrs<T>(g, &ds);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(counter, 0, sizeof(int), ex.s);
-  if (e != cudaSuccess) return e;
 #define MGRX_REC(TI)                                                                                   \
   if (g.tile_rows == TI)                                                                              \
     MGRX_LAUNCH(ex, "f3_rec_plane",                                                                   \
@@ -976,7 +1142,7 @@ cudaError_t fused3d_recompose_level(const T* shell, T* coarse, T* fine, void* sc
 #undef MGRX_REC
   launch_col<T>(G, nullptr, 0.0, g, 1, th.w[1], th.inv_d[1], ex);
   launch_col<T>(G, coarse, -1.0, g, 0, th.w[0], th.inv_d[0], ex);
-  constexpr int kTRI = 16;
+  constexpr int kTRI = 8;
   MGRX_LAUNCH(ex, "f3_rec_interp",
               k_f3_rec_interp<T, kTRI><<<dim3(unsigned((g.n1 + kTRI - 1) / kTRI), unsigned(g.n0)), g.threads, 0, ex.s>>>(
                   shell, coarse, fine, g));

@@ -229,6 +229,202 @@ __global__ void __launch_bounds__(256) k_rec_interp(const T* __restrict__ shell,
   }
 }
 
+// ------------------------------------------------------------------ tail
+// All small levels of a hierarchy in one CTA: the level blocks, the fp64
+// component and the sweep buffer live in shared memory, and each step of the
+// per-level sequence above (coefficients, the d sweeps, apply) is a
+// block-wide loop separated by __syncthreads.  Same arithmetic as the
+// per-step kernels, so results stay bit-identical to the reference.
+struct TailLevel {
+  LevelGeom g;
+  ThomasLevel th;
+  int64_t shell_off;  // node_count(l-1): shell position in the level-centric buffer
+};
+
+__device__ __forceinline__ void tail_sweeps(double* comp, double* tmp, const LevelGeom& g, const ThomasLevel& th,
+                                            double** result) {
+  int64_t cur[kMaxD];
+  for (int i = 0; i < g.d; ++i) cur[i] = g.n[i];
+  double* x = comp;
+  double* y = tmp;
+  for (int a = 0; a < g.d; ++a) {
+    int64_t outer = 1, inner = 1;
+    for (int i = 0; i < a; ++i) outer *= cur[i];
+    for (int i = a + 1; i < g.d; ++i) inner *= cur[i];
+    const int64_t n = g.n[a], m = g.m[a];
+    const double* w = th.w[a];
+    const double* inv_d = th.inv_d[a];
+    for (int64_t t0 = threadIdx.x; t0 < outer * inner; t0 += blockDim.x) {
+      const int64_t o = t0 / inner, t = t0 - o * inner;
+      const double* c = x + o * n * inner + t;
+      double* f = y + o * m * inner + t;
+      double prev = 0.0;
+      for (int64_t i = 0; i < m; ++i) {
+        double acc = 0.0;
+        if (i >= 1) {
+          acc = add_(acc, mul_(kW12, c[(2 * i - 2) * inner]));
+          acc = add_(acc, mul_(0.5, c[(2 * i - 1) * inner]));
+        }
+        acc = add_(acc, mul_((i == 0 || i + 1 == m) ? kW5_12 : kW5_6, c[(2 * i) * inner]));
+        if (2 * i + 1 < n) acc = add_(acc, mul_(0.5, c[(2 * i + 1) * inner]));
+        if (2 * i + 2 < n) acc = add_(acc, mul_(kW12, c[(2 * i + 2) * inner]));
+        if (i > 0) acc = sub_(acc, mul_(w[i], prev));
+        f[i * inner] = acc;
+        prev = acc;
+      }
+      double nxt = mul_(prev, inv_d[m - 1]);
+      f[(m - 1) * inner] = nxt;
+      for (int64_t i = m - 2; i >= 0; --i) {
+        const double v = mul_(sub_(f[i * inner], mul_(kOff, nxt)), inv_d[i]);
+        f[i * inner] = v;
+        nxt = v;
+      }
+    }
+    __syncthreads();
+    cur[a] = g.m[a];
+    double* tswap = x;
+    x = y;
+    y = tswap;
+  }
+  *result = x;
+}
+
+// Decompose levels levels[0] (finest, block read from `blk`) down to the
+// last entry; shells go to out + shell_off, the final coarse block to `coarse_out`.
+template <typename T>
+__global__ void __launch_bounds__(1024) k_tail_decompose(const T* __restrict__ blk, T* __restrict__ out,
+                                                         T* __restrict__ coarse_out, const TailLevel* __restrict__ lv,
+                                                         int nlev, int64_t nmax) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* comp = reinterpret_cast<double*>(smem);
+  double* tmp = comp + nmax;
+  T* A = reinterpret_cast<T*>(tmp + nmax);
+  T* B = A + nmax;
+  const NuLevel nu{};
+  for (int64_t p = threadIdx.x; p < lv[0].g.N; p += blockDim.x) A[p] = blk[p];
+  __syncthreads();
+  T* cur = A;
+  T* nxt = B;
+  for (int k = 0; k < nlev; ++k) {
+    const LevelGeom& g = lv[k].g;
+    T* shell = out + lv[k].shell_off;
+    for (int64_t p = threadIdx.x; p < g.N; p += blockDim.x) {
+      int64_t j[kMaxD];
+      unravel<true>(p, g, j);
+      bool nodal = true;
+      for (int i = 0; i < g.d; ++i) nodal &= !(j[i] & 1);
+      if (nodal) {
+        int64_t cc = 0;
+        for (int i = 0; i < g.d; ++i) cc += (j[i] >> 1) * g.cst[i];
+        nxt[cc] = cur[p];
+        comp[p] = 0.0;
+      } else {
+        const double pred = predict<T, false>(cur, false, g, nu, j);
+        const T v = to_t<T>(sub_(double(cur[p]), pred));
+        comp[p] = double(v);
+        shell[shell_pos(g, j)] = v;
+      }
+    }
+    __syncthreads();
+    double* z = nullptr;
+    tail_sweeps(comp, tmp, g, lv[k].th, &z);
+    for (int64_t p = threadIdx.x; p < g.Nc; p += blockDim.x) nxt[p] = to_t<T>(add_(double(nxt[p]), mul_(1.0, z[p])));
+    __syncthreads();
+    T* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+  for (int64_t p = threadIdx.x; p < lv[nlev - 1].g.Nc; p += blockDim.x) coarse_out[p] = cur[p];
+}
+
+// Recompose from the coarse block (`coarse_in`, level of the first entry's
+// coarse side) up through the entries (coarsest first); the last fine block
+// goes to `fine_out`.
+template <typename T>
+__global__ void __launch_bounds__(1024) k_tail_recompose(const T* __restrict__ coeffs, const T* __restrict__ coarse_in,
+                                                         T* __restrict__ fine_out, const TailLevel* __restrict__ lv,
+                                                         int nlev, int64_t nmax) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* comp = reinterpret_cast<double*>(smem);
+  double* tmp = comp + nmax;
+  T* A = reinterpret_cast<T*>(tmp + nmax);
+  T* B = A + nmax;
+  const NuLevel nu{};
+  for (int64_t p = threadIdx.x; p < lv[0].g.Nc; p += blockDim.x) A[p] = coarse_in[p];
+  __syncthreads();
+  T* cur = A;  // coarse block of the current level
+  T* fin = B;
+  for (int k = 0; k < nlev; ++k) {
+    const LevelGeom& g = lv[k].g;
+    const T* shell = coeffs + lv[k].shell_off;
+    for (int64_t p = threadIdx.x; p < g.N; p += blockDim.x) {
+      int64_t j[kMaxD];
+      unravel<true>(p, g, j);
+      bool nodal = true;
+      for (int i = 0; i < g.d; ++i) nodal &= !(j[i] & 1);
+      comp[p] = nodal ? 0.0 : double(shell[shell_pos(g, j)]);
+    }
+    __syncthreads();
+    double* z = nullptr;
+    tail_sweeps(comp, tmp, g, lv[k].th, &z);
+    for (int64_t p = threadIdx.x; p < g.Nc; p += blockDim.x) cur[p] = to_t<T>(add_(double(cur[p]), mul_(-1.0, z[p])));
+    __syncthreads();
+    T* dst = (k == nlev - 1) ? fine_out : fin;
+    for (int64_t p = threadIdx.x; p < g.N; p += blockDim.x) {
+      int64_t j[kMaxD];
+      unravel<true>(p, g, j);
+      bool nodal = true;
+      for (int i = 0; i < g.d; ++i) nodal &= !(j[i] & 1);
+      if (nodal) {
+        int64_t cc = 0;
+        for (int i = 0; i < g.d; ++i) cc += (j[i] >> 1) * g.cst[i];
+        dst[p] = cur[cc];
+      } else {
+        const double pred = predict<T, false>(cur, true, g, nu, j);
+        dst[p] = to_t<T>(add_(double(shell[shell_pos(g, j)]), pred));
+      }
+    }
+    __syncthreads();
+    T* t = cur;
+    cur = fin;
+    fin = t;
+  }
+}
+
+size_t tail_smem_bytes(int64_t nmax, int esize) { return size_t(nmax) * (16 + 2 * size_t(esize)); }
+
+template <typename T>
+cudaError_t tail_decompose(const T* blk, T* out, T* coarse_out, const void* d_levels, int nlev, int64_t nmax,
+                           const Exec& ex) {
+  const size_t sm = tail_smem_bytes(nmax, sizeof(T));
+  cudaError_t e = cudaFuncSetAttribute(k_tail_decompose<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  if (e != cudaSuccess) return e;
+  MGRX_LAUNCH(ex, "tail_dec", k_tail_decompose<T><<<1, 1024, sm, ex.s>>>(
+                                  blk, out, coarse_out, static_cast<const TailLevel*>(d_levels), nlev, nmax));
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t tail_recompose(const T* coeffs, const T* coarse_in, T* fine_out, const void* d_levels, int nlev,
+                           int64_t nmax, const Exec& ex) {
+  const size_t sm = tail_smem_bytes(nmax, sizeof(T));
+  cudaError_t e = cudaFuncSetAttribute(k_tail_recompose<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  if (e != cudaSuccess) return e;
+  MGRX_LAUNCH(ex, "tail_rec", k_tail_recompose<T><<<1, 1024, sm, ex.s>>>(
+                                  coeffs, coarse_in, fine_out, static_cast<const TailLevel*>(d_levels), nlev, nmax));
+  return cudaGetLastError();
+}
+
+size_t tail_level_bytes() { return sizeof(TailLevel); }
+
+void tail_fill_level(void* dst, const LevelGeom& g, const ThomasLevel& th, int64_t shell_off) {
+  TailLevel t;
+  t.g = g;
+  t.th = th;
+  t.shell_off = shell_off;
+  *static_cast<TailLevel*>(dst) = t;
+}
+
 // ------------------------------------------------------------- launchers
 
 template <typename T>
@@ -323,5 +519,11 @@ cudaError_t general_recompose_level(const T* shell, T* coarse, T* fine, double* 
 MGRX_INST(float)
 MGRX_INST(double)
 #undef MGRX_INST
+
+template cudaError_t tail_decompose<float>(const float*, float*, float*, const void*, int, int64_t, const Exec&);
+template cudaError_t tail_decompose<double>(const double*, double*, double*, const void*, int, int64_t, const Exec&);
+template cudaError_t tail_recompose<float>(const float*, const float*, float*, const void*, int, int64_t, const Exec&);
+template cudaError_t tail_recompose<double>(const double*, const double*, double*, const void*, int, int64_t,
+                                            const Exec&);
 
 }  // namespace mgrx_b200
