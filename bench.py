@@ -270,18 +270,40 @@ def run_ours(args, ws, rank, local):
     peak, peak_src = measured_peak()
     step_achieved = 2 * alg_dir / (ms * 1e-3) / 1e9
 
-    # per-kernel device times (CUDA events on the library's stream) over the
-    # same number of steps, right after the timed region
+    # per-kernel device times (CUDA events on the library's stream, keyed
+    # "<kernel>@<level>"), decompose and recompose profiled separately over
+    # the same number of steps right after the timed region
+    mc = mg.decompose(field, h, 0, wsp)
     wsp.profile_begin()
     for _ in range(args.steps):
-        step()
-    prof = wsp.profile_end()
-    dominant = max(prof.items(), key=lambda kv: kv[1][0]) if prof else ("none", (0.0, 1))
-    kernel_bytes = kernel_algorithmic_bytes(dominant[0], h, esize)
-    kern_ms = dominant[1][0] / max(dominant[1][1], 1)
-    kern_achieved = kernel_bytes / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else 0.0
+        mg.decompose(field, h, 0, wsp)
+    prof_dec = wsp.profile_end()
+    wsp.profile_begin()
+    for _ in range(args.steps):
+        mg.recompose(mc, wsp)
+    prof_rec = wsp.profile_end()
+    del mc
+    prof = {}
+    for src, tagd in ((prof_dec, "dec"), (prof_rec, "rec")):
+        for k, (t, n) in src.items():
+            key = k if k.split("@")[0] not in ("f3_col0", "f3_col1", "tail_dec", "tail_rec") else f"{k}[{tagd}]"
+            prof[key] = (t, n)
     prof_total = sum(v[0] for v in prof.values()) / args.steps
-
+    L = h.num_levels()
+    dominant = max(prof.items(), key=lambda kv: kv[1][0]) if prof else ("none", (0.0, 1))
+    dom_tag = dominant[0]
+    dom_level = int(dom_tag.split("@")[1].split("[")[0]) if "@" in dom_tag else L
+    kern_ms = dominant[1][0] / max(dominant[1][1], 1)
+    # algorithmic bytes of a level pass: read + write the level block once
+    # (2 * s * #N_l); the dominant kernel carries that pass
+    kernel_bytes = 2 * esize * h.node_count(dom_level)
+    kern_achieved = kernel_bytes / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else 0.0
+    traffic = measured_traffic(dom_tag)
+    # finest-level passes: all kernels of level L per direction
+    lvl_ms = {}
+    for name, src in (("decompose", prof_dec), ("recompose", prof_rec)):
+        lvl_ms[name] = sum(t for k, (t, n) in src.items() if k.endswith("@%d" % L)) / args.steps
+    lvl_bytes = 2 * esize * h.node_count(L)
     # end-to-end through the host-buffer C-ABI entry points (pinned host
     # memory; H2D of the field + D2H of the coefficients for decompose, H2D
     # of the coefficients + D2H of the field for recompose, every step)
@@ -301,8 +323,12 @@ def run_ours(args, ws, rank, local):
                        "l2": "inputs larger than L2 (540 MB field vs 126 MB L2); no flush",
                        "parallelism": f"batch: {ws} independent field(s), one per GPU, no collective"},
             "roofline": {"bound": "hbm", "achieved": kern_achieved, "peak": peak, "unit": "GB/s",
-                         "frac": kern_achieved / peak, "traffic": None, "kernel": dominant[0],
-                         "kernel_ms": kern_ms, "kernel_alg_bytes": kernel_bytes, "peak_source": peak_src},
+                         "frac": kern_achieved / peak, "traffic": traffic, "kernel": dom_tag,
+                         "kernel_ms": kern_ms, "kernel_alg_bytes": kernel_bytes, "peak_source": peak_src,
+                         "definition": "2*s*#N_l of the kernel's level / its average CUDA-event duration"},
+            "finest_level_roofline": {
+                k: {"ms": v, "achieved": lvl_bytes / (v * 1e-3) / 1e9 if v else 0.0,
+                    "frac": (lvl_bytes / (v * 1e-3) / 1e9) / peak if v else 0.0} for k, v in lvl_ms.items()},
             "step_roofline": {"achieved": step_achieved, "peak": peak, "frac": step_achieved / peak,
                               "alg_bytes_per_step": 2 * alg_dir,
                               "definition": "sum_l 2*s*#N_l per direction, dec+rec, / device step time"},
@@ -318,25 +344,16 @@ def run_ours(args, ws, rank, local):
         print(json.dumps(line), flush=True)
 
 
-def kernel_algorithmic_bytes(tag, h, esize):
-    """Minimum bytes per launch of a kernel family at the finest level (the
-    level that dominates): the level pass must read and write the level block
-    once (2*s*#N_L); for the column passes the coarse-grid fp64 volume."""
-    L = h.num_levels()
-    nL = h.node_count(L)
-    nc = h.node_count(L - 1)
-    table = {
-        "f3_dec_plane": 2 * esize * nL,
-        "f3_rec_plane": 2 * esize * nL,
-        "f3_rec_interp": 2 * esize * nL,
-        "f3_col": 2 * 8 * nc,
-        "gen_dec_coef": 2 * esize * nL,
-        "gen_rec_interp": 2 * esize * nL,
-        "gen_rec_comp": esize * nL + 8 * nL,
-        "gen_sweep": 8 * nL,
-        "gen_apply": 2 * esize * nc,
-    }
-    return table.get(tag, 2 * esize * nL)
+def measured_traffic(tag):
+    """DRAM bytes (read + write) per launch of `tag` from the committed ncu
+    launch list summary (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)
+        v = d.get("kernels", {}).get(tag)
+        return None if v is None else float(v)
+    except Exception:
+        return None
 
 
 def e2e_measure(mg, wsp, field, h, args):

@@ -156,6 +156,15 @@ int mgrx_host_decompose(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t*
 int mgrx_host_recompose(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels,
                         int stop_level, const void* h_coeffs, void* h_field);
 
+/* quantize / dequantize on host buffers (same semantics as the device
+ * versions; outliers written to host arrays of outlier_capacity entries). */
+int mgrx_host_quantize(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels, int stop_level,
+                       const double* bin_widths, const void* h_coeffs, int32_t* h_labels, uint64_t* h_outlier_pos,
+                       void* h_outlier_val, uint64_t outlier_capacity, uint64_t* n_outliers);
+int mgrx_host_dequantize(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels, int stop_level,
+                         const double* bin_widths, const int32_t* h_labels, const uint64_t* h_outlier_pos,
+                         const void* h_outlier_val, uint64_t n_outliers, void* h_coeffs);
+
 /* Device scratch a decompose/recompose of this shape needs (bytes). */
 int mgrx_gpu_workspace_size(int dtype, int ndims, const uint64_t* dims, int levels, int stop_level,
                             uint64_t* bytes);

@@ -177,6 +177,7 @@ struct Plan {
 struct mgrx_b200::Profiler {
   struct Rec {
     const char* tag;
+    int level;
     cudaEvent_t a, b;
   };
   std::vector<Rec> recs;
@@ -200,7 +201,7 @@ void mgrx_b200::prof_mark(const Exec& ex, const char* tag, bool begin) {
   if (begin) {
     cudaEvent_t a = p->get();
     cudaEventRecord(a, ex.s);
-    p->recs.push_back({tag, a, nullptr});
+    p->recs.push_back({tag, ex.level, a, nullptr});
   } else {
     cudaEvent_t b = p->get();
     cudaEventRecord(b, ex.s);
@@ -231,7 +232,9 @@ struct mgrx_gpu_ctx {
 
 namespace {
 
-Exec exec(mgrx_gpu_ctx* c) { return Exec{c->stream, &c->launches, c->profiling ? &c->prof : nullptr}; }
+Exec exec(mgrx_gpu_ctx* c, int level = -1) {
+  return Exec{c->stream, &c->launches, c->profiling ? &c->prof : nullptr, level};
+}
 
 void set_device(mgrx_gpu_ctx* c) { cuda_check(cudaSetDevice(c->device), "cudaSetDevice"); }
 
@@ -479,7 +482,7 @@ void decompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, T* d_out, const 
   const T* blk = d_field;
   for (int l = L; l > stop; --l) {
     if (!nu && l == p.tail_top) {  // levels l..stop+1 in one CTA
-      cuda_check(tail_decompose<T>(blk, d_out, d_out, p.d_tail_dec, l - stop, p.tail_nmax, exec(c)), "tail");
+      cuda_check(tail_decompose<T>(blk, d_out, d_out, p.d_tail_dec, l - stop, p.tail_nmax, exec(c, l)), "tail");
       break;
     }
     T* shell = d_out + h.node[l - 1];
@@ -487,10 +490,10 @@ void decompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, T* d_out, const 
     const Fused3DPlan& fp = p.fused[l];
     cudaError_t e;
     if (!nu && c->path == 0 && fp.enabled) {
-      e = fused3d_decompose_level<T>(blk, shell, coarse, s + fp.scratch_off, p.geom[l], fp, p.thomas[l], exec(c));
+      e = fused3d_decompose_level<T>(blk, shell, coarse, s + fp.scratch_off, p.geom[l], fp, p.thomas[l], exec(c, l));
     } else {
       e = general_decompose_level<T>(blk, shell, coarse, comp, tmp, p.geom[l], &p.thomas[l],
-                                     nu ? &(*nu)[l] : nullptr, exec(c));
+                                     nu ? &(*nu)[l] : nullptr, exec(c, l));
     }
     cuda_check(e, "decompose level");
     blk = coarse;
@@ -517,7 +520,7 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
   if (!nu && p.tail_top > stop) {  // levels stop+1..tail_top in one CTA
     const int top = p.tail_top;
     T* fine = (top == L) ? d_field : reinterpret_cast<T*>(s + p.blk_off[top]);
-    cuda_check(tail_recompose<T>(d_coeffs, d_coeffs, fine, p.d_tail_rec, top - stop, p.tail_nmax, exec(c)), "tail");
+    cuda_check(tail_recompose<T>(d_coeffs, d_coeffs, fine, p.d_tail_rec, top - stop, p.tail_nmax, exec(c, top)), "tail");
     coarse = fine;
     l0 = top + 1;
   } else {
@@ -532,10 +535,10 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
     cudaError_t e;
     if (!nu && c->path == 0 && fp.enabled) {
       e = fused3d_recompose_level<T>(shell, coarse, fine, s + fp.scratch_off, p.geom[l], fp, p.thomas[l],
-                                     exec(c));
+                                     exec(c, l));
     } else {
       e = general_recompose_level<T>(shell, coarse, fine, comp, tmp, p.geom[l], &p.thomas[l],
-                                     nu ? &(*nu)[l] : nullptr, exec(c));
+                                     nu ? &(*nu)[l] : nullptr, exec(c, l));
     }
     cuda_check(e, "recompose level");
     coarse = fine;
@@ -660,10 +663,11 @@ int mgrx_gpu_profile_end(mgrx_gpu_ctx* c, char* tags, double* ms, uint64_t* coun
     for (const auto& r : c->prof.recs) {
       float t = 0.f;
       cuda_check(cudaEventElapsedTime(&t, r.a, r.b), "cudaEventElapsedTime");
+      const std::string key = r.level >= 0 ? std::string(r.tag) + "@" + std::to_string(r.level) : std::string(r.tag);
       size_t i = 0;
-      while (i < names.size() && names[i] != r.tag) ++i;
+      while (i < names.size() && names[i] != key) ++i;
       if (i == names.size()) {
-        names.push_back(r.tag);
+        names.push_back(key);
         tot.push_back(0.0);
         cnt.push_back(0);
       }
@@ -865,6 +869,69 @@ static int host_roundtrip(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* di
       else recompose_impl<double>(c, *p, reinterpret_cast<double*>(din), reinterpret_cast<double*>(dout), nullptr);
     }
     cuda_check(cudaMemcpyAsync(h_out, dout, bytes, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int mgrx_host_quantize(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
+                       const double* q, const void* h_coeffs, int32_t* h_labels, uint64_t* h_opos, void* h_oval,
+                       uint64_t capacity, uint64_t* n_outliers) {
+  int rc = guarded(c, [&] {
+    if (!dims || !q || !h_coeffs || !h_labels || !n_outliers) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    Plan* p = get_plan(c, dtype, nd, dims, levels, stop);
+    const size_t n = size_t(p->h.node[p->h.L]);
+    const size_t base = stop == 0 ? 0 : size_t(p->h.node[stop]);
+    const size_t es = p->esize;
+    const size_t need = align_up(n * es) + align_up((n - base) * 4) + align_up(n * 8) + align_up(n * es);
+    ensure(&c->io, &c->io_bytes, need, c, "cudaMalloc(io)");
+    char* b = static_cast<char*>(c->io);
+    char* dc = b;
+    int32_t* dl = reinterpret_cast<int32_t*>(b + align_up(n * es));
+    uint64_t* dp = reinterpret_cast<uint64_t*>(b + align_up(n * es) + align_up((n - base) * 4));
+    char* dv = reinterpret_cast<char*>(dp) + align_up(n * 8);
+    cuda_check(cudaMemcpyAsync(dc, h_coeffs, n * es, cudaMemcpyHostToDevice, c->stream), "H2D");
+    const int r = mgrx_gpu_quantize(c, dtype, nd, dims, levels, stop, q, dc, dl, dp, dv, n, n_outliers);
+    if (r != MGRX_OK) throw Fail{r, c->last_error};
+    if (*n_outliers > capacity) fail(MGRX_CAPACITY_EXCEEDED, "%llu outliers exceed capacity %llu",
+                                     (unsigned long long)*n_outliers, (unsigned long long)capacity);
+    cuda_check(cudaMemcpyAsync(h_labels, dl, (n - base) * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    if (*n_outliers) {
+      cuda_check(cudaMemcpyAsync(h_opos, dp, *n_outliers * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+      cuda_check(cudaMemcpyAsync(h_oval, dv, *n_outliers * es, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    }
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+  });
+  return rc;
+}
+
+int mgrx_host_dequantize(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
+                         const double* q, const int32_t* h_labels, const uint64_t* h_opos, const void* h_oval,
+                         uint64_t n_outliers, void* h_coeffs) {
+  return guarded(c, [&] {
+    if (!dims || !q || !h_labels || !h_coeffs) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    if (n_outliers && (!h_opos || !h_oval)) fail(MGRX_INVALID_ARGUMENT, "null outlier buffers");
+    Plan* p = get_plan(c, dtype, nd, dims, levels, stop);
+    const size_t n = size_t(p->h.node[p->h.L]);
+    const size_t base = stop == 0 ? 0 : size_t(p->h.node[stop]);
+    const size_t es = p->esize;
+    const size_t no = size_t(n_outliers);
+    const size_t need = align_up(n * es) + align_up((n - base) * 4) + align_up(no * 8 + 8) + align_up(no * es + 8);
+    ensure(&c->io, &c->io_bytes, need, c, "cudaMalloc(io)");
+    char* b = static_cast<char*>(c->io);
+    char* dc = b;
+    int32_t* dl = reinterpret_cast<int32_t*>(b + align_up(n * es));
+    uint64_t* dp = reinterpret_cast<uint64_t*>(b + align_up(n * es) + align_up((n - base) * 4));
+    char* dv = reinterpret_cast<char*>(dp) + align_up(no * 8 + 8);
+    // the coarse block of a tail dequantize is preserved: start from the caller's buffer
+    cuda_check(cudaMemcpyAsync(dc, h_coeffs, n * es, cudaMemcpyHostToDevice, c->stream), "H2D");
+    cuda_check(cudaMemcpyAsync(dl, h_labels, (n - base) * 4, cudaMemcpyHostToDevice, c->stream), "H2D");
+    if (no) {
+      cuda_check(cudaMemcpyAsync(dp, h_opos, no * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+      cuda_check(cudaMemcpyAsync(dv, h_oval, no * es, cudaMemcpyHostToDevice, c->stream), "H2D");
+    }
+    const int r = mgrx_gpu_dequantize(c, dtype, nd, dims, levels, stop, q, dl, dp, dv, n_outliers, dc);
+    if (r != MGRX_OK) throw Fail{r, c->last_error};
+    cuda_check(cudaMemcpyAsync(h_coeffs, dc, n * es, cudaMemcpyDeviceToHost, c->stream), "D2H");
     cuda_check(cudaStreamSynchronize(c->stream), "sync");
   });
 }

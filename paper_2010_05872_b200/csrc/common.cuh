@@ -94,6 +94,7 @@ struct Exec {
   cudaStream_t s;
   uint64_t* launches;
   Profiler* prof;
+  int level = -1;  // hierarchy level being processed (profiling key), -1 = none
 };
 // Records a CUDA event before/after a tagged launch when profiling
 // (api.cu); no-op otherwise.

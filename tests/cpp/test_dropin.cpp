@@ -1,0 +1,140 @@
+// Integration test of include/mgrx_b200.hpp against the unmodified reference
+// (compiled by `make -C oracle dropin`; run on a GPU box by
+// tests/test_gpu_dropin.py).  Checks the drop-in calls against the
+// reference's own decompose / recompose / quantize / compress / decompress
+// and that errors come back as mgrx::Error with the reference's errc.
+#include <cmath>
+#include <cstdio>
+#include <random>
+
+#include "mgrx/pipeline.hpp"
+#include "mgrx_b200.hpp"
+
+static int failures = 0;
+#define EXPECT(cond, ...)                       \
+  do {                                          \
+    if (!(cond)) {                              \
+      ++failures;                               \
+      std::printf("FAIL %s:%d: ", __FILE__, __LINE__); \
+      std::printf(__VA_ARGS__);                 \
+      std::printf("\n");                        \
+    }                                           \
+  } while (0)
+
+template <typename T>
+mgrx::TensorField<T> bumps(const mgrx::Dims& dims, unsigned seed) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> u(0.0, 1.0);
+  mgrx::TensorField<T> f(dims);
+  const int d = int(dims.size());
+  double c[8][3], w[8], a[8];
+  for (int b = 0; b < 8; ++b) {
+    for (int i = 0; i < 3; ++i) c[b][i] = u(rng);
+    w[b] = 0.05 + 0.15 * u(rng);
+    a[b] = 2.0 * u(rng) - 1.0;
+  }
+  std::vector<size_t> idx(dims.size(), 0);
+  for (size_t p = 0; p < f.size(); ++p) {
+    double v = 0.0;
+    for (int b = 0; b < 8; ++b) {
+      double r2 = 0.0;
+      for (int i = 0; i < d; ++i) {
+        const double x = double(idx[i]) / double(dims[i] - 1) - c[b][i % 3];
+        r2 += x * x;
+      }
+      v += a[b] * std::exp(-r2 / (2.0 * w[b] * w[b]));
+    }
+    f.data[p] = T(v + 1e-3 * (u(rng) - 0.5));
+    for (int i = d - 1; i >= 0; --i) {
+      if (++idx[size_t(i)] < dims[size_t(i)]) break;
+      idx[size_t(i)] = 0;
+    }
+  }
+  return f;
+}
+
+template <typename T>
+void check_shape(const mgrx::Dims& dims, double tol) {
+  mgrx::b200::Workspace ws;
+  auto f = bumps<T>(dims, 7);
+  double lo = f.data[0], hi = f.data[0];
+  for (T v : f.data) {
+    lo = std::min(lo, double(v));
+    hi = std::max(hi, double(v));
+  }
+  const double range = hi - lo;
+  const auto h = mgrx::GridHierarchy::create(dims);
+  mgrx::SolverWorkspace sws;
+  for (int stop : {0, 1}) {
+    auto ref = mgrx::decompose(f, h, stop, sws);
+    auto gpu = mgrx::b200::decompose(f, h, stop, ws);
+    double err = 0.0;
+    for (size_t i = 0; i < ref.buffer.size(); ++i)
+      err = std::max(err, std::fabs(double(ref.buffer[i]) - double(gpu.buffer[i])));
+    EXPECT(err <= tol * range, "decompose stop %d err %g", stop, err / range);
+    auto back = mgrx::b200::recompose(gpu, ws);
+    auto rback = mgrx::recompose(ref, sws);
+    double e2 = 0.0;
+    for (size_t i = 0; i < f.size(); ++i) e2 = std::max(e2, std::fabs(double(back.data[i]) - double(rback.data[i])));
+    EXPECT(e2 <= tol * range, "recompose stop %d err %g", stop, e2 / range);
+  }
+  // quantize / dequantize: bit-exact labels from identical coefficients
+  auto ref = mgrx::decompose(f, h, 0, sws);
+  const auto plan = mgrx::make_plan(mgrx::QuantMode::levelwise, 1e-3 * range / 2.0, h);
+  auto ls_ref = mgrx::quantize(ref, plan);
+  auto ls_gpu = mgrx::b200::quantize(ref, plan, ws);
+  EXPECT(ls_ref.labels == ls_gpu.labels, "labels differ");
+  EXPECT(ls_ref.outliers.size() == ls_gpu.outliers.size(), "outlier count differs");
+  auto dq_ref = mgrx::dequantize(ls_ref, plan, h);
+  auto dq_gpu = mgrx::b200::dequantize(ls_gpu, plan, h, ws);
+  EXPECT(dq_ref.buffer == dq_gpu.buffer, "dequantize differs");
+  // compress on the GPU, decompress with the reference (and vice versa)
+  mgrx::CompressOptions opt;
+  opt.budget = 1e-3 * range / 2.0;
+  opt.adaptive = false;
+  auto bytes = mgrx::b200::compress(f, opt, ws);
+  auto any = mgrx::decompress(bytes);
+  const auto& rf = std::get<mgrx::TensorField<T>>(any);
+  double linf = 0.0;
+  for (size_t i = 0; i < f.size(); ++i) linf = std::max(linf, std::fabs(double(rf.data[i]) - double(f.data[i])));
+  EXPECT(linf <= 1e-3 * range, "GPU-compressed artifact: linf/tau %g", linf / (1e-3 * range));
+  auto bytes_ref = mgrx::compress(f, opt);
+  auto gf = mgrx::b200::decompress_field<T>(mgrx::read_artifact(bytes_ref), ws);
+  double linf2 = 0.0;
+  for (size_t i = 0; i < f.size(); ++i) linf2 = std::max(linf2, std::fabs(double(gf.data[i]) - double(f.data[i])));
+  EXPECT(linf2 <= 1e-3 * range, "reference artifact via GPU: linf/tau %g", linf2 / (1e-3 * range));
+  std::printf("shape ok: %zu dims, range %g, linf/tau %g\n", dims.size(), range, linf / (1e-3 * range));
+}
+
+int main() {
+  check_shape<double>({33, 33, 33}, 1e-12);
+  check_shape<float>({65, 65, 65}, 1e-5);
+  check_shape<float>({40, 36, 66}, 1e-5);
+  check_shape<double>({17, 12}, 1e-12);
+  check_shape<float>({5, 5, 5, 5}, 1e-5);
+  // errors keep the reference's errc
+  mgrx::b200::Workspace ws;
+  const auto h = mgrx::GridHierarchy::create({9, 9});
+  try {
+    mgrx::b200::decompose(mgrx::TensorField<double>({9, 8}), h, 0, ws);
+    EXPECT(false, "no throw");
+  } catch (const mgrx::Error& e) {
+    EXPECT(e.code() == mgrx::errc::shape_error, "errc %d", int(e.code()));
+  }
+  try {
+    mgrx::b200::decompose(mgrx::TensorField<double>({9, 9}), h, 7, ws);
+    EXPECT(false, "no throw");
+  } catch (const mgrx::Error& e) {
+    EXPECT(e.code() == mgrx::errc::invalid_level, "errc %d", int(e.code()));
+  }
+  mgrx::MultilevelCoefficients<double> bad{std::vector<double>(h.total_count(), 0.0), h, 0};
+  bad.buffer[3] = NAN;
+  try {
+    mgrx::b200::quantize(bad, mgrx::make_plan(mgrx::QuantMode::uniform, 0.1, h), ws);
+    EXPECT(false, "no throw");
+  } catch (const mgrx::Error& e) {
+    EXPECT(e.code() == mgrx::errc::nonfinite_data, "errc %d", int(e.code()));
+  }
+  std::printf("%s (%d failures)\n", failures ? "FAILED" : "ALL OK", failures);
+  return failures ? 1 : 0;
+}
