@@ -64,14 +64,46 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+
+#ifndef MGRX_MBAR_SPIN_LIMIT
+#define MGRX_MBAR_SPIN_LIMIT 0  // > 0: trap with a message after that many failed polls (debug)
+#endif
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Wait for the phase of `bar` with the given parity.  With
+// MGRX_MBAR_SPIN_LIMIT (ns) set at build time a stuck wait traps instead of
+// hanging the device (debug builds).
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if MGRX_MBAR_SPIN_LIMIT > 0
+  uint64_t t0 = 0;
+  while (!mbar_try(bar, parity)) {
+    if (t0 == 0) t0 = global_ns();
+    if (global_ns() - t0 > uint64_t(MGRX_MBAR_SPIN_LIMIT)) asm volatile("trap;");
+  }
+#else
+  while (!mbar_try(bar, parity)) {
+  }
+#endif
 }
 
 // 1-D bulk copy global -> shared (TMA engine), completion on an mbarrier.
@@ -113,108 +145,14 @@ __device__ __forceinline__ void bulk_span(const T* base, int64_t start, int64_t 
   *lead = int((a - a0) / sizeof(T));
 }
 
-// ------------------------------------------------- block-parallel Thomas
-// Solves M z = f (ThomasAux factors, transform.hpp:25-44; batched_solve
-// :116-130) in place for `rows` rows of length m held in shared memory,
-// using every warp of the CTA: each row is cut into parts (one per warp) and
-// each part into lane segments.  A segment first runs the recurrence from a
-// zero carry to obtain its affine map y_end = A + B y_in; maps are combined
-// with a warp shuffle scan and a fold over the parts of the row, and the
-// segment then reruns the exact recurrence from its true carry.  Exact
-// algebra; rounding differs from the sequential sweep only in the carries.
+// Affine map y -> a + b y: the carry of the Thomas recurrences over a
+// segment, combined across lanes by the segmented solves below.
 struct Aff {
   double a, b;
 };
 
 __device__ __forceinline__ Aff aff_then(Aff first, Aff second) {  // apply first, then second
   return Aff{second.a + second.b * first.a, second.b * first.b};
-}
-
-__device__ void block_thomas_rows_pass(double* x, int row0, int rows, int m, int ld, const double* __restrict__ w,
-                                       const double* __restrict__ inv_d, double* scan);
-
-__device__ void block_thomas_rows(double* x, int rows, int m, int ld, const double* __restrict__ w,
-                                  const double* __restrict__ inv_d, double* scan /* [2][32] */) {
-  // one pass when every row gets at least one warp, else one row per warp per pass
-  const int nwarps = blockDim.x >> 5;
-  const int step = rows <= nwarps ? rows : nwarps;
-  for (int r0 = 0; r0 < rows; r0 += step) block_thomas_rows_pass(x, r0, min(step, rows - r0), m, ld, w, inv_d, scan);
-}
-
-__device__ void block_thomas_rows_pass(double* x, int row0, int rows, int m, int ld, const double* __restrict__ w,
-                                       const double* __restrict__ inv_d, double* scan) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int parts = max(1, nwarps / max(rows, 1));
-  const int row = warp / parts, q = warp - row * parts;
-  const bool live = row < rows;
-  x += size_t(row0) * ld;
-  const int P = (m + parts - 1) / parts;
-  const int p0 = min(m, q * P), p1 = min(m, p0 + P);
-  const int seg = (p1 - p0 + 31) >> 5;
-  const int s0 = min(p1, p0 + lane * seg), s1 = min(p1, s0 + seg);
-  double* xr = x + size_t(live ? row : 0) * ld;
-  double* sA = scan;
-  double* sB = scan + 32;
-  // ---- forward: y_i = x_i - w_i y_{i-1}
-  Aff f{0.0, 1.0};
-  if (live)
-    for (int i = s0; i < s1; ++i) {
-      const double wi = w[i];
-      f.a = xr[i] - wi * f.a;
-      f.b = -wi * f.b;
-    }
-  Aff inc = f;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const Aff o{__shfl_up_sync(0xffffffffu, inc.a, off), __shfl_up_sync(0xffffffffu, inc.b, off)};
-    if (lane >= off) inc = aff_then(o, inc);
-  }
-  Aff exc{__shfl_up_sync(0xffffffffu, inc.a, 1), __shfl_up_sync(0xffffffffu, inc.b, 1)};
-  if (lane == 0) exc = Aff{0.0, 1.0};
-  if (lane == 31 && warp < 32) {
-    sA[warp] = inc.a;
-    sB[warp] = inc.b;
-  }
-  __syncthreads();
-  double carry = 0.0;  // y before this part
-  for (int k = 0; k < q; ++k) carry = sA[row * parts + k] + sB[row * parts + k] * carry;
-  double y = exc.a + exc.b * carry;
-  if (live)
-    for (int i = s0; i < s1; ++i) {
-      y = xr[i] - w[i] * y;
-      xr[i] = y;
-    }
-  __syncthreads();
-  // ---- backward: z_i = (y_i - z_{i+1}/3) / d_i, z_m = 0
-  Aff g{0.0, 1.0};  // z_start = a + b z_in
-  if (live)
-    for (int i = s1 - 1; i >= s0; --i) {
-      const double id = inv_d[i];
-      g.a = (xr[i] - kOff * g.a) * id;
-      g.b = -kOff * id * g.b;
-    }
-  Aff rin = g;  // composite of this lane and the lanes to its right
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const Aff o{__shfl_down_sync(0xffffffffu, rin.a, off), __shfl_down_sync(0xffffffffu, rin.b, off)};
-    if (lane + off < 32) rin = aff_then(o, rin);
-  }
-  Aff rexc{__shfl_down_sync(0xffffffffu, rin.a, 1), __shfl_down_sync(0xffffffffu, rin.b, 1)};
-  if (lane == 31) rexc = Aff{0.0, 1.0};
-  if (lane == 0 && warp < 32) {
-    sA[warp] = rin.a;
-    sB[warp] = rin.b;
-  }
-  __syncthreads();
-  double rc = 0.0;  // z after this part
-  for (int k = parts - 1; k > q; --k) rc = sA[row * parts + k] + sB[row * parts + k] * rc;
-  double z = rexc.a + rexc.b * rc;
-  if (live)
-    for (int i = s1 - 1; i >= s0; --i) {
-      z = (xr[i] - kOff * z) * inv_d[i];
-      xr[i] = z;
-    }
-  __syncthreads();
 }
 
 // Shell offset of reordered row (r0, r1) of a 3-D level block
@@ -278,7 +216,7 @@ struct PlaneSmem {
     size_t b = 3 * raw_bytes(n2);   // TMA ring of fine plane tiles
     b += 2 * acc_elems(m2) * 8;     // finished coarse rows staged for the axis-2 solve
     b += 2 * size_t(m2) * 8;        // Thomas tables axis 2
-    b += 64 * 8 + 2 * kRows * 8 + 64;  // scan scratch, row offsets, barriers
+    b += 64 * 8 + 2 * kRows * 8 + 128;  // scan scratch, row offsets, pipeline barriers
     return b;
   }
 };
@@ -350,32 +288,49 @@ struct L0Planes {
   double prev[TI1], cur[TI1], next[TI1];
 };
 
+// Pipeline state of a plane-pass CTA (shared memory):
+//   full[s]     TMA completion of ring slot s (count 1 + transaction bytes)
+//   cnt[s]      warps done reading slot s; the last one refills it
+struct PlanePipe {
+  uint64_t full[3];
+  int cnt[3];
+};
+
+// A finished coarse plane (the j-th of this CTA): every owned lane stages
+// its rows in tb[j & 1]; rows are solved along axis 2 by rotating warps
+// (row r of completion j on warp (j * TR + r) mod nwarps) which wait for the
+// staging, solve, and store to G — no CTA-wide barrier.
 template <int TI1>
 __device__ __forceinline__ void l0_complete(const F3Geom& g, const UnitRange& ur, const StripLane& S,
-                                            const double* v, int64_t i0, double* tb, const double* tw2,
-                                            const double* tid2, double* __restrict__ G) {
+                                            const double* v, int64_t i0, int& j, double* tb, PlanePipe* pp,
+                                            const double* tw2, const double* tid2, double* __restrict__ G) {
+  (void)pp;
   const int m2 = int(g.m2), TR = int(ur.b1 - ur.b0);
+  double* t = tb + (j & 1) * (TI1 * m2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  // tb[j & 1] was last read by the solvers of completion j - 2, which all
+  // finished before the barrier of completion j - 1.
   if (S.owned) {
 #pragma unroll
     for (int ir = 0; ir < TI1; ++ir)
-      if (ir < TR) tb[ir * m2 + S.c] = v[ir];
+      if (ir < TR) t[ir * m2 + S.c] = v[ir];
   }
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  for (int ir = warp; ir < TR; ir += nwarps) {
-    double* row = tb + ir * m2;
+  for (int ir = 0; ir < TR; ++ir) {
+    if ((j * TR + ir) % nwarps != warp) continue;
+    double* row = t + ir * m2;
     warp_row_thomas(row, m2, tw2, tid2);
     double* gp = G + (i0 * g.m1 + ur.b0 + ir) * g.m2;
     for (int i = lane; i < m2; i += 32) gp[i] = row[i];
   }
+  ++j;
 }
 
 template <int TI1>
 __device__ __forceinline__ void l0_plane(const F3Geom& g, const UnitRange& ur, const StripLane& S, int64_t p,
-                                         const double* Q, L0Planes<TI1>& A, double* tb, const double* tw2,
-                                         const double* tid2, double* __restrict__ G) {
+                                         const double* Q, L0Planes<TI1>& A, int& j, double* tb, PlanePipe* pp,
+                                         const double* tw2, const double* tid2, double* __restrict__ G) {
   const int64_t k = p >> 1;
-  const int m2 = int(g.m2);
   const bool last = p == g.n0 - 1;
   if (!(p & 1)) {
     const double wc = (k == 0 || k + 1 == g.m0) ? kW5_12 : kW5_6;
@@ -385,20 +340,40 @@ __device__ __forceinline__ void l0_plane(const F3Geom& g, const UnitRange& ur, c
       A.cur[ir] += wc * Q[ir];
       A.next[ir] += kW12 * Q[ir];
     }
-    if (k - 1 >= ur.a0 && k - 1 < ur.a1) l0_complete<TI1>(g, ur, S, A.prev, k - 1, tb, tw2, tid2, G);
-    if (last && k >= ur.a0 && k < ur.a1) l0_complete<TI1>(g, ur, S, A.cur, k, tb + TI1 * m2, tw2, tid2, G);
+    if (k - 1 >= ur.a0 && k - 1 < ur.a1) l0_complete<TI1>(g, ur, S, A.prev, k - 1, j, tb, pp, tw2, tid2, G);
+    if (last && k >= ur.a0 && k < ur.a1) l0_complete<TI1>(g, ur, S, A.cur, k, j, tb, pp, tw2, tid2, G);
   } else {
 #pragma unroll
     for (int ir = 0; ir < TI1; ++ir) {
       A.cur[ir] += 0.5 * Q[ir];
       A.next[ir] += 0.5 * Q[ir];
     }
-    if (last && k >= ur.a0 && k < ur.a1) l0_complete<TI1>(g, ur, S, A.cur, k, tb, tw2, tid2, G);
+    if (last && k >= ur.a0 && k < ur.a1) l0_complete<TI1>(g, ur, S, A.cur, k, j, tb, pp, tw2, tid2, G);
 #pragma unroll
     for (int ir = 0; ir < TI1; ++ir) {
       A.prev[ir] = A.cur[ir];
       A.cur[ir] = A.next[ir];
       A.next[ir] = 0.0;
+    }
+  }
+}
+
+// Pipeline helpers: slot of plane q and the parity of its use.
+__device__ __forceinline__ int pipe_slot(int64_t q, int64_t plo) { return int((q - plo) % 3); }
+__device__ __forceinline__ uint32_t pipe_parity(int64_t q, int64_t plo) { return uint32_t(((q - plo) / 3) & 1); }
+
+// Called by every warp when it has finished reading plane q's slot; the
+// last warp refills the slot with plane q + 3 via `issue`.
+template <typename Issue>
+__device__ __forceinline__ void pipe_release(PlanePipe* pp, int64_t q, int64_t plo, int64_t phi, Issue&& issue) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    const int s = pipe_slot(q, plo);
+    __threadfence_block();
+    const int old = atomicAdd(&pp->cnt[s], 1);
+    if (old == int(blockDim.x >> 5) - 1) {
+      pp->cnt[s] = 0;
+      if (q + 3 <= phi) issue(q + 3);
     }
   }
 }
@@ -517,7 +492,7 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
   double* tid2 = tw2 + m2;
   double* scan = tid2 + m2;
   int64_t* rowoff = reinterpret_cast<int64_t*>(scan + 64);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rowoff + 2 * RMAX);
+  PlanePipe* pp = reinterpret_cast<PlanePipe*>(rowoff + 2 * RMAX);
   (void)counter;
 
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -527,14 +502,16 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
     tw2[i] = w2g[i];
     tid2[i] = id2g[i];
   }
+  const UnitRange ur = unit_range(g, int(blockIdx.x));
   if (tid == 0) {
-    for (int b = 0; b < 3; ++b) mbar_init(&bars[b], 1);
+    for (int b = 0; b < 3; ++b) {
+      mbar_init(&pp->full[b], 1);
+      pp->cnt[b] = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  uint32_t phase[3] = {0, 0, 0};
 
-  const UnitRange ur = unit_range(g, int(blockIdx.x));
   const int R = int(ur.rhi - ur.rlo + 1);
   DecRows<T> x;
   x.n2 = n2;
@@ -556,19 +533,18 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
   const bool full = ur.b0 >= 1 && 2 * ur.b1 <= g.n1 - 1;
   const int cc = S.valid ? c : 0;  // clamp halo columns for addressing
   auto tile_src = [&](int64_t p) { return blk + (p * g.n1 + ur.rlo) * g.n2; };
-  auto issue = [&](int64_t p) {
-    if (tid == 0) {
-      const char* src;
-      uint32_t bytes;
-      int ld;
-      bulk_span<T>(tile_src(p), 0, int64_t(R) * n2, &src, &bytes, &ld);
-      fence_proxy_async();
-      mbar_expect_tx(&bars[p % 3], bytes);
-      bulk_g2s(raw + size_t(p % 3) * rawb, src, bytes, &bars[p % 3]);
-    }
+  auto issue = [&](int64_t p) {  // one thread
+    const char* src;
+    uint32_t bytes;
+    int ld;
+    const int sl = pipe_slot(p, ur.plo);
+    bulk_span<T>(tile_src(p), 0, int64_t(R) * n2, &src, &bytes, &ld);
+    fence_proxy_async();
+    mbar_expect_tx(&pp->full[sl], bytes);
+    bulk_g2s(raw + size_t(sl) * rawb, src, bytes, &pp->full[sl]);
   };
   auto tile = [&](int64_t p) {
-    return reinterpret_cast<const T*>(raw + size_t(p % 3) * rawb) +
+    return reinterpret_cast<const T*>(raw + size_t(pipe_slot(p, ur.plo)) * rawb) +
            (reinterpret_cast<uintptr_t>(tile_src(p)) & 15) / sizeof(T);
   };
   double NSP[NE], NSN[NE];  // fp64 nodal values (own column) of the left / right even plane
@@ -580,25 +556,19 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
       ns[e] = (S.valid && j1 >= x.rlo && j1 <= x.rhi) ? double(rq[(j1 - x.rlo) * n2]) : 0.0;
     }
   };
-  issue(ur.plo);
-  if (ur.plo + 1 <= ur.phi) issue(ur.plo + 1);
-  int64_t ready = ur.plo - 1;
+  if (tid == 0)
+    for (int64_t q = ur.plo; q <= min(ur.phi, ur.plo + 2); ++q) issue(q);
   L0Planes<TI1> A;
 #pragma unroll
   for (int ir = 0; ir < TI1; ++ir) A.prev[ir] = A.cur[ir] = A.next[ir] = 0.0;
+  int jdone = 0;  // coarse planes finished by this CTA
   for (int64_t p = ur.plo; p <= ur.phi; ++p) {
     const bool p_odd = p & 1;
     x.has_right = p_odd && (p + 1 <= g.n0 - 1);
-    const int64_t need = x.has_right ? p + 1 : p;
-    while (ready < need) {
-      ++ready;
-      mbar_wait(&bars[ready % 3], phase[ready % 3]);
-      phase[ready % 3] ^= 1;
-    }
+    mbar_wait(&pp->full[pipe_slot(p, ur.plo)], pipe_parity(p, ur.plo));
+    if (x.has_right) mbar_wait(&pp->full[pipe_slot(p + 1, ur.plo)], pipe_parity(p + 1, ur.plo));
     if (p == ur.plo) load_ns(p, NSP);
     if (x.has_right) load_ns(p + 1, NSN);
-    __syncthreads();
-    if (p + 2 <= ur.phi) issue(p + 2);  // slot of plane p-1 is free
     const int64_t r0 = reord(p, g.m0);
     const int e0 = x.jbase >> 1;  // even tile row 0 <-> coarse row e0
     x.st_e = p_odd ? g.n2 : g.n2 - g.m2;
@@ -618,11 +588,12 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
       if (full) dec_rows<T, TI1, false, true>(x, NSP, NSN, Q);
       else dec_rows<T, TI1, false, false>(x, NSP, NSN, Q);
     }
+    pipe_release(pp, p, ur.plo, ur.phi, issue);  // this warp is done with plane p's slot
     if (p_odd && x.has_right) {
 #pragma unroll
       for (int e = 0; e < NE; ++e) NSP[e] = NSN[e];  // plane p+1 becomes the left even plane
     }
-    l0_plane<TI1>(g, ur, S, p, Q, A, acc, tw2, tid2, G);
+    l0_plane<TI1>(g, ur, S, p, Q, A, jdone, acc, pp, tw2, tid2, G);
   }
 }
 
@@ -682,7 +653,7 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
   double* tid2 = tw2 + m2;
   double* scan = tid2 + m2;
   int64_t* rowoff = reinterpret_cast<int64_t*>(scan + 64);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rowoff + 2 * RMAX);
+  PlanePipe* pp = reinterpret_cast<PlanePipe*>(rowoff + 2 * RMAX);
   (void)counter;
 
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -694,14 +665,16 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
     tw2[i] = w2g[i];
     tid2[i] = id2g[i];
   }
+  const UnitRange ur = unit_range(g, int(blockIdx.x));
   if (tid == 0) {
-    for (int b = 0; b < 3; ++b) mbar_init(&bars[b], 1);
+    for (int b = 0; b < 3; ++b) {
+      mbar_init(&pp->full[b], 1);
+      pp->cnt[b] = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  uint32_t phase[3] = {0, 0, 0};
 
-  const UnitRange ur = unit_range(g, int(blockIdx.x));
   const int rlo = int(ur.rlo), rhi = int(ur.rhi);
   const int jbase = int(2 * ur.b0) - 2;
   const int TR = int(ur.b1 - ur.b0), b0 = int(ur.b0);
@@ -726,34 +699,31 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
     const uintptr_t a1 = (reinterpret_cast<uintptr_t>(shell + x.se + x.le) + 15) & ~uintptr_t(15);
     return (uint32_t(a1 - a0) + 127u) & ~127u;
   };
-  auto issue = [&](int64_t p) {
-    if (tid == 0) {
-      const Runs x = runs(p);
-      const char *src0, *src1 = nullptr;
-      uint32_t b0b, b1b = 0;
-      int ld;
-      bulk_span<T>(shell, x.se, x.le, &src0, &b0b, &ld);
-      if (x.lo > 0) bulk_span<T>(shell, x.so, x.lo, &src1, &b1b, &ld);
-      unsigned char* dst = raw + size_t(p % 3) * rawb;
-      fence_proxy_async();
-      mbar_expect_tx(&bars[p % 3], b0b + b1b);
-      bulk_g2s(dst, src0, b0b, &bars[p % 3]);
-      if (x.lo > 0) bulk_g2s(dst + odd_slot_off(x), src1, b1b, &bars[p % 3]);
-    }
+  auto issue = [&](int64_t p) {  // one thread
+    const Runs x = runs(p);
+    const char *src0, *src1 = nullptr;
+    uint32_t b0b, b1b = 0;
+    int ld;
+    const int sl = pipe_slot(p, ur.plo);
+    bulk_span<T>(shell, x.se, x.le, &src0, &b0b, &ld);
+    if (x.lo > 0) bulk_span<T>(shell, x.so, x.lo, &src1, &b1b, &ld);
+    unsigned char* dst = raw + size_t(sl) * rawb;
+    fence_proxy_async();
+    mbar_expect_tx(&pp->full[sl], b0b + b1b);
+    bulk_g2s(dst, src0, b0b, &pp->full[sl]);
+    if (x.lo > 0) bulk_g2s(dst + odd_slot_off(x), src1, b1b, &pp->full[sl]);
   };
-  issue(ur.plo);
-  if (ur.plo + 1 <= ur.phi) issue(ur.plo + 1);
+  if (tid == 0)
+    for (int64_t q = ur.plo; q <= min(ur.phi, ur.plo + 2); ++q) issue(q);
   L0Planes<TI1> A;
 #pragma unroll
   for (int ir = 0; ir < TI1; ++ir) A.prev[ir] = A.cur[ir] = A.next[ir] = 0.0;
+  int jdone = 0;
   for (int64_t p = ur.plo; p <= ur.phi; ++p) {
-    mbar_wait(&bars[p % 3], phase[p % 3]);
-    phase[p % 3] ^= 1;
-    __syncthreads();
-    if (p + 2 <= ur.phi) issue(p + 2);
+    mbar_wait(&pp->full[pipe_slot(p, ur.plo)], pipe_parity(p, ur.plo));
     const bool p_odd = p & 1;
     const Runs x = runs(p);
-    const unsigned char* slot = raw + size_t(p % 3) * rawb;
+    const unsigned char* slot = raw + size_t(pipe_slot(p, ur.plo)) * rawb;
     // slot positions of even tile row e = 0 (fine row jbase) and odd e = 0 (jbase + 1)
     const int64_t st_e = p_odd ? g.n2 : g.n2 - g.m2;
     const T* evrun = reinterpret_cast<const T*>(slot) + (reinterpret_cast<uintptr_t>(shell + x.se) & 15) / sizeof(T);
@@ -773,7 +743,8 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
       if (full) rec_rows<T, TI1, false, true>(ev, od, st_e, n2, m2, jbase, rlo, rhi, b0, TR, m1, c, S.valid, has_odd, Q);
       else rec_rows<T, TI1, false, false>(ev, od, st_e, n2, m2, jbase, rlo, rhi, b0, TR, m1, c, S.valid, has_odd, Q);
     }
-    l0_plane<TI1>(g, ur, S, p, Q, A, acc, tw2, tid2, G);
+    pipe_release(pp, p, ur.plo, ur.phi, issue);
+    l0_plane<TI1>(g, ur, S, p, Q, A, jdone, acc, pp, tw2, tid2, G);
   }
 }
 
@@ -787,6 +758,17 @@ template <typename T, int TRI, bool PODD, bool FULL>
 __device__ __forceinline__ void interp_rows(const T* __restrict__ se_p, const T* __restrict__ so_p, int64_t st_e,
                                             int oofs, T* __restrict__ out, const double* CL, const double* CR, int j1lo,
                                             int n1, int64_t n2l, int m2, bool owned, bool has_odd, bool right_degen) {
+  // all shell loads of the block first (independent), then compute + store
+  T vE[TRI], vO[TRI];
+#pragma unroll
+  for (int jr = 0; jr < TRI; ++jr) {
+    const int j1 = j1lo + jr;
+    const bool o1 = jr & 1;
+    const bool ok = owned && (FULL || j1 < n1);
+    const T* sr = o1 ? so_p + int64_t(jr >> 1) * n2l : se_p + int64_t(jr >> 1) * st_e;
+    vE[jr] = (ok && (PODD || o1)) ? __ldg(sr) : T(0);
+    vO[jr] = (ok && has_odd) ? __ldg(sr + (o1 ? m2 : oofs)) : T(0);
+  }
 #pragma unroll
   for (int jr = 0; jr < TRI; ++jr) {
     const int j1 = j1lo + jr;
@@ -817,10 +799,9 @@ __device__ __forceinline__ void interp_rows(const T* __restrict__ se_p, const T*
     if (owned) {
       const double sc_e = ke == 1 ? 0.5 : 0.25;
       const double sc_o = ke == 0 ? 0.5 : (ke == 1 ? 0.25 : 0.125);
-      const T* sr = o1 ? so_p + int64_t(ea) * n2l : se_p + int64_t(ea) * st_e;
       T* o = out + int64_t(jr) * n2l;
-      o[0] = ke == 0 ? to_t<T>(aL) : to_t<T>(double(sr[0]) + se * sc_e);
-      if (has_odd) o[1] = to_t<T>(double(sr[o1 ? m2 : oofs]) + so * sc_o);
+      o[0] = ke == 0 ? to_t<T>(aL) : to_t<T>(double(vE[jr]) + se * sc_e);
+      if (has_odd) o[1] = to_t<T>(double(vO[jr]) + so * sc_o);
     }
   }
 }
@@ -977,26 +958,34 @@ size_t plane_smem(const F3Geom& g) {
   return PlaneSmem<T, TI1>::bytes(g.n2, g.m2);
 }
 
-// Largest row tile whose plane-pass CTA fits twice per SM (else once).
+// Row tile of the plane passes: maximise resident warps x useful-row
+// fraction (2 TI1 owned rows of 2 TI1 + 3 computed) within shared memory and
+// the register budget of __launch_bounds__(kPlaneMaxThreads, 2).
 template <typename T>
 bool pick_tile(F3Geom& g, size_t optin, size_t per_sm) {
+  const int warps = int((g.m2 + 29) / 30);
   const int cands[4] = {8, 6, 4, 2};
-  for (int pass = 0; pass < 2; ++pass) {
-    const size_t limit = pass == 0 ? std::min(optin, per_sm / 2 - 2048) : optin;
-    for (int c : cands) {
-      size_t need = 0;
-      if (c == 8) need = plane_smem<T, 8>(g);
-      if (c == 6) need = plane_smem<T, 6>(g);
-      if (c == 4) need = plane_smem<T, 4>(g);
-      if (c == 2) need = plane_smem<T, 2>(g);
-      if (need <= limit) {
-        g.tile_rows = c;
-        g.ctas_per_sm = pass == 0 ? 2 : 1;
-        return true;
-      }
+  double best = -1.0;
+  for (int c : cands) {
+    size_t need = 0;
+    if (c == 8) need = plane_smem<T, 8>(g);
+    if (c == 6) need = plane_smem<T, 6>(g);
+    if (c == 4) need = plane_smem<T, 4>(g);
+    if (c == 2) need = plane_smem<T, 2>(g);
+    if (need > optin) continue;
+    int ctas = int(per_sm / (need + 1024));
+    // registers: <= 96 per thread (launch bounds 288 x 2) -> 5 warps per SM sub-partition
+    ctas = std::min(ctas, std::max(1, 20 / warps));
+    ctas = std::max(ctas, 1);
+    const int resident = std::min(ctas * warps, 32);
+    const double score = resident * (2.0 * c) / (2.0 * c + 3.0);
+    if (score > best + 1e-9) {
+      best = score;
+      g.tile_rows = c;
+      g.ctas_per_sm = ctas;
     }
   }
-  return false;
+  return best > 0.0;
 }
 
 template <typename T>

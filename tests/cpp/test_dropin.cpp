@@ -89,8 +89,10 @@ void check_shape(const mgrx::Dims& dims, double tol) {
   auto dq_gpu = mgrx::b200::dequantize(ls_gpu, plan, h, ws);
   EXPECT(dq_ref.buffer == dq_gpu.buffer, "dequantize differs");
   // compress on the GPU, decompress with the reference (and vice versa)
+  // budget = tau / C with C = 4: the reference's budget is not an L-inf
+  // bound and C = 2 is exceeded on this field
   mgrx::CompressOptions opt;
-  opt.budget = 1e-3 * range / 2.0;
+  opt.budget = 1e-3 * range / 4.0;
   opt.adaptive = false;
   auto bytes = mgrx::b200::compress(f, opt, ws);
   auto any = mgrx::decompress(bytes);
@@ -103,6 +105,7 @@ void check_shape(const mgrx::Dims& dims, double tol) {
   double linf2 = 0.0;
   for (size_t i = 0; i < f.size(); ++i) linf2 = std::max(linf2, std::fabs(double(gf.data[i]) - double(f.data[i])));
   EXPECT(linf2 <= 1e-3 * range, "reference artifact via GPU: linf/tau %g", linf2 / (1e-3 * range));
+  EXPECT(std::fabs(linf - linf2) <= 1e-5 * range, "GPU and reference reconstructions differ: %g vs %g", linf, linf2);
   std::printf("shape ok: %zu dims, range %g, linf/tau %g\n", dims.size(), range, linf / (1e-3 * range));
 }
 
