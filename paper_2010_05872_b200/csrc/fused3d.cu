@@ -205,15 +205,27 @@ __device__ __forceinline__ StripLane strip_lane(int m2) {
   return s;
 }
 
+// Shared memory of the plane passes.  Decompose: a 4-slot ring of tile
+// planes (2 TI1 + 3 fine rows; an odd plane reads its two even neighbours in
+// place).  Recompose: a 3-slot ring of shell runs (even + odd rows).
 template <typename T, int TI1>
 struct PlaneSmem {
   static constexpr int kRows = 2 * TI1 + 3;
+  static constexpr int kDecRows = 2 * TI1 + 3;
+  static constexpr int kDecSlots = 4, kRecSlots = 3;
   static __host__ __device__ size_t raw_bytes(int64_t n2) {
     return (size_t(kRows) * size_t(n2) * sizeof(T) + 256 + 127) / 128 * 128;
   }
+  static __host__ __device__ size_t dec_raw_bytes(int64_t n2) {
+    return (size_t(kDecRows) * size_t(n2) * sizeof(T) + 32 + 127) / 128 * 128;
+  }
+  static __host__ __device__ size_t ring_bytes(int64_t n2) {
+    const size_t d = kDecSlots * dec_raw_bytes(n2), r = kRecSlots * raw_bytes(n2);
+    return d > r ? d : r;
+  }
   static __host__ __device__ size_t acc_elems(int64_t m2) { return size_t(TI1) * size_t(m2); }
   static __host__ __device__ size_t bytes(int64_t n2, int64_t m2) {
-    size_t b = 3 * raw_bytes(n2);   // TMA ring of fine plane tiles
+    size_t b = ring_bytes(n2);      // TMA ring of fine plane tiles / shell runs
     b += 2 * acc_elems(m2) * 8;     // finished coarse rows staged for the axis-2 solve
     b += 2 * size_t(m2) * 8;        // Thomas tables axis 2
     b += 64 * 8 + 2 * kRows * 8 + 128;  // scan scratch, row offsets, pipeline barriers
@@ -292,8 +304,8 @@ struct L0Planes {
 //   full[s]     TMA completion of ring slot s (count 1 + transaction bytes)
 //   cnt[s]      warps done reading slot s; the last one refills it
 struct PlanePipe {
-  uint64_t full[3];
-  int cnt[3];
+  uint64_t full[4];
+  int cnt[4];
 };
 
 // A finished coarse plane (the j-th of this CTA): every owned lane stages
@@ -316,8 +328,9 @@ __device__ __forceinline__ void l0_complete(const F3Geom& g, const UnitRange& ur
       if (ir < TR) t[ir * m2 + S.c] = v[ir];
   }
   __syncthreads();
-  for (int ir = 0; ir < TR; ++ir) {
-    if ((j * TR + ir) % nwarps != warp) continue;
+  int sw = (j * TR) % nwarps;  // solver warp of row 0
+  for (int ir = 0; ir < TR; ++ir, sw = (sw + 1 == nwarps) ? 0 : sw + 1) {
+    if (sw != warp) continue;
     double* row = t + ir * m2;
     warp_row_thomas(row, m2, tw2, tid2);
     double* gp = G + (i0 * g.m1 + ur.b0 + ir) * g.m2;
@@ -358,22 +371,25 @@ __device__ __forceinline__ void l0_plane(const F3Geom& g, const UnitRange& ur, c
   }
 }
 
-// Pipeline helpers: slot of plane q and the parity of its use.
-__device__ __forceinline__ int pipe_slot(int64_t q, int64_t plo) { return int((q - plo) % 3); }
-__device__ __forceinline__ uint32_t pipe_parity(int64_t q, int64_t plo) { return uint32_t(((q - plo) / 3) & 1); }
+// Pipeline helpers: ring slot of the d-th plane of a unit and the parity of
+// its use (NS slots).
+template <int NS>
+__device__ __forceinline__ int pipe_slot(int d) { return d % NS; }
+template <int NS>
+__device__ __forceinline__ uint32_t pipe_parity(int d) { return uint32_t((d / NS) & 1); }
 
-// Called by every warp when it has finished reading plane q's slot; the
-// last warp refills the slot with plane q + 3 via `issue`.
-template <typename Issue>
-__device__ __forceinline__ void pipe_release(PlanePipe* pp, int64_t q, int64_t plo, int64_t phi, Issue&& issue) {
+// Called by every warp when it has finished reading the d-th plane's slot;
+// the last warp refills the slot with plane d + NS via `issue` (d <= dmax).
+template <int NS, typename Issue>
+__device__ __forceinline__ void pipe_release(PlanePipe* pp, int d, int dmax, Issue&& issue) {
   __syncwarp();
   if ((threadIdx.x & 31) == 0) {
-    const int s = pipe_slot(q, plo);
+    const int s = pipe_slot<NS>(d);
     __threadfence_block();
     const int old = atomicAdd(&pp->cnt[s], 1);
     if (old == int(blockDim.x >> 5) - 1) {
       pp->cnt[s] = 0;
-      if (q + 3 <= phi) issue(q + 3);
+      if (d + NS <= dmax) issue(d + NS);
     }
   }
 }
@@ -403,31 +419,48 @@ struct DecRows {
 // PODD: plane parity; FULL: interior tile (all rows present, no degenerate
 // row, interior axis-1 weights) — every row test is then compile-time.
 template <typename T, int TI1, bool PODD, bool FULL>
-__device__ __forceinline__ void dec_rows(const DecRows<T>& x, const double* NSP, const double* NSN, double* Q) {
+__device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const T* nr, double* Q) {
   constexpr int RMAX = 2 * TI1 + 3;
   const int n2 = x.n2;
   const T* rr = x.rp + (x.jbase - x.rlo) * n2;  // tile row of jr = 0 (may precede the tile when not FULL)
+  // nodal values (own column, even tile rows) of the left / right even
+  // plane, read from their ring slots: nl / nr point at tile row jr = 0
+  auto ns = [&](const T* base, int e) -> double {
+    const int j1 = x.jbase + 2 * e;
+    if (!FULL && (j1 < x.rlo || j1 > x.rhi)) return 0.0;
+    return double(base[2 * e * n2]);
+  };
+  double aLc = ns(nl, 0), aRc = (PODD && x.has_right) ? ns(nr, 0) : aLc;
+  double aLn = 0.0, aRn = 0.0;
 #pragma unroll
   for (int jr = 0; jr < RMAX; ++jr, rr += n2) {
     const int j1 = x.jbase + jr;
-    if (!FULL && (j1 < x.rlo || j1 > x.rhi)) continue;  // uniform
-    constexpr int dummy = 0;
-    (void)dummy;
     const bool o1 = jr & 1;
     const int ea = jr >> 1;
+    if (!o1 && jr + 1 < RMAX) {
+      aLn = ns(nl, ea + 1);
+      aRn = (PODD && x.has_right) ? ns(nr, ea + 1) : aLn;
+    }
+    if (!FULL && (j1 < x.rlo || j1 > x.rhi)) {  // uniform
+      if (o1) {
+        aLc = aLn;
+        aRc = aRn;
+      }
+      continue;
+    }
     const bool rdeg = !FULL && o1 && (j1 + 1 >= x.n1);
     const double rawE = double(rr[0]);
     const double rawO = x.has_odd ? double(rr[1]) : 0.0;
-    const double aL = NSP[ea];
-    const double bL = o1 ? (rdeg ? aL : NSP[ea + 1]) : aL;
+    const double aL = aLc;
+    const double bL = o1 ? (rdeg ? aL : aLn) : aL;
     double se;
     int ke;
     if (!PODD) {
       se = o1 ? aL + bL : aL;
       ke = o1 ? 1 : 0;
     } else {
-      const double aR = x.has_right ? NSN[ea] : aL;
-      const double bR = o1 ? (x.has_right ? (rdeg ? aR : NSN[ea + 1]) : bL) : aR;
+      const double aR = aRc;
+      const double bR = o1 ? (rdeg ? aR : aRn) : aR;
       se = aL + aR;
       if (o1) {
         se += bL;
@@ -470,6 +503,10 @@ __device__ __forceinline__ void dec_rows(const DecRows<T>& x, const double* NSP,
       else if (ir < x.TR)
         Q[ir] += load_w(k, x.b0 + ir, x.m1) * h;
     }
+    if (o1) {
+      aLc = aLn;
+      aRc = aRn;
+    }
   }
 }
 
@@ -482,12 +519,12 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
                    const F3Geom g) {
   using SM = PlaneSmem<T, TI1>;
   constexpr int RMAX = SM::kRows;
-  constexpr int NE = TI1 + 2;  // even rows of a tile
+  constexpr int NS = SM::kDecSlots;
   extern __shared__ __align__(128) unsigned char smem[];
   const int m2 = int(g.m2), n2 = int(g.n2), n1 = int(g.n1), m1 = int(g.m1);
-  const size_t rawb = SM::raw_bytes(g.n2);
+  const size_t rawb = SM::dec_raw_bytes(g.n2);
   unsigned char* raw = smem;
-  double* acc = reinterpret_cast<double*>(smem + 3 * rawb);
+  double* acc = reinterpret_cast<double*>(smem + SM::ring_bytes(g.n2));
   double* tw2 = acc + 2 * SM::acc_elems(g.m2);
   double* tid2 = tw2 + m2;
   double* scan = tid2 + m2;
@@ -504,7 +541,7 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
   }
   const UnitRange ur = unit_range(g, int(blockIdx.x));
   if (tid == 0) {
-    for (int b = 0; b < 3; ++b) {
+    for (int b = 0; b < NS; ++b) {
       mbar_init(&pp->full[b], 1);
       pp->cnt[b] = 0;
     }
@@ -532,43 +569,35 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
   x.n2l = g.n2;
   const bool full = ur.b0 >= 1 && 2 * ur.b1 <= g.n1 - 1;
   const int cc = S.valid ? c : 0;  // clamp halo columns for addressing
-  auto tile_src = [&](int64_t p) { return blk + (p * g.n1 + ur.rlo) * g.n2; };
-  auto issue = [&](int64_t p) {  // one thread
+  const int D = int(ur.phi - ur.plo);  // planes of the unit: plo + [0, D]
+  auto tile_src = [&](int d) { return blk + ((ur.plo + d) * g.n1 + ur.rlo) * g.n2; };
+  auto issue = [&](int d) {  // one thread
     const char* src;
     uint32_t bytes;
     int ld;
-    const int sl = pipe_slot(p, ur.plo);
-    bulk_span<T>(tile_src(p), 0, int64_t(R) * n2, &src, &bytes, &ld);
+    const int sl = pipe_slot<NS>(d);
+    bulk_span<T>(tile_src(d), 0, int64_t(R) * n2, &src, &bytes, &ld);
     fence_proxy_async();
     mbar_expect_tx(&pp->full[sl], bytes);
     bulk_g2s(raw + size_t(sl) * rawb, src, bytes, &pp->full[sl]);
   };
-  auto tile = [&](int64_t p) {
-    return reinterpret_cast<const T*>(raw + size_t(pipe_slot(p, ur.plo)) * rawb) +
-           (reinterpret_cast<uintptr_t>(tile_src(p)) & 15) / sizeof(T);
-  };
-  double NSP[NE], NSN[NE];  // fp64 nodal values (own column) of the left / right even plane
-  auto load_ns = [&](int64_t q, double* ns) {
-    const T* rq = tile(q) + 2 * cc;
-#pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      const int j1 = x.jbase + 2 * e;
-      ns[e] = (S.valid && j1 >= x.rlo && j1 <= x.rhi) ? double(rq[(j1 - x.rlo) * n2]) : 0.0;
-    }
+  // tile row jbase of plane d, column 2 cc (the row may precede the slot when not FULL; never read then)
+  auto row0 = [&](int d) {
+    return reinterpret_cast<const T*>(raw + size_t(pipe_slot<NS>(d)) * rawb) +
+           (reinterpret_cast<uintptr_t>(tile_src(d)) & 15) / sizeof(T) + (x.jbase - x.rlo) * n2 + 2 * cc;
   };
   if (tid == 0)
-    for (int64_t q = ur.plo; q <= min(ur.phi, ur.plo + 2); ++q) issue(q);
+    for (int d = 0; d <= min(D, NS - 1); ++d) issue(d);
   L0Planes<TI1> A;
 #pragma unroll
   for (int ir = 0; ir < TI1; ++ir) A.prev[ir] = A.cur[ir] = A.next[ir] = 0.0;
   int jdone = 0;  // coarse planes finished by this CTA
-  for (int64_t p = ur.plo; p <= ur.phi; ++p) {
-    const bool p_odd = p & 1;
+  for (int d = 0; d <= D; ++d) {
+    const int64_t p = ur.plo + d;  // plo is even
+    const bool p_odd = d & 1;
     x.has_right = p_odd && (p + 1 <= g.n0 - 1);
-    mbar_wait(&pp->full[pipe_slot(p, ur.plo)], pipe_parity(p, ur.plo));
-    if (x.has_right) mbar_wait(&pp->full[pipe_slot(p + 1, ur.plo)], pipe_parity(p + 1, ur.plo));
-    if (p == ur.plo) load_ns(p, NSP);
-    if (x.has_right) load_ns(p + 1, NSN);
+    mbar_wait(&pp->full[pipe_slot<NS>(d)], pipe_parity<NS>(d));
+    if (x.has_right) mbar_wait(&pp->full[pipe_slot<NS>(d + 1)], pipe_parity<NS>(d + 1));
     const int64_t r0 = reord(p, g.m0);
     const int e0 = x.jbase >> 1;  // even tile row 0 <-> coarse row e0
     x.st_e = p_odd ? g.n2 : g.n2 - g.m2;
@@ -577,21 +606,22 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
     x.so = shell + (shell_row_start(g, r0, g.m1 + e0 + 1) - g.n2) + cc;
     x.cpe = coarse + ((p >> 1) * g.m1 + e0) * g.m2 + cc;
     x.own = S.owned && p >= 2 * ur.a0 && p < 2 * ur.a1;
-    x.rp = tile(p) + 2 * cc;
+    const T* r_own = row0(d);
+    x.rp = r_own - (x.jbase - x.rlo) * n2;
     double Q[TI1];
 #pragma unroll
     for (int ir = 0; ir < TI1; ++ir) Q[ir] = 0.0;
     if (p_odd) {
-      if (full) dec_rows<T, TI1, true, true>(x, NSP, NSN, Q);
-      else dec_rows<T, TI1, true, false>(x, NSP, NSN, Q);
+      const T* nl = row0(d - 1);
+      const T* nr = x.has_right ? row0(d + 1) : nl;
+      if (full) dec_rows<T, TI1, true, true>(x, nl, nr, Q);
+      else dec_rows<T, TI1, true, false>(x, nl, nr, Q);
+      pipe_release<NS>(pp, d - 1, D, issue);  // the left even plane is done
+      pipe_release<NS>(pp, d, D, issue);
     } else {
-      if (full) dec_rows<T, TI1, false, true>(x, NSP, NSN, Q);
-      else dec_rows<T, TI1, false, false>(x, NSP, NSN, Q);
-    }
-    pipe_release(pp, p, ur.plo, ur.phi, issue);  // this warp is done with plane p's slot
-    if (p_odd && x.has_right) {
-#pragma unroll
-      for (int e = 0; e < NE; ++e) NSP[e] = NSN[e];  // plane p+1 becomes the left even plane
+      if (full) dec_rows<T, TI1, false, true>(x, r_own, r_own, Q);
+      else dec_rows<T, TI1, false, false>(x, r_own, r_own, Q);
+      // an even plane stays resident for the odd plane after it
     }
     l0_plane<TI1>(g, ur, S, p, Q, A, jdone, acc, pp, tw2, tid2, G);
   }
@@ -648,7 +678,8 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
   const int m2 = int(g.m2), n2 = int(g.n2), m1 = int(g.m1);
   const size_t rawb = SM::raw_bytes(g.n2);
   unsigned char* raw = smem;
-  double* acc = reinterpret_cast<double*>(smem + 3 * rawb);
+  double* acc = reinterpret_cast<double*>(smem + SM::ring_bytes(g.n2));
+  constexpr int NS = SM::kRecSlots;
   double* tw2 = acc + 2 * SM::acc_elems(g.m2);
   double* tid2 = tw2 + m2;
   double* scan = tid2 + m2;
@@ -667,7 +698,7 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
   }
   const UnitRange ur = unit_range(g, int(blockIdx.x));
   if (tid == 0) {
-    for (int b = 0; b < 3; ++b) {
+    for (int b = 0; b < NS; ++b) {
       mbar_init(&pp->full[b], 1);
       pp->cnt[b] = 0;
     }
@@ -699,12 +730,13 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
     const uintptr_t a1 = (reinterpret_cast<uintptr_t>(shell + x.se + x.le) + 15) & ~uintptr_t(15);
     return (uint32_t(a1 - a0) + 127u) & ~127u;
   };
-  auto issue = [&](int64_t p) {  // one thread
-    const Runs x = runs(p);
+  const int D = int(ur.phi - ur.plo);
+  auto issue = [&](int d) {  // one thread
+    const Runs x = runs(ur.plo + d);
     const char *src0, *src1 = nullptr;
     uint32_t b0b, b1b = 0;
     int ld;
-    const int sl = pipe_slot(p, ur.plo);
+    const int sl = pipe_slot<NS>(d);
     bulk_span<T>(shell, x.se, x.le, &src0, &b0b, &ld);
     if (x.lo > 0) bulk_span<T>(shell, x.so, x.lo, &src1, &b1b, &ld);
     unsigned char* dst = raw + size_t(sl) * rawb;
@@ -714,16 +746,17 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
     if (x.lo > 0) bulk_g2s(dst + odd_slot_off(x), src1, b1b, &pp->full[sl]);
   };
   if (tid == 0)
-    for (int64_t q = ur.plo; q <= min(ur.phi, ur.plo + 2); ++q) issue(q);
+    for (int d = 0; d <= min(D, NS - 1); ++d) issue(d);
   L0Planes<TI1> A;
 #pragma unroll
   for (int ir = 0; ir < TI1; ++ir) A.prev[ir] = A.cur[ir] = A.next[ir] = 0.0;
   int jdone = 0;
-  for (int64_t p = ur.plo; p <= ur.phi; ++p) {
-    mbar_wait(&pp->full[pipe_slot(p, ur.plo)], pipe_parity(p, ur.plo));
+  for (int d = 0; d <= D; ++d) {
+    const int64_t p = ur.plo + d;
+    mbar_wait(&pp->full[pipe_slot<NS>(d)], pipe_parity<NS>(d));
     const bool p_odd = p & 1;
     const Runs x = runs(p);
-    const unsigned char* slot = raw + size_t(pipe_slot(p, ur.plo)) * rawb;
+    const unsigned char* slot = raw + size_t(pipe_slot<NS>(d)) * rawb;
     // slot positions of even tile row e = 0 (fine row jbase) and odd e = 0 (jbase + 1)
     const int64_t st_e = p_odd ? g.n2 : g.n2 - g.m2;
     const T* evrun = reinterpret_cast<const T*>(slot) + (reinterpret_cast<uintptr_t>(shell + x.se) & 15) / sizeof(T);
@@ -743,7 +776,7 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
       if (full) rec_rows<T, TI1, false, true>(ev, od, st_e, n2, m2, jbase, rlo, rhi, b0, TR, m1, c, S.valid, has_odd, Q);
       else rec_rows<T, TI1, false, false>(ev, od, st_e, n2, m2, jbase, rlo, rhi, b0, TR, m1, c, S.valid, has_odd, Q);
     }
-    pipe_release(pp, p, ur.plo, ur.phi, issue);
+    pipe_release<NS>(pp, d, D, issue);
     l0_plane<TI1>(g, ur, S, p, Q, A, jdone, acc, pp, tw2, tid2, G);
   }
 }
