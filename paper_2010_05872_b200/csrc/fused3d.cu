@@ -784,30 +784,35 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
 // ----------------------------------------------------------- interpolate
 // add_interpolant (transform.hpp:317) + inverse_reorder_level
 // (reorder.hpp:138) + unpack of the shell: fine block of level l from the
-// corrected coarse block and the shell.  blockIdx.y = fine plane, blockIdx.x
-// = group of TRI fine rows; strip lanes as the plane passes, the coarse
-// values of the block's rows kept in registers.
-template <typename T, int TRI, bool PODD, bool FULL>
-__device__ __forceinline__ void interp_rows(const T* __restrict__ se_p, const T* __restrict__ so_p, int64_t st_e,
-                                            int oofs, T* __restrict__ out, const double* CL, const double* CR, int j1lo,
-                                            int n1, int64_t n2l, int m2, bool owned, bool has_odd, bool right_degen) {
-  // all shell loads of the block first (independent), then compute + store
-  T vE[TRI], vO[TRI];
-#pragma unroll
-  for (int jr = 0; jr < TRI; ++jr) {
-    const int j1 = j1lo + jr;
-    const bool o1 = jr & 1;
-    const bool ok = owned && (FULL || j1 < n1);
-    const T* sr = o1 ? so_p + int64_t(jr >> 1) * n2l : se_p + int64_t(jr >> 1) * st_e;
-    vE[jr] = (ok && (PODD || o1)) ? __ldg(sr) : T(0);
-    vO[jr] = (ok && has_odd) ? __ldg(sr + (o1 ? m2 : oofs)) : T(0);
+// corrected coarse block and the shell.  One CTA per (chunk of fine planes,
+// tile of TRI fine rows) unit; each fine plane's shell runs (even rows, odd
+// rows) and the coarse rows it interpolates from stream through a 3-slot
+// TMA ring (no CTA barrier: the last warp done with a slot refills it).
+// Strip lanes as the plane passes; every computed row is owned.
+template <typename T, int TRI>
+struct InterpSmem {
+  static constexpr int NS = 3;
+  static constexpr int NE = TRI / 2 + 1;  // coarse rows of a tile
+  static __host__ __device__ size_t run_bytes(int64_t rows, int64_t len) {
+    return (size_t(rows) * size_t(len) * sizeof(T) + 32 + 127) / 128 * 128;
   }
+  static __host__ __device__ size_t ev_bytes(int64_t n2) { return run_bytes(TRI / 2, n2); }
+  static __host__ __device__ size_t co_bytes(int64_t m2) { return run_bytes(NE, m2); }
+  static __host__ __device__ size_t slot_bytes(int64_t n2, int64_t m2) { return 2 * ev_bytes(n2) + co_bytes(m2); }
+  static __host__ __device__ size_t bytes(int64_t n2, int64_t m2) { return NS * slot_bytes(n2, m2) + 128; }
+};
+
+template <typename T, int TRI, bool PODD, bool FULL>
+__device__ __forceinline__ void interp_rows(const T* ev, const T* od, int64_t st_e, int oofs, T* __restrict__ out,
+                                            const double* CL, const double* CR, int j1lo, int n1, int64_t n2l,
+                                            int m2, bool owned, bool has_odd, bool right_degen) {
 #pragma unroll
   for (int jr = 0; jr < TRI; ++jr) {
     const int j1 = j1lo + jr;
     if (!FULL && j1 >= n1) break;  // uniform
     const bool o1 = jr & 1;
     const int ea = jr >> 1;
+    const T* sr = o1 ? od + ea * n2l : ev + ea * st_e;
     const bool rdeg = !FULL && o1 && (j1 + 1 >= n1);
     const double aL = CL[ea];
     const double bL = o1 ? (rdeg ? aL : CL[ea + 1]) : aL;
@@ -833,51 +838,106 @@ __device__ __forceinline__ void interp_rows(const T* __restrict__ se_p, const T*
       const double sc_e = ke == 1 ? 0.5 : 0.25;
       const double sc_o = ke == 0 ? 0.5 : (ke == 1 ? 0.25 : 0.125);
       T* o = out + int64_t(jr) * n2l;
-      o[0] = ke == 0 ? to_t<T>(aL) : to_t<T>(double(vE[jr]) + se * sc_e);
-      if (has_odd) o[1] = to_t<T>(double(vO[jr]) + so * sc_o);
+      o[0] = ke == 0 ? to_t<T>(aL) : to_t<T>(double(sr[0]) + se * sc_e);
+      if (has_odd) o[1] = to_t<T>(double(sr[o1 ? m2 : oofs]) + so * sc_o);
     }
   }
 }
 
 template <typename T, int TRI>
-__global__ void __launch_bounds__(kPlaneMaxThreads)
-    k_f3_rec_interp(const T* __restrict__ shell, const T* __restrict__ coarse, T* __restrict__ fine, const F3Geom g) {
-  constexpr int NE = TRI / 2 + 1;
+__global__ void __launch_bounds__(kPlaneMaxThreads, 3)
+    k_f3_rec_interp(const T* __restrict__ shell, const T* __restrict__ coarse, T* __restrict__ fine, const F3Geom g,
+                    int ich, int ntile) {
+  using SM = InterpSmem<T, TRI>;
+  constexpr int NS = SM::NS, NE = SM::NE;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const size_t evb = SM::ev_bytes(g.n2), slotb = SM::slot_bytes(g.n2, g.m2);
+  PlanePipe* pp = reinterpret_cast<PlanePipe*>(smem + NS * slotb);
   const int m2 = int(g.m2), n2 = int(g.n2), n1 = int(g.n1), m1 = int(g.m1);
   const StripLane S = strip_lane(m2);
   const int c = S.c;
   const int cc = S.valid ? c : 0;
   const bool has_odd = S.valid && 2 * c + 1 < n2;
   const bool right_degen = 2 * c + 2 >= n2;
-  const int p = int(blockIdx.y);
-  const int j1lo = int(blockIdx.x) * TRI;  // even
-  const bool p_odd = p & 1;
-  const int cp = p >> 1;
-  const int cpr = p_odd ? ((p + 1 < g.n0) ? cp + 1 : cp) : cp;
-  const int64_t r0 = reord(p, g.m0);
+  const int chunk = int(blockIdx.x) / ntile, tile = int(blockIdx.x) - chunk * ntile;
+  const int64_t p0 = int64_t(chunk) * ich;  // even
+  const int D = int(min(g.n0, p0 + ich) - 1 - p0);
+  const int j1lo = tile * TRI;  // even
+  const int nrows = min(TRI, n1 - j1lo);
   const int e0 = j1lo >> 1;
-  const int64_t st_e = p_odd ? g.n2 : g.n2 - g.m2;
-  // shell slots of even tile row 0 (fine row j1lo) and odd tile row 0 (j1lo + 1)
-  const T* se_p = shell + shell_row_start(g, r0, e0) + cc;
-  const T* so_p = shell + shell_row_start(g, r0, g.m1 + e0) + cc;
-  double CL[NE], CR[NE];
-  const T* cLp = coarse + (int64_t(cp) * g.m1 + e0) * g.m2 + cc;
-  const T* cRp = coarse + (int64_t(cpr) * g.m1 + e0) * g.m2 + cc;
-#pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    const bool ok = S.valid && e0 + e < m1;
-    CL[e] = ok ? double(__ldg(cLp + int64_t(e) * m2)) : 0.0;
-    CR[e] = p_odd ? (ok ? double(__ldg(cRp + int64_t(e) * m2)) : 0.0) : CL[e];
+  const int ne = (nrows + 1) >> 1, no = nrows >> 1, nc = min(NE, m1 - e0);
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NS; ++b) {
+      mbar_init(&pp->full[b], 1);
+      pp->cnt[b] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  T* out = fine + (int64_t(p) * g.n1 + j1lo) * g.n2 + 2 * cc;
+  __syncthreads();
+  struct Src {
+    int64_t se, le, so, lo, cs;
+  };
+  auto src = [&](int d) {
+    const int64_t p = p0 + d;
+    const int64_t r0 = reord(p, g.m0);
+    Src x;
+    x.se = shell_row_start(g, r0, e0);
+    x.le = shell_row_start(g, r0, e0 + ne) - x.se;
+    x.so = shell_row_start(g, r0, g.m1 + e0);
+    x.lo = shell_row_start(g, r0, g.m1 + e0 + no) - x.so;
+    const int64_t k = ((p & 1) && p + 1 < g.n0) ? (p >> 1) + 1 : (p >> 1);
+    x.cs = (k * g.m1 + e0) * g.m2;
+    return x;
+  };
+  auto issue = [&](int d) {  // one thread
+    const Src x = src(d);
+    const char *s0, *s1 = nullptr, *s2;
+    uint32_t b0 = 0, b1 = 0, b2 = 0;
+    int ld;
+    bulk_span<T>(shell, x.se, x.le, &s0, &b0, &ld);
+    if (x.lo > 0) bulk_span<T>(shell, x.so, x.lo, &s1, &b1, &ld);
+    bulk_span<T>(coarse, x.cs, int64_t(nc) * g.m2, &s2, &b2, &ld);
+    const int sl = pipe_slot<NS>(d);
+    unsigned char* dst = smem + size_t(sl) * slotb;
+    fence_proxy_async();
+    mbar_expect_tx(&pp->full[sl], b0 + b1 + b2);
+    bulk_g2s(dst, s0, b0, &pp->full[sl]);
+    if (x.lo > 0) bulk_g2s(dst + evb, s1, b1, &pp->full[sl]);
+    bulk_g2s(dst + 2 * evb, s2, b2, &pp->full[sl]);
+  };
+  if (threadIdx.x == 0)
+    for (int d = 0; d <= min(D, NS - 1); ++d) issue(d);
   const bool full = j1lo + TRI + 1 <= n1 - 1;
-  const int oofs = p_odd ? m2 : 0;
-  if (p_odd) {
-    if (full) interp_rows<T, TRI, true, true>(se_p, so_p, st_e, oofs, out, CL, CR, j1lo, n1, g.n2, m2, S.owned, has_odd, right_degen);
-    else interp_rows<T, TRI, true, false>(se_p, so_p, st_e, oofs, out, CL, CR, j1lo, n1, g.n2, m2, S.owned, has_odd, right_degen);
-  } else {
-    if (full) interp_rows<T, TRI, false, true>(se_p, so_p, st_e, oofs, out, CL, CR, j1lo, n1, g.n2, m2, S.owned, has_odd, right_degen);
-    else interp_rows<T, TRI, false, false>(se_p, so_p, st_e, oofs, out, CL, CR, j1lo, n1, g.n2, m2, S.owned, has_odd, right_degen);
+  double Cp[NE];  // coarse rows of the last even plane
+#pragma unroll
+  for (int e = 0; e < NE; ++e) Cp[e] = 0.0;
+  for (int d = 0; d <= D; ++d) {
+    const int64_t p = p0 + d;
+    const bool p_odd = d & 1;
+    const int sl = pipe_slot<NS>(d);
+    mbar_wait(&pp->full[sl], pipe_parity<NS>(d));
+    const Src x = src(d);
+    const unsigned char* slot = smem + size_t(sl) * slotb;
+    auto lead = [&](const T* base, int64_t off) { return int((reinterpret_cast<uintptr_t>(base + off) & 15) / sizeof(T)); };
+    const T* ev = reinterpret_cast<const T*>(slot) + lead(shell, x.se) + cc;
+    const T* od = reinterpret_cast<const T*>(slot + evb) + lead(shell, x.so) + cc;
+    const T* co = reinterpret_cast<const T*>(slot + 2 * evb) + lead(coarse, x.cs) + cc;
+    double C[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) C[e] = (e < nc) ? double(co[e * m2]) : 0.0;
+    T* out = fine + (p * g.n1 + j1lo) * g.n2 + 2 * cc;
+    const int64_t st_e = p_odd ? g.n2 : g.n2 - g.m2;
+    if (p_odd) {
+      const double* CR = (p + 1 < g.n0) ? C : Cp;
+      if (full) interp_rows<T, TRI, true, true>(ev, od, st_e, m2, out, Cp, CR, j1lo, n1, g.n2, m2, S.owned, has_odd, right_degen);
+      else interp_rows<T, TRI, true, false>(ev, od, st_e, m2, out, Cp, CR, j1lo, n1, g.n2, m2, S.owned, has_odd, right_degen);
+    } else {
+      if (full) interp_rows<T, TRI, false, true>(ev, od, st_e, 0, out, C, C, j1lo, n1, g.n2, m2, S.owned, has_odd, right_degen);
+      else interp_rows<T, TRI, false, false>(ev, od, st_e, 0, out, C, C, j1lo, n1, g.n2, m2, S.owned, has_odd, right_degen);
+#pragma unroll
+      for (int e = 0; e < NE; ++e) Cp[e] = C[e];
+    }
+    pipe_release<NS>(pp, d, D, issue);
   }
 }
 
@@ -1103,6 +1163,34 @@ Fused3DPlan fused3d_plan(const LevelGeom& lg, int esize) {
   return fp;
 }
 
+// Interpolation pass: TRI = 8 fine rows per tile (4 for fp64, keeping three
+// CTAs per SM); an even number of fine planes per unit, sized for about
+// eight units per resident CTA slot.
+template <typename T, int TRI>
+static cudaError_t launch_interp_t(const T* shell, const T* coarse, T* fine, const F3Geom& g, const Exec& ex) {
+  const size_t smem = InterpSmem<T, TRI>::bytes(g.n2, g.m2);
+  cudaError_t e = cudaFuncSetAttribute(k_f3_rec_interp<T, TRI>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int ntile = int((g.n1 + TRI - 1) / TRI);
+  const int64_t want = int64_t(sms) * 3 * 8;
+  int64_t ich = (g.n0 * ntile) / want;
+  ich = std::max<int64_t>(2, std::min<int64_t>(32, ich & ~int64_t(1)));
+  const int64_t chunks = (g.n0 + ich - 1) / ich;
+  MGRX_LAUNCH(ex, "f3_rec_interp",
+              k_f3_rec_interp<T, TRI><<<unsigned(chunks * ntile), g.threads, smem, ex.s>>>(shell, coarse, fine, g,
+                                                                                           int(ich), ntile));
+  return cudaSuccess;
+}
+
+template <typename T>
+static cudaError_t launch_interp(const T* shell, const T* coarse, T* fine, const F3Geom& g, const Exec& ex) {
+  if (sizeof(T) == 4) return launch_interp_t<T, 8>(shell, coarse, fine, g, ex);
+  return launch_interp_t<T, 4>(shell, coarse, fine, g, ex);
+}
+
 template <typename T>
 static cudaError_t set_attrs(const F3Geom& g, size_t* smem) {
   cudaError_t e = cudaSuccess;
@@ -1164,10 +1252,8 @@ cudaError_t fused3d_recompose_level(const T* shell, T* coarse, T* fine, void* sc
 #undef MGRX_REC
   launch_col<T>(G, nullptr, 0.0, g, 1, th.w[1], th.inv_d[1], ex);
   launch_col<T>(G, coarse, -1.0, g, 0, th.w[0], th.inv_d[0], ex);
-  constexpr int kTRI = 8;
-  MGRX_LAUNCH(ex, "f3_rec_interp",
-              k_f3_rec_interp<T, kTRI><<<dim3(unsigned((g.n1 + kTRI - 1) / kTRI), unsigned(g.n0)), g.threads, 0, ex.s>>>(
-                  shell, coarse, fine, g));
+  e = launch_interp<T>(shell, coarse, fine, g, ex);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
