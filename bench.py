@@ -96,27 +96,39 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def dist_init():
+def dist_init(backend="nccl"):
+    """One process per GPU (torchrun env).  Batch sharding: rank r runs its
+    own field (seed r); the only collectives are the timing barrier and the
+    max-over-ranks of the device time.  `backend` gloo is for the CPU tests."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch.distributed as dist
 
-        backend = "nccl"
         dist.init_process_group(backend=backend)
     return ws, rank, local
 
 
-def max_over_ranks(x, ws):
+def field_seed(rank):
+    """Seed of the field a rank processes (config 5a: seed = field index)."""
+    return rank
+
+
+def max_over_ranks(x, ws, device="cuda"):
     if ws == 1:
         return x
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def aggregate_gbs(ws, nbytes_per_rank, ms_max):
+    """Whole-job throughput: bytes of all ranks over the slowest rank's time."""
+    return ws * nbytes_per_rank / (ms_max * 1e-3) / 1e9
 
 
 def barrier(ws):
@@ -234,7 +246,7 @@ def run_ours(args, ws, rank, local):
     dev = torch.device("cuda", local)
     esize = 4
     alg_dir, h = hierarchy_bytes(DIMS, esize)
-    field = config2_field(DIMS, seed=rank, device=dev)
+    field = config2_field(DIMS, seed=field_seed(rank), device=dev)
     nbytes = field.numel() * esize
     wsp = mg.SolverWorkspace(device=local, path=args.path)
     stream = torch.cuda.current_stream(dev)
@@ -266,7 +278,7 @@ def run_ours(args, ws, rank, local):
     launches = (wsp.launch_count() - l0) // max(args.steps, 1)
     ms = e0.elapsed_time(e1) / args.steps
     ms_max = max_over_ranks(ms, ws)
-    value = ws * nbytes / (ms_max * 1e-3) / 1e9
+    value = aggregate_gbs(ws, nbytes, ms_max)
     peak, peak_src = measured_peak()
     step_achieved = 2 * alg_dir / (ms * 1e-3) / 1e9
 
