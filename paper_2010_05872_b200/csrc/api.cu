@@ -482,7 +482,7 @@ void decompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, T* d_out, const 
   const T* blk = d_field;
   for (int l = L; l > stop; --l) {
     if (!nu && l == p.tail_top) {  // levels l..stop+1 in one CTA
-      cuda_check(tail_decompose<T>(blk, d_out, d_out, p.d_tail_dec, l - stop, p.tail_nmax, exec(c, l)), "tail");
+      cuda_check(tail_decompose<T>(blk, d_out, d_out, p.d_tail_dec, l - stop, p.tail_nmax, h.d, exec(c, l)), "tail");
       break;
     }
     T* shell = d_out + h.node[l - 1];
@@ -520,7 +520,8 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
   if (!nu && p.tail_top > stop) {  // levels stop+1..tail_top in one CTA
     const int top = p.tail_top;
     T* fine = (top == L) ? d_field : reinterpret_cast<T*>(s + p.blk_off[top]);
-    cuda_check(tail_recompose<T>(d_coeffs, d_coeffs, fine, p.d_tail_rec, top - stop, p.tail_nmax, exec(c, top)), "tail");
+    cuda_check(tail_recompose<T>(d_coeffs, d_coeffs, fine, p.d_tail_rec, top - stop, p.tail_nmax, h.d,
+                                    exec(c, top)), "tail");
     coarse = fine;
     l0 = top + 1;
   } else {

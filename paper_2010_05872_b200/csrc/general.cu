@@ -21,18 +21,23 @@ namespace mgrx_b200 {
 
 // --------------------------------------------------------------- indexing
 
-template <bool kIdx32>
+// D > 0: rank known at compile time (loops unroll, indices stay in
+// registers); D == 0: runtime rank g.d.
+#define MGRX_ND(g) (D > 0 ? D : (g).d)
+
+template <bool kIdx32, int D = 0>
 __device__ __forceinline__ void unravel(int64_t p, const LevelGeom& g, int64_t* j) {
   if (kIdx32) {
     uint32_t q = uint32_t(p);
-    for (int i = g.d - 1; i > 0; --i) {
+#pragma unroll
+    for (int i = MGRX_ND(g) - 1; i > 0; --i) {
       const uint32_t qq = g.fn[i].div(q);
       j[i] = int64_t(q - qq * uint32_t(g.n[i]));
       q = qq;
     }
     j[0] = q;
   } else {
-    for (int i = g.d - 1; i > 0; --i) {
+    for (int i = MGRX_ND(g) - 1; i > 0; --i) {
       j[i] = p % g.n[i];
       p /= g.n[i];
     }
@@ -44,10 +49,12 @@ __device__ __forceinline__ void unravel(int64_t p, const LevelGeom& g, int64_t* 
 // reorder.hpp:180-215): rows of the reordered level block in row-major
 // order; a row whose leading reordered indices are all nodal contributes
 // only its coefficient tail [m_{d-1}, n_{d-1}).
+template <int D = 0>
 __device__ __forceinline__ int64_t shell_pos(const LevelGeom& g, const int64_t* j) {
-  const int d = g.d;
+  const int d = MGRX_ND(g);
   int64_t row = 0, before = 0;
   bool inside = true;
+#pragma unroll
   for (int i = 0; i + 1 < d; ++i) {
     const int64_t r = (j[i] & 1) ? g.m[i] + (j[i] >> 1) : (j[i] >> 1);
     row = row * g.n[i] + r;
@@ -71,16 +78,16 @@ __device__ __forceinline__ int64_t shell_pos(const LevelGeom& g, const int64_t* 
 // even-axis end counting its single neighbour twice, sum * 2^-k.
 // src is either the natural fine block (coarse == false) or the compact
 // coarse block (coarse == true).
-template <typename T, bool kNu>
+template <typename T, bool kNu, int D = 0>
 __device__ __forceinline__ double predict(const T* __restrict__ src, bool coarse, const LevelGeom& g,
                                           const NuLevel& nu, const int64_t* j) {
-  int set[kMaxD];
   int k = 0;
   int64_t base = 0;
-  for (int i = 0; i < g.d; ++i) {
+#pragma unroll
+  for (int i = 0; i < MGRX_ND(g); ++i) {
     const int64_t stride = coarse ? g.cst[i] : g.st[i];
     if (j[i] & 1) {
-      set[k++] = i;
+      ++k;
       base += (coarse ? (j[i] - 1) >> 1 : j[i] - 1) * stride;
     } else {
       base += (coarse ? j[i] >> 1 : j[i]) * stride;
@@ -90,9 +97,12 @@ __device__ __forceinline__ double predict(const T* __restrict__ src, bool coarse
   for (unsigned cm = 0; cm < (1u << k); ++cm) {
     int64_t off = base;
     double wprod = 1.0;
-    for (int b = 0; b < k; ++b) {
-      const int ax = set[b];
+    int b = 0;  // bit of cm for the b-th odd axis (axes ascending)
+#pragma unroll
+    for (int ax = 0; ax < MGRX_ND(g); ++ax) {
+      if (!(j[ax] & 1)) continue;
       const bool right = (cm >> b) & 1u;
+      ++b;
       const bool has_right = j[ax] + 1 < g.n[ax];
       if (right && has_right) off += coarse ? g.cst[ax] : 2 * g.st[ax];
       if (kNu) wprod = mul_(wprod, right ? nu.ax[ax].wr[j[ax]] : nu.ax[ax].wl[j[ax]]);
@@ -241,25 +251,31 @@ struct TailLevel {
   int64_t shell_off;  // node_count(l-1): shell position in the level-centric buffer
 };
 
+template <int D>
 __device__ __forceinline__ void tail_sweeps(double* comp, double* tmp, const LevelGeom& g, const ThomasLevel& th,
                                             double** result) {
-  int64_t cur[kMaxD];
-  for (int i = 0; i < g.d; ++i) cur[i] = g.n[i];
+  int cur[kMaxD];
+#pragma unroll
+  for (int i = 0; i < MGRX_ND(g); ++i) cur[i] = int(g.n[i]);
   double* x = comp;
   double* y = tmp;
-  for (int a = 0; a < g.d; ++a) {
-    int64_t outer = 1, inner = 1;
-    for (int i = 0; i < a; ++i) outer *= cur[i];
-    for (int i = a + 1; i < g.d; ++i) inner *= cur[i];
-    const int64_t n = g.n[a], m = g.m[a];
+#pragma unroll
+  for (int a = 0; a < MGRX_ND(g); ++a) {
+    int outer = 1, inner = 1;
+#pragma unroll
+    for (int i = 0; i < MGRX_ND(g); ++i) {
+      if (i < a) outer *= cur[i];
+      if (i > a) inner *= cur[i];
+    }
+    const int n = int(g.n[a]), m = int(g.m[a]);
     const double* w = th.w[a];
     const double* inv_d = th.inv_d[a];
-    for (int64_t t0 = threadIdx.x; t0 < outer * inner; t0 += blockDim.x) {
-      const int64_t o = t0 / inner, t = t0 - o * inner;
+    for (int t0 = threadIdx.x; t0 < outer * inner; t0 += blockDim.x) {
+      const int o = t0 / inner, t = t0 - o * inner;
       const double* c = x + o * n * inner + t;
       double* f = y + o * m * inner + t;
       double prev = 0.0;
-      for (int64_t i = 0; i < m; ++i) {
+      for (int i = 0; i < m; ++i) {
         double acc = 0.0;
         if (i >= 1) {
           acc = add_(acc, mul_(kW12, c[(2 * i - 2) * inner]));
@@ -274,7 +290,7 @@ __device__ __forceinline__ void tail_sweeps(double* comp, double* tmp, const Lev
       }
       double nxt = mul_(prev, inv_d[m - 1]);
       f[(m - 1) * inner] = nxt;
-      for (int64_t i = m - 2; i >= 0; --i) {
+      for (int i = m - 2; i >= 0; --i) {
         const double v = mul_(sub_(f[i * inner], mul_(kOff, nxt)), inv_d[i]);
         f[i * inner] = v;
         nxt = v;
@@ -291,7 +307,7 @@ __device__ __forceinline__ void tail_sweeps(double* comp, double* tmp, const Lev
 
 // Decompose levels levels[0] (finest, block read from `blk`) down to the
 // last entry; shells go to out + shell_off, the final coarse block to `coarse_out`.
-template <typename T>
+template <typename T, int D>
 __global__ void __launch_bounds__(1024) k_tail_decompose(const T* __restrict__ blk, T* __restrict__ out,
                                                          T* __restrict__ coarse_out, const TailLevel* __restrict__ lv,
                                                          int nlev, int64_t nmax) {
@@ -310,24 +326,24 @@ __global__ void __launch_bounds__(1024) k_tail_decompose(const T* __restrict__ b
     T* shell = out + lv[k].shell_off;
     for (int64_t p = threadIdx.x; p < g.N; p += blockDim.x) {
       int64_t j[kMaxD];
-      unravel<true>(p, g, j);
+      unravel<true, D>(p, g, j);
       bool nodal = true;
-      for (int i = 0; i < g.d; ++i) nodal &= !(j[i] & 1);
+      for (int i = 0; i < MGRX_ND(g); ++i) nodal &= !(j[i] & 1);
       if (nodal) {
         int64_t cc = 0;
-        for (int i = 0; i < g.d; ++i) cc += (j[i] >> 1) * g.cst[i];
+        for (int i = 0; i < MGRX_ND(g); ++i) cc += (j[i] >> 1) * g.cst[i];
         nxt[cc] = cur[p];
         comp[p] = 0.0;
       } else {
-        const double pred = predict<T, false>(cur, false, g, nu, j);
+        const double pred = predict<T, false, D>(cur, false, g, nu, j);
         const T v = to_t<T>(sub_(double(cur[p]), pred));
         comp[p] = double(v);
-        shell[shell_pos(g, j)] = v;
+        shell[shell_pos<D>(g, j)] = v;
       }
     }
     __syncthreads();
     double* z = nullptr;
-    tail_sweeps(comp, tmp, g, lv[k].th, &z);
+    tail_sweeps<D>(comp, tmp, g, lv[k].th, &z);
     for (int64_t p = threadIdx.x; p < g.Nc; p += blockDim.x) nxt[p] = to_t<T>(add_(double(nxt[p]), mul_(1.0, z[p])));
     __syncthreads();
     T* t = cur;
@@ -340,7 +356,7 @@ __global__ void __launch_bounds__(1024) k_tail_decompose(const T* __restrict__ b
 // Recompose from the coarse block (`coarse_in`, level of the first entry's
 // coarse side) up through the entries (coarsest first); the last fine block
 // goes to `fine_out`.
-template <typename T>
+template <typename T, int D>
 __global__ void __launch_bounds__(1024) k_tail_recompose(const T* __restrict__ coeffs, const T* __restrict__ coarse_in,
                                                          T* __restrict__ fine_out, const TailLevel* __restrict__ lv,
                                                          int nlev, int64_t nmax) {
@@ -359,29 +375,29 @@ __global__ void __launch_bounds__(1024) k_tail_recompose(const T* __restrict__ c
     const T* shell = coeffs + lv[k].shell_off;
     for (int64_t p = threadIdx.x; p < g.N; p += blockDim.x) {
       int64_t j[kMaxD];
-      unravel<true>(p, g, j);
+      unravel<true, D>(p, g, j);
       bool nodal = true;
-      for (int i = 0; i < g.d; ++i) nodal &= !(j[i] & 1);
-      comp[p] = nodal ? 0.0 : double(shell[shell_pos(g, j)]);
+      for (int i = 0; i < MGRX_ND(g); ++i) nodal &= !(j[i] & 1);
+      comp[p] = nodal ? 0.0 : double(shell[shell_pos<D>(g, j)]);
     }
     __syncthreads();
     double* z = nullptr;
-    tail_sweeps(comp, tmp, g, lv[k].th, &z);
+    tail_sweeps<D>(comp, tmp, g, lv[k].th, &z);
     for (int64_t p = threadIdx.x; p < g.Nc; p += blockDim.x) cur[p] = to_t<T>(add_(double(cur[p]), mul_(-1.0, z[p])));
     __syncthreads();
     T* dst = (k == nlev - 1) ? fine_out : fin;
     for (int64_t p = threadIdx.x; p < g.N; p += blockDim.x) {
       int64_t j[kMaxD];
-      unravel<true>(p, g, j);
+      unravel<true, D>(p, g, j);
       bool nodal = true;
-      for (int i = 0; i < g.d; ++i) nodal &= !(j[i] & 1);
+      for (int i = 0; i < MGRX_ND(g); ++i) nodal &= !(j[i] & 1);
       if (nodal) {
         int64_t cc = 0;
-        for (int i = 0; i < g.d; ++i) cc += (j[i] >> 1) * g.cst[i];
+        for (int i = 0; i < MGRX_ND(g); ++i) cc += (j[i] >> 1) * g.cst[i];
         dst[p] = cur[cc];
       } else {
-        const double pred = predict<T, false>(cur, true, g, nu, j);
-        dst[p] = to_t<T>(add_(double(shell[shell_pos(g, j)]), pred));
+        const double pred = predict<T, false, D>(cur, true, g, nu, j);
+        dst[p] = to_t<T>(add_(double(shell[shell_pos<D>(g, j)]), pred));
       }
     }
     __syncthreads();
@@ -393,26 +409,50 @@ __global__ void __launch_bounds__(1024) k_tail_recompose(const T* __restrict__ c
 
 size_t tail_smem_bytes(int64_t nmax, int esize) { return size_t(nmax) * (16 + 2 * size_t(esize)); }
 
-template <typename T>
-cudaError_t tail_decompose(const T* blk, T* out, T* coarse_out, const void* d_levels, int nlev, int64_t nmax,
-                           const Exec& ex) {
+template <typename T, int D>
+static cudaError_t tail_dec_t(const T* blk, T* out, T* coarse_out, const void* d_levels, int nlev, int64_t nmax,
+                              const Exec& ex) {
   const size_t sm = tail_smem_bytes(nmax, sizeof(T));
-  cudaError_t e = cudaFuncSetAttribute(k_tail_decompose<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  cudaError_t e = cudaFuncSetAttribute(k_tail_decompose<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
   if (e != cudaSuccess) return e;
-  MGRX_LAUNCH(ex, "tail_dec", k_tail_decompose<T><<<1, 1024, sm, ex.s>>>(
+  MGRX_LAUNCH(ex, "tail_dec", k_tail_decompose<T, D><<<1, 1024, sm, ex.s>>>(
                                   blk, out, coarse_out, static_cast<const TailLevel*>(d_levels), nlev, nmax));
   return cudaGetLastError();
 }
 
-template <typename T>
-cudaError_t tail_recompose(const T* coeffs, const T* coarse_in, T* fine_out, const void* d_levels, int nlev,
-                           int64_t nmax, const Exec& ex) {
+template <typename T, int D>
+static cudaError_t tail_rec_t(const T* coeffs, const T* coarse_in, T* fine_out, const void* d_levels, int nlev,
+                              int64_t nmax, const Exec& ex) {
   const size_t sm = tail_smem_bytes(nmax, sizeof(T));
-  cudaError_t e = cudaFuncSetAttribute(k_tail_recompose<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  cudaError_t e = cudaFuncSetAttribute(k_tail_recompose<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
   if (e != cudaSuccess) return e;
-  MGRX_LAUNCH(ex, "tail_rec", k_tail_recompose<T><<<1, 1024, sm, ex.s>>>(
+  MGRX_LAUNCH(ex, "tail_rec", k_tail_recompose<T, D><<<1, 1024, sm, ex.s>>>(
                                   coeffs, coarse_in, fine_out, static_cast<const TailLevel*>(d_levels), nlev, nmax));
   return cudaGetLastError();
+}
+
+// Rank-specialised tails for 1-3 dimensions (the common cases), runtime
+// rank otherwise.
+template <typename T>
+cudaError_t tail_decompose(const T* blk, T* out, T* coarse_out, const void* d_levels, int nlev, int64_t nmax, int d,
+                           const Exec& ex) {
+  switch (d) {
+    case 1: return tail_dec_t<T, 1>(blk, out, coarse_out, d_levels, nlev, nmax, ex);
+    case 2: return tail_dec_t<T, 2>(blk, out, coarse_out, d_levels, nlev, nmax, ex);
+    case 3: return tail_dec_t<T, 3>(blk, out, coarse_out, d_levels, nlev, nmax, ex);
+    default: return tail_dec_t<T, 0>(blk, out, coarse_out, d_levels, nlev, nmax, ex);
+  }
+}
+
+template <typename T>
+cudaError_t tail_recompose(const T* coeffs, const T* coarse_in, T* fine_out, const void* d_levels, int nlev,
+                           int64_t nmax, int d, const Exec& ex) {
+  switch (d) {
+    case 1: return tail_rec_t<T, 1>(coeffs, coarse_in, fine_out, d_levels, nlev, nmax, ex);
+    case 2: return tail_rec_t<T, 2>(coeffs, coarse_in, fine_out, d_levels, nlev, nmax, ex);
+    case 3: return tail_rec_t<T, 3>(coeffs, coarse_in, fine_out, d_levels, nlev, nmax, ex);
+    default: return tail_rec_t<T, 0>(coeffs, coarse_in, fine_out, d_levels, nlev, nmax, ex);
+  }
 }
 
 size_t tail_level_bytes() { return sizeof(TailLevel); }
@@ -520,10 +560,12 @@ MGRX_INST(float)
 MGRX_INST(double)
 #undef MGRX_INST
 
-template cudaError_t tail_decompose<float>(const float*, float*, float*, const void*, int, int64_t, const Exec&);
-template cudaError_t tail_decompose<double>(const double*, double*, double*, const void*, int, int64_t, const Exec&);
-template cudaError_t tail_recompose<float>(const float*, const float*, float*, const void*, int, int64_t, const Exec&);
-template cudaError_t tail_recompose<double>(const double*, const double*, double*, const void*, int, int64_t,
+template cudaError_t tail_decompose<float>(const float*, float*, float*, const void*, int, int64_t, int, const Exec&);
+template cudaError_t tail_decompose<double>(const double*, double*, double*, const void*, int, int64_t, int,
+                                            const Exec&);
+template cudaError_t tail_recompose<float>(const float*, const float*, float*, const void*, int, int64_t, int,
+                                           const Exec&);
+template cudaError_t tail_recompose<double>(const double*, const double*, double*, const void*, int, int64_t, int,
                                             const Exec&);
 
 }  // namespace mgrx_b200
