@@ -1151,9 +1151,20 @@ Fused3DPlan fused3d_plan(const LevelGeom& lg, int esize) {
   while (g.tile_rows > 2 && ((g.m1 + g.tile_rows - 1) / g.tile_rows) * g.m0 < 2 * int64_t(ctas))
     g.tile_rows = g.tile_rows == 8 ? 6 : (g.tile_rows == 6 ? 4 : 2);
   g.ntile1 = int((g.m1 + g.tile_rows - 1) / g.tile_rows);
-  // axis-0 chunks: the largest chunk that still gives about four waves
-  int64_t chunk = std::max<int64_t>(1, (int64_t(g.ntile1) * g.m0) / (4 * int64_t(ctas)));
-  chunk = std::min<int64_t>(chunk, 32);
+  // axis-0 chunk of a unit: a unit of c coarse planes streams 2c + 3 fine
+  // planes (two halo planes are recomputed by the neighbour) plus a fixed
+  // pipeline fill; pick c minimising waves x per-unit time.
+  int64_t chunk = 1;
+  double best = 1e300;
+  for (int64_t c = 1; c <= 32 && c <= g.m0; ++c) {
+    const int64_t units = ((g.m0 + c - 1) / c) * g.ntile1;
+    const int64_t waves = (units + ctas - 1) / ctas;
+    const double cost = double(waves) * double(2 * c + 3 + 3);
+    if (cost < best - 1e-9) {
+      best = cost;
+      chunk = c;
+    }
+  }
   const int64_t nchunk = (g.m0 + chunk - 1) / chunk;
   g.chunk = chunk;
   g.units = int(nchunk * g.ntile1);
