@@ -950,8 +950,8 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 3)
 // from its true carry.  With `coarse` set the result is applied:
 // coarse += sign * z (apply_correction, transform.hpp:435-477); otherwise it
 // is written back to G.
-template <typename T, int LS>
-__global__ void __launch_bounds__(kColThreads, 2)
+template <typename T, int LS, bool APPLY>
+__global__ void __launch_bounds__(kColThreads, LS <= 16 ? 3 : 2)
     k_f3_col(double* __restrict__ G, T* __restrict__ coarse, double sign, int64_t ncols, int m, int64_t stride,
              int64_t outer_stride, int64_t inner, const double* __restrict__ w, const double* __restrict__ inv_d) {
   extern __shared__ double sc[];
@@ -972,16 +972,12 @@ __global__ void __launch_bounds__(kColThreads, 2)
   const int s0 = min(m, s * seg), s1 = min(m, s0 + seg);
   const int len = s1 - s0;
   double v[LS];
-  T cv[LS];  // coarse values to update (prefetched with G)
   {
     const double* gp = G + base + int64_t(s0) * stride;
-    const T* cp = coarse ? coarse + base + int64_t(s0) * stride : nullptr;
 #pragma unroll
     for (int k = 0; k < LS; ++k) {
       v[k] = (valid && k < len) ? *gp : 0.0;
-      cv[k] = (cp && valid && k < len) ? *cp : T(0);
       gp += stride;
-      if (cp) cp += stride;
     }
   }
   __syncthreads();
@@ -1027,8 +1023,11 @@ __global__ void __launch_bounds__(kColThreads, 2)
       v[k] = z;
     }
   if (!valid) return;
-  if (coarse) {
+  if (APPLY) {  // coarse values loaded only now: fewer live registers, more resident warps
     T* c = coarse + base + int64_t(s0) * stride;
+    T cv[LS];
+#pragma unroll
+    for (int k = 0; k < LS; ++k) cv[k] = k < len ? c[int64_t(k) * stride] : T(0);
 #pragma unroll
     for (int k = 0; k < LS; ++k) {
       if (k < len) *c = to_t<T>(double(cv[k]) + sign * v[k]);
@@ -1101,15 +1100,18 @@ void launch_col(double* G, T* coarse, double sign, const F3Geom& g, int axis, co
   }
   const unsigned blocks = unsigned((ncols + 15) / 16);
   const char* tag = axis == 1 ? "f3_col1" : "f3_col0";
-  if (m <= 320) {
-    const int SY = (m + 2 * 16 - 1) / (2 * 16);
-    MGRX_LAUNCH(ex, tag, k_f3_col<T, 16><<<blocks, dim3(32, SY), (2 * m + 2 * 2 * SY * 16) * 8, ex.s>>>(
-                             G, coarse, sign, ncols, m, stride, outer_stride, inner, w, id));
-  } else {
-    const int SY = (m + 2 * 32 - 1) / (2 * 32);
-    MGRX_LAUNCH(ex, tag, k_f3_col<T, 32><<<blocks, dim3(32, SY), (2 * m + 2 * 2 * SY * 16) * 8, ex.s>>>(
-                             G, coarse, sign, ncols, m, stride, outer_stride, inner, w, id));
+#define MGRX_COL(LS, AP)                                                                                  \
+  {                                                                                                       \
+    const int SY = (m + 2 * LS - 1) / (2 * LS);                                                          \
+    MGRX_LAUNCH(ex, tag, k_f3_col<T, LS, AP><<<blocks, dim3(32, SY), (2 * m + 2 * 2 * SY * 16) * 8, ex.s>>>( \
+                             G, coarse, sign, ncols, m, stride, outer_stride, inner, w, id));             \
   }
+  if (m <= 320) {
+    if (coarse) MGRX_COL(16, true) else MGRX_COL(16, false)
+  } else {
+    if (coarse) MGRX_COL(32, true) else MGRX_COL(32, false)
+  }
+#undef MGRX_COL
 }
 
 }  // namespace
