@@ -223,7 +223,7 @@ struct PlaneSmem {
     const size_t d = kDecSlots * dec_raw_bytes(n2), r = kRecSlots * raw_bytes(n2);
     return d > r ? d : r;
   }
-  static __host__ __device__ size_t acc_elems(int64_t m2) { return size_t(TI1) * size_t(m2); }
+  static __host__ __device__ size_t acc_elems(int64_t) { return 0; }
   static __host__ __device__ size_t bytes(int64_t n2, int64_t m2) {
     size_t b = ring_bytes(n2);      // TMA ring of fine plane tiles / shell runs
     b += 2 * acc_elems(m2) * 8;     // finished coarse rows staged for the axis-2 solve
@@ -308,33 +308,24 @@ struct PlanePipe {
   int cnt[4];
 };
 
-// A finished coarse plane (the j-th of this CTA): every owned lane stages
-// its rows in tb[j & 1]; rows are solved along axis 2 by rotating warps
-// (row r of completion j on warp (j * TR + r) mod nwarps) which wait for the
-// staging, solve, and store to G — no CTA-wide barrier.
+// A finished coarse plane (the j-th of this CTA): every owned lane stores
+// its rows of the axis-0/1/2 load vector to G.  The axis-2 solve of these
+// rows runs in the row pass (k_f3_row) after the plane pass, so the plane
+// pass needs no CTA-wide barrier.
 template <int TI1>
 __device__ __forceinline__ void l0_complete(const F3Geom& g, const UnitRange& ur, const StripLane& S,
                                             const double* v, int64_t i0, int& j, double* tb, PlanePipe* pp,
                                             const double* tw2, const double* tid2, double* __restrict__ G) {
+  (void)tb;
   (void)pp;
-  const int m2 = int(g.m2), TR = int(ur.b1 - ur.b0);
-  double* t = tb + (j & 1) * (TI1 * m2);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  // tb[j & 1] was last read by the solvers of completion j - 2, which all
-  // finished before the barrier of completion j - 1.
+  (void)tw2;
+  (void)tid2;
+  const int TR = int(ur.b1 - ur.b0);
   if (S.owned) {
+    double* gp = G + (i0 * g.m1 + ur.b0) * g.m2 + S.c;
 #pragma unroll
     for (int ir = 0; ir < TI1; ++ir)
-      if (ir < TR) t[ir * m2 + S.c] = v[ir];
-  }
-  __syncthreads();
-  int sw = (j * TR) % nwarps;  // solver warp of row 0
-  for (int ir = 0; ir < TR; ++ir, sw = (sw + 1 == nwarps) ? 0 : sw + 1) {
-    if (sw != warp) continue;
-    double* row = t + ir * m2;
-    warp_row_thomas(row, m2, tw2, tid2);
-    double* gp = G + (i0 * g.m1 + ur.b0 + ir) * g.m2;
-    for (int i = lane; i < m2; i += 32) gp[i] = row[i];
+      if (ir < TR) gp[int64_t(ir) * g.m2] = v[ir];
   }
   ++j;
 }
@@ -941,6 +932,42 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 3)
   }
 }
 
+// --------------------------------------------------------------- row pass
+// Thomas along axis 2 (batched_solve, transform.hpp:116-130) of every row of
+// the coarse fp64 volume G, in place: one warp per row, the row staged in
+// shared memory for the segmented solve (warp_row_thomas).
+__global__ void __launch_bounds__(256) k_f3_row(double* __restrict__ G, int64_t rows, int m,
+                                                const double* __restrict__ w, const double* __restrict__ inv_d) {
+  extern __shared__ double rs[];
+  double* tw = rs;
+  double* tid = rs + m;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double* buf = tid + m + warp * m;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    tw[i] = w[i];
+    tid[i] = inv_d[i];
+  }
+  __syncthreads();
+  for (int64_t r = int64_t(blockIdx.x) * nw + warp; r < rows; r += int64_t(gridDim.x) * nw) {
+    double* gr = G + r * m;
+    for (int i = lane; i < m; i += 32) buf[i] = gr[i];
+    __syncwarp();
+    warp_row_thomas(buf, m, tw, tid);
+    for (int i = lane; i < m; i += 32) gr[i] = buf[i];
+    __syncwarp();
+  }
+}
+
+void launch_row(double* G, const F3Geom& g, const double* w, const double* id, const Exec& ex) {
+  const int m = int(g.m2);
+  const int64_t rows = g.m0 * g.m1;
+  const int threads = 256;
+  const size_t smem = size_t(2 + threads / 32) * m * 8;
+  cudaFuncSetAttribute(k_f3_row, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  const int64_t blocks = std::min<int64_t>((rows + 7) / 8, int64_t(kNumSMs) * 8);
+  MGRX_LAUNCH(ex, "f3_row", k_f3_row<<<unsigned(blocks), threads, smem, ex.s>>>(G, rows, m, w, id));
+}
+
 // ------------------------------------------------------------ column pass
 // Thomas along axis 0 or 1 of the coarse fp64 volume G (m0 x m1 x m2).
 // 16 consecutive columns per block; each column is split into S segments
@@ -1240,6 +1267,7 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
   MGRX_DEC(4)
   MGRX_DEC(2)
 #undef MGRX_DEC
+  launch_row(G, g, th.w[2], th.inv_d[2], ex);
   launch_col<T>(G, nullptr, 0.0, g, 1, th.w[1], th.inv_d[1], ex);
   launch_col<T>(G, coarse, 1.0, g, 0, th.w[0], th.inv_d[0], ex);
   return cudaGetLastError();
@@ -1263,6 +1291,7 @@ cudaError_t fused3d_recompose_level(const T* shell, T* coarse, T* fine, void* sc
   MGRX_REC(4)
   MGRX_REC(2)
 #undef MGRX_REC
+  launch_row(G, g, th.w[2], th.inv_d[2], ex);
   launch_col<T>(G, nullptr, 0.0, g, 1, th.w[1], th.inv_d[1], ex);
   launch_col<T>(G, coarse, -1.0, g, 0, th.w[0], th.inv_d[0], ex);
   e = launch_interp<T>(shell, coarse, fine, g, ex);
