@@ -164,6 +164,27 @@ __device__ __forceinline__ int64_t shell_row_start(const F3Geom& g, int64_t r0, 
 
 __device__ __forceinline__ int64_t reord(int64_t j, int64_t m) { return (j & 1) ? m + (j >> 1) : (j >> 1); }
 
+// shell_row_start(reord(p), r1) is linear in k = p / 2 for each parity of p:
+// b[p & 1] + k * s[p & 1] (per-CTA tables in shared memory).
+struct ShellLin {
+  int64_t b[2], s[2];
+};
+
+__device__ __forceinline__ ShellLin shell_lin(const F3Geom& g, int64_t r1) {
+  ShellLin l;
+  l.b[0] = shell_row_start(g, 0, r1);
+  l.s[0] = g.n1 * g.n2 - g.m1 * g.m2;  // r0 = k < m0: one more nodal row of m1 entries per plane
+  l.b[1] = shell_row_start(g, g.m0, r1);
+  l.s[1] = g.n1 * g.n2;
+  return l;
+}
+
+__device__ __forceinline__ int64_t lin_at(const ShellLin* l, int par, int64_t k) {
+  const volatile int64_t* b = l->b;
+  const volatile int64_t* s = l->s;
+  return b[par] + k * s[par];
+}
+
 struct UnitRange {
   int64_t a0, a1, b0, b1;  // coarse planes [a0,a1), coarse rows [b0,b1)
   int64_t plo, phi;        // fine planes touched, inclusive
@@ -212,7 +233,7 @@ template <typename T, int TI1>
 struct PlaneSmem {
   static constexpr int kRows = 2 * TI1 + 3;
   static constexpr int kDecRows = 2 * TI1 + 3;
-  static constexpr int kDecSlots = 4, kRecSlots = 3;
+  static constexpr int kDecSlots = 4, kRecSlots = 4;
   static __host__ __device__ size_t raw_bytes(int64_t n2) {
     return (size_t(kRows) * size_t(n2) * sizeof(T) + 256 + 127) / 128 * 128;
   }
@@ -228,7 +249,7 @@ struct PlaneSmem {
     size_t b = ring_bytes(n2);      // TMA ring of fine plane tiles / shell runs
     b += 2 * acc_elems(m2) * 8;     // finished coarse rows staged for the axis-2 solve
     b += 2 * size_t(m2) * 8;        // Thomas tables axis 2
-    b += 64 * 8 + 2 * kRows * 8 + 128;  // scan scratch, row offsets, pipeline barriers
+    b += 64 * 8 + 2 * kRows * 8 + 256;  // scan scratch, row offsets, pipeline state
     return b;
   }
 };
@@ -306,6 +327,7 @@ struct L0Planes {
 struct PlanePipe {
   uint64_t full[4];
   int cnt[4];
+  ShellLin lin[4];  // recompose: shell run bounds of the unit's rows
 };
 
 // A finished coarse plane (the j-th of this CTA): every owned lane stores
@@ -694,6 +716,10 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
       pp->cnt[b] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    pp->lin[0] = shell_lin(g, ur.rlo >> 1);
+    pp->lin[1] = shell_lin(g, (ur.rhi >> 1) + 1);
+    pp->lin[2] = shell_lin(g, g.m1 + ((ur.rlo + 1) >> 1));
+    pp->lin[3] = shell_lin(g, g.m1 + ((ur.rhi - 1) >> 1) + 1);
   }
   __syncthreads();
 
@@ -708,12 +734,13 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
     int64_t se, le, so, lo;
   };
   auto runs = [&](int64_t p) {
-    const int64_t r0 = reord(p, g.m0);
+    const int par = int(p & 1);
+    const int64_t k = p >> 1;
     Runs x;
-    x.se = shell_row_start(g, r0, e_lo);
-    x.le = shell_row_start(g, r0, e_hi + 1) - x.se;
-    x.so = o_hi >= o_lo ? shell_row_start(g, r0, g.m1 + o_lo) : 0;
-    x.lo = o_hi >= o_lo ? shell_row_start(g, r0, g.m1 + o_hi + 1) - x.so : 0;
+    x.se = lin_at(&pp->lin[0], par, k);
+    x.le = lin_at(&pp->lin[1], par, k) - x.se;
+    x.so = o_hi >= o_lo ? lin_at(&pp->lin[2], par, k) : 0;
+    x.lo = o_hi >= o_lo ? lin_at(&pp->lin[3], par, k) - x.so : 0;
     return x;
   };
   auto odd_slot_off = [&](const Runs& x) {
