@@ -250,6 +250,7 @@ struct PlaneSmem {
     b += 2 * acc_elems(m2) * 8;     // finished coarse rows staged for the axis-2 solve
     b += 2 * size_t(m2) * 8;        // Thomas tables axis 2
     b += 64 * 8 + 2 * kRows * 8 + 256;  // scan scratch, row offsets, pipeline state
+    b += size_t(TI1 + 2) * kPlaneMaxThreads * sizeof(T);  // per-thread nodal values of the last even plane
     return b;
   }
 };
@@ -432,7 +433,7 @@ struct DecRows {
 // PODD: plane parity; FULL: interior tile (all rows present, no degenerate
 // row, interior axis-1 weights) — every row test is then compile-time.
 template <typename T, int TI1, bool PODD, bool FULL>
-__device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const T* nr, double* Q) {
+__device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const T* nr, T* nb, int nbs, double* Q) {
   constexpr int RMAX = 2 * TI1 + 3;
   const int n2 = x.n2;
   const T* rr = x.rp + (x.jbase - x.rlo) * n2;  // tile row of jr = 0 (may precede the tile when not FULL)
@@ -443,7 +444,15 @@ __device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const
     if (!FULL && (j1 < x.rlo || j1 > x.rhi)) return 0.0;
     return double(base[2 * e * n2]);
   };
-  double aLc = ns(nl, 0), aRc = (PODD && x.has_right) ? ns(nr, 0) : aLc;
+  // left nodal values: an even plane reads its own slot and keeps them in
+  // this thread's private buffer nb (stride nbs) for the odd plane after it
+  auto nsl = [&](int e) -> double {
+    if (PODD) return double(nb[e * nbs]);
+    const double v = ns(nl, e);
+    nb[e * nbs] = T(v);
+    return v;
+  };
+  double aLc = nsl(0), aRc = (PODD && x.has_right) ? ns(nr, 0) : aLc;
   double aLn = 0.0, aRn = 0.0;
 #pragma unroll
   for (int jr = 0; jr < RMAX; ++jr, rr += n2) {
@@ -451,7 +460,7 @@ __device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const
     const bool o1 = jr & 1;
     const int ea = jr >> 1;
     if (!o1 && jr + 1 < RMAX) {
-      aLn = ns(nl, ea + 1);
+      aLn = nsl(ea + 1);
       aRn = (PODD && x.has_right) ? ns(nr, ea + 1) : aLn;
     }
     if (!FULL && (j1 < x.rlo || j1 > x.rhi)) {  // uniform
@@ -543,6 +552,7 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
   double* scan = tid2 + m2;
   int64_t* rowoff = reinterpret_cast<int64_t*>(scan + 64);
   PlanePipe* pp = reinterpret_cast<PlanePipe*>(rowoff + 2 * RMAX);
+  T* nb = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(pp) + 256) + threadIdx.x;
   (void)counter;
 
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -625,17 +635,14 @@ __global__ void __launch_bounds__(kPlaneMaxThreads, 2)
 #pragma unroll
     for (int ir = 0; ir < TI1; ++ir) Q[ir] = 0.0;
     if (p_odd) {
-      const T* nl = row0(d - 1);
-      const T* nr = x.has_right ? row0(d + 1) : nl;
-      if (full) dec_rows<T, TI1, true, true>(x, nl, nr, Q);
-      else dec_rows<T, TI1, true, false>(x, nl, nr, Q);
-      pipe_release<NS>(pp, d - 1, D, issue);  // the left even plane is done
-      pipe_release<NS>(pp, d, D, issue);
+      const T* nr = x.has_right ? row0(d + 1) : r_own;
+      if (full) dec_rows<T, TI1, true, true>(x, r_own, nr, nb, nt, Q);
+      else dec_rows<T, TI1, true, false>(x, r_own, nr, nb, nt, Q);
     } else {
-      if (full) dec_rows<T, TI1, false, true>(x, r_own, r_own, Q);
-      else dec_rows<T, TI1, false, false>(x, r_own, r_own, Q);
-      // an even plane stays resident for the odd plane after it
+      if (full) dec_rows<T, TI1, false, true>(x, r_own, r_own, nb, nt, Q);
+      else dec_rows<T, TI1, false, false>(x, r_own, r_own, nb, nt, Q);
     }
+    pipe_release<NS>(pp, d, D, issue);  // this warp is done with plane d's slot
     l0_plane<TI1>(g, ur, S, p, Q, A, jdone, acc, pp, tw2, tid2, G);
   }
 }
