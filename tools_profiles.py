@@ -8,37 +8,15 @@ import csv
 import json
 import sys
 
+from tools_ncu_csv import last_step, read_launches, short
+
 src, rnd = sys.argv[1], sys.argv[2]
-rows = list(csv.reader(open(src)))
-hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
-h = rows[hi]
-ki, mi, vi, idi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
-per = collections.OrderedDict()
-for r in rows[hi + 1:]:
-    if len(r) <= vi:
-        continue
-    per.setdefault((int(r[idi]), r[ki]), {})[r[mi]] = float(r[vi].replace(",", ""))
-items = list(per.items())
-# last step: from the last launch of the finest-level decompose plane kernel
-starts = [n for n, ((i, k), m) in enumerate(items) if "k_f3_dec_plane" in k]
-# the finest-level plane kernel is the first of a run of dec planes
-first_of_run = [n for n in starts if n == 0 or "k_f3_dec_plane" not in items[n - 3][0][1]]
-start = first_of_run[-1]
-step = items[start:]
-# decompose levels L..., recompose ...; tag by order of appearance per kernel name
-L = 9
-names = []
-dec_level = {}
-counter = collections.Counter()
+step = last_step(read_launches(src))
 out_rows = []
 traffic = {}
-for (i, k), m in step:
-    name = k.split("(")[0].replace("void mgrx_b200::", "").replace("<unnamed>::", "")
-    base = name.split("<")[0]
-    t = m.get("gpu__time_duration.sum", 0) / 1e3
-    rd = m.get("dram__bytes_read.sum", 0)
-    wr = m.get("dram__bytes_write.sum", 0)
-    out_rows.append((i, name, t, rd, wr))
+for i, k, m in step:
+    t = m.get("gpu__time_duration.sum", 0) * 1e6
+    out_rows.append((i, short(k), t, m.get("dram__bytes_read.sum", 0), m.get("dram__bytes_write.sum", 0)))
 tot = sum(r[2] for r in out_rows)
 with open(f"profiles/{rnd}_launches.md", "w") as f:
     f.write(f"# {rnd}: ncu launch list, one decompose + recompose step of the 513^3 fp32 bench\n\n")
