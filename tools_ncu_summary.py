@@ -7,7 +7,9 @@ import subprocess
 import sys
 
 csv.field_size_limit(10**9)
-WANT = [("gpu__time_duration.sum", "duration us", 1e-3),
+from tools_ncu_csv import SCALE
+
+WANT = [("gpu__time_duration.sum", "duration us", 1e6),
         ("dram__bytes_read.sum", "DRAM read MB", 1e-6),
         ("dram__bytes_write.sum", "DRAM write MB", 1e-6),
         ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % peak", 1),
@@ -23,7 +25,13 @@ WANT = [("gpu__time_duration.sum", "duration us", 1e-3),
 def raw(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    return dict(zip(rows[0], rows[2]))
+    vals = {}
+    for name, unit, val in zip(rows[0], rows[1], rows[2]):
+        try:
+            vals[name] = float(val.replace(",", "")) * SCALE.get(unit, 1.0)
+        except ValueError:
+            vals[name] = val
+    return vals
 
 
 def lines(rep, top=6):
@@ -58,18 +66,15 @@ def main():
           "Captured with tools_ncu_full.sh on the B200 box after the same bench command exited 0 without ncu.", ""]
     for rep in reps:
         v = raw(rep)
-        name = v.get("Kernel Name", rep)
+        name = str(v.get("Kernel Name", rep))
         md.append(f"## `{name[:90]}`")
         md.append("")
         md.append("| metric | value |")
         md.append("|---|---|")
         for key, label, sc in WANT:
-            if key in v and v[key]:
-                try:
-                    md.append(f"| {label} | {float(v[key].replace(',', '')) * sc:.1f} |")
-                except ValueError:
-                    pass
-        st = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(x or 0) for k, x in v.items()
+            if isinstance(v.get(key), float):
+                md.append(f"| {label} | {v[key] * sc:.1f} |")
+        st = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): (x if isinstance(x, float) else 0.0) for k, x in v.items()
               if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")}
         tot = sum(st.values()) or 1.0
         top = sorted(st.items(), key=lambda kv: -kv[1])[:6]
