@@ -363,7 +363,7 @@ def run_ours(args, ws, rank, local):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "field": list(DIMS), "field_dtype": FIELD_DTYPE,
                        "levels": h.num_levels(), "path": args.path,
-                       "l2": "inputs larger than L2 (540 MB field vs 126 MB L2); no flush",
+                       "l2": f"inputs larger than L2 ({nbytes / 1e6:.0f} MB field vs 126 MB L2); no flush",
                        "parallelism": f"batch: {ws} independent field(s), one per GPU, no collective",
                        "launch": "eager" if graph is None else "cuda_graph (one captured decompose+recompose step, replayed)",
                        "eager_ms_per_step": eager_ms},
@@ -442,9 +442,18 @@ def main():
     ap.add_argument("--path", choices=["auto", "general"], default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of CUDA-graph replay")
+    ap.add_argument("--dims", default="513,513,513",
+                    help="field extents (config-2 generator); 1025,1025,1025 is BASELINE config 5b")
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--warmup-ref", type=int, default=0, help="untimed reference steps (CPU code needs none)")
     args = ap.parse_args()
+    global DIMS, WORKLOAD
+    dims = tuple(int(x) for x in args.dims.split(","))
+    if dims != DIMS:
+        DIMS = dims
+        tag = "config5b" if dims == (1025, 1025, 1025) else "config2-generator"
+        WORKLOAD = (f"{tag}: {'x'.join(map(str, dims))} fp32 field (16 bumps + 8 oblique sine modes + 1e-4 noise), "
+                    "full decompose + recompose (stop 0)")
     if args.impl == "reference":
         # rank 0 alone runs the CPU reference; other torchrun ranks exit 0
         run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))

@@ -44,6 +44,10 @@ namespace mgrx_b200 {
 namespace {
 
 constexpr int kPlaneMaxThreads = 288;  // plane passes: up to 9 strips of 30 coarse columns, 2 CTAs per SM
+constexpr int kWideThreads = 576;      // wide rows (n2 <= 1079): up to 18 strips, 1 CTA per SM
+// register budget of the wide variants: launch bounds of 640 threads keep
+// ptxas at <= 96 registers (18 warps = 5 on some SM sub-partitions)
+constexpr int kWideBound = 640;
 constexpr int kColMaxM = 640;       // column passes: register-resident columns up to this length
 // column-pass block: 16 columns x S segments of up to LS registers, two
 // segments per warp row; LS = 16 for m <= 320, 32 for m <= 640
@@ -250,7 +254,7 @@ struct PlaneSmem {
     b += 2 * acc_elems(m2) * 8;     // finished coarse rows staged for the axis-2 solve
     b += 2 * size_t(m2) * 8;        // Thomas tables axis 2
     b += 64 * 8 + 2 * kRows * 8 + 256;  // scan scratch, row offsets, pipeline state
-    b += size_t(TI1 + 2) * kPlaneMaxThreads * sizeof(T);  // per-thread nodal values of the last even plane
+    b += size_t(TI1 + 2) * size_t((m2 + 29) / 30 * 32) * sizeof(T);  // per-thread nodal values of the last even plane
     return b;
   }
 };
@@ -534,8 +538,8 @@ __device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const
 
 // Decompose plane pass: one CTA per (axis-0 chunk, axis-1 tile) unit; the
 // unit's fine planes stream through a 3-deep TMA ring.
-template <typename T, int TI1>
-__global__ void __launch_bounds__(kPlaneMaxThreads, 2)
+template <typename T, int TI1, int MAXT>
+__global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
     k_f3_dec_plane(const T* __restrict__ blk, T* __restrict__ shell, T* __restrict__ coarse, double* __restrict__ G,
                    const double* __restrict__ w2g, const double* __restrict__ id2g, int* __restrict__ counter,
                    const F3Geom g) {
@@ -688,8 +692,8 @@ __device__ __forceinline__ void rec_rows(const T* ev, const T* od, int64_t st_e,
 // component read from the level's shell.  Per fine plane the tile's shell
 // rows form two contiguous runs (even fine rows, odd fine rows), fetched
 // with two bulk copies into one ring slot.
-template <typename T, int TI1>
-__global__ void __launch_bounds__(kPlaneMaxThreads, 2)
+template <typename T, int TI1, int MAXT>
+__global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
     k_f3_rec_plane(const T* __restrict__ shell, double* __restrict__ G, const double* __restrict__ w2g,
                    const double* __restrict__ id2g, int* __restrict__ counter, const F3Geom g) {
   using SM = PlaneSmem<T, TI1>;
@@ -869,8 +873,8 @@ __device__ __forceinline__ void interp_rows(const T* ev, const T* od, int64_t st
   }
 }
 
-template <typename T, int TRI>
-__global__ void __launch_bounds__(kPlaneMaxThreads, 3)
+template <typename T, int TRI, int MAXT>
+__global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 3 : 1)
     k_f3_rec_interp(const T* __restrict__ shell, const T* __restrict__ coarse, T* __restrict__ fine, const F3Geom g,
                     int ich, int ntile) {
   using SM = InterpSmem<T, TRI>;
@@ -1011,8 +1015,8 @@ void launch_row(double* G, const F3Geom& g, const double* w, const double* id, c
 // from its true carry.  With `coarse` set the result is applied:
 // coarse += sign * z (apply_correction, transform.hpp:435-477); otherwise it
 // is written back to G.
-template <typename T, int LS, bool APPLY>
-__global__ void __launch_bounds__(kColThreads, LS <= 16 ? 3 : 2)
+template <typename T, int LS, bool APPLY, int MAXT>
+__global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : 1)
     k_f3_col(double* __restrict__ G, T* __restrict__ coarse, double sign, int64_t ncols, int m, int64_t stride,
              int64_t outer_stride, int64_t inner, const double* __restrict__ w, const double* __restrict__ inv_d) {
   extern __shared__ double sc[];
@@ -1117,12 +1121,10 @@ size_t plane_smem(const F3Geom& g) {
 template <typename T>
 bool pick_tile(F3Geom& g, size_t optin, size_t per_sm) {
   const int warps = int((g.m2 + 29) / 30);
-  const int cands[4] = {8, 6, 4, 2};
+  const int cands[2] = {4, 2};
   double best = -1.0;
   for (int c : cands) {
     size_t need = 0;
-    if (c == 8) need = plane_smem<T, 8>(g);
-    if (c == 6) need = plane_smem<T, 6>(g);
     if (c == 4) need = plane_smem<T, 4>(g);
     if (c == 2) need = plane_smem<T, 2>(g);
     if (need > optin) continue;
@@ -1161,16 +1163,18 @@ void launch_col(double* G, T* coarse, double sign, const F3Geom& g, int axis, co
   }
   const unsigned blocks = unsigned((ncols + 15) / 16);
   const char* tag = axis == 1 ? "f3_col1" : "f3_col0";
-#define MGRX_COL(LS, AP)                                                                                  \
+// segments of <= 16 values: up to 10 warp rows (320 threads, 3 blocks/SM)
+  // for m <= 320, up to 20 (640 threads, 1 block/SM) for m <= 640
+#define MGRX_COL(AP, MT)                                                                                  \
   {                                                                                                       \
-    const int SY = (m + 2 * LS - 1) / (2 * LS);                                                          \
-    MGRX_LAUNCH(ex, tag, k_f3_col<T, LS, AP><<<blocks, dim3(32, SY), (2 * m + 2 * 2 * SY * 16) * 8, ex.s>>>( \
+    const int SY = (m + 2 * 16 - 1) / (2 * 16);                                                          \
+    MGRX_LAUNCH(ex, tag, k_f3_col<T, 16, AP, MT><<<blocks, dim3(32, SY), (2 * m + 2 * 2 * SY * 16) * 8, ex.s>>>( \
                              G, coarse, sign, ncols, m, stride, outer_stride, inner, w, id));             \
   }
   if (m <= 320) {
-    if (coarse) MGRX_COL(16, true) else MGRX_COL(16, false)
+    if (coarse) MGRX_COL(true, kColThreads) else MGRX_COL(false, kColThreads)
   } else {
-    if (coarse) MGRX_COL(32, true) else MGRX_COL(32, false)
+    if (coarse) MGRX_COL(true, 2 * kColThreads) else MGRX_COL(false, 2 * kColThreads)
   }
 #undef MGRX_COL
 }
@@ -1188,7 +1192,7 @@ Fused3DPlan fused3d_plan(const LevelGeom& lg, int esize) {
   g.m1 = lg.m[1];
   g.m2 = lg.m[2];
   if (g.n2 < 33 || g.m1 > kColMaxM || g.m0 > kColMaxM || g.n1 < 5 || g.n0 < 5) return fp;
-  if ((g.m2 + 29) / 30 * 32 > kPlaneMaxThreads) return fp;
+  if ((g.m2 + 29) / 30 * 32 > kWideThreads) return fp;
   // small levels stay on the general kernels (launch-latency bound either way)
   {
     int64_t min_elems = int64_t(1) << 15;
@@ -1240,10 +1244,11 @@ Fused3DPlan fused3d_plan(const LevelGeom& lg, int esize) {
 // Interpolation pass: TRI = 8 fine rows per tile (4 for fp64, keeping three
 // CTAs per SM); an even number of fine planes per unit, sized for about
 // eight units per resident CTA slot.
-template <typename T, int TRI>
+template <typename T, int TRI, int MAXT>
 static cudaError_t launch_interp_t(const T* shell, const T* coarse, T* fine, const F3Geom& g, const Exec& ex) {
   const size_t smem = InterpSmem<T, TRI>::bytes(g.n2, g.m2);
-  cudaError_t e = cudaFuncSetAttribute(k_f3_rec_interp<T, TRI>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaError_t e =
+      cudaFuncSetAttribute(k_f3_rec_interp<T, TRI, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -1254,31 +1259,36 @@ static cudaError_t launch_interp_t(const T* shell, const T* coarse, T* fine, con
   ich = std::max<int64_t>(2, std::min<int64_t>(32, ich & ~int64_t(1)));
   const int64_t chunks = (g.n0 + ich - 1) / ich;
   MGRX_LAUNCH(ex, "f3_rec_interp",
-              k_f3_rec_interp<T, TRI><<<unsigned(chunks * ntile), g.threads, smem, ex.s>>>(shell, coarse, fine, g,
+              k_f3_rec_interp<T, TRI, MAXT><<<unsigned(chunks * ntile), g.threads, smem, ex.s>>>(shell, coarse, fine, g,
                                                                                            int(ich), ntile));
   return cudaSuccess;
 }
 
 template <typename T>
 static cudaError_t launch_interp(const T* shell, const T* coarse, T* fine, const F3Geom& g, const Exec& ex) {
-  if (sizeof(T) == 4) return launch_interp_t<T, 8>(shell, coarse, fine, g, ex);
-  return launch_interp_t<T, 4>(shell, coarse, fine, g, ex);
+  if (g.threads > kPlaneMaxThreads) {
+    if (sizeof(T) == 4) return launch_interp_t<T, 8, kWideBound>(shell, coarse, fine, g, ex);
+    return launch_interp_t<T, 4, kWideBound>(shell, coarse, fine, g, ex);
+  }
+  if (sizeof(T) == 4) return launch_interp_t<T, 8, kPlaneMaxThreads>(shell, coarse, fine, g, ex);
+  return launch_interp_t<T, 4, kPlaneMaxThreads>(shell, coarse, fine, g, ex);
 }
 
 template <typename T>
 static cudaError_t set_attrs(const F3Geom& g, size_t* smem) {
   cudaError_t e = cudaSuccess;
-#define MGRX_ATTR(TI)                                                                                        \
-  if (g.tile_rows == TI) {                                                                                  \
+#define MGRX_ATTR(TI, MT)                                                                                      \
+  if (g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads)) {                        \
     *smem = plane_smem<T, TI>(g);                                                                           \
-    e = cudaFuncSetAttribute(k_f3_dec_plane<T, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(*smem)); \
+    e = cudaFuncSetAttribute(k_f3_dec_plane<T, TI, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(*smem)); \
     if (e == cudaSuccess)                                                                                   \
-      e = cudaFuncSetAttribute(k_f3_rec_plane<T, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(*smem)); \
+      e = cudaFuncSetAttribute(k_f3_rec_plane<T, TI, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                               int(*smem));                                                                 \
   }
-  MGRX_ATTR(8)
-  MGRX_ATTR(6)
-  MGRX_ATTR(4)
-  MGRX_ATTR(2)
+  MGRX_ATTR(4, kPlaneMaxThreads)
+  MGRX_ATTR(2, kPlaneMaxThreads)
+  MGRX_ATTR(4, kWideBound)
+  MGRX_ATTR(2, kWideBound)
 #undef MGRX_ATTR
   return e;
 }
@@ -1292,14 +1302,14 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
   size_t ds = 0;
   cudaError_t e = set_attrs<T>(g, &ds);
   if (e != cudaSuccess) return e;
-#define MGRX_DEC(TI)                                                                                   \
-  if (g.tile_rows == TI)                                                                              \
-    MGRX_LAUNCH(ex, "f3_dec_plane", k_f3_dec_plane<T, TI><<<g.grid, g.threads, ds, ex.s>>>(            \
+#define MGRX_DEC(TI, MT)                                                                               \
+  if (g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))                      \
+    MGRX_LAUNCH(ex, "f3_dec_plane", k_f3_dec_plane<T, TI, MT><<<g.grid, g.threads, ds, ex.s>>>(        \
                                         blk, shell, coarse, G, th.w[2], th.inv_d[2], counter, g));
-  MGRX_DEC(8)
-  MGRX_DEC(6)
-  MGRX_DEC(4)
-  MGRX_DEC(2)
+  MGRX_DEC(4, kPlaneMaxThreads)
+  MGRX_DEC(2, kPlaneMaxThreads)
+  MGRX_DEC(4, kWideBound)
+  MGRX_DEC(2, kWideBound)
 #undef MGRX_DEC
   launch_row(G, g, th.w[2], th.inv_d[2], ex);
   launch_col<T>(G, nullptr, 0.0, g, 1, th.w[1], th.inv_d[1], ex);
@@ -1316,14 +1326,14 @@ cudaError_t fused3d_recompose_level(const T* shell, T* coarse, T* fine, void* sc
   size_t ds = 0;
   cudaError_t e = set_attrs<T>(g, &ds);
   if (e != cudaSuccess) return e;
-#define MGRX_REC(TI)                                                                                   \
-  if (g.tile_rows == TI)                                                                              \
-    MGRX_LAUNCH(ex, "f3_rec_plane",                                                                   \
-                k_f3_rec_plane<T, TI><<<g.grid, g.threads, ds, ex.s>>>(shell, G, th.w[2], th.inv_d[2], counter, g));
-  MGRX_REC(8)
-  MGRX_REC(6)
-  MGRX_REC(4)
-  MGRX_REC(2)
+#define MGRX_REC(TI, MT)                                                                               \
+  if (g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))                      \
+    MGRX_LAUNCH(ex, "f3_rec_plane", k_f3_rec_plane<T, TI, MT><<<g.grid, g.threads, ds, ex.s>>>(        \
+                                        shell, G, th.w[2], th.inv_d[2], counter, g));
+  MGRX_REC(4, kPlaneMaxThreads)
+  MGRX_REC(2, kPlaneMaxThreads)
+  MGRX_REC(4, kWideBound)
+  MGRX_REC(2, kWideBound)
 #undef MGRX_REC
   launch_row(G, g, th.w[2], th.inv_d[2], ex);
   launch_col<T>(G, nullptr, 0.0, g, 1, th.w[1], th.inv_d[1], ex);

@@ -222,7 +222,8 @@ def test_config1_against_reference(torch, mg):
 
 
 FUSED_SHAPES = [(33, 33, 33), (65, 65, 65), (40, 36, 66), (35, 34, 100), (129, 65, 33), (6, 7, 300), (17, 100, 64),
-                (66, 66, 66), (5, 200, 34)]
+                (66, 66, 66), (5, 200, 34),
+                (9, 11, 700), (6, 9, 1025), (17, 12, 1079)]  # wide rows: 12..18 strips, one CTA per SM
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
