@@ -608,10 +608,14 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
     mbar_expect_tx(&pp->full[sl], bytes);
     bulk_g2s(raw + size_t(sl) * rawb, src, bytes, &pp->full[sl]);
   };
-  // tile row jbase of plane d, column 2 cc (the row may precede the slot when not FULL; never read then)
+  // tile row jbase of plane d, column 2 cc (the row may precede the slot
+  // when not FULL; never read then); the 16-byte lead of a plane's bulk copy
+  // advances by a constant per plane
+  const int row_off = (x.jbase - x.rlo) * n2 + 2 * cc;
+  const int lead0 = int(reinterpret_cast<uintptr_t>(tile_src(0)) & 15);
+  const int lead_inc = int((g.n1 * g.n2 * int64_t(sizeof(T))) & 15);
   auto row0 = [&](int d) {
-    return reinterpret_cast<const T*>(raw + size_t(pipe_slot<NS>(d)) * rawb) +
-           (reinterpret_cast<uintptr_t>(tile_src(d)) & 15) / sizeof(T) + (x.jbase - x.rlo) * n2 + 2 * cc;
+    return reinterpret_cast<const T*>(raw + pipe_slot<NS>(d) * int(rawb) + ((lead0 + d * lead_inc) & 15)) + row_off;
   };
   if (tid == 0)
     for (int d = 0; d <= min(D, NS - 1); ++d) issue(d);
@@ -619,35 +623,65 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
 #pragma unroll
   for (int ir = 0; ir < TI1; ++ir) A.prev[ir] = A.cur[ir] = A.next[ir] = 0.0;
   int jdone = 0;  // coarse planes finished by this CTA
-  for (int d = 0; d <= D; ++d) {
-    const int64_t p = ur.plo + d;  // plo is even
-    const bool p_odd = d & 1;
-    x.has_right = p_odd && (p + 1 <= g.n0 - 1);
-    mbar_wait(&pp->full[pipe_slot<NS>(d)], pipe_parity<NS>(d));
-    if (x.has_right) mbar_wait(&pp->full[pipe_slot<NS>(d + 1)], pipe_parity<NS>(d + 1));
-    const int64_t r0 = reord(p, g.m0);
-    const int e0 = x.jbase >> 1;  // even tile row 0 <-> coarse row e0
-    x.st_e = p_odd ? g.n2 : g.n2 - g.m2;
-    x.oofs = p_odd ? m2 : 0;
-    x.se = shell + (shell_row_start(g, r0, e0 + 1) - x.st_e) + cc;
-    x.so = shell + (shell_row_start(g, r0, g.m1 + e0 + 1) - g.n2) + cc;
-    x.cpe = coarse + ((p >> 1) * g.m1 + e0) * g.m2 + cc;
-    x.own = S.owned && p >= 2 * ur.a0 && p < 2 * ur.a1;
-    const T* r_own = row0(d);
-    x.rp = r_own - (x.jbase - x.rlo) * n2;
-    double Q[TI1];
+  // Shell / coarse pointers of the unit's first even and odd plane, advanced
+  // by a constant per plane pair (shell_row_start is linear in k = p / 2 for
+  // each parity: +n1 n2 - m1 m2 for even planes, +n1 n2 for odd ones).
+  const int e0 = x.jbase >> 1;  // even tile row 0 <-> coarse row e0
+  const int64_t k0 = ur.plo >> 1;
+  T* se_e = shell + (shell_row_start(g, k0, e0 + 1) - (g.n2 - g.m2)) + cc;
+  T* so_e = shell + (shell_row_start(g, k0, g.m1 + e0 + 1) - g.n2) + cc;
+  T* se_o = shell + (shell_row_start(g, g.m0 + k0, e0 + 1) - g.n2) + cc;
+  T* so_o = shell + (shell_row_start(g, g.m0 + k0, g.m1 + e0 + 1) - g.n2) + cc;
+  T* cpe = coarse + (k0 * g.m1 + e0) * g.m2 + cc;
+  const int64_t step_e = g.n1 * g.n2 - g.m1 * g.m2, step_o = g.n1 * g.n2, step_c = g.m1 * g.m2;
+  const int plo = int(ur.plo), n0 = int(g.n0), a0x2 = int(2 * ur.a0), a1x2 = int(2 * ur.a1);
+  for (int d = 0; d <= D; d += 2) {
+    {  // even plane p = plo + d
+      const int p = plo + d;
+      mbar_wait(&pp->full[pipe_slot<NS>(d)], pipe_parity<NS>(d));
+      x.has_right = false;
+      x.st_e = g.n2 - g.m2;
+      x.oofs = 0;
+      x.se = se_e;
+      x.so = so_e;
+      x.cpe = cpe;
+      x.own = S.owned && p >= a0x2 && p < a1x2;
+      const T* r_own = row0(d);
+      x.rp = r_own - (x.jbase - x.rlo) * n2;
+      double Q[TI1];
 #pragma unroll
-    for (int ir = 0; ir < TI1; ++ir) Q[ir] = 0.0;
-    if (p_odd) {
-      const T* nr = x.has_right ? row0(d + 1) : r_own;
-      if (full) dec_rows<T, TI1, true, true>(x, r_own, nr, nb, nt, Q);
-      else dec_rows<T, TI1, true, false>(x, r_own, nr, nb, nt, Q);
-    } else {
+      for (int ir = 0; ir < TI1; ++ir) Q[ir] = 0.0;
       if (full) dec_rows<T, TI1, false, true>(x, r_own, r_own, nb, nt, Q);
       else dec_rows<T, TI1, false, false>(x, r_own, r_own, nb, nt, Q);
+      pipe_release<NS>(pp, d, D, issue);  // this warp is done with plane d's slot
+      l0_plane<TI1>(g, ur, S, p, Q, A, jdone, acc, pp, tw2, tid2, G);
+      se_e += step_e;
+      so_e += step_e;
+      cpe += step_c;
     }
-    pipe_release<NS>(pp, d, D, issue);  // this warp is done with plane d's slot
-    l0_plane<TI1>(g, ur, S, p, Q, A, jdone, acc, pp, tw2, tid2, G);
+    if (d + 1 <= D) {  // odd plane p = plo + d + 1
+      const int p = plo + d + 1;
+      x.has_right = p + 1 <= n0 - 1;
+      mbar_wait(&pp->full[pipe_slot<NS>(d + 1)], pipe_parity<NS>(d + 1));
+      if (x.has_right) mbar_wait(&pp->full[pipe_slot<NS>(d + 2)], pipe_parity<NS>(d + 2));
+      x.st_e = g.n2;
+      x.oofs = m2;
+      x.se = se_o;
+      x.so = so_o;
+      x.own = S.owned && p >= a0x2 && p < a1x2;
+      const T* r_own = row0(d + 1);
+      x.rp = r_own - (x.jbase - x.rlo) * n2;
+      double Q[TI1];
+#pragma unroll
+      for (int ir = 0; ir < TI1; ++ir) Q[ir] = 0.0;
+      const T* nr = x.has_right ? row0(d + 2) : r_own;
+      if (full) dec_rows<T, TI1, true, true>(x, r_own, nr, nb, nt, Q);
+      else dec_rows<T, TI1, true, false>(x, r_own, nr, nb, nt, Q);
+      pipe_release<NS>(pp, d + 1, D, issue);
+      l0_plane<TI1>(g, ur, S, p, Q, A, jdone, acc, pp, tw2, tid2, G);
+      se_o += step_o;
+      so_o += step_o;
+    }
   }
 }
 
