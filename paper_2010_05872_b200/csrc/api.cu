@@ -228,12 +228,34 @@ struct mgrx_gpu_ctx {
   std::map<PlanKey, std::unique_ptr<Plan>> plans;
   Profiler prof;
   bool profiling = false;
+  // recompose: side streams for the levels' independent corrections
+  static constexpr int kSide = 4;
+  cudaStream_t side[kSide] = {};
+  cudaEvent_t fork = nullptr;
+  std::vector<cudaEvent_t> lvl_done;
 };
 
 namespace {
 
 Exec exec(mgrx_gpu_ctx* c, int level = -1) {
   return Exec{c->stream, &c->launches, c->profiling ? &c->prof : nullptr, level};
+}
+
+Exec exec_on(mgrx_gpu_ctx* c, cudaStream_t s, int level) {
+  return Exec{s, &c->launches, c->profiling ? &c->prof : nullptr, level};
+}
+
+void ensure_side(mgrx_gpu_ctx* c, int levels) {
+  if (!c->fork) {
+    for (int i = 0; i < mgrx_gpu_ctx::kSide; ++i)
+      cuda_check(cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking), "cudaStreamCreate(side)");
+    cuda_check(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming), "cudaEventCreate");
+  }
+  while (int(c->lvl_done.size()) < levels) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    c->lvl_done.push_back(e);
+  }
 }
 
 void set_device(mgrx_gpu_ctx* c) { cuda_check(cudaSetDevice(c->device), "cudaSetDevice"); }
@@ -529,12 +551,39 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
                                c->stream),
                "copy coarse");
   }
+  // Corrections of the fused levels below the finest depend only on their
+  // shells: fork them onto side streams (they overlap each other and the
+  // tail); the finest level's correction stays on the main stream.
+  std::vector<char> forked(L + 1, 0);
+  if (!nu && c->path == 0) {
+    int nf = 0;
+    for (int l = stop + 1; l < L; ++l) nf += p.fused[l].enabled ? 1 : 0;
+    if (nf > 0) {
+      ensure_side(c, L + 1);
+      cuda_check(cudaEventRecord(c->fork, c->stream), "cudaEventRecord(fork)");
+      int k = 0;
+      for (int l = L - 1; l > stop; --l) {
+        const Fused3DPlan& fp = p.fused[l];
+        if (!fp.enabled) continue;
+        cudaStream_t sd = c->side[k++ % mgrx_gpu_ctx::kSide];
+        cuda_check(cudaStreamWaitEvent(sd, c->fork, 0), "cudaStreamWaitEvent");
+        cuda_check(fused3d_recompose_correction<T>(d_coeffs + h.node[l - 1], s + fp.scratch_off, fp, p.thomas[l],
+                                                   exec_on(c, sd, l)),
+                   "recompose correction");
+        cuda_check(cudaEventRecord(c->lvl_done[l], sd), "cudaEventRecord");
+        forked[l] = 1;
+      }
+    }
+  }
   for (int l = l0; l <= L; ++l) {
     const T* shell = d_coeffs + h.node[l - 1];
     T* fine = (l == L) ? d_field : reinterpret_cast<T*>(s + p.blk_off[l]);
     const Fused3DPlan& fp = p.fused[l];
     cudaError_t e;
-    if (!nu && c->path == 0 && fp.enabled) {
+    if (forked[l]) {
+      cuda_check(cudaStreamWaitEvent(c->stream, c->lvl_done[l], 0), "cudaStreamWaitEvent");
+      e = fused3d_recompose_finish<T>(shell, coarse, fine, s + fp.scratch_off, fp, p.thomas[l], exec(c, l));
+    } else if (!nu && c->path == 0 && fp.enabled) {
       e = fused3d_recompose_level<T>(shell, coarse, fine, s + fp.scratch_off, p.geom[l], fp, p.thomas[l],
                                      exec(c, l));
     } else {
@@ -628,6 +677,10 @@ int mgrx_gpu_ctx_destroy(mgrx_gpu_ctx* c) {
   if (c->nu_tables) cudaFree(c->nu_tables);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->own) cudaStreamDestroy(c->own);
+  for (int i = 0; i < mgrx_gpu_ctx::kSide; ++i)
+    if (c->side[i]) cudaStreamDestroy(c->side[i]);
+  if (c->fork) cudaEventDestroy(c->fork);
+  for (cudaEvent_t e : c->lvl_done) cudaEventDestroy(e);
   delete c;
   return MGRX_OK;
 }

@@ -1351,9 +1351,13 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
   return cudaGetLastError();
 }
 
+// Recompose correction of a level (rec plane + row + axis-1 column pass,
+// into the level's G): depends only on the level's shell, so the levels'
+// corrections may run concurrently (transform.hpp:343-366: the component
+// is zero on the coarse nodes).
 template <typename T>
-cudaError_t fused3d_recompose_level(const T* shell, T* coarse, T* fine, void* scratch, const LevelGeom&,
-                                    const Fused3DPlan& fp, const ThomasLevel& th, const Exec& ex) {
+cudaError_t fused3d_recompose_correction(const T* shell, void* scratch, const Fused3DPlan& fp, const ThomasLevel& th,
+                                         const Exec& ex) {
   const F3Geom& g = fp.g;
   double* G = static_cast<double*>(scratch);
   int* counter = reinterpret_cast<int*>(static_cast<char*>(scratch) + size_t(g.m0) * g.m1 * g.m2 * 8);
@@ -1370,18 +1374,39 @@ cudaError_t fused3d_recompose_level(const T* shell, T* coarse, T* fine, void* sc
   MGRX_REC(2, kWideBound)
 #undef MGRX_REC
   launch_row(G, g, th.w[2], th.inv_d[2], ex);
-  launch_col<T>(G, nullptr, 0.0, g, 1, th.w[1], th.inv_d[1], ex);
+  launch_col<T>(G, static_cast<T*>(nullptr), 0.0, g, 1, th.w[1], th.inv_d[1], ex);
+  return cudaGetLastError();
+}
+
+// The sequential part: axis-0 solve + coarse -= z, then interpolation.
+template <typename T>
+cudaError_t fused3d_recompose_finish(const T* shell, T* coarse, T* fine, void* scratch, const Fused3DPlan& fp,
+                                     const ThomasLevel& th, const Exec& ex) {
+  const F3Geom& g = fp.g;
+  double* G = static_cast<double*>(scratch);
   launch_col<T>(G, coarse, -1.0, g, 0, th.w[0], th.inv_d[0], ex);
-  e = launch_interp<T>(shell, coarse, fine, g, ex);
+  cudaError_t e = launch_interp<T>(shell, coarse, fine, g, ex);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t fused3d_recompose_level(const T* shell, T* coarse, T* fine, void* scratch, const LevelGeom&,
+                                    const Fused3DPlan& fp, const ThomasLevel& th, const Exec& ex) {
+  cudaError_t e = fused3d_recompose_correction<T>(shell, scratch, fp, th, ex);
+  if (e != cudaSuccess) return e;
+  return fused3d_recompose_finish<T>(shell, coarse, fine, scratch, fp, th, ex);
 }
 
 #define MGRX_INST(T)                                                                                     \
   template cudaError_t fused3d_decompose_level<T>(const T*, T*, T*, void*, const LevelGeom&, const Fused3DPlan&, \
                                                   const ThomasLevel&, const Exec&);                      \
   template cudaError_t fused3d_recompose_level<T>(const T*, T*, T*, void*, const LevelGeom&, const Fused3DPlan&, \
-                                                  const ThomasLevel&, const Exec&);
+                                                  const ThomasLevel&, const Exec&);                      \
+  template cudaError_t fused3d_recompose_correction<T>(const T*, void*, const Fused3DPlan&, const ThomasLevel&,   \
+                                                       const Exec&);                                     \
+  template cudaError_t fused3d_recompose_finish<T>(const T*, T*, T*, void*, const Fused3DPlan&, const ThomasLevel&, \
+                                                   const Exec&);
 MGRX_INST(float)
 MGRX_INST(double)
 #undef MGRX_INST

@@ -37,5 +37,12 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
 template <typename T>
 cudaError_t fused3d_recompose_level(const T* shell, T* coarse, T* fine, void* scratch, const LevelGeom& g,
                                     const Fused3DPlan& fp, const ThomasLevel& th, const Exec& ex);
+// recompose_level split in its shell-only correction and the sequential finish
+template <typename T>
+cudaError_t fused3d_recompose_correction(const T* shell, void* scratch, const Fused3DPlan& fp, const ThomasLevel& th,
+                                         const Exec& ex);
+template <typename T>
+cudaError_t fused3d_recompose_finish(const T* shell, T* coarse, T* fine, void* scratch, const Fused3DPlan& fp,
+                                     const ThomasLevel& th, const Exec& ex);
 
 }  // namespace mgrx_b200
