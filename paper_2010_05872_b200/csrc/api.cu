@@ -557,12 +557,12 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
   std::vector<char> forked(L + 1, 0);
   if (!nu && c->path == 0) {
     int nf = 0;
-    for (int l = stop + 1; l < L; ++l) nf += p.fused[l].enabled ? 1 : 0;
+    for (int l = stop + 1; l <= L; ++l) nf += p.fused[l].enabled ? 1 : 0;
     if (nf > 0) {
       ensure_side(c, L + 1);
       cuda_check(cudaEventRecord(c->fork, c->stream), "cudaEventRecord(fork)");
       int k = 0;
-      for (int l = L - 1; l > stop; --l) {
+      for (int l = L; l > stop; --l) {
         const Fused3DPlan& fp = p.fused[l];
         if (!fp.enabled) continue;
         cudaStream_t sd = c->side[k++ % mgrx_gpu_ctx::kSide];
