@@ -554,8 +554,9 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
   // Corrections of the fused levels below the finest depend only on their
   // shells: fork them onto side streams (they overlap each other and the
   // tail); the finest level's correction stays on the main stream.
+  // (not while profiling: per-kernel event times need the serial order)
   std::vector<char> forked(L + 1, 0);
-  if (!nu && c->path == 0) {
+  if (!nu && c->path == 0 && !c->profiling) {
     int nf = 0;
     for (int l = stop + 1; l <= L; ++l) nf += p.fused[l].enabled ? 1 : 0;
     if (nf > 0) {

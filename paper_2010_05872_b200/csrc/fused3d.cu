@@ -248,12 +248,9 @@ struct PlaneSmem {
     const size_t d = kDecSlots * dec_raw_bytes(n2), r = kRecSlots * raw_bytes(n2);
     return d > r ? d : r;
   }
-  static __host__ __device__ size_t acc_elems(int64_t) { return 0; }
   static __host__ __device__ size_t bytes(int64_t n2, int64_t m2) {
     size_t b = ring_bytes(n2);      // TMA ring of fine plane tiles / shell runs
-    b += 2 * acc_elems(m2) * 8;     // finished coarse rows staged for the axis-2 solve
-    b += 2 * size_t(m2) * 8;        // Thomas tables axis 2
-    b += 64 * 8 + 2 * kRows * 8 + 256;  // scan scratch, row offsets, pipeline state
+    b += 256;                       // pipeline state (PlanePipe)
     b += size_t(TI1 + 2) * size_t((m2 + 29) / 30 * 32) * sizeof(T);  // per-thread nodal values of the last even plane
     return b;
   }
@@ -341,12 +338,7 @@ struct PlanePipe {
 // pass needs no CTA-wide barrier.
 template <int TI1>
 __device__ __forceinline__ void l0_complete(const F3Geom& g, const UnitRange& ur, const StripLane& S,
-                                            const double* v, int64_t i0, int& j, double* tb, PlanePipe* pp,
-                                            const double* tw2, const double* tid2, double* __restrict__ G) {
-  (void)tb;
-  (void)pp;
-  (void)tw2;
-  (void)tid2;
+                                            const double* v, int64_t i0, int& j, double* __restrict__ G) {
   const int TR = int(ur.b1 - ur.b0);
   if (S.owned) {
     double* gp = G + (i0 * g.m1 + ur.b0) * g.m2 + S.c;
@@ -359,8 +351,7 @@ __device__ __forceinline__ void l0_complete(const F3Geom& g, const UnitRange& ur
 
 template <int TI1>
 __device__ __forceinline__ void l0_plane(const F3Geom& g, const UnitRange& ur, const StripLane& S, int64_t p,
-                                         const double* Q, L0Planes<TI1>& A, int& j, double* tb, PlanePipe* pp,
-                                         const double* tw2, const double* tid2, double* __restrict__ G) {
+                                         const double* Q, L0Planes<TI1>& A, int& j, double* __restrict__ G) {
   const int64_t k = p >> 1;
   const bool last = p == g.n0 - 1;
   if (!(p & 1)) {
@@ -371,15 +362,15 @@ __device__ __forceinline__ void l0_plane(const F3Geom& g, const UnitRange& ur, c
       A.cur[ir] += wc * Q[ir];
       A.next[ir] += kW12 * Q[ir];
     }
-    if (k - 1 >= ur.a0 && k - 1 < ur.a1) l0_complete<TI1>(g, ur, S, A.prev, k - 1, j, tb, pp, tw2, tid2, G);
-    if (last && k >= ur.a0 && k < ur.a1) l0_complete<TI1>(g, ur, S, A.cur, k, j, tb, pp, tw2, tid2, G);
+    if (k - 1 >= ur.a0 && k - 1 < ur.a1) l0_complete<TI1>(g, ur, S, A.prev, k - 1, j, G);
+    if (last && k >= ur.a0 && k < ur.a1) l0_complete<TI1>(g, ur, S, A.cur, k, j, G);
   } else {
 #pragma unroll
     for (int ir = 0; ir < TI1; ++ir) {
       A.cur[ir] += 0.5 * Q[ir];
       A.next[ir] += 0.5 * Q[ir];
     }
-    if (last && k >= ur.a0 && k < ur.a1) l0_complete<TI1>(g, ur, S, A.cur, k, j, tb, pp, tw2, tid2, G);
+    if (last && k >= ur.a0 && k < ur.a1) l0_complete<TI1>(g, ur, S, A.cur, k, j, G);
 #pragma unroll
     for (int ir = 0; ir < TI1; ++ir) {
       A.prev[ir] = A.cur[ir];
@@ -541,7 +532,6 @@ __device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const
 template <typename T, int TI1, int MAXT>
 __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
     k_f3_dec_plane(const T* __restrict__ blk, T* __restrict__ shell, T* __restrict__ coarse, double* __restrict__ G,
-                   const double* __restrict__ w2g, const double* __restrict__ id2g, int* __restrict__ counter,
                    const F3Geom g) {
   using SM = PlaneSmem<T, TI1>;
   constexpr int RMAX = SM::kRows;
@@ -550,22 +540,11 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
   const int m2 = int(g.m2), n2 = int(g.n2), n1 = int(g.n1), m1 = int(g.m1);
   const size_t rawb = SM::dec_raw_bytes(g.n2);
   unsigned char* raw = smem;
-  double* acc = reinterpret_cast<double*>(smem + SM::ring_bytes(g.n2));
-  double* tw2 = acc + 2 * SM::acc_elems(g.m2);
-  double* tid2 = tw2 + m2;
-  double* scan = tid2 + m2;
-  int64_t* rowoff = reinterpret_cast<int64_t*>(scan + 64);
-  PlanePipe* pp = reinterpret_cast<PlanePipe*>(rowoff + 2 * RMAX);
+  PlanePipe* pp = reinterpret_cast<PlanePipe*>(smem + SM::ring_bytes(g.n2));
   T* nb = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(pp) + 256) + threadIdx.x;
-  (void)counter;
-
   const int tid = threadIdx.x, nt = blockDim.x;
   const StripLane S = strip_lane(m2);
   const int c = S.c;
-  for (int i = tid; i < m2; i += nt) {
-    tw2[i] = w2g[i];
-    tid2[i] = id2g[i];
-  }
   const UnitRange ur = unit_range(g, int(blockIdx.x));
   if (tid == 0) {
     for (int b = 0; b < NS; ++b) {
@@ -654,7 +633,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
       if (full) dec_rows<T, TI1, false, true>(x, r_own, r_own, nb, nt, Q);
       else dec_rows<T, TI1, false, false>(x, r_own, r_own, nb, nt, Q);
       pipe_release<NS>(pp, d, D, issue);  // this warp is done with plane d's slot
-      l0_plane<TI1>(g, ur, S, p, Q, A, jdone, acc, pp, tw2, tid2, G);
+      l0_plane<TI1>(g, ur, S, p, Q, A, jdone, G);
       se_e += step_e;
       so_e += step_e;
       cpe += step_c;
@@ -678,7 +657,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
       if (full) dec_rows<T, TI1, true, true>(x, r_own, nr, nb, nt, Q);
       else dec_rows<T, TI1, true, false>(x, r_own, nr, nb, nt, Q);
       pipe_release<NS>(pp, d + 1, D, issue);
-      l0_plane<TI1>(g, ur, S, p, Q, A, jdone, acc, pp, tw2, tid2, G);
+      l0_plane<TI1>(g, ur, S, p, Q, A, jdone, G);
       se_o += step_o;
       so_o += step_o;
     }
@@ -728,32 +707,21 @@ __device__ __forceinline__ void rec_rows(const T* ev, const T* od, int64_t st_e,
 // with two bulk copies into one ring slot.
 template <typename T, int TI1, int MAXT>
 __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
-    k_f3_rec_plane(const T* __restrict__ shell, double* __restrict__ G, const double* __restrict__ w2g,
-                   const double* __restrict__ id2g, int* __restrict__ counter, const F3Geom g) {
+    k_f3_rec_plane(const T* __restrict__ shell, double* __restrict__ G, const F3Geom g) {
   using SM = PlaneSmem<T, TI1>;
   constexpr int RMAX = SM::kRows;
   extern __shared__ __align__(128) unsigned char smem[];
   const int m2 = int(g.m2), n2 = int(g.n2), m1 = int(g.m1);
   const size_t rawb = SM::raw_bytes(g.n2);
   unsigned char* raw = smem;
-  double* acc = reinterpret_cast<double*>(smem + SM::ring_bytes(g.n2));
   constexpr int NS = SM::kRecSlots;
-  double* tw2 = acc + 2 * SM::acc_elems(g.m2);
-  double* tid2 = tw2 + m2;
-  double* scan = tid2 + m2;
-  int64_t* rowoff = reinterpret_cast<int64_t*>(scan + 64);
-  PlanePipe* pp = reinterpret_cast<PlanePipe*>(rowoff + 2 * RMAX);
-  (void)counter;
+  PlanePipe* pp = reinterpret_cast<PlanePipe*>(smem + SM::ring_bytes(g.n2));
 
   const int tid = threadIdx.x, nt = blockDim.x;
   const StripLane S = strip_lane(m2);
   const int c = S.c;
   const int cc = S.valid ? c : 0;
   const bool has_odd = S.valid && 2 * c + 1 < n2;
-  for (int i = tid; i < m2; i += nt) {
-    tw2[i] = w2g[i];
-    tid2[i] = id2g[i];
-  }
   const UnitRange ur = unit_range(g, int(blockIdx.x));
   if (tid == 0) {
     for (int b = 0; b < NS; ++b) {
@@ -840,7 +808,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
       else rec_rows<T, TI1, false, false>(ev, od, st_e, n2, m2, jbase, rlo, rhi, b0, TR, m1, c, S.valid, has_odd, Q);
     }
     pipe_release<NS>(pp, d, D, issue);
-    l0_plane<TI1>(g, ur, S, p, Q, A, jdone, acc, pp, tw2, tid2, G);
+    l0_plane<TI1>(g, ur, S, p, Q, A, jdone, G);
   }
 }
 
@@ -1332,14 +1300,13 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
                                     const Fused3DPlan& fp, const ThomasLevel& th, const Exec& ex) {
   const F3Geom& g = fp.g;
   double* G = static_cast<double*>(scratch);
-  int* counter = reinterpret_cast<int*>(static_cast<char*>(scratch) + size_t(g.m0) * g.m1 * g.m2 * 8);
   size_t ds = 0;
   cudaError_t e = set_attrs<T>(g, &ds);
   if (e != cudaSuccess) return e;
 #define MGRX_DEC(TI, MT)                                                                               \
   if (g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))                      \
     MGRX_LAUNCH(ex, "f3_dec_plane", k_f3_dec_plane<T, TI, MT><<<g.grid, g.threads, ds, ex.s>>>(        \
-                                        blk, shell, coarse, G, th.w[2], th.inv_d[2], counter, g));
+                                        blk, shell, coarse, G, g));
   MGRX_DEC(4, kPlaneMaxThreads)
   MGRX_DEC(2, kPlaneMaxThreads)
   MGRX_DEC(4, kWideBound)
@@ -1360,14 +1327,13 @@ cudaError_t fused3d_recompose_correction(const T* shell, void* scratch, const Fu
                                          const Exec& ex) {
   const F3Geom& g = fp.g;
   double* G = static_cast<double*>(scratch);
-  int* counter = reinterpret_cast<int*>(static_cast<char*>(scratch) + size_t(g.m0) * g.m1 * g.m2 * 8);
   size_t ds = 0;
   cudaError_t e = set_attrs<T>(g, &ds);
   if (e != cudaSuccess) return e;
 #define MGRX_REC(TI, MT)                                                                               \
   if (g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))                      \
     MGRX_LAUNCH(ex, "f3_rec_plane", k_f3_rec_plane<T, TI, MT><<<g.grid, g.threads, ds, ex.s>>>(        \
-                                        shell, G, th.w[2], th.inv_d[2], counter, g));
+                                        shell, G, g));
   MGRX_REC(4, kPlaneMaxThreads)
   MGRX_REC(2, kPlaneMaxThreads)
   MGRX_REC(4, kWideBound)
