@@ -1225,10 +1225,12 @@ Fused3DPlan fused3d_plan(const LevelGeom& lg, int esize) {
   // pipeline fill; pick c minimising waves x per-unit time.
   int64_t chunk = 1;
   double best = 1e300;
+  double fill_planes = 3.0;  // pipeline fill of a unit, in plane-times (MGRX_FILL_PLANES overrides)
+  if (const char* env = std::getenv("MGRX_FILL_PLANES")) fill_planes = std::atof(env);
   for (int64_t c = 1; c <= 32 && c <= g.m0; ++c) {
     const int64_t units = ((g.m0 + c - 1) / c) * g.ntile1;
     const int64_t waves = (units + ctas - 1) / ctas;
-    const double cost = double(waves) * double(2 * c + 3 + 3);
+    const double cost = double(waves) * double(2 * c + 3 + fill_planes);
     if (cost < best - 1e-9) {
       best = cost;
       chunk = c;
@@ -1256,7 +1258,9 @@ static cudaError_t launch_interp_t(const T* shell, const T* coarse, T* fine, con
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int ntile = int((g.n1 + TRI - 1) / TRI);
-  const int64_t want = int64_t(sms) * 3 * 8;
+  int64_t per_slot = 8;  // units per resident CTA slot (MGRX_INTERP_UNITS overrides)
+  if (const char* env = std::getenv("MGRX_INTERP_UNITS")) per_slot = std::max(1, std::atoi(env));
+  const int64_t want = int64_t(sms) * 3 * per_slot;
   int64_t ich = (g.n0 * ntile) / want;
   ich = std::max<int64_t>(2, std::min<int64_t>(32, ich & ~int64_t(1)));
   const int64_t chunks = (g.n0 + ich - 1) / ich;
