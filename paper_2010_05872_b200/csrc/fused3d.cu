@@ -330,7 +330,9 @@ struct PlanePipe {
   uint64_t full[4];
   int cnt[4];
   ShellLin lin[4];  // recompose: shell run bounds of the unit's rows
+  int lead[4][4];   // interpolation: 16-byte leads of the runs in slot s (written by the issuing thread)
 };
+static_assert(sizeof(PlanePipe) <= 256, "PlaneSmem reserves 256 bytes for the pipeline state");
 
 // A finished coarse plane (the j-th of this CTA): every owned lane stores
 // its rows of the axis-0/1/2 load vector to G.  The axis-2 solve of these
@@ -830,7 +832,7 @@ struct InterpSmem {
   static __host__ __device__ size_t ev_bytes(int64_t n2) { return run_bytes(TRI / 2, n2); }
   static __host__ __device__ size_t co_bytes(int64_t m2) { return run_bytes(NE, m2); }
   static __host__ __device__ size_t slot_bytes(int64_t n2, int64_t m2) { return 2 * ev_bytes(n2) + co_bytes(m2); }
-  static __host__ __device__ size_t bytes(int64_t n2, int64_t m2) { return NS * slot_bytes(n2, m2) + 128; }
+  static __host__ __device__ size_t bytes(int64_t n2, int64_t m2) { return NS * slot_bytes(n2, m2) + sizeof(PlanePipe); }
 };
 
 template <typename T, int TRI, bool PODD, bool FULL>
@@ -930,8 +932,11 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 3 : 1)
     bulk_span<T>(coarse, x.cs, int64_t(nc) * g.m2, &s2, &b2, &ld);
     const int sl = pipe_slot<NS>(d);
     unsigned char* dst = smem + size_t(sl) * slotb;
+    pp->lead[sl][0] = int(reinterpret_cast<uintptr_t>(shell + x.se) & 15);
+    pp->lead[sl][1] = int(reinterpret_cast<uintptr_t>(shell + x.so) & 15);
+    pp->lead[sl][2] = int(reinterpret_cast<uintptr_t>(coarse + x.cs) & 15);
     fence_proxy_async();
-    mbar_expect_tx(&pp->full[sl], b0 + b1 + b2);
+    mbar_expect_tx(&pp->full[sl], b0 + b1 + b2);  // release: the leads are visible to the waiters
     bulk_g2s(dst, s0, b0, &pp->full[sl]);
     if (x.lo > 0) bulk_g2s(dst + evb, s1, b1, &pp->full[sl]);
     bulk_g2s(dst + 2 * evb, s2, b2, &pp->full[sl]);
@@ -947,12 +952,11 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 3 : 1)
     const bool p_odd = d & 1;
     const int sl = pipe_slot<NS>(d);
     mbar_wait(&pp->full[sl], pipe_parity<NS>(d));
-    const Src x = src(d);
-    const unsigned char* slot = smem + size_t(sl) * slotb;
-    auto lead = [&](const T* base, int64_t off) { return int((reinterpret_cast<uintptr_t>(base + off) & 15) / sizeof(T)); };
-    const T* ev = reinterpret_cast<const T*>(slot) + lead(shell, x.se) + cc;
-    const T* od = reinterpret_cast<const T*>(slot + evb) + lead(shell, x.so) + cc;
-    const T* co = reinterpret_cast<const T*>(slot + 2 * evb) + lead(coarse, x.cs) + cc;
+    const unsigned char* slot = smem + sl * int(slotb);
+    const volatile int* ld = pp->lead[sl];
+    const T* ev = reinterpret_cast<const T*>(slot + ld[0]) + cc;
+    const T* od = reinterpret_cast<const T*>(slot + evb + ld[1]) + cc;
+    const T* co = reinterpret_cast<const T*>(slot + 2 * evb + ld[2]) + cc;
     double C[NE];
 #pragma unroll
     for (int e = 0; e < NE; ++e) C[e] = (e < nc) ? double(co[e * m2]) : 0.0;
