@@ -773,10 +773,13 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
     bulk_span<T>(shell, x.se, x.le, &src0, &b0b, &ld);
     if (x.lo > 0) bulk_span<T>(shell, x.so, x.lo, &src1, &b1b, &ld);
     unsigned char* dst = raw + size_t(sl) * rawb;
+    const uint32_t oso = odd_slot_off(x);
+    pp->lead[sl][0] = int(reinterpret_cast<uintptr_t>(shell + x.se) & 15);
+    pp->lead[sl][1] = int(oso + (reinterpret_cast<uintptr_t>(shell + x.so) & 15));
     fence_proxy_async();
-    mbar_expect_tx(&pp->full[sl], b0b + b1b);
+    mbar_expect_tx(&pp->full[sl], b0b + b1b);  // release: the leads are visible to the waiters
     bulk_g2s(dst, src0, b0b, &pp->full[sl]);
-    if (x.lo > 0) bulk_g2s(dst + odd_slot_off(x), src1, b1b, &pp->full[sl]);
+    if (x.lo > 0) bulk_g2s(dst + oso, src1, b1b, &pp->full[sl]);
   };
   if (tid == 0)
     for (int d = 0; d <= min(D, NS - 1); ++d) issue(d);
@@ -788,13 +791,13 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
     const int64_t p = ur.plo + d;
     mbar_wait(&pp->full[pipe_slot<NS>(d)], pipe_parity<NS>(d));
     const bool p_odd = p & 1;
-    const Runs x = runs(p);
-    const unsigned char* slot = raw + size_t(pipe_slot<NS>(d)) * rawb;
+    const int sl = pipe_slot<NS>(d);
+    const unsigned char* slot = raw + sl * int(rawb);
+    const volatile int* ld = pp->lead[sl];
     // slot positions of even tile row e = 0 (fine row jbase) and odd e = 0 (jbase + 1)
     const int64_t st_e = p_odd ? g.n2 : g.n2 - g.m2;
-    const T* evrun = reinterpret_cast<const T*>(slot) + (reinterpret_cast<uintptr_t>(shell + x.se) & 15) / sizeof(T);
-    const T* odrun = reinterpret_cast<const T*>(slot + odd_slot_off(x)) +
-                     (reinterpret_cast<uintptr_t>(shell + x.so) & 15) / sizeof(T);
+    const T* evrun = reinterpret_cast<const T*>(slot + ld[0]);
+    const T* odrun = reinterpret_cast<const T*>(slot + ld[1]);
     // even run starts at fine row 2 e_lo = rlo (rlo is even); jbase may be rlo - 2
     const T* ev = evrun + (int64_t((jbase - rlo) >> 1)) * st_e + cc;
     // odd run starts at fine row 2 o_lo + 1; tile odd row e = 0 is fine row jbase + 1
