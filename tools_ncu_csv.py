@@ -32,8 +32,10 @@ def nbytes(m):
 
 
 def last_step(items):
-    """Launches of the last step: from the last finest-level decompose plane
-    launch (the dec-plane launch moving the most bytes) to the end."""
+    """Launches of the last step (library kernels only): from the last
+    finest-level decompose plane launch (the dec-plane launch moving the most
+    bytes) to the end."""
+    items = [it for it in items if "mgrx_b200" in it[1] or "k_f3_" in it[1] or "k_tail" in it[1]]
     dec = [n for n, (i, k, m) in enumerate(items) if "dec_plane" in k or "k_dec_coef" in k]
     if not dec:
         return items

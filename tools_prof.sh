@@ -1,7 +1,7 @@
 #!/bin/bash
 # Profiling helper run on the GPU box (see profiles/README.md).
 set -x
-CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline"
+CMD="python tools_step.py"
 $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1

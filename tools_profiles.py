@@ -31,12 +31,11 @@ with open(f"profiles/{rnd}_launches.md", "w") as f:
 dec = [r for r in out_rows if r[1].startswith("k_f3_dec_plane")]
 rec = [r for r in out_rows if r[1].startswith("k_f3_rec_plane")]
 itp = [r for r in out_rows if r[1].startswith("k_f3_rec_interp")]
-if dec:
-    traffic["f3_dec_plane@9"] = dec[0][3] + dec[0][4]
-if rec:
-    traffic["f3_rec_plane@9"] = rec[-1][3] + rec[-1][4]
-if itp:
-    traffic["f3_rec_interp@9"] = itp[-1][3] + itp[-1][4]
+# the finest level's launch of each kind moves the most bytes
+for tag, rows_ in (("f3_dec_plane@9", dec), ("f3_rec_plane@9", rec), ("f3_rec_interp@9", itp)):
+    if rows_:
+        r = max(rows_, key=lambda r: r[3] + r[4])
+        traffic[tag] = r[3] + r[4]
 json.dump({"round": rnd, "source": f"profiles/{rnd}_launches.md", "kernels": traffic}, open("profiles/traffic.json", "w"),
           indent=1)
 print(open(f"profiles/{rnd}_launches.md").read()[-1500:])
