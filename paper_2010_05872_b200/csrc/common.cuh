@@ -108,6 +108,31 @@ void prof_mark(const Exec& ex, const char* tag, bool begin);
     if ((ex).prof) prof_mark(ex, tag, false); \
   } while (0)
 
+// Programmatic dependent launch: kernels of a level chain are launched with
+// programmatic stream serialization, so the next kernel's CTAs are launched
+// (and run their prologue) while the previous kernel drains; they call
+// pdl_wait() before touching memory the previous kernel writes or reads
+// (griddepcontrol.wait returns once the previous grid has completed and its
+// memory is visible; a no-op when launched without the attribute).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 inline int grid_for(int64_t work, int block, int per_sm = 16) {
   int64_t g = (work + block - 1) / block;
   const int64_t cap = int64_t(kNumSMs) * per_sm;

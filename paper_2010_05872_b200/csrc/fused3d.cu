@@ -556,6 +556,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();
 
   const int R = int(ur.rhi - ur.rlo + 1);
   DecRows<T> x;
@@ -664,6 +665,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
       so_o += step_o;
     }
   }
+  pdl_trigger();
 }
 
 // Rows of one fine plane (recompose plane pass): component from the shell
@@ -737,6 +739,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
     pp->lin[3] = shell_lin(g, g.m1 + ((ur.rhi - 1) >> 1) + 1);
   }
   __syncthreads();
+  pdl_wait();
 
   const int rlo = int(ur.rlo), rhi = int(ur.rhi);
   const int jbase = int(2 * ur.b0) - 2;
@@ -815,6 +818,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
     pipe_release<NS>(pp, d, D, issue);
     l0_plane<TI1>(g, ur, S, p, Q, A, jdone, G);
   }
+  pdl_trigger();
 }
 
 // ----------------------------------------------------------- interpolate
@@ -910,6 +914,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 3 : 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();
   struct Src {
     int64_t se, le, so, lo, cs;
   };
@@ -977,6 +982,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 3 : 1)
     }
     pipe_release<NS>(pp, d, D, issue);
   }
+  pdl_trigger();
 }
 
 // --------------------------------------------------------------- row pass
@@ -995,6 +1001,7 @@ __global__ void __launch_bounds__(256) k_f3_row(double* __restrict__ G, int64_t 
     tid[i] = inv_d[i];
   }
   __syncthreads();
+  pdl_wait();
   for (int64_t r = int64_t(blockIdx.x) * nw + warp; r < rows; r += int64_t(gridDim.x) * nw) {
     double* gr = G + r * m;
     for (int i = lane; i < m; i += 32) buf[i] = gr[i];
@@ -1012,7 +1019,7 @@ void launch_row(double* G, const F3Geom& g, const double* w, const double* id, c
   const size_t smem = size_t(2 + threads / 32) * m * 8;
   cudaFuncSetAttribute(k_f3_row, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   const int64_t blocks = std::min<int64_t>((rows + 7) / 8, int64_t(kNumSMs) * 8);
-  MGRX_LAUNCH(ex, "f3_row", k_f3_row<<<unsigned(blocks), threads, smem, ex.s>>>(G, rows, m, w, id));
+  MGRX_LAUNCH(ex, "f3_row", pdl_launch(k_f3_row, dim3(unsigned(blocks)), dim3(threads), smem, ex.s, G, rows, m, w, id));
 }
 
 // ------------------------------------------------------------ column pass
@@ -1046,6 +1053,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : 1)
   const int s0 = min(m, s * seg), s1 = min(m, s0 + seg);
   const int len = s1 - s0;
   double v[LS];
+  pdl_wait();
   {
     const double* gp = G + base + int64_t(s0) * stride;
 #pragma unroll
@@ -1096,6 +1104,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : 1)
       z = (v[k] - kOff * z) * ld_volatile(tid + s0 + k);
       v[k] = z;
     }
+  pdl_trigger();
   if (!valid) return;
   if (APPLY) {  // coarse values loaded only now: fewer live registers, more resident warps
     T* c = coarse + base + int64_t(s0) * stride;
@@ -1177,8 +1186,9 @@ void launch_col(double* G, T* coarse, double sign, const F3Geom& g, int axis, co
 #define MGRX_COL(AP, MT)                                                                                  \
   {                                                                                                       \
     const int SY = (m + 2 * 16 - 1) / (2 * 16);                                                          \
-    MGRX_LAUNCH(ex, tag, k_f3_col<T, 16, AP, MT><<<blocks, dim3(32, SY), (2 * m + 2 * 2 * SY * 16) * 8, ex.s>>>( \
-                             G, coarse, sign, ncols, m, stride, outer_stride, inner, w, id));             \
+    MGRX_LAUNCH(ex, tag, pdl_launch(k_f3_col<T, 16, AP, MT>, dim3(blocks), dim3(32, SY),                      \
+                                    size_t(2 * m + 2 * 2 * SY * 16) * 8, ex.s, G, coarse, sign, ncols, m,       \
+                                    stride, outer_stride, inner, w, id));                                       \
   }
   if (m <= 320) {
     if (coarse) MGRX_COL(true, kColThreads) else MGRX_COL(false, kColThreads)
@@ -1272,8 +1282,8 @@ static cudaError_t launch_interp_t(const T* shell, const T* coarse, T* fine, con
   ich = std::max<int64_t>(2, std::min<int64_t>(32, ich & ~int64_t(1)));
   const int64_t chunks = (g.n0 + ich - 1) / ich;
   MGRX_LAUNCH(ex, "f3_rec_interp",
-              k_f3_rec_interp<T, TRI, MAXT><<<unsigned(chunks * ntile), g.threads, smem, ex.s>>>(shell, coarse, fine, g,
-                                                                                           int(ich), ntile));
+              pdl_launch(k_f3_rec_interp<T, TRI, MAXT>, dim3(unsigned(chunks * ntile)), dim3(g.threads), smem, ex.s,
+                         shell, coarse, fine, g, int(ich), ntile));
   return cudaSuccess;
 }
 
@@ -1316,8 +1326,8 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
   if (e != cudaSuccess) return e;
 #define MGRX_DEC(TI, MT)                                                                               \
   if (g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))                      \
-    MGRX_LAUNCH(ex, "f3_dec_plane", k_f3_dec_plane<T, TI, MT><<<g.grid, g.threads, ds, ex.s>>>(        \
-                                        blk, shell, coarse, G, g));
+    MGRX_LAUNCH(ex, "f3_dec_plane", pdl_launch(k_f3_dec_plane<T, TI, MT>, dim3(g.grid), dim3(g.threads), ds, \
+                                               ex.s, blk, shell, coarse, G, g));
   MGRX_DEC(4, kPlaneMaxThreads)
   MGRX_DEC(2, kPlaneMaxThreads)
   MGRX_DEC(4, kWideBound)
@@ -1343,8 +1353,8 @@ cudaError_t fused3d_recompose_correction(const T* shell, void* scratch, const Fu
   if (e != cudaSuccess) return e;
 #define MGRX_REC(TI, MT)                                                                               \
   if (g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))                      \
-    MGRX_LAUNCH(ex, "f3_rec_plane", k_f3_rec_plane<T, TI, MT><<<g.grid, g.threads, ds, ex.s>>>(        \
-                                        shell, G, g));
+    MGRX_LAUNCH(ex, "f3_rec_plane", pdl_launch(k_f3_rec_plane<T, TI, MT>, dim3(g.grid), dim3(g.threads), ds, \
+                                               ex.s, shell, G, g));
   MGRX_REC(4, kPlaneMaxThreads)
   MGRX_REC(2, kPlaneMaxThreads)
   MGRX_REC(4, kWideBound)

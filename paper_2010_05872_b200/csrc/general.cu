@@ -317,6 +317,7 @@ __global__ void __launch_bounds__(1024) k_tail_decompose(const T* __restrict__ b
   T* A = reinterpret_cast<T*>(tmp + nmax);
   T* B = A + nmax;
   const NuLevel nu{};
+  pdl_wait();
   for (int64_t p = threadIdx.x; p < lv[0].g.N; p += blockDim.x) A[p] = blk[p];
   __syncthreads();
   T* cur = A;
@@ -366,6 +367,7 @@ __global__ void __launch_bounds__(1024) k_tail_recompose(const T* __restrict__ c
   T* A = reinterpret_cast<T*>(tmp + nmax);
   T* B = A + nmax;
   const NuLevel nu{};
+  pdl_wait();
   for (int64_t p = threadIdx.x; p < lv[0].g.Nc; p += blockDim.x) A[p] = coarse_in[p];
   __syncthreads();
   T* cur = A;  // coarse block of the current level
@@ -415,8 +417,8 @@ static cudaError_t tail_dec_t(const T* blk, T* out, T* coarse_out, const void* d
   const size_t sm = tail_smem_bytes(nmax, sizeof(T));
   cudaError_t e = cudaFuncSetAttribute(k_tail_decompose<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
   if (e != cudaSuccess) return e;
-  MGRX_LAUNCH(ex, "tail_dec", k_tail_decompose<T, D><<<1, 1024, sm, ex.s>>>(
-                                  blk, out, coarse_out, static_cast<const TailLevel*>(d_levels), nlev, nmax));
+  MGRX_LAUNCH(ex, "tail_dec", pdl_launch(k_tail_decompose<T, D>, dim3(1), dim3(1024), sm, ex.s, blk, out, coarse_out,
+                                         static_cast<const TailLevel*>(d_levels), nlev, nmax));
   return cudaGetLastError();
 }
 
@@ -426,8 +428,8 @@ static cudaError_t tail_rec_t(const T* coeffs, const T* coarse_in, T* fine_out, 
   const size_t sm = tail_smem_bytes(nmax, sizeof(T));
   cudaError_t e = cudaFuncSetAttribute(k_tail_recompose<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
   if (e != cudaSuccess) return e;
-  MGRX_LAUNCH(ex, "tail_rec", k_tail_recompose<T, D><<<1, 1024, sm, ex.s>>>(
-                                  coeffs, coarse_in, fine_out, static_cast<const TailLevel*>(d_levels), nlev, nmax));
+  MGRX_LAUNCH(ex, "tail_rec", pdl_launch(k_tail_recompose<T, D>, dim3(1), dim3(1024), sm, ex.s, coeffs, coarse_in,
+                                         fine_out, static_cast<const TailLevel*>(d_levels), nlev, nmax));
   return cudaGetLastError();
 }
 
