@@ -231,7 +231,8 @@ struct mgrx_gpu_ctx {
   // recompose: side streams for the levels' independent corrections
   static constexpr int kSide = 4;
   cudaStream_t side[kSide] = {};
-  cudaEvent_t fork = nullptr;
+  cudaStream_t chain = nullptr;  // high priority: the sequential recompose chain
+  cudaEvent_t fork = nullptr, join = nullptr;
   std::vector<cudaEvent_t> lvl_done;
 };
 
@@ -247,9 +248,13 @@ Exec exec_on(mgrx_gpu_ctx* c, cudaStream_t s, int level) {
 
 void ensure_side(mgrx_gpu_ctx* c, int levels) {
   if (!c->fork) {
+    int least = 0, greatest = 0;
+    cuda_check(cudaDeviceGetStreamPriorityRange(&least, &greatest), "cudaDeviceGetStreamPriorityRange");
     for (int i = 0; i < mgrx_gpu_ctx::kSide; ++i)
-      cuda_check(cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking), "cudaStreamCreate(side)");
+      cuda_check(cudaStreamCreateWithPriority(&c->side[i], cudaStreamNonBlocking, least), "cudaStreamCreate(side)");
+    cuda_check(cudaStreamCreateWithPriority(&c->chain, cudaStreamNonBlocking, greatest), "cudaStreamCreate(chain)");
     cuda_check(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming), "cudaEventCreate");
   }
   while (int(c->lvl_done.size()) < levels) {
     cudaEvent_t e;
@@ -536,29 +541,19 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
   char* s = static_cast<char*>(c->scratch);
   double* comp = reinterpret_cast<double*>(s + p.off_comp);
   double* tmp = reinterpret_cast<double*>(s + p.off_tmp);
-  // unpack_level_centric's coarse block (reorder.hpp:231-238)
-  T* coarse = reinterpret_cast<T*>(s + p.blk_off[stop]);
-  int l0 = stop + 1;
-  if (!nu && p.tail_top > stop) {  // levels stop+1..tail_top in one CTA
-    const int top = p.tail_top;
-    T* fine = (top == L) ? d_field : reinterpret_cast<T*>(s + p.blk_off[top]);
-    cuda_check(tail_recompose<T>(d_coeffs, d_coeffs, fine, p.d_tail_rec, top - stop, p.tail_nmax, h.d,
-                                    exec(c, top)), "tail");
-    coarse = fine;
-    l0 = top + 1;
-  } else {
-    cuda_check(cudaMemcpyAsync(coarse, d_coeffs, size_t(h.node[stop]) * sizeof(T), cudaMemcpyDeviceToDevice,
-                               c->stream),
-               "copy coarse");
-  }
-  // Corrections of the fused levels below the finest depend only on their
-  // shells: fork them onto side streams (they overlap each other and the
-  // tail); the finest level's correction stays on the main stream.
-  // (not while profiling: per-kernel event times need the serial order)
+  // Corrections of the fused levels depend only on their shells
+  // (transform.hpp:343-366: the component is zero on the coarse nodes): fork
+  // them onto side streams at the start; the sequential chain (tail, then per
+  // level axis-0 solve + apply + interpolation) runs on a high-priority
+  // stream, waiting for each level's correction; everything joins back into
+  // the caller's stream.  Not while profiling (per-kernel event times need
+  // the serial order).
   std::vector<char> forked(L + 1, 0);
-  if (!nu && c->path == 0 && !c->profiling) {
+  cudaStream_t cs = c->stream;  // the chain's stream
+  {
     int nf = 0;
-    for (int l = stop + 1; l <= L; ++l) nf += p.fused[l].enabled ? 1 : 0;
+    if (!nu && c->path == 0 && !c->profiling)
+      for (int l = stop + 1; l <= L; ++l) nf += p.fused[l].enabled ? 1 : 0;
     if (nf > 0) {
       ensure_side(c, L + 1);
       cuda_check(cudaEventRecord(c->fork, c->stream), "cudaEventRecord(fork)");
@@ -574,7 +569,23 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
         cuda_check(cudaEventRecord(c->lvl_done[l], sd), "cudaEventRecord");
         forked[l] = 1;
       }
+      cs = c->chain;
+      cuda_check(cudaStreamWaitEvent(cs, c->fork, 0), "cudaStreamWaitEvent");
     }
+  }
+  // unpack_level_centric's coarse block (reorder.hpp:231-238)
+  T* coarse = reinterpret_cast<T*>(s + p.blk_off[stop]);
+  int l0 = stop + 1;
+  if (!nu && p.tail_top > stop) {  // levels stop+1..tail_top in one CTA
+    const int top = p.tail_top;
+    T* fine = (top == L) ? d_field : reinterpret_cast<T*>(s + p.blk_off[top]);
+    cuda_check(tail_recompose<T>(d_coeffs, d_coeffs, fine, p.d_tail_rec, top - stop, p.tail_nmax, h.d,
+                                    exec_on(c, cs, top)), "tail");
+    coarse = fine;
+    l0 = top + 1;
+  } else {
+    cuda_check(cudaMemcpyAsync(coarse, d_coeffs, size_t(h.node[stop]) * sizeof(T), cudaMemcpyDeviceToDevice, cs),
+               "copy coarse");
   }
   for (int l = l0; l <= L; ++l) {
     const T* shell = d_coeffs + h.node[l - 1];
@@ -582,17 +593,21 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
     const Fused3DPlan& fp = p.fused[l];
     cudaError_t e;
     if (forked[l]) {
-      cuda_check(cudaStreamWaitEvent(c->stream, c->lvl_done[l], 0), "cudaStreamWaitEvent");
-      e = fused3d_recompose_finish<T>(shell, coarse, fine, s + fp.scratch_off, fp, p.thomas[l], exec(c, l));
+      cuda_check(cudaStreamWaitEvent(cs, c->lvl_done[l], 0), "cudaStreamWaitEvent");
+      e = fused3d_recompose_finish<T>(shell, coarse, fine, s + fp.scratch_off, fp, p.thomas[l], exec_on(c, cs, l));
     } else if (!nu && c->path == 0 && fp.enabled) {
       e = fused3d_recompose_level<T>(shell, coarse, fine, s + fp.scratch_off, p.geom[l], fp, p.thomas[l],
-                                     exec(c, l));
+                                     exec_on(c, cs, l));
     } else {
       e = general_recompose_level<T>(shell, coarse, fine, comp, tmp, p.geom[l], &p.thomas[l],
-                                     nu ? &(*nu)[l] : nullptr, exec(c, l));
+                                     nu ? &(*nu)[l] : nullptr, exec_on(c, cs, l));
     }
     cuda_check(e, "recompose level");
     coarse = fine;
+  }
+  if (cs != c->stream) {  // join the chain (which joined every side stream)
+    cuda_check(cudaEventRecord(c->join, cs), "cudaEventRecord(join)");
+    cuda_check(cudaStreamWaitEvent(c->stream, c->join, 0), "cudaStreamWaitEvent");
   }
 }
 
@@ -680,7 +695,9 @@ int mgrx_gpu_ctx_destroy(mgrx_gpu_ctx* c) {
   if (c->own) cudaStreamDestroy(c->own);
   for (int i = 0; i < mgrx_gpu_ctx::kSide; ++i)
     if (c->side[i]) cudaStreamDestroy(c->side[i]);
+  if (c->chain) cudaStreamDestroy(c->chain);
   if (c->fork) cudaEventDestroy(c->fork);
+  if (c->join) cudaEventDestroy(c->join);
   for (cudaEvent_t e : c->lvl_done) cudaEventDestroy(e);
   delete c;
   return MGRX_OK;
