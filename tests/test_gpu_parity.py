@@ -253,3 +253,68 @@ def test_fused_path_against_oracle(torch, mg, ws_auto, dtype):
             assert err <= tol * rg, (shape, dtype, stop, "rec", err / rg)
             rt = mg.recompose(mc, ws_auto).cpu().numpy()
             assert float(np.max(np.abs(rt.astype(np.float64) - x))) <= (1e-9 if dtype == "f64" else 1e-4) * rg
+
+
+def test_graph_capture_matches_eager(torch, mg):
+    """decompose + recompose captured in a CUDA graph (the recompose forks
+    its level corrections onto the context's side streams and joins them)
+    replays bit-identically to eager execution, for fp32 and fp64."""
+    rng = np.random.default_rng(11)
+    for shape, dt in (((129, 129, 129), np.float32), ((65, 66, 67), np.float64)):
+        x = to_dev(torch, rng.uniform(-1, 1, shape).astype(dt))
+        h = mg.GridHierarchy.create(shape)
+        ws = mg.SolverWorkspace()
+
+        def step():
+            mc = mg.decompose(x, h, 0, ws)
+            return mc.buffer, mg.recompose(mc, ws)
+
+        c_e, f_e = step()
+        torch.cuda.synchronize()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            step()
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            c_g, f_g = step()
+        for _ in range(2):
+            g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(c_g, c_e), shape
+        assert torch.equal(f_g, f_e), shape
+
+
+def test_contexts_on_threads(torch, mg):
+    """One context per host thread (the SolverWorkspace contract): two
+    threads transforming different fields concurrently get the same results
+    as a serial run."""
+    import threading
+
+    rng = np.random.default_rng(12)
+    shape = (97, 65, 129)
+    xs = [to_dev(torch, rng.uniform(-1, 1, shape).astype(np.float32)) for _ in range(2)]
+    h = mg.GridHierarchy.create(shape)
+    ref = []
+    ws0 = mg.SolverWorkspace()
+    for x in xs:
+        ref.append(mg.decompose(x, h, 0, ws0).buffer.clone())
+    torch.cuda.synchronize()
+    out = [None, None]
+
+    def work(i):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            ws = mg.SolverWorkspace()
+            for _ in range(3):
+                out[i] = mg.decompose(xs[i], h, 0, ws).buffer
+        s.synchronize()
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for i in range(2):
+        assert torch.equal(out[i], ref[i])
