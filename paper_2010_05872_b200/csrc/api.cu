@@ -621,6 +621,7 @@ QuantLevels quant_levels(const Plan& p, const double* q) {
   for (int l = 0; l <= h.L; ++l) {
     ql.end[l] = h.node[l];
     ql.q[l] = q[l];
+    ql.inv[l] = 1.0 / q[l];
   }
   return ql;
 }

@@ -34,6 +34,7 @@ struct QuantLevels {
   int64_t base, total;     // quantized positions [base, total)
   int64_t end[kMaxLevels]; // end position (exclusive) of level l = node_count(l)
   double q[kMaxLevels];    // bin widths
+  double inv[kMaxLevels];  // 1 / q (fast path of the division; exact fallback near ties)
 };
 int64_t quant_num_chunks(const QuantLevels& ql);
 template <typename T>
