@@ -351,6 +351,7 @@ def run_ours(args, ws, rank, local):
     # memory; H2D of the field + D2H of the coefficients for decompose, H2D
     # of the coefficients + D2H of the field for recompose, every step)
     e2e = e2e_measure(mg, wsp, field, h, args)
+    quant = quant_measure(mg, wsp, field, h, args)
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -381,6 +382,7 @@ def run_ours(args, ws, rank, local):
             "kernels_launches_per_step": {k: v[1] // args.steps for k, v in prof.items()},
             "profiled_step_ms": prof_total,
             "e2e": e2e,
+            "quantize": quant,
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": int(launches),
@@ -399,6 +401,38 @@ def measured_traffic(tag):
         return None if v is None else float(v)
     except Exception:
         return None
+
+
+def quant_measure(mg, wsp, field, h, args):
+    """Level-wise quantize + dequantize of the step's coefficients (the rest
+    of the path, quantize.hpp:39-150) at tau = 1e-3 * range, budget tau / 4;
+    device time with CUDA events.  Bytes: N*s + 4N each way."""
+    import torch
+
+    mc = mg.decompose(field, h, 0, wsp)
+    rg = float((field.max() - field.min()).item())
+    plan = mg.make_plan(mg.QuantMode.levelwise, 1e-3 * rg / 4.0, h)
+    s = mg.quantize(mc, plan, wsp)
+    mg.dequantize(s, plan, h, wsp)
+    torch.cuda.synchronize()
+    k = max(1, min(args.steps, 10))
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    e0.record()
+    for _ in range(k):
+        s = mg.quantize(mc, plan, wsp)
+    e1.record()
+    for _ in range(k):
+        d = mg.dequantize(s, plan, h, wsp)
+    e2.record()
+    torch.cuda.synchronize()
+    q_ms, d_ms = e0.elapsed_time(e1) / k, e1.elapsed_time(e2) / k
+    nb = field.numel() * (field.element_size() + 4)
+    back = mg.recompose(d, wsp)
+    linf = float((back - field).abs().max().item())
+    return {"quantize_ms": q_ms, "dequantize_ms": d_ms, "quantize_gbs": nb / (q_ms * 1e-3) / 1e9,
+            "dequantize_gbs": nb / (d_ms * 1e-3) / 1e9, "outliers": int(s.outlier_positions.numel()),
+            "linf_over_tau": linf / (1e-3 * rg), "tau": "1e-3 * range, budget tau/4",
+            "note": "quantize includes the outlier-count readback (synchronous, as the reference's API)"}
 
 
 def e2e_measure(mg, wsp, field, h, args, workers=2):
