@@ -6,12 +6,13 @@
 //
 //   reference                                      drop-in
 //   mgrx::decompose        (transform.hpp:509)     mgrx::b200::decompose
+//   mgrx::decompose_with   (transform.hpp:486)     mgrx::b200::decompose_with (level by level; the decider runs on the host)
 //   mgrx::recompose        (transform.hpp:517)     mgrx::b200::recompose
 //   mgrx::quantize         (quantize.hpp:79)       mgrx::b200::quantize
 //   mgrx::quantize_tail    (quantize.hpp:99)       mgrx::b200::quantize_tail
 //   mgrx::dequantize       (quantize.hpp:118)      mgrx::b200::dequantize
 //   mgrx::dequantize_tail  (quantize.hpp:137)      mgrx::b200::dequantize_tail
-//   mgrx::compress         (pipeline.hpp:130)      mgrx::b200::compress   (adaptive == false or force_stop_level)
+//   mgrx::compress         (pipeline.hpp:130)      mgrx::b200::compress   (fixed, forced or adaptive stop)
 //   mgrx::decompress_field (pipeline.hpp:198)      mgrx::b200::decompress_field
 //   mgrx::SolverWorkspace  (transform.hpp:48)      mgrx::b200::Workspace  (owns the GPU context)
 //
@@ -22,7 +23,9 @@
 #ifndef MGRX_B200_HPP
 #define MGRX_B200_HPP
 
+#include <algorithm>
 #include <cstdint>
+#include <optional>
 #include <span>
 #include <string>
 #include <utility>
@@ -74,6 +77,41 @@ MultilevelCoefficients<T> decompose(TensorField<T> field, const GridHierarchy& h
                             field.data.data(), out.buffer.data()),
         ws.get());
   return out;
+}
+
+// decompose_with (transform.hpp:485-506): before each level the decider sees
+// that level's block (natural order) and may stop the recursion there.  The
+// level steps run on the GPU one at a time (the level block decomposed as a
+// field of `l` levels, stopped at l - 1 — the same arithmetic as the full
+// decompose); each step's coarse block comes back to the host for the next
+// decision.
+template <typename T>
+MultilevelCoefficients<T> decompose_with(TensorField<T> field, const GridHierarchy& h, Workspace& ws,
+                                         const StopDecider<T>& decider, int min_stop_level = 0) {
+  const int L = h.num_levels();
+  if (field.dims != h.level_dims(L)) fail(errc::shape_error, "field dims do not match hierarchy");
+  if (min_stop_level < 0 || min_stop_level > L) fail(errc::invalid_level, "stop level out of range");
+  if (!decider) return decompose(std::move(field), h, min_stop_level, ws);
+  std::vector<T> out(h.total_count());
+  std::vector<T> block = std::move(field.data);  // level-l block, natural order
+  int stop = min_stop_level;
+  for (int l = L; l > min_stop_level; --l) {
+    const Dims dl = h.level_dims(l);
+    if (decider(l, BlockView<const T>{block.data(), dl, row_major_strides(dl)})) {
+      stop = l;
+      break;
+    }
+    const auto d = detail::dims64(dl);
+    std::vector<T> step(h.node_count(l));  // [coarse block of l - 1 | shell of level l]
+    check(mgrx_host_decompose(ws.get(), detail::dtype<T>(), int(d.size()), d.data(), l, l - 1, block.data(),
+                              step.data()),
+          ws.get());
+    const std::ptrdiff_t nc = static_cast<std::ptrdiff_t>(h.node_count(l - 1));
+    std::copy(step.begin() + nc, step.end(), out.begin() + nc);
+    block.assign(step.begin(), step.begin() + nc);
+  }
+  std::copy(block.begin(), block.end(), out.begin());  // coarse block of the stop level
+  return MultilevelCoefficients<T>{std::move(out), h, stop};
 }
 
 template <typename T>
@@ -175,19 +213,28 @@ void dequantize_tail(std::span<T> buffer, const LabelStream<T>& stream, const Gr
 }
 
 // compress (pipeline.hpp:130-196) with the transform and quantizer on the
-// GPU.  The adaptive stop decision (adaptive.hpp, host heuristic) is not on
-// the hot path: callers use adaptive = false or force_stop_level, exactly
-// as the benchmark configurations do; an adaptive request is refused.
+// GPU.  The adaptive stop decision is the reference's own host heuristic
+// (choose_stop, adaptive.hpp:99-104) called through decompose_with.
 template <typename T>
 std::vector<std::uint8_t> compress(const TensorField<T>& field, const CompressOptions& opt, Workspace& ws) {
-  if (opt.adaptive && !opt.force_stop_level)
-    fail(errc::invalid_input, "mgrx::b200::compress needs adaptive = false or force_stop_level");
   mgrx::detail::check_finite(field);
   const GridHierarchy h = GridHierarchy::create(field.dims, opt.levels);
   const int L = h.num_levels();
   const QuantizationPlan plan = make_plan(opt.quant_mode, opt.budget, h);
-  const int stop = opt.force_stop_level ? *opt.force_stop_level : 0;
+  int stop = opt.force_stop_level ? *opt.force_stop_level : 0;
   if (stop < 0 || stop > L) fail(errc::invalid_level, "forced stop level out of range");
+  std::optional<MultilevelCoefficients<T>> adaptive_coeffs;
+  if (!opt.force_stop_level && opt.adaptive) {
+    const int d = static_cast<int>(field.dims.size());
+    StopDecider<T> decider = [&](int level, const BlockView<const T>& block) {
+      const double e_l = plan.bin_widths[static_cast<std::size_t>(level)] / 2.0;
+      const double kappa = plan.bin_widths[static_cast<std::size_t>(level)] /
+                           plan.bin_widths[static_cast<std::size_t>(level - 1)];
+      return choose_stop(block, e_l, penalty_model_for(d, kappa, opt.seed));
+    };
+    adaptive_coeffs = decompose_with(field, h, ws, decider);
+    stop = adaptive_coeffs->stop_level;
+  }
   Artifact a;
   a.element_type = element_type_of<T>();
   a.dims = field.dims;
@@ -202,7 +249,8 @@ std::vector<std::uint8_t> compress(const TensorField<T>& field, const CompressOp
     a.sections.push_back(mgrx::detail::lorenzo_section(stream));
     return write_artifact(a);
   }
-  MultilevelCoefficients<T> coeffs = decompose(field, h, stop, ws);
+  MultilevelCoefficients<T> coeffs =
+      adaptive_coeffs ? std::move(*adaptive_coeffs) : decompose(field, h, stop, ws);
   LabelStream<T> labels = stop == 0 ? quantize(coeffs, plan, ws)
                                     : quantize_tail<T>(std::span<const T>(coeffs.buffer), h, stop, plan, ws);
   for (const auto& lv : labels.labels) a.sections.push_back(mgrx::detail::label_section<T>(lv));

@@ -106,7 +106,44 @@ void check_shape(const mgrx::Dims& dims, double tol) {
   for (size_t i = 0; i < f.size(); ++i) linf2 = std::max(linf2, std::fabs(double(gf.data[i]) - double(f.data[i])));
   EXPECT(linf2 <= 1e-3 * range, "reference artifact via GPU: linf/tau %g", linf2 / (1e-3 * range));
   EXPECT(std::fabs(linf - linf2) <= 1e-5 * range, "GPU and reference reconstructions differ: %g vs %g", linf, linf2);
-  std::printf("shape ok: %zu dims, range %g, linf/tau %g\n", dims.size(), range, linf / (1e-3 * range));
+  // decompose_with: a decider stopping at level L - 1 (and one never
+  // stopping) gives the reference's buffer and stop level
+  const int L = h.num_levels();
+  for (int want : {L - 1, -1}) {
+    std::vector<int> seen_ref, seen_gpu;
+    mgrx::StopDecider<T> dref = [&](int level, const mgrx::BlockView<const T>&) {
+      seen_ref.push_back(level);
+      return level == want;
+    };
+    mgrx::StopDecider<T> dgpu = [&](int level, const mgrx::BlockView<const T>& b) {
+      seen_gpu.push_back(level);
+      EXPECT(b.extents == h.level_dims(level), "decider block extents at level %d", level);
+      return level == want;
+    };
+    auto rw = mgrx::decompose_with(f, h, sws, dref);
+    auto gw = mgrx::b200::decompose_with(f, h, ws, dgpu);
+    EXPECT(rw.stop_level == gw.stop_level, "decompose_with stop %d vs %d", rw.stop_level, gw.stop_level);
+    EXPECT(seen_ref == seen_gpu, "decider call sequence differs");
+    double ew = 0.0;
+    for (size_t i = 0; i < rw.buffer.size(); ++i)
+      ew = std::max(ew, std::fabs(double(rw.buffer[i]) - double(gw.buffer[i])));
+    EXPECT(ew <= tol * range, "decompose_with (stop at %d) err %g", want, ew / range);
+  }
+  // adaptive compress (the reference's choose_stop decider) round trip
+  mgrx::CompressOptions aopt;
+  aopt.budget = 1e-3 * range / 4.0;
+  aopt.adaptive = true;
+  auto abytes = mgrx::b200::compress(f, aopt, ws);
+  const auto ra = mgrx::read_artifact(abytes);
+  const auto rr = mgrx::read_artifact(mgrx::compress(f, aopt));
+  EXPECT(ra.stop_level == rr.stop_level, "adaptive stop %d vs reference %d", int(ra.stop_level), int(rr.stop_level));
+  const auto aany = mgrx::decompress(abytes);
+  const auto& af = std::get<mgrx::TensorField<T>>(aany);
+  double alinf = 0.0;
+  for (size_t i = 0; i < f.size(); ++i) alinf = std::max(alinf, std::fabs(double(af.data[i]) - double(f.data[i])));
+  EXPECT(alinf <= 1e-3 * range, "adaptive GPU artifact: linf/tau %g", alinf / (1e-3 * range));
+  std::printf("shape ok: %zu dims, range %g, linf/tau %g, adaptive stop %d\n", dims.size(), range,
+              linf / (1e-3 * range), int(ra.stop_level));
 }
 
 int main() {
