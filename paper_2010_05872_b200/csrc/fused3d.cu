@@ -412,8 +412,8 @@ struct DecRows {
   T* se;              // shell slot of even tile row e = 0 (fine row jbase), at column c
   T* so;              // shell slot of odd tile row e = 0 (fine row jbase + 1), at column c
   T* cpe;             // coarse row of even tile row e = 0, at column c
-  int64_t st_e;       // shell stride between consecutive even rows
-  int64_t n2l;        // shell stride between consecutive odd rows
+  int st_e;           // shell stride between consecutive even rows
+  int n2l;            // shell stride between consecutive odd rows
   int n2, m2, n1, m1; // extents
   int jbase, rlo, rhi, b0, TR, jlo_own, jhi_own;
   int oofs;           // odd-node offset inside an even row's shell slot
@@ -499,13 +499,13 @@ __device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const
     const bool own_row = FULL ? (jr >= 2 && jr < 2 * TI1 + 2) : (j1 >= x.jlo_own && j1 < x.jhi_own);
     if (x.own && own_row) {
       if (o1) {
-        T* sr = x.so + int64_t(ea) * x.n2l;
+        T* sr = x.so + ea * x.n2l;
         sr[0] = tE;
         if (x.has_odd) sr[x.m2] = tO;
       } else {
-        T* sr = x.se + int64_t(ea) * x.st_e;
+        T* sr = x.se + ea * x.st_e;
         if (ke == 0)
-          x.cpe[int64_t(ea) * x.m2] = rr[0];
+          x.cpe[ea * x.m2] = rr[0];
         else
           sr[0] = tE;
         if (x.has_odd) sr[x.oofs] = tO;
@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
   x.has_odd = S.valid && 2 * c + 1 < n2;
   x.right_degen = 2 * c + 2 >= n2;
   x.c = c;
-  x.n2l = g.n2;
+  x.n2l = int(g.n2);
   const bool full = ur.b0 >= 1 && 2 * ur.b1 <= g.n1 - 1;
   const int cc = S.valid ? c : 0;  // clamp halo columns for addressing
   const int D = int(ur.phi - ur.plo);  // planes of the unit: plo + [0, D]
@@ -622,7 +622,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
       const int p = plo + d;
       mbar_wait(&pp->full[pipe_slot<NS>(d)], pipe_parity<NS>(d));
       x.has_right = false;
-      x.st_e = g.n2 - g.m2;
+      x.st_e = int(g.n2 - g.m2);
       x.oofs = 0;
       x.se = se_e;
       x.so = so_e;
@@ -646,7 +646,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
       x.has_right = p + 1 <= n0 - 1;
       mbar_wait(&pp->full[pipe_slot<NS>(d + 1)], pipe_parity<NS>(d + 1));
       if (x.has_right) mbar_wait(&pp->full[pipe_slot<NS>(d + 2)], pipe_parity<NS>(d + 2));
-      x.st_e = g.n2;
+      x.st_e = int(g.n2);
       x.oofs = m2;
       x.se = se_o;
       x.so = so_o;
