@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
 // slot (coefficients; 0 on nodal points), axis-2 restriction through
 // shuffles, axis-1 restriction into Q.  FULL as in dec_rows.
 template <typename T, int TI1, bool PODD, bool FULL>
-__device__ __forceinline__ void rec_rows(const T* ev, const T* od, int64_t st_e, int n2, int m2, int jbase, int rlo,
+__device__ __forceinline__ void rec_rows(const T* ev, const T* od, int st_e, int n2, int m2, int jbase, int rlo,
                                          int rhi, int b0, int TR, int m1, int c, bool valid, bool has_odd, double* Q) {
   constexpr int RMAX = 2 * TI1 + 3;
 #pragma unroll
@@ -683,11 +683,11 @@ __device__ __forceinline__ void rec_rows(const T* ev, const T* od, int64_t st_e,
     const int ea = jr >> 1;
     double cE, cO;
     if (o1) {
-      const T* r = od + int64_t(ea) * n2;
+      const T* r = od + ea * n2;
       cE = valid ? double(r[0]) : 0.0;
       cO = has_odd ? double(r[m2]) : 0.0;
     } else {
-      const T* r = ev + int64_t(ea) * st_e;
+      const T* r = ev + ea * st_e;
       cE = (PODD && valid) ? double(r[0]) : 0.0;
       cO = has_odd ? double(r[PODD ? m2 : 0]) : 0.0;
     }
@@ -798,7 +798,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
     const unsigned char* slot = raw + sl * int(rawb);
     const volatile int* ld = pp->lead[sl];
     // slot positions of even tile row e = 0 (fine row jbase) and odd e = 0 (jbase + 1)
-    const int64_t st_e = p_odd ? g.n2 : g.n2 - g.m2;
+    const int st_e = int(p_odd ? g.n2 : g.n2 - g.m2);
     const T* evrun = reinterpret_cast<const T*>(slot + ld[0]);
     const T* odrun = reinterpret_cast<const T*>(slot + ld[1]);
     // even run starts at fine row 2 e_lo = rlo (rlo is even); jbase may be rlo - 2
