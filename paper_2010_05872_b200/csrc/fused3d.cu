@@ -52,6 +52,7 @@ constexpr int kColMaxM = 640;       // column passes: register-resident columns 
 // column-pass block: 16 columns x S segments of up to LS registers, two
 // segments per warp row; LS = 16 for m <= 320, 32 for m <= 640
 constexpr int kColThreads = 16 * 20;
+constexpr int kColThreads12 = 32 * 11;  // 12-value segments, up to 11 warp rows (m <= 264)
 
 // ------------------------------------------------------------ PTX helpers
 
@@ -1032,7 +1033,7 @@ void launch_row(double* G, const F3Geom& g, const double* w, const double* id, c
 // coarse += sign * z (apply_correction, transform.hpp:435-477); otherwise it
 // is written back to G.
 template <typename T, int LS, bool APPLY, int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : 1)
+__global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : (MAXT == kColThreads12 ? 3 : 1))
     k_f3_col(double* __restrict__ G, T* __restrict__ coarse, double sign, int64_t ncols, int m, int64_t stride,
              int64_t outer_stride, int64_t inner, const double* __restrict__ w, const double* __restrict__ inv_d) {
   extern __shared__ double sc[];
@@ -1183,19 +1184,23 @@ void launch_col(double* G, T* coarse, double sign, const F3Geom& g, int axis, co
   const char* tag = axis == 1 ? "f3_col1" : "f3_col0";
 // segments of <= 16 values: up to 10 warp rows (320 threads, 3 blocks/SM)
   // for m <= 320, up to 20 (640 threads, 1 block/SM) for m <= 640
-#define MGRX_COL(AP, MT)                                                                                  \
+#define MGRX_COL(AP, MT) MGRX_COLL(16, AP, MT)
+#define MGRX_COLL(LS, AP, MT)                                                                             \
   {                                                                                                       \
-    const int SY = (m + 2 * 16 - 1) / (2 * 16);                                                          \
-    MGRX_LAUNCH(ex, tag, pdl_launch(k_f3_col<T, 16, AP, MT>, dim3(blocks), dim3(32, SY),                      \
+    const int SY = (m + 2 * LS - 1) / (2 * LS);                                                          \
+    MGRX_LAUNCH(ex, tag, pdl_launch(k_f3_col<T, LS, AP, MT>, dim3(blocks), dim3(32, SY),                      \
                                     size_t(2 * m + 2 * 2 * SY * 16) * 8, ex.s, G, coarse, sign, ncols, m,       \
                                     stride, outer_stride, inner, w, id));                                       \
   }
-  if (m <= 320) {
+  if (m <= 264) {
+    if (coarse) MGRX_COLL(12, true, kColThreads12) else MGRX_COLL(12, false, kColThreads12)
+  } else if (m <= 320) {
     if (coarse) MGRX_COL(true, kColThreads) else MGRX_COL(false, kColThreads)
   } else {
     if (coarse) MGRX_COL(true, 2 * kColThreads) else MGRX_COL(false, 2 * kColThreads)
   }
 #undef MGRX_COL
+#undef MGRX_COLL
 }
 
 }  // namespace
