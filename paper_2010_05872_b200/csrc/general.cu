@@ -117,26 +117,26 @@ __device__ __forceinline__ double predict(const T* __restrict__ src, bool coarse
 // reorder_level + compute_coefficients (transform.hpp:310) + the component
 // materialisation of compute_correction (:343-381) + the shell part of
 // pack_level_centric, one thread per fine node.
-template <typename T, bool kIdx32, bool kNu>
+template <typename T, bool kIdx32, bool kNu, int D>
 __global__ void __launch_bounds__(256) k_dec_coef(const T* __restrict__ blk, T* __restrict__ shell,
                                                   T* __restrict__ coarse, double* __restrict__ comp,
                                                   const LevelGeom g, const NuLevel nu) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < g.N; p += stride) {
     int64_t j[kMaxD];
-    unravel<kIdx32>(p, g, j);
+    unravel<kIdx32, D>(p, g, j);
     bool nodal = true;
-    for (int i = 0; i < g.d; ++i) nodal &= !(j[i] & 1);
+    for (int i = 0; i < MGRX_ND(g); ++i) nodal &= !(j[i] & 1);
     if (nodal) {
       int64_t c = 0;
-      for (int i = 0; i < g.d; ++i) c += (j[i] >> 1) * g.cst[i];
+      for (int i = 0; i < MGRX_ND(g); ++i) c += (j[i] >> 1) * g.cst[i];
       coarse[c] = blk[p];
       comp[p] = 0.0;
     } else {
-      const double pred = predict<T, kNu>(blk, false, g, nu, j);
+      const double pred = predict<T, kNu, D>(blk, false, g, nu, j);
       const T v = to_t<T>(sub_(double(blk[p]), pred));
       comp[p] = double(v);
-      shell[shell_pos(g, j)] = v;
+      shell[shell_pos<D>(g, j)] = v;
     }
   }
 }
@@ -203,38 +203,38 @@ __global__ void __launch_bounds__(256) k_apply(T* __restrict__ coarse, const dou
 // ------------------------------------------------------------ recompose
 // Component of a level from its shell (unpack_level_centric reorder.hpp:221
 // + the materialisation of compute_correction).
-template <typename T, bool kIdx32>
+template <typename T, bool kIdx32, int D>
 __global__ void __launch_bounds__(256) k_rec_comp(const T* __restrict__ shell, double* __restrict__ comp,
                                                   const LevelGeom g) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < g.N; p += stride) {
     int64_t j[kMaxD];
-    unravel<kIdx32>(p, g, j);
+    unravel<kIdx32, D>(p, g, j);
     bool nodal = true;
-    for (int i = 0; i < g.d; ++i) nodal &= !(j[i] & 1);
-    comp[p] = nodal ? 0.0 : double(shell[shell_pos(g, j)]);
+    for (int i = 0; i < MGRX_ND(g); ++i) nodal &= !(j[i] & 1);
+    comp[p] = nodal ? 0.0 : double(shell[shell_pos<D>(g, j)]);
   }
 }
 
 // add_interpolant (transform.hpp:317) + inverse_reorder_level
 // (reorder.hpp:138): fine natural block from corrected coarse nodes and the
 // shell coefficients.
-template <typename T, bool kIdx32, bool kNu>
+template <typename T, bool kIdx32, bool kNu, int D>
 __global__ void __launch_bounds__(256) k_rec_interp(const T* __restrict__ shell, const T* __restrict__ coarse,
                                                     T* __restrict__ fine, const LevelGeom g, const NuLevel nu) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < g.N; p += stride) {
     int64_t j[kMaxD];
-    unravel<kIdx32>(p, g, j);
+    unravel<kIdx32, D>(p, g, j);
     bool nodal = true;
-    for (int i = 0; i < g.d; ++i) nodal &= !(j[i] & 1);
+    for (int i = 0; i < MGRX_ND(g); ++i) nodal &= !(j[i] & 1);
     if (nodal) {
       int64_t c = 0;
-      for (int i = 0; i < g.d; ++i) c += (j[i] >> 1) * g.cst[i];
+      for (int i = 0; i < MGRX_ND(g); ++i) c += (j[i] >> 1) * g.cst[i];
       fine[p] = coarse[c];
     } else {
-      const double pred = predict<T, kNu>(coarse, true, g, nu, j);
-      fine[p] = to_t<T>(add_(double(shell[shell_pos(g, j)]), pred));
+      const double pred = predict<T, kNu, D>(coarse, true, g, nu, j);
+      fine[p] = to_t<T>(add_(double(shell[shell_pos<D>(g, j)]), pred));
     }
   }
 }
@@ -469,41 +469,56 @@ void tail_fill_level(void* dst, const LevelGeom& g, const ThomasLevel& th, int64
 
 // ------------------------------------------------------------- launchers
 
+// Rank-specialised variants (32-bit indexing, d = 2, 3, 4: the index
+// arithmetic unrolls and stays in registers); the runtime-rank kernels
+// cover the rest and 64-bit node counts.
+#define MGRX_BY_RANK(LAUNCH)                          \
+  if (g.N < (int64_t(1) << 32) && g.d == 2) {          \
+    LAUNCH(true, 2);                                   \
+  } else if (g.N < (int64_t(1) << 32) && g.d == 3) {   \
+    LAUNCH(true, 3);                                   \
+  } else if (g.N < (int64_t(1) << 32) && g.d == 4) {   \
+    LAUNCH(true, 4);                                   \
+  } else if (g.N < (int64_t(1) << 32)) {               \
+    LAUNCH(true, 0);                                   \
+  } else {                                             \
+    LAUNCH(false, 0);                                  \
+  }
+
 template <typename T>
 static void launch_dec_coef(const T* blk, T* shell, T* coarse, double* comp, const LevelGeom& g, const NuLevel* nu,
                             const Exec& ex) {
   const int grid = grid_for(g.N, 256);
-  const bool i32 = g.N < (int64_t(1) << 32);
   const NuLevel z = nu ? *nu : NuLevel{};
-  if (nu) {
-    if (i32) MGRX_LAUNCH(ex, "gen_dec_coef", k_dec_coef<T, true, true><<<grid, 256, 0, ex.s>>>(blk, shell, coarse, comp, g, z));
-    else MGRX_LAUNCH(ex, "gen_dec_coef", k_dec_coef<T, false, true><<<grid, 256, 0, ex.s>>>(blk, shell, coarse, comp, g, z));
-  } else {
-    if (i32) MGRX_LAUNCH(ex, "gen_dec_coef", k_dec_coef<T, true, false><<<grid, 256, 0, ex.s>>>(blk, shell, coarse, comp, g, z));
-    else MGRX_LAUNCH(ex, "gen_dec_coef", k_dec_coef<T, false, false><<<grid, 256, 0, ex.s>>>(blk, shell, coarse, comp, g, z));
-  }
+#define L_(I32, D)                                                                                              \
+  if (nu)                                                                                                       \
+    MGRX_LAUNCH(ex, "gen_dec_coef", k_dec_coef<T, I32, true, D><<<grid, 256, 0, ex.s>>>(blk, shell, coarse, comp, g, z)); \
+  else                                                                                                          \
+    MGRX_LAUNCH(ex, "gen_dec_coef", k_dec_coef<T, I32, false, D><<<grid, 256, 0, ex.s>>>(blk, shell, coarse, comp, g, z))
+  MGRX_BY_RANK(L_)
+#undef L_
 }
 
 template <typename T>
 static void launch_rec_comp(const T* shell, double* comp, const LevelGeom& g, const Exec& ex) {
   const int grid = grid_for(g.N, 256);
-  if (g.N < (int64_t(1) << 32)) MGRX_LAUNCH(ex, "gen_rec_comp", k_rec_comp<T, true><<<grid, 256, 0, ex.s>>>(shell, comp, g));
-  else MGRX_LAUNCH(ex, "gen_rec_comp", k_rec_comp<T, false><<<grid, 256, 0, ex.s>>>(shell, comp, g));
+#define L_(I32, D) MGRX_LAUNCH(ex, "gen_rec_comp", k_rec_comp<T, I32, D><<<grid, 256, 0, ex.s>>>(shell, comp, g))
+  MGRX_BY_RANK(L_)
+#undef L_
 }
 
 template <typename T>
 static void launch_rec_interp(const T* shell, const T* coarse, T* fine, const LevelGeom& g, const NuLevel* nu,
                               const Exec& ex) {
   const int grid = grid_for(g.N, 256);
-  const bool i32 = g.N < (int64_t(1) << 32);
   const NuLevel z = nu ? *nu : NuLevel{};
-  if (nu) {
-    if (i32) MGRX_LAUNCH(ex, "gen_rec_interp", k_rec_interp<T, true, true><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, g, z));
-    else MGRX_LAUNCH(ex, "gen_rec_interp", k_rec_interp<T, false, true><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, g, z));
-  } else {
-    if (i32) MGRX_LAUNCH(ex, "gen_rec_interp", k_rec_interp<T, true, false><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, g, z));
-    else MGRX_LAUNCH(ex, "gen_rec_interp", k_rec_interp<T, false, false><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, g, z));
-  }
+#define L_(I32, D)                                                                                              \
+  if (nu)                                                                                                       \
+    MGRX_LAUNCH(ex, "gen_rec_interp", k_rec_interp<T, I32, true, D><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, g, z)); \
+  else                                                                                                          \
+    MGRX_LAUNCH(ex, "gen_rec_interp", k_rec_interp<T, I32, false, D><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, g, z))
+  MGRX_BY_RANK(L_)
+#undef L_
 }
 
 // compute_correction sweeps on `comp` (natural fine extents); the result
