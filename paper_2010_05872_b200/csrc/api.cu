@@ -532,7 +532,7 @@ void decompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, T* d_out, const 
       e = fused3d_decompose_level<T>(blk, shell, coarse, s + fp.scratch_off, p.geom[l], fp, p.thomas[l], exec(c, l));
     } else {
       e = general_decompose_level<T>(blk, shell, coarse, comp, tmp, p.geom[l], &p.thomas[l],
-                                     nu ? &(*nu)[l] : nullptr, exec(c, l));
+                                     nu ? &(*nu)[l] : nullptr, exec(c, l), c->path == 0);
     }
     cuda_check(e, "decompose level");
     blk = coarse;
@@ -612,7 +612,7 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
                                      exec_on(c, cs, l));
     } else {
       e = general_recompose_level<T>(shell, coarse, fine, comp, tmp, p.geom[l], &p.thomas[l],
-                                     nu ? &(*nu)[l] : nullptr, exec_on(c, cs, l));
+                                     nu ? &(*nu)[l] : nullptr, exec_on(c, cs, l), c->path == 0);
     }
     cuda_check(e, "recompose level");
     coarse = fine;

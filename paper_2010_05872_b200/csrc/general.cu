@@ -14,6 +14,8 @@
 // natural order (the reference materialises it in reordered order,
 // transform.hpp:343-381).  The level-centric output layout is produced
 // directly by computing each coefficient's shell position.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -188,6 +190,95 @@ __global__ void __launch_bounds__(128) k_sweep(const double* __restrict__ x, dou
       f[i * inner] = v;
       nxt = v;
     }
+  }
+}
+
+// Parallel form of a sweep (path "auto"): the load vector as one fully
+// parallel stencil pass (same arithmetic and order as k_sweep, so the load
+// is bit-identical), then the Thomas solve split into segments per line
+// (affine carries folded through shared memory, each segment rerun from its
+// true carry) — rounding-level differences from the serial sweep only.
+template <bool kNu>
+__global__ void __launch_bounds__(256) k_axis_load(const double* __restrict__ x, double* __restrict__ y,
+                                                   int64_t outer, int64_t inner, int64_t n, int64_t m,
+                                                   const double* __restrict__ s5) {
+  const int64_t total = outer * m * inner;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total; q += stride) {
+    const int64_t t = q % inner, oi = q / inner;
+    const int64_t i = oi % m, o = oi / m;
+    const double* c = x + o * n * inner + t;
+    double acc = 0.0;
+    if (kNu) {
+      const double* sk = s5 + 5 * i;
+      for (int k = 0; k < 5; ++k) {
+        const int64_t jj = 2 * i + k - 2;
+        if (jj >= 0 && jj < n) acc = add_(acc, mul_(sk[k], c[jj * inner]));
+      }
+    } else {
+      if (i >= 1) {
+        acc = add_(acc, mul_(kW12, c[(2 * i - 2) * inner]));
+        acc = add_(acc, mul_(0.5, c[(2 * i - 1) * inner]));
+      }
+      acc = add_(acc, mul_((i == 0 || i + 1 == m) ? kW5_12 : kW5_6, c[(2 * i) * inner]));
+      if (2 * i + 1 < n) acc = add_(acc, mul_(0.5, c[(2 * i + 1) * inner]));
+      if (2 * i + 2 < n) acc = add_(acc, mul_(kW12, c[(2 * i + 2) * inner]));
+    }
+    y[q] = acc;
+  }
+}
+
+// Thomas (batched_solve, transform.hpp:116-130; nonuniform: super-diagonal
+// table `off`) along lines of m values at stride `inner`, in place.  16
+// lines per block, S = 2 blockDim.y segments per line; values stream from
+// global memory (L1/L2) in each of the four segment passes.
+__global__ void __launch_bounds__(1024) k_axis_solve(double* __restrict__ y, int64_t nlines, int64_t m, int64_t inner,
+                                                     const double* __restrict__ w, const double* __restrict__ inv_d,
+                                                     const double* __restrict__ off) {
+  __shared__ double A[64][16], B[64][16];
+  const int lane = threadIdx.x, c16 = lane & 15, s = 2 * threadIdx.y + (lane >> 4), S = 2 * blockDim.y;
+  const int64_t line = int64_t(blockIdx.x) * 16 + c16;
+  const bool valid = line < nlines;
+  const int64_t base = valid ? (line / inner) * m * inner + line % inner : 0;
+  const int64_t seg = (m + S - 1) / S;
+  const int64_t s0 = min(m, int64_t(s) * seg), s1 = min(m, s0 + seg);
+  double* p = y + base;
+  // forward y_i = f_i - w_i y_{i-1}: segment map from a zero carry
+  double ya = 0.0, yb = 1.0;
+  for (int64_t i = s0; i < s1; ++i) {
+    const double f = valid ? p[i * inner] : 0.0;
+    const double wi = w[i];
+    ya = f - wi * ya;
+    yb = -wi * yb;
+  }
+  A[s][c16] = ya;
+  B[s][c16] = yb;
+  __syncthreads();
+  double c = 0.0;
+  for (int q = 0; q < s; ++q) c = A[q][c16] + B[q][c16] * c;
+  __syncthreads();
+  for (int64_t i = s0; i < s1; ++i) {
+    const double f = valid ? p[i * inner] : 0.0;
+    c = f - w[i] * c;
+    if (valid) p[i * inner] = c;
+  }
+  // back substitution z_i = (y_i - off_i z_{i+1}) / d_i, z_m = 0
+  double za = 0.0, zb = 1.0;
+  for (int64_t i = s1 - 1; i >= s0; --i) {
+    const double yv = valid ? p[i * inner] : 0.0;
+    const double id = inv_d[i], oi = off ? off[i] : kOff;
+    za = (yv - oi * za) * id;
+    zb = -oi * id * zb;
+  }
+  A[s][c16] = za;
+  B[s][c16] = zb;
+  __syncthreads();
+  double z = 0.0;
+  for (int q = S - 1; q > s; --q) z = A[q][c16] + B[q][c16] * z;
+  for (int64_t i = s1 - 1; i >= s0; --i) {
+    const double yv = valid ? p[i * inner] : 0.0;
+    z = (yv - (off ? off[i] : kOff) * z) * inv_d[i];
+    if (valid) p[i * inner] = z;
   }
 }
 
@@ -524,7 +615,7 @@ static void launch_rec_interp(const T* shell, const T* coarse, T* fine, const Le
 // compute_correction sweeps on `comp` (natural fine extents); the result
 // (coarse extents, row-major) ends in *result, which points into comp or tmp.
 static void run_sweeps(double* comp, double* tmp, const LevelGeom& g, const ThomasLevel* th, const NuLevel* nu,
-                       double** result, const Exec& ex) {
+                       double** result, const Exec& ex, bool fast) {
   int64_t cur[kMaxD];
   for (int i = 0; i < g.d; ++i) cur[i] = g.n[i];
   double* x = comp;
@@ -535,7 +626,20 @@ static void run_sweeps(double* comp, double* tmp, const LevelGeom& g, const Thom
     for (int i = a + 1; i < g.d; ++i) inner *= cur[i];
     const int64_t lines = outer * inner;
     const int grid = grid_for(lines, 128, 32);
-    if (nu)
+    // the serial per-line sweep saturates the GPU when there are many lines;
+    // few long lines (2-D levels) need the segmented solve
+    if (fast && lines < (int64_t(1) << 17)) {
+      const int64_t outs = outer * g.m[a] * inner;
+      if (nu)
+        MGRX_LAUNCH(ex, "gen_load", k_axis_load<true><<<grid_for(outs, 256), 256, 0, ex.s>>>(x, y, outer, inner, g.n[a], g.m[a], nu->ax[a].s));
+      else
+        MGRX_LAUNCH(ex, "gen_load", k_axis_load<false><<<grid_for(outs, 256), 256, 0, ex.s>>>(x, y, outer, inner, g.n[a], g.m[a], nullptr));
+      const int SY = int(std::max<int64_t>(1, std::min<int64_t>(32, (g.m[a] + 31) / 32)));
+      const double* w = nu ? nu->ax[a].tw : th->w[a];
+      const double* id = nu ? nu->ax[a].tid : th->inv_d[a];
+      const double* of = nu ? nu->ax[a].off : nullptr;
+      MGRX_LAUNCH(ex, "gen_solve", k_axis_solve<<<unsigned((lines + 15) / 16), dim3(32, SY), 0, ex.s>>>(y, lines, g.m[a], inner, w, id, of));
+    } else if (nu)
       MGRX_LAUNCH(ex, "gen_sweep", k_sweep<true><<<grid, 128, 0, ex.s>>>(x, y, outer, inner, g.n[a], g.m[a], nullptr, nullptr, nu->ax[a]));
     else
       MGRX_LAUNCH(ex, "gen_sweep", k_sweep<false><<<grid, 128, 0, ex.s>>>(x, y, outer, inner, g.n[a], g.m[a], th->w[a], th->inv_d[a], NuAxis{}));
@@ -549,20 +653,20 @@ static void run_sweeps(double* comp, double* tmp, const LevelGeom& g, const Thom
 
 template <typename T>
 cudaError_t general_decompose_level(const T* blk, T* shell, T* coarse, double* comp, double* tmp, const LevelGeom& g,
-                                    const ThomasLevel* th, const NuLevel* nu, const Exec& ex) {
+                                    const ThomasLevel* th, const NuLevel* nu, const Exec& ex, bool fast) {
   launch_dec_coef<T>(blk, shell, coarse, comp, g, nu, ex);
   double* z = nullptr;
-  run_sweeps(comp, tmp, g, th, nu, &z, ex);
+  run_sweeps(comp, tmp, g, th, nu, &z, ex, fast);
   MGRX_LAUNCH(ex, "gen_apply", k_apply<T><<<grid_for(g.Nc, 256), 256, 0, ex.s>>>(coarse, z, g.Nc, 1.0));
   return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t general_recompose_level(const T* shell, T* coarse, T* fine, double* comp, double* tmp, const LevelGeom& g,
-                                    const ThomasLevel* th, const NuLevel* nu, const Exec& ex) {
+                                    const ThomasLevel* th, const NuLevel* nu, const Exec& ex, bool fast) {
   launch_rec_comp<T>(shell, comp, g, ex);
   double* z = nullptr;
-  run_sweeps(comp, tmp, g, th, nu, &z, ex);
+  run_sweeps(comp, tmp, g, th, nu, &z, ex, fast);
   MGRX_LAUNCH(ex, "gen_apply", k_apply<T><<<grid_for(g.Nc, 256), 256, 0, ex.s>>>(coarse, z, g.Nc, -1.0));
   launch_rec_interp<T>(shell, coarse, fine, g, nu, ex);
   return cudaGetLastError();
@@ -570,9 +674,9 @@ cudaError_t general_recompose_level(const T* shell, T* coarse, T* fine, double* 
 
 #define MGRX_INST(T)                                                                                           \
   template cudaError_t general_decompose_level<T>(const T*, T*, T*, double*, double*, const LevelGeom&,         \
-                                                  const ThomasLevel*, const NuLevel*, const Exec&);             \
+                                                  const ThomasLevel*, const NuLevel*, const Exec&, bool);       \
   template cudaError_t general_recompose_level<T>(const T*, T*, T*, double*, double*, const LevelGeom&,         \
-                                                  const ThomasLevel*, const NuLevel*, const Exec&);
+                                                  const ThomasLevel*, const NuLevel*, const Exec&, bool);
 MGRX_INST(float)
 MGRX_INST(double)
 #undef MGRX_INST

@@ -11,11 +11,15 @@ namespace mgrx_b200 {
 
 // ---- general per-step path (general.cu) -----------------------------------
 template <typename T>
+// fast: parallel load + segmented Thomas sweeps (path "auto"); false: the
+// serial per-line sweeps, bit-identical to the reference (path "general")
 cudaError_t general_decompose_level(const T* blk, T* shell, T* coarse, double* comp, double* tmp,
-                                    const LevelGeom& g, const ThomasLevel* th, const NuLevel* nu, const Exec& ex);
+                                    const LevelGeom& g, const ThomasLevel* th, const NuLevel* nu, const Exec& ex,
+                                    bool fast);
 template <typename T>
 cudaError_t general_recompose_level(const T* shell, T* coarse, T* fine, double* comp, double* tmp,
-                                    const LevelGeom& g, const ThomasLevel* th, const NuLevel* nu, const Exec& ex);
+                                    const LevelGeom& g, const ThomasLevel* th, const NuLevel* nu, const Exec& ex,
+                                    bool fast);
 
 // ---- tail: all small levels in one CTA (general.cu) -------------------------
 size_t tail_smem_bytes(int64_t nmax, int esize);
