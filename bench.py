@@ -405,7 +405,7 @@ def measured_traffic(tag):
         return None
 
 
-def batch_measure(mg, field, h, args, dev, inflight=2):
+def batch_measure(mg, field, h, args, dev, inflight=None):
     """Config 5a on one GPU: independent fields in flight on separate
     streams (one context and one captured step graph each), so one field's
     latency-bound coarse levels overlap another's finest-level passes.
@@ -414,6 +414,7 @@ def batch_measure(mg, field, h, args, dev, inflight=2):
 
     from paper_2010_05872_b200.fields import config2_field
 
+    inflight = inflight or args.batch_inflight
     fields = [field] + [config2_field(DIMS, seed=1000 + i, device=dev) for i in range(inflight - 1)]
     streams = [torch.cuda.Stream(dev) for _ in fields]
     graphs, contexts = [], []  # contexts must outlive the graphs (their scratch is captured)
@@ -551,6 +552,7 @@ def main():
     ap.add_argument("--path", choices=["auto", "general"], default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of CUDA-graph replay")
+    ap.add_argument("--batch-inflight", type=int, default=2, help="fields in flight for the batch measurement")
     ap.add_argument("--dims", default="513,513,513",
                     help="field extents (config-2 generator); 1025,1025,1025 is BASELINE config 5b")
     ap.add_argument("--ref-threads", type=int, default=0)
