@@ -1020,7 +1020,7 @@ void launch_row(double* G, const F3Geom& g, const double* w, const double* id, c
   const size_t smem = size_t(2 + threads / 32) * m * 8;
   cudaFuncSetAttribute(k_f3_row, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   const int64_t blocks = std::min<int64_t>((rows + 7) / 8, int64_t(kNumSMs) * 8);
-  MGRX_LAUNCH(ex, "f3_row", pdl_launch(k_f3_row, dim3(unsigned(blocks)), dim3(threads), smem, ex.s, G, rows, m, w, id));
+  MGRX_LAUNCH(ex, "f3_row", pdl_launch(k_f3_row, dim3(unsigned(blocks)), dim3(threads), smem, ex.s, !ex.prof, G, rows, m, w, id));
 }
 
 // ------------------------------------------------------------ column pass
@@ -1189,7 +1189,7 @@ void launch_col(double* G, T* coarse, double sign, const F3Geom& g, int axis, co
   {                                                                                                       \
     const int SY = (m + 2 * LS - 1) / (2 * LS);                                                          \
     MGRX_LAUNCH(ex, tag, pdl_launch(k_f3_col<T, LS, AP, MT>, dim3(blocks), dim3(32, SY),                      \
-                                    size_t(2 * m + 2 * 2 * SY * 16) * 8, ex.s, G, coarse, sign, ncols, m,       \
+                                    size_t(2 * m + 2 * 2 * SY * 16) * 8, ex.s, !ex.prof, G, coarse, sign, ncols, m,       \
                                     stride, outer_stride, inner, w, id));                                       \
   }
   if (m <= 264) {
@@ -1287,7 +1287,7 @@ static cudaError_t launch_interp_t(const T* shell, const T* coarse, T* fine, con
   ich = std::max<int64_t>(2, std::min<int64_t>(32, ich & ~int64_t(1)));
   const int64_t chunks = (g.n0 + ich - 1) / ich;
   MGRX_LAUNCH(ex, "f3_rec_interp",
-              pdl_launch(k_f3_rec_interp<T, TRI, MAXT>, dim3(unsigned(chunks * ntile)), dim3(g.threads), smem, ex.s,
+              pdl_launch(k_f3_rec_interp<T, TRI, MAXT>, dim3(unsigned(chunks * ntile)), dim3(g.threads), smem, ex.s, !ex.prof,
                          shell, coarse, fine, g, int(ich), ntile));
   return cudaSuccess;
 }
@@ -1332,7 +1332,7 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
 #define MGRX_DEC(TI, MT)                                                                               \
   if (g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))                      \
     MGRX_LAUNCH(ex, "f3_dec_plane", pdl_launch(k_f3_dec_plane<T, TI, MT>, dim3(g.grid), dim3(g.threads), ds, \
-                                               ex.s, blk, shell, coarse, G, g));
+                                               ex.s, !ex.prof, blk, shell, coarse, G, g));
   MGRX_DEC(4, kPlaneMaxThreads)
   MGRX_DEC(2, kPlaneMaxThreads)
   MGRX_DEC(4, kWideBound)
@@ -1359,7 +1359,7 @@ cudaError_t fused3d_recompose_correction(const T* shell, void* scratch, const Fu
 #define MGRX_REC(TI, MT)                                                                               \
   if (g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))                      \
     MGRX_LAUNCH(ex, "f3_rec_plane", pdl_launch(k_f3_rec_plane<T, TI, MT>, dim3(g.grid), dim3(g.threads), ds, \
-                                               ex.s, shell, G, g));
+                                               ex.s, !ex.prof, shell, G, g));
   MGRX_REC(4, kPlaneMaxThreads)
   MGRX_REC(2, kPlaneMaxThreads)
   MGRX_REC(4, kWideBound)

@@ -508,7 +508,7 @@ static cudaError_t tail_dec_t(const T* blk, T* out, T* coarse_out, const void* d
   const size_t sm = tail_smem_bytes(nmax, sizeof(T));
   cudaError_t e = cudaFuncSetAttribute(k_tail_decompose<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
   if (e != cudaSuccess) return e;
-  MGRX_LAUNCH(ex, "tail_dec", pdl_launch(k_tail_decompose<T, D>, dim3(1), dim3(1024), sm, ex.s, blk, out, coarse_out,
+  MGRX_LAUNCH(ex, "tail_dec", pdl_launch(k_tail_decompose<T, D>, dim3(1), dim3(1024), sm, ex.s, !ex.prof, blk, out, coarse_out,
                                          static_cast<const TailLevel*>(d_levels), nlev, nmax));
   return cudaGetLastError();
 }
@@ -519,7 +519,7 @@ static cudaError_t tail_rec_t(const T* coeffs, const T* coarse_in, T* fine_out, 
   const size_t sm = tail_smem_bytes(nmax, sizeof(T));
   cudaError_t e = cudaFuncSetAttribute(k_tail_recompose<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
   if (e != cudaSuccess) return e;
-  MGRX_LAUNCH(ex, "tail_rec", pdl_launch(k_tail_recompose<T, D>, dim3(1), dim3(1024), sm, ex.s, coeffs, coarse_in,
+  MGRX_LAUNCH(ex, "tail_rec", pdl_launch(k_tail_recompose<T, D>, dim3(1), dim3(1024), sm, ex.s, !ex.prof, coeffs, coarse_in,
                                          fine_out, static_cast<const TailLevel*>(d_levels), nlev, nmax));
   return cudaGetLastError();
 }
