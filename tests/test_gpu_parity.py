@@ -318,3 +318,28 @@ def test_contexts_on_threads(torch, mg):
         t.join()
     for i in range(2):
         assert torch.equal(out[i], ref[i])
+
+
+@pytest.mark.parametrize("shape", [(3, 2, 3, 2, 3, 2), (2, 3, 2, 3, 2, 3, 2), (3, 2, 2, 3, 2, 2, 2, 3)])
+def test_high_rank_general_path(torch, mg, shape):
+    """Ranks 6-8 (the C-ABI's maximum) on the general path: bit-identical to
+    the oracle (itself bit-identical to the reference), both directions."""
+    from oracle.oracle import Oracle
+
+    o = Oracle()
+    rng = np.random.default_rng(len(shape))
+    x = rng.uniform(-1, 1, shape)
+    h = mg.GridHierarchy.create(shape)
+    ws = mg.SolverWorkspace(path="general")
+    for stop in sorted({0, h.num_levels()}):
+        got = mg.decompose(to_dev(torch, x), h, stop, ws).buffer.cpu().numpy()
+        want = o.decompose(x, stop)
+        assert bits(got) == bits(want), (shape, stop)
+        back = mg.recompose(mg.MultilevelCoefficients(to_dev(torch, want), h, stop), ws).cpu().numpy()
+        assert bits(back) == bits(o.recompose(want, shape, stop)), (shape, stop)
+
+
+def test_rank_above_limit_is_rejected(mg):
+    with pytest.raises(mg.Error) as e:
+        mg.GridHierarchy.create((2,) * 9)
+    assert e.value.code == "invalid_dims"
