@@ -1258,6 +1258,7 @@ Fused3DPlan fused3d_plan(const LevelGeom& lg, int esize) {
       chunk = c;
     }
   }
+  if (const char* env = std::getenv("MGRX_CHUNK")) chunk = std::max<int64_t>(1, std::min<int64_t>(g.m0, std::atoll(env)));
   const int64_t nchunk = (g.m0 + chunk - 1) / chunk;
   g.chunk = chunk;
   g.units = int(nchunk * g.ntile1);
