@@ -570,7 +570,9 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
       ensure_side(c, L + 1);
       cuda_check(cudaEventRecord(c->fork, c->stream), "cudaEventRecord(fork)");
       int k = 0;
-      for (int l = L; l > stop; --l) {
+      // coarse levels first: their corrections are small and the chain needs
+      // them first; the finest level's large correction is enqueued last
+      for (int l = stop + 1; l <= L; ++l) {
         const Fused3DPlan& fp = p.fused[l];
         if (!fp.enabled) continue;
         cudaStream_t sd = c->side[k++ % mgrx_gpu_ctx::kSide];
