@@ -7,7 +7,6 @@
 
 #include <cmath>
 #include <cstdarg>
-#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -238,7 +237,6 @@ struct mgrx_gpu_ctx {
   cudaStream_t chain = nullptr;  // high priority: the sequential recompose chain
   cudaEvent_t fork = nullptr, join = nullptr;
   std::vector<cudaEvent_t> lvl_done;
-  int reserve_sms = 0;  // SMs the finest-level correction leaves to the chain (MGRX_RESERVE_SMS; measured: no gain)
 };
 
 namespace {
@@ -580,7 +578,7 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
         cudaStream_t sd = c->side[k++ % mgrx_gpu_ctx::kSide];
         cuda_check(cudaStreamWaitEvent(sd, c->fork, 0), "cudaStreamWaitEvent");
         cuda_check(fused3d_recompose_correction<T>(d_coeffs + h.node[l - 1], s + fp.scratch_off, fp, p.thomas[l],
-                                                   exec_on(c, sd, l), l == L ? c->reserve_sms : 0),
+                                                   exec_on(c, sd, l)),
                    "recompose correction");
         cuda_check(cudaEventRecord(c->lvl_done[l], sd), "cudaEventRecord");
         forked[l] = 1;
@@ -686,7 +684,6 @@ int mgrx_gpu_ctx_create(int device, mgrx_gpu_ctx** out) {
   auto* c = new (std::nothrow) mgrx_gpu_ctx;
   if (!c) return MGRX_OUT_OF_MEMORY;
   c->device = device;
-  if (const char* env = std::getenv("MGRX_RESERVE_SMS")) c->reserve_sms = std::max(0, std::atoi(env));
   int rc = guarded(c, [&] {
     cuda_check(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own;

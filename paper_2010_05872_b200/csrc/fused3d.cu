@@ -710,10 +710,9 @@ __device__ __forceinline__ void rec_rows(const T* ev, const T* od, int st_e, int
 // component read from the level's shell.  Per fine plane the tile's shell
 // rows form two contiguous runs (even fine rows, odd fine rows), fetched
 // with two bulk copies into one ring slot.
-// One unit of the recompose plane pass (see k_f3_rec_plane).
-template <typename T, int TI1>
-__device__ __forceinline__ void rec_plane_unit(const T* __restrict__ shell, double* __restrict__ G, const F3Geom& g,
-                                               int u) {
+template <typename T, int TI1, int MAXT>
+__global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
+    k_f3_rec_plane(const T* __restrict__ shell, double* __restrict__ G, const F3Geom g) {
   using SM = PlaneSmem<T, TI1>;
   constexpr int RMAX = SM::kRows;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -728,7 +727,7 @@ __device__ __forceinline__ void rec_plane_unit(const T* __restrict__ shell, doub
   const int c = S.c;
   const int cc = S.valid ? c : 0;
   const bool has_odd = S.valid && 2 * c + 1 < n2;
-  const UnitRange ur = unit_range(g, u);
+  const UnitRange ur = unit_range(g, int(blockIdx.x));
   if (tid == 0) {
     for (int b = 0; b < NS; ++b) {
       mbar_init(&pp->full[b], 1);
@@ -819,18 +818,6 @@ __device__ __forceinline__ void rec_plane_unit(const T* __restrict__ shell, doub
     }
     pipe_release<NS>(pp, d, D, issue);
     l0_plane<TI1>(g, ur, S, p, Q, A, jdone, G);
-  }
-}
-
-// Recompose plane pass: the same restrictions from the shell.  Units are
-// strided over the grid, so a launch may use fewer CTAs than units (leaving
-// SMs to concurrent work) — one CTA per unit when gridDim.x == g.units.
-template <typename T, int TI1, int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
-    k_f3_rec_plane(const T* __restrict__ shell, double* __restrict__ G, const F3Geom g) {
-  for (int u = int(blockIdx.x); u < g.units; u += int(gridDim.x)) {
-    if (u != int(blockIdx.x)) __syncthreads();  // the previous unit's pipeline state is free
-    rec_plane_unit<T, TI1>(shell, G, g, u);
   }
   pdl_trigger();
 }
@@ -1364,14 +1351,8 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
 // is zero on the coarse nodes).
 template <typename T>
 cudaError_t fused3d_recompose_correction(const T* shell, void* scratch, const Fused3DPlan& fp, const ThomasLevel& th,
-                                         const Exec& ex, int reserve_sms) {
-  F3Geom g = fp.g;
-  if (reserve_sms > 0) {  // leave SMs to concurrent work: fewer CTAs, units strided over them
-    int dev = 0, nsm = kNumSMs;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    g.grid = std::max(1, std::min(g.units, g.ctas_per_sm * std::max(1, nsm - reserve_sms)));
-  }
+                                         const Exec& ex) {
+  const F3Geom& g = fp.g;
   double* G = static_cast<double*>(scratch);
   size_t ds = 0;
   cudaError_t e = set_attrs<T>(g, &ds);
@@ -1405,7 +1386,7 @@ cudaError_t fused3d_recompose_finish(const T* shell, T* coarse, T* fine, void* s
 template <typename T>
 cudaError_t fused3d_recompose_level(const T* shell, T* coarse, T* fine, void* scratch, const LevelGeom&,
                                     const Fused3DPlan& fp, const ThomasLevel& th, const Exec& ex) {
-  cudaError_t e = fused3d_recompose_correction<T>(shell, scratch, fp, th, ex, 0);
+  cudaError_t e = fused3d_recompose_correction<T>(shell, scratch, fp, th, ex);
   if (e != cudaSuccess) return e;
   return fused3d_recompose_finish<T>(shell, coarse, fine, scratch, fp, th, ex);
 }
@@ -1416,7 +1397,7 @@ cudaError_t fused3d_recompose_level(const T* shell, T* coarse, T* fine, void* sc
   template cudaError_t fused3d_recompose_level<T>(const T*, T*, T*, void*, const LevelGeom&, const Fused3DPlan&, \
                                                   const ThomasLevel&, const Exec&);                      \
   template cudaError_t fused3d_recompose_correction<T>(const T*, void*, const Fused3DPlan&, const ThomasLevel&,   \
-                                                       const Exec&, int);                                \
+                                                       const Exec&);                                     \
   template cudaError_t fused3d_recompose_finish<T>(const T*, T*, T*, void*, const Fused3DPlan&, const ThomasLevel&, \
                                                    const Exec&);
 MGRX_INST(float)

@@ -38,11 +38,9 @@ template <typename T>
 cudaError_t fused3d_recompose_level(const T* shell, T* coarse, T* fine, void* scratch, const LevelGeom& g,
                                     const Fused3DPlan& fp, const ThomasLevel& th, const Exec& ex);
 // recompose_level split in its shell-only correction and the sequential finish
-// reserve_sms > 0: the plane pass uses CTAs for only (SMs - reserve_sms)
-// SMs, leaving room for concurrent (latency-bound) work
 template <typename T>
 cudaError_t fused3d_recompose_correction(const T* shell, void* scratch, const Fused3DPlan& fp, const ThomasLevel& th,
-                                         const Exec& ex, int reserve_sms);
+                                         const Exec& ex);
 template <typename T>
 cudaError_t fused3d_recompose_finish(const T* shell, T* coarse, T* fine, void* scratch, const Fused3DPlan& fp,
                                      const ThomasLevel& th, const Exec& ex);
