@@ -83,31 +83,33 @@ __device__ __forceinline__ int64_t shell_pos(const LevelGeom& g, const int64_t* 
 template <typename T, bool kNu, int D = 0>
 __device__ __forceinline__ double predict(const T* __restrict__ src, bool coarse, const LevelGeom& g,
                                           const NuLevel& nu, const int64_t* j) {
+  // per axis (compile-time indices, registers): is it odd, the offset of the
+  // right corner (0 on a degenerate even-axis end), its bit in the cmask
+  // (odd axes ascending)
   int k = 0;
   int64_t base = 0;
+  int64_t dl[kMaxD];
+  int bit[kMaxD];
 #pragma unroll
   for (int i = 0; i < MGRX_ND(g); ++i) {
     const int64_t stride = coarse ? g.cst[i] : g.st[i];
-    if (j[i] & 1) {
-      ++k;
-      base += (coarse ? (j[i] - 1) >> 1 : j[i] - 1) * stride;
-    } else {
-      base += (coarse ? j[i] >> 1 : j[i]) * stride;
-    }
+    const bool odd = j[i] & 1;
+    dl[i] = (odd && j[i] + 1 < g.n[i]) ? (coarse ? g.cst[i] : 2 * g.st[i]) : 0;
+    bit[i] = odd ? k : -1;
+    k += odd ? 1 : 0;
+    base += (coarse ? (odd ? (j[i] - 1) >> 1 : j[i] >> 1) : (odd ? j[i] - 1 : j[i])) * stride;
   }
+  // corners in cmask order, summed in that order
   double sum = 0.0;
   for (unsigned cm = 0; cm < (1u << k); ++cm) {
     int64_t off = base;
     double wprod = 1.0;
-    int b = 0;  // bit of cm for the b-th odd axis (axes ascending)
 #pragma unroll
-    for (int ax = 0; ax < MGRX_ND(g); ++ax) {
-      if (!(j[ax] & 1)) continue;
-      const bool right = (cm >> b) & 1u;
-      ++b;
-      const bool has_right = j[ax] + 1 < g.n[ax];
-      if (right && has_right) off += coarse ? g.cst[ax] : 2 * g.st[ax];
-      if (kNu) wprod = mul_(wprod, right ? nu.ax[ax].wr[j[ax]] : nu.ax[ax].wl[j[ax]]);
+    for (int i = 0; i < MGRX_ND(g); ++i) {
+      if (bit[i] < 0) continue;
+      const bool right = (cm >> bit[i]) & 1u;
+      if (right) off += dl[i];
+      if (kNu) wprod = mul_(wprod, right ? nu.ax[i].wr[j[i]] : nu.ax[i].wl[j[i]]);
     }
     const double v = double(src[off]);
     sum = kNu ? add_(sum, mul_(wprod, v)) : add_(sum, v);
