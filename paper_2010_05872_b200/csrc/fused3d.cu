@@ -1239,7 +1239,8 @@ Fused3DPlan fused3d_plan(const LevelGeom& lg, int esize) {
   const int ctas = nsm * g.ctas_per_sm;
   // Small levels are latency bound (a unit streams its planes serially):
   // shrink the row tile until single-plane-pair units give two waves.
-  while (g.tile_rows > 2 && ((g.m1 + g.tile_rows - 1) / g.tile_rows) * g.m0 < 2 * int64_t(ctas))
+  const bool shrink = std::getenv("MGRX_NO_TILE_SHRINK") == nullptr;
+  while (shrink && g.tile_rows > 2 && ((g.m1 + g.tile_rows - 1) / g.tile_rows) * g.m0 < 2 * int64_t(ctas))
     g.tile_rows = g.tile_rows == 8 ? 6 : (g.tile_rows == 6 ? 4 : 2);
   g.ntile1 = int((g.m1 + g.tile_rows - 1) / g.tile_rows);
   // axis-0 chunk of a unit: a unit of c coarse planes streams 2c + 3 fine
