@@ -157,7 +157,7 @@ struct Plan {
   size_t off_comp = 0, off_tmp = 0, off_blk = 0, bytes = 0;
   std::vector<size_t> blk_off;     // level block offsets (levels stop..L-1)
   std::vector<Fused3DPlan> fused;  // index l; .enabled false when not applicable
-  // tail: levels stop+1..tail_top run in one CTA (uniform coordinates)
+  // tail: levels stop+1..tail_top run in one CTA (uniform or nonuniform coordinates)
   int tail_top = -1;
   int64_t tail_nmax = 0;
   void* d_tail_dec = nullptr;  // TailLevel[] finest first
@@ -227,6 +227,8 @@ struct mgrx_gpu_ctx {
   uint64_t nu_key = 0;          // hash of (plan, coordinates) the tables were built for
   const void* nu_plan = nullptr;
   std::vector<NuLevel> nu_levels;
+  NuLevel* d_tail_nu = nullptr;  // NuLevel of the tail levels: [dec order | rec order]
+  size_t tail_nu_bytes = 0;
   size_t nu_bytes = 0;
   std::map<PlanKey, std::unique_ptr<Plan>> plans;
   Profiler prof;
@@ -489,7 +491,6 @@ std::vector<NuLevel> upload_nu(mgrx_gpu_ctx* c, const Plan& p, const double* con
   size_t need = host.size() * sizeof(double);
   ensure(reinterpret_cast<void**>(&c->nu_tables), &c->nu_bytes, need ? need : 8, c, "cudaMalloc(nu tables)");
   cuda_check(cudaMemcpyAsync(c->nu_tables, host.data(), need, cudaMemcpyHostToDevice, c->stream), "upload nu");
-  cuda_check(cudaStreamSynchronize(c->stream), "sync nu upload");
   std::vector<NuLevel> out(h.L + 1);
   for (int l = p.stop + 1; l <= h.L; ++l)
     for (int a = 0; a < h.d; ++a) {
@@ -497,6 +498,18 @@ std::vector<NuLevel> upload_nu(mgrx_gpu_ctx* c, const Plan& p, const double* con
       out[l].ax[a] = NuAxis{c->nu_tables + o.wl, c->nu_tables + o.wr, c->nu_tables + o.s,
                             c->nu_tables + o.tw, c->nu_tables + o.tid, c->nu_tables + o.off};
     }
+  // the tail kernels' per-level tables, in their level orders
+  std::vector<NuLevel> tail;
+  if (p.tail_top > p.stop) {
+    for (int l = p.tail_top; l > p.stop; --l) tail.push_back(out[l]);   // decompose: finest first
+    for (int l = p.stop + 1; l <= p.tail_top; ++l) tail.push_back(out[l]);  // recompose: coarsest first
+    ensure(reinterpret_cast<void**>(&c->d_tail_nu), &c->tail_nu_bytes, tail.size() * sizeof(NuLevel), c,
+           "cudaMalloc(tail nu)");
+    cuda_check(cudaMemcpyAsync(c->d_tail_nu, tail.data(), tail.size() * sizeof(NuLevel), cudaMemcpyHostToDevice,
+                               c->stream),
+               "upload tail nu");
+  }
+  cuda_check(cudaStreamSynchronize(c->stream), "sync nu upload");
   c->nu_plan = &p;
   c->nu_key = key;
   c->nu_levels = out;
@@ -520,8 +533,10 @@ void decompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, T* d_out, const 
   double* tmp = reinterpret_cast<double*>(s + p.off_tmp);
   const T* blk = d_field;
   for (int l = L; l > stop; --l) {
-    if (!nu && l == p.tail_top) {  // levels l..stop+1 in one CTA
-      cuda_check(tail_decompose<T>(blk, d_out, d_out, p.d_tail_dec, l - stop, p.tail_nmax, h.d, exec(c, l)), "tail");
+    if (l == p.tail_top) {  // levels l..stop+1 in one CTA
+      cuda_check(tail_decompose<T>(blk, d_out, d_out, p.d_tail_dec, nu ? c->d_tail_nu : nullptr, l - stop,
+                                   p.tail_nmax, h.d, exec(c, l)),
+                 "tail");
       break;
     }
     T* shell = d_out + h.node[l - 1];
@@ -590,10 +605,12 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
   // unpack_level_centric's coarse block (reorder.hpp:231-238)
   T* coarse = reinterpret_cast<T*>(s + p.blk_off[stop]);
   int l0 = stop + 1;
-  if (!nu && p.tail_top > stop) {  // levels stop+1..tail_top in one CTA
+  if (p.tail_top > stop) {  // levels stop+1..tail_top in one CTA
     const int top = p.tail_top;
     T* fine = (top == L) ? d_field : reinterpret_cast<T*>(s + p.blk_off[top]);
-    cuda_check(tail_recompose<T>(d_coeffs, d_coeffs, fine, p.d_tail_rec, top - stop, p.tail_nmax, h.d,
+    cuda_check(tail_recompose<T>(d_coeffs, d_coeffs, fine, p.d_tail_rec,
+                                 nu ? static_cast<const void*>(c->d_tail_nu + (top - stop)) : nullptr, top - stop,
+                                 p.tail_nmax, h.d,
                                     exec_on(c, cs, top)), "tail");
     coarse = fine;
     l0 = top + 1;
@@ -706,6 +723,7 @@ int mgrx_gpu_ctx_destroy(mgrx_gpu_ctx* c) {
   if (c->io) cudaFree(c->io);
   if (c->qtmp) cudaFree(c->qtmp);
   if (c->nu_tables) cudaFree(c->nu_tables);
+  if (c->d_tail_nu) cudaFree(c->d_tail_nu);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->own) cudaStreamDestroy(c->own);
   for (int i = 0; i < mgrx_gpu_ctx::kSide; ++i)

@@ -344,9 +344,9 @@ struct TailLevel {
   int64_t shell_off;  // node_count(l-1): shell position in the level-centric buffer
 };
 
-template <int D>
+template <int D, bool kNu>
 __device__ __forceinline__ void tail_sweeps(double* comp, double* tmp, const LevelGeom& g, const ThomasLevel& th,
-                                            double** result) {
+                                            const NuLevel& nu, double** result) {
   int cur[kMaxD];
 #pragma unroll
   for (int i = 0; i < MGRX_ND(g); ++i) cur[i] = int(g.n[i]);
@@ -370,21 +370,31 @@ __device__ __forceinline__ void tail_sweeps(double* comp, double* tmp, const Lev
       double prev = 0.0;
       for (int i = 0; i < m; ++i) {
         double acc = 0.0;
-        if (i >= 1) {
-          acc = add_(acc, mul_(kW12, c[(2 * i - 2) * inner]));
-          acc = add_(acc, mul_(0.5, c[(2 * i - 1) * inner]));
+        if (kNu) {  // same arithmetic as k_sweep<true>
+          const double* sk = nu.ax[a].s + 5 * i;
+          for (int k = 0; k < 5; ++k) {
+            const int jj = 2 * i + k - 2;
+            if (jj >= 0 && jj < n) acc = add_(acc, mul_(sk[k], c[jj * inner]));
+          }
+          if (i > 0) acc = sub_(acc, mul_(nu.ax[a].tw[i], prev));
+        } else {
+          if (i >= 1) {
+            acc = add_(acc, mul_(kW12, c[(2 * i - 2) * inner]));
+            acc = add_(acc, mul_(0.5, c[(2 * i - 1) * inner]));
+          }
+          acc = add_(acc, mul_((i == 0 || i + 1 == m) ? kW5_12 : kW5_6, c[(2 * i) * inner]));
+          if (2 * i + 1 < n) acc = add_(acc, mul_(0.5, c[(2 * i + 1) * inner]));
+          if (2 * i + 2 < n) acc = add_(acc, mul_(kW12, c[(2 * i + 2) * inner]));
+          if (i > 0) acc = sub_(acc, mul_(w[i], prev));
         }
-        acc = add_(acc, mul_((i == 0 || i + 1 == m) ? kW5_12 : kW5_6, c[(2 * i) * inner]));
-        if (2 * i + 1 < n) acc = add_(acc, mul_(0.5, c[(2 * i + 1) * inner]));
-        if (2 * i + 2 < n) acc = add_(acc, mul_(kW12, c[(2 * i + 2) * inner]));
-        if (i > 0) acc = sub_(acc, mul_(w[i], prev));
         f[i * inner] = acc;
         prev = acc;
       }
-      double nxt = mul_(prev, inv_d[m - 1]);
+      double nxt = mul_(prev, kNu ? nu.ax[a].tid[m - 1] : inv_d[m - 1]);
       f[(m - 1) * inner] = nxt;
       for (int i = m - 2; i >= 0; --i) {
-        const double v = mul_(sub_(f[i * inner], mul_(kOff, nxt)), inv_d[i]);
+        const double v = kNu ? mul_(sub_(f[i * inner], mul_(nu.ax[a].off[i], nxt)), nu.ax[a].tid[i])
+                             : mul_(sub_(f[i * inner], mul_(kOff, nxt)), inv_d[i]);
         f[i * inner] = v;
         nxt = v;
       }
@@ -400,16 +410,15 @@ __device__ __forceinline__ void tail_sweeps(double* comp, double* tmp, const Lev
 
 // Decompose levels levels[0] (finest, block read from `blk`) down to the
 // last entry; shells go to out + shell_off, the final coarse block to `coarse_out`.
-template <typename T, int D>
+template <typename T, int D, bool kNu>
 __global__ void __launch_bounds__(1024) k_tail_decompose(const T* __restrict__ blk, T* __restrict__ out,
                                                          T* __restrict__ coarse_out, const TailLevel* __restrict__ lv,
-                                                         int nlev, int64_t nmax) {
+                                                         const NuLevel* __restrict__ nul, int nlev, int64_t nmax) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* comp = reinterpret_cast<double*>(smem);
   double* tmp = comp + nmax;
   T* A = reinterpret_cast<T*>(tmp + nmax);
   T* B = A + nmax;
-  const NuLevel nu{};
   pdl_wait();
   for (int64_t p = threadIdx.x; p < lv[0].g.N; p += blockDim.x) A[p] = blk[p];
   __syncthreads();
@@ -417,6 +426,7 @@ __global__ void __launch_bounds__(1024) k_tail_decompose(const T* __restrict__ b
   T* nxt = B;
   for (int k = 0; k < nlev; ++k) {
     const LevelGeom& g = lv[k].g;
+    const NuLevel nu = kNu ? nul[k] : NuLevel{};
     T* shell = out + lv[k].shell_off;
     for (int64_t p = threadIdx.x; p < g.N; p += blockDim.x) {
       int64_t j[kMaxD];
@@ -429,7 +439,7 @@ __global__ void __launch_bounds__(1024) k_tail_decompose(const T* __restrict__ b
         nxt[cc] = cur[p];
         comp[p] = 0.0;
       } else {
-        const double pred = predict<T, false, D>(cur, false, g, nu, j);
+        const double pred = predict<T, kNu, D>(cur, false, g, nu, j);
         const T v = to_t<T>(sub_(double(cur[p]), pred));
         comp[p] = double(v);
         shell[shell_pos<D>(g, j)] = v;
@@ -437,7 +447,7 @@ __global__ void __launch_bounds__(1024) k_tail_decompose(const T* __restrict__ b
     }
     __syncthreads();
     double* z = nullptr;
-    tail_sweeps<D>(comp, tmp, g, lv[k].th, &z);
+    tail_sweeps<D, kNu>(comp, tmp, g, lv[k].th, nu, &z);
     for (int64_t p = threadIdx.x; p < g.Nc; p += blockDim.x) nxt[p] = to_t<T>(add_(double(nxt[p]), mul_(1.0, z[p])));
     __syncthreads();
     T* t = cur;
@@ -450,16 +460,15 @@ __global__ void __launch_bounds__(1024) k_tail_decompose(const T* __restrict__ b
 // Recompose from the coarse block (`coarse_in`, level of the first entry's
 // coarse side) up through the entries (coarsest first); the last fine block
 // goes to `fine_out`.
-template <typename T, int D>
+template <typename T, int D, bool kNu>
 __global__ void __launch_bounds__(1024) k_tail_recompose(const T* __restrict__ coeffs, const T* __restrict__ coarse_in,
                                                          T* __restrict__ fine_out, const TailLevel* __restrict__ lv,
-                                                         int nlev, int64_t nmax) {
+                                                         const NuLevel* __restrict__ nul, int nlev, int64_t nmax) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* comp = reinterpret_cast<double*>(smem);
   double* tmp = comp + nmax;
   T* A = reinterpret_cast<T*>(tmp + nmax);
   T* B = A + nmax;
-  const NuLevel nu{};
   pdl_wait();
   for (int64_t p = threadIdx.x; p < lv[0].g.Nc; p += blockDim.x) A[p] = coarse_in[p];
   __syncthreads();
@@ -467,6 +476,7 @@ __global__ void __launch_bounds__(1024) k_tail_recompose(const T* __restrict__ c
   T* fin = B;
   for (int k = 0; k < nlev; ++k) {
     const LevelGeom& g = lv[k].g;
+    const NuLevel nu = kNu ? nul[k] : NuLevel{};
     const T* shell = coeffs + lv[k].shell_off;
     for (int64_t p = threadIdx.x; p < g.N; p += blockDim.x) {
       int64_t j[kMaxD];
@@ -477,7 +487,7 @@ __global__ void __launch_bounds__(1024) k_tail_recompose(const T* __restrict__ c
     }
     __syncthreads();
     double* z = nullptr;
-    tail_sweeps<D>(comp, tmp, g, lv[k].th, &z);
+    tail_sweeps<D, kNu>(comp, tmp, g, lv[k].th, nu, &z);
     for (int64_t p = threadIdx.x; p < g.Nc; p += blockDim.x) cur[p] = to_t<T>(add_(double(cur[p]), mul_(-1.0, z[p])));
     __syncthreads();
     T* dst = (k == nlev - 1) ? fine_out : fin;
@@ -491,7 +501,7 @@ __global__ void __launch_bounds__(1024) k_tail_recompose(const T* __restrict__ c
         for (int i = 0; i < MGRX_ND(g); ++i) cc += (j[i] >> 1) * g.cst[i];
         dst[p] = cur[cc];
       } else {
-        const double pred = predict<T, false, D>(cur, true, g, nu, j);
+        const double pred = predict<T, kNu, D>(cur, true, g, nu, j);
         dst[p] = to_t<T>(add_(double(shell[shell_pos<D>(g, j)]), pred));
       }
     }
@@ -505,48 +515,71 @@ __global__ void __launch_bounds__(1024) k_tail_recompose(const T* __restrict__ c
 size_t tail_smem_bytes(int64_t nmax, int esize) { return size_t(nmax) * (16 + 2 * size_t(esize)); }
 
 template <typename T, int D>
-static cudaError_t tail_dec_t(const T* blk, T* out, T* coarse_out, const void* d_levels, int nlev, int64_t nmax,
-                              const Exec& ex) {
+static cudaError_t tail_dec_t(const T* blk, T* out, T* coarse_out, const void* d_levels, const void* d_nu, int nlev,
+                              int64_t nmax, const Exec& ex) {
   const size_t sm = tail_smem_bytes(nmax, sizeof(T));
-  cudaError_t e = cudaFuncSetAttribute(k_tail_decompose<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-  if (e != cudaSuccess) return e;
-  MGRX_LAUNCH(ex, "tail_dec", pdl_launch(k_tail_decompose<T, D>, dim3(1), dim3(1024), sm, ex.s, !ex.prof, blk, out, coarse_out,
-                                         static_cast<const TailLevel*>(d_levels), nlev, nmax));
+  const TailLevel* lv = static_cast<const TailLevel*>(d_levels);
+  const NuLevel* nul = static_cast<const NuLevel*>(d_nu);
+  if (nul) {
+    cudaError_t e = cudaFuncSetAttribute(k_tail_decompose<T, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(sm));
+    if (e != cudaSuccess) return e;
+    MGRX_LAUNCH(ex, "tail_dec", pdl_launch(k_tail_decompose<T, D, true>, dim3(1), dim3(1024), sm, ex.s, !ex.prof, blk,
+                                           out, coarse_out, lv, nul, nlev, nmax));
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(k_tail_decompose<T, D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(sm));
+    if (e != cudaSuccess) return e;
+    MGRX_LAUNCH(ex, "tail_dec", pdl_launch(k_tail_decompose<T, D, false>, dim3(1), dim3(1024), sm, ex.s, !ex.prof, blk,
+                                           out, coarse_out, lv, nul, nlev, nmax));
+  }
   return cudaGetLastError();
 }
 
 template <typename T, int D>
-static cudaError_t tail_rec_t(const T* coeffs, const T* coarse_in, T* fine_out, const void* d_levels, int nlev,
-                              int64_t nmax, const Exec& ex) {
+static cudaError_t tail_rec_t(const T* coeffs, const T* coarse_in, T* fine_out, const void* d_levels, const void* d_nu,
+                              int nlev, int64_t nmax, const Exec& ex) {
   const size_t sm = tail_smem_bytes(nmax, sizeof(T));
-  cudaError_t e = cudaFuncSetAttribute(k_tail_recompose<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-  if (e != cudaSuccess) return e;
-  MGRX_LAUNCH(ex, "tail_rec", pdl_launch(k_tail_recompose<T, D>, dim3(1), dim3(1024), sm, ex.s, !ex.prof, coeffs, coarse_in,
-                                         fine_out, static_cast<const TailLevel*>(d_levels), nlev, nmax));
+  const TailLevel* lv = static_cast<const TailLevel*>(d_levels);
+  const NuLevel* nul = static_cast<const NuLevel*>(d_nu);
+  if (nul) {
+    cudaError_t e = cudaFuncSetAttribute(k_tail_recompose<T, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(sm));
+    if (e != cudaSuccess) return e;
+    MGRX_LAUNCH(ex, "tail_rec", pdl_launch(k_tail_recompose<T, D, true>, dim3(1), dim3(1024), sm, ex.s, !ex.prof,
+                                           coeffs, coarse_in, fine_out, lv, nul, nlev, nmax));
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(k_tail_recompose<T, D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(sm));
+    if (e != cudaSuccess) return e;
+    MGRX_LAUNCH(ex, "tail_rec", pdl_launch(k_tail_recompose<T, D, false>, dim3(1), dim3(1024), sm, ex.s, !ex.prof,
+                                           coeffs, coarse_in, fine_out, lv, nul, nlev, nmax));
+  }
   return cudaGetLastError();
 }
 
 // Rank-specialised tails for 1-3 dimensions (the common cases), runtime
-// rank otherwise.
+// rank otherwise; d_nu: per-level nonuniform tables (same order as the
+// levels) or null for uniform coordinates.
 template <typename T>
-cudaError_t tail_decompose(const T* blk, T* out, T* coarse_out, const void* d_levels, int nlev, int64_t nmax, int d,
-                           const Exec& ex) {
+cudaError_t tail_decompose(const T* blk, T* out, T* coarse_out, const void* d_levels, const void* d_nu, int nlev,
+                           int64_t nmax, int d, const Exec& ex) {
   switch (d) {
-    case 1: return tail_dec_t<T, 1>(blk, out, coarse_out, d_levels, nlev, nmax, ex);
-    case 2: return tail_dec_t<T, 2>(blk, out, coarse_out, d_levels, nlev, nmax, ex);
-    case 3: return tail_dec_t<T, 3>(blk, out, coarse_out, d_levels, nlev, nmax, ex);
-    default: return tail_dec_t<T, 0>(blk, out, coarse_out, d_levels, nlev, nmax, ex);
+    case 1: return tail_dec_t<T, 1>(blk, out, coarse_out, d_levels, d_nu, nlev, nmax, ex);
+    case 2: return tail_dec_t<T, 2>(blk, out, coarse_out, d_levels, d_nu, nlev, nmax, ex);
+    case 3: return tail_dec_t<T, 3>(blk, out, coarse_out, d_levels, d_nu, nlev, nmax, ex);
+    default: return tail_dec_t<T, 0>(blk, out, coarse_out, d_levels, d_nu, nlev, nmax, ex);
   }
 }
 
 template <typename T>
-cudaError_t tail_recompose(const T* coeffs, const T* coarse_in, T* fine_out, const void* d_levels, int nlev,
-                           int64_t nmax, int d, const Exec& ex) {
+cudaError_t tail_recompose(const T* coeffs, const T* coarse_in, T* fine_out, const void* d_levels, const void* d_nu,
+                           int nlev, int64_t nmax, int d, const Exec& ex) {
   switch (d) {
-    case 1: return tail_rec_t<T, 1>(coeffs, coarse_in, fine_out, d_levels, nlev, nmax, ex);
-    case 2: return tail_rec_t<T, 2>(coeffs, coarse_in, fine_out, d_levels, nlev, nmax, ex);
-    case 3: return tail_rec_t<T, 3>(coeffs, coarse_in, fine_out, d_levels, nlev, nmax, ex);
-    default: return tail_rec_t<T, 0>(coeffs, coarse_in, fine_out, d_levels, nlev, nmax, ex);
+    case 1: return tail_rec_t<T, 1>(coeffs, coarse_in, fine_out, d_levels, d_nu, nlev, nmax, ex);
+    case 2: return tail_rec_t<T, 2>(coeffs, coarse_in, fine_out, d_levels, d_nu, nlev, nmax, ex);
+    case 3: return tail_rec_t<T, 3>(coeffs, coarse_in, fine_out, d_levels, d_nu, nlev, nmax, ex);
+    default: return tail_rec_t<T, 0>(coeffs, coarse_in, fine_out, d_levels, d_nu, nlev, nmax, ex);
   }
 }
 
@@ -683,12 +716,13 @@ MGRX_INST(float)
 MGRX_INST(double)
 #undef MGRX_INST
 
-template cudaError_t tail_decompose<float>(const float*, float*, float*, const void*, int, int64_t, int, const Exec&);
-template cudaError_t tail_decompose<double>(const double*, double*, double*, const void*, int, int64_t, int,
-                                            const Exec&);
-template cudaError_t tail_recompose<float>(const float*, const float*, float*, const void*, int, int64_t, int,
+template cudaError_t tail_decompose<float>(const float*, float*, float*, const void*, const void*, int, int64_t, int,
                                            const Exec&);
-template cudaError_t tail_recompose<double>(const double*, const double*, double*, const void*, int, int64_t, int,
-                                            const Exec&);
+template cudaError_t tail_decompose<double>(const double*, double*, double*, const void*, const void*, int, int64_t,
+                                            int, const Exec&);
+template cudaError_t tail_recompose<float>(const float*, const float*, float*, const void*, const void*, int, int64_t,
+                                           int, const Exec&);
+template cudaError_t tail_recompose<double>(const double*, const double*, double*, const void*, const void*, int,
+                                            int64_t, int, const Exec&);
 
 }  // namespace mgrx_b200

@@ -26,11 +26,11 @@ size_t tail_smem_bytes(int64_t nmax, int esize);
 size_t tail_level_bytes();
 void tail_fill_level(void* dst, const LevelGeom& g, const ThomasLevel& th, int64_t shell_off);
 template <typename T>
-cudaError_t tail_decompose(const T* blk, T* out, T* coarse_out, const void* d_levels, int nlev, int64_t nmax, int d,
-                           const Exec& ex);
-template <typename T>
-cudaError_t tail_recompose(const T* coeffs, const T* coarse_in, T* fine_out, const void* d_levels, int nlev,
+cudaError_t tail_decompose(const T* blk, T* out, T* coarse_out, const void* d_levels, const void* d_nu, int nlev,
                            int64_t nmax, int d, const Exec& ex);
+template <typename T>
+cudaError_t tail_recompose(const T* coeffs, const T* coarse_in, T* fine_out, const void* d_levels, const void* d_nu,
+                           int nlev, int64_t nmax, int d, const Exec& ex);
 
 // ---- quantization (quantize.cu) --------------------------------------------
 struct QuantLevels {
