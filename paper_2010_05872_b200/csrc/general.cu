@@ -284,6 +284,70 @@ __global__ void __launch_bounds__(1024) k_axis_solve(double* __restrict__ y, int
   }
 }
 
+// Last-axis variant (contiguous lines): one warp per line, the line staged
+// in shared memory, lanes own contiguous segments (affine carries combined
+// with a warp shuffle scan, then exact reruns).
+__global__ void __launch_bounds__(128) k_axis_solve_rows(double* __restrict__ y, int64_t nlines, int m,
+                                                         const double* __restrict__ w,
+                                                         const double* __restrict__ inv_d,
+                                                         const double* __restrict__ off) {
+  extern __shared__ double rowbuf[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double* x = rowbuf + int64_t(warp) * m;
+  const int seg = (m + 31) >> 5;
+  const int s0 = min(m, lane * seg), s1 = min(m, s0 + seg);
+  for (int64_t line = int64_t(blockIdx.x) * nw + warp; line < nlines; line += int64_t(gridDim.x) * nw) {
+    double* gl = y + line * m;
+    for (int i = lane; i < m; i += 32) x[i] = gl[i];
+    __syncwarp();
+    // forward
+    double fa = 0.0, fb = 1.0;
+    for (int i = s0; i < s1; ++i) {
+      const double wi = w[i];
+      fa = x[i] - wi * fa;
+      fb = -wi * fb;
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double pa = __shfl_up_sync(0xffffffffu, fa, o), pb = __shfl_up_sync(0xffffffffu, fb, o);
+      if (lane >= o) {
+        fa = fa + fb * pa;
+        fb = fb * pb;
+      }
+    }
+    double c = __shfl_up_sync(0xffffffffu, fa, 1);
+    if (lane == 0) c = 0.0;
+    for (int i = s0; i < s1; ++i) {
+      c = x[i] - w[i] * c;
+      x[i] = c;
+    }
+    // backward z_i = (y_i - off_i z_{i+1}) / d_i
+    double ga = 0.0, gb = 1.0;
+    for (int i = s1 - 1; i >= s0; --i) {
+      const double id = inv_d[i], oi = off ? off[i] : kOff;
+      ga = (x[i] - oi * ga) * id;
+      gb = -oi * id * gb;
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double na = __shfl_down_sync(0xffffffffu, ga, o), nb = __shfl_down_sync(0xffffffffu, gb, o);
+      if (lane + o < 32) {
+        ga = ga + gb * na;
+        gb = gb * nb;
+      }
+    }
+    double z = __shfl_down_sync(0xffffffffu, ga, 1);
+    if (lane == 31) z = 0.0;
+    for (int i = s1 - 1; i >= s0; --i) {
+      z = (x[i] - (off ? off[i] : kOff) * z) * inv_d[i];
+      x[i] = z;
+    }
+    __syncwarp();
+    for (int i = lane; i < m; i += 32) gl[i] = x[i];
+    __syncwarp();
+  }
+}
+
 // apply_correction (transform.hpp:435-477): corner <- T(double(corner) + s*z).
 template <typename T>
 __global__ void __launch_bounds__(256) k_apply(T* __restrict__ coarse, const double* __restrict__ z, int64_t nc,
@@ -673,7 +737,14 @@ static void run_sweeps(double* comp, double* tmp, const LevelGeom& g, const Thom
       const double* w = nu ? nu->ax[a].tw : th->w[a];
       const double* id = nu ? nu->ax[a].tid : th->inv_d[a];
       const double* of = nu ? nu->ax[a].off : nullptr;
-      MGRX_LAUNCH(ex, "gen_solve", k_axis_solve<<<unsigned((lines + 15) / 16), dim3(32, SY), 0, ex.s>>>(y, lines, g.m[a], inner, w, id, of));
+      const size_t row_smem = size_t(4) * size_t(g.m[a]) * 8;
+      if (inner == 1 && row_smem <= size_t(200) * 1024) {
+        cudaFuncSetAttribute(k_axis_solve_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, int(row_smem));
+        const int64_t blocks = std::min<int64_t>((lines + 3) / 4, int64_t(kNumSMs) * 8);
+        MGRX_LAUNCH(ex, "gen_solve", k_axis_solve_rows<<<unsigned(blocks), 128, row_smem, ex.s>>>(y, lines, int(g.m[a]), w, id, of));
+      } else {
+        MGRX_LAUNCH(ex, "gen_solve", k_axis_solve<<<unsigned((lines + 15) / 16), dim3(32, SY), 0, ex.s>>>(y, lines, g.m[a], inner, w, id, of));
+      }
     } else if (nu)
       MGRX_LAUNCH(ex, "gen_sweep", k_sweep<true><<<grid, 128, 0, ex.s>>>(x, y, outer, inner, g.n[a], g.m[a], nullptr, nullptr, nu->ax[a]));
     else
