@@ -230,6 +230,280 @@ __global__ void __launch_bounds__(256) k_axis_load(const double* __restrict__ x,
   }
 }
 
+// Coefficients (or, on recompose, the component read back from the shell)
+// fused with the axis-0 load vector (path "auto", rank >= 2): each thread
+// owns one position t of the trailing axes and a chunk of coarse rows
+// [i0, i1) along axis 0, streams the fine rows 2 i0 - 2 .. 2 i1 through
+// three rolling accumulators and writes the finished load entries f0[i][t]
+// — the fp64 component is never materialised.  Per entry the products are
+// added in load_entry's order (k = -2 .. 2, transform.hpp:84-96) starting
+// from 0.0, exactly as k_axis_load does, so f0 is bit-identical to
+// k_axis_load over k_dec_coef's component; coefficients are bit-identical
+// to k_dec_coef.  Halo rows are recomputed by the neighbouring chunk, only
+// the owned rows [2 i0, 2 i1) are written to the shell / coarse block.
+template <typename T, bool kRec, bool kNu, int D>
+__global__ void __launch_bounds__(256) k_coef_load0(const T* __restrict__ blk, T* __restrict__ shell,
+                                                    T* __restrict__ coarse, double* __restrict__ f0,
+                                                    const LevelGeom g, const NuLevel nu, int64_t inner, int chunk) {
+  const int64_t n0 = g.n[0], m0 = g.m[0];
+  const int64_t nch = (m0 + chunk - 1) / chunk;
+  const int64_t total = nch * inner;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const double* s5 = kNu ? nu.ax[0].s : nullptr;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total; q += stride) {
+    const int64_t ch = q / inner, t = q - ch * inner;
+    const int64_t i0 = ch * chunk, i1 = min(m0, i0 + chunk);
+    int64_t j[kMaxD];
+    bool even_tail = true;
+    int64_t ct = 0;
+    {
+      int64_t r = t;
+#pragma unroll
+      for (int i = MGRX_ND(g) - 1; i >= 1; --i) {
+        j[i] = r % g.n[i];
+        r /= g.n[i];
+        even_tail &= !(j[i] & 1);
+        ct += (j[i] >> 1) * g.cst[i];
+      }
+    }
+    const int64_t p_lo = i0 > 0 ? 2 * i0 - 2 : 0;
+    const int64_t p_hi = min(n0 - 1, 2 * i1);
+    double a_prev = 0.0, a_cur = 0.0, a_next = 0.0;  // rows k-1, k, k+1 for k = p >> 1
+    for (int64_t p = p_lo; p <= p_hi; ++p) {
+      const bool owned = p >= 2 * i0 && p < 2 * i1;
+      j[0] = p;
+      double c;
+      if (!(p & 1) && even_tail) {  // nodal: component 0
+        if (!kRec && owned) coarse[(p >> 1) * g.cst[0] + ct] = blk[p * inner + t];
+        c = 0.0;
+      } else if (kRec) {
+        c = double(blk[shell_pos<D>(g, j)]);
+      } else {
+        const double pred = predict<T, kNu, D>(blk, false, g, nu, j);
+        const T v = to_t<T>(sub_(double(blk[p * inner + t]), pred));
+        if (owned) shell[shell_pos<D>(g, j)] = v;
+        c = double(v);
+      }
+      const int64_t k = p >> 1;
+      if (!(p & 1)) {
+        if (k >= 1) {  // last term (offset +2) of row k-1
+          a_prev = add_(a_prev, mul_(kNu ? s5[5 * (k - 1) + 4] : kW12, c));
+          if (k - 1 >= i0 && k - 1 < i1) f0[(k - 1) * inner + t] = a_prev;
+        }
+        a_cur = add_(a_cur, mul_(kNu ? s5[5 * k + 2] : ((k == 0 || k + 1 == m0) ? kW5_12 : kW5_6), c));
+        a_next = (k + 1 < m0) ? add_(0.0, mul_(kNu ? s5[5 * (k + 1)] : kW12, c)) : 0.0;
+      } else {
+        a_cur = add_(a_cur, mul_(kNu ? s5[5 * k + 3] : 0.5, c));
+        if (k + 1 < m0) a_next = add_(a_next, mul_(kNu ? s5[5 * (k + 1) + 1] : 0.5, c));
+        // advance: the next even row 2k+2 makes k+1 the current row
+        if (p < p_hi) {
+          a_prev = a_cur;
+          a_cur = a_next;
+          a_next = 0.0;
+        }
+      }
+      if (p == n0 - 1 && k >= i0 && k < i1) f0[k * inner + t] = a_cur;  // the last row: row k is complete
+    }
+  }
+}
+
+// ---- 2-D specialisations (path "auto"): the same arithmetic as predict<T,
+// kNu, 2> / shell_pos<2> written out per parity case (the generic corner
+// loop costs ~250 instructions per node), bit-identical.  Corner order =
+// cmask order (axis 0 is bit 0 when odd); shell positions: an even row
+// holds only its odd-column tail, (r, k) -> r (n1 - m1) + k; odd row r of
+// the reordered block starts at (m0 + r) n1 - m0 m1.
+
+// Rolling axis-0 load accumulators of one column (see k_coef_load0): rows
+// k-1, k, k+1 around fine row p, k = p >> 1; finished rows go to f0.
+struct Roll0 {
+  double prev = 0.0, cur = 0.0, next = 0.0;
+};
+
+template <bool kNu>
+__device__ __forceinline__ void roll0(Roll0& A, double c, int64_t p, int64_t p_hi, int64_t n0, int64_t m0, int64_t i0,
+                                      int64_t i1, const double* __restrict__ s5, double* __restrict__ f0col,
+                                      int64_t ld) {
+  const int64_t k = p >> 1;
+  if (!(p & 1)) {
+    if (k >= 1) {
+      A.prev = add_(A.prev, mul_(kNu ? s5[5 * (k - 1) + 4] : kW12, c));
+      if (k - 1 >= i0 && k - 1 < i1) f0col[(k - 1) * ld] = A.prev;
+    }
+    A.cur = add_(A.cur, mul_(kNu ? s5[5 * k + 2] : ((k == 0 || k + 1 == m0) ? kW5_12 : kW5_6), c));
+    A.next = (k + 1 < m0) ? add_(0.0, mul_(kNu ? s5[5 * (k + 1)] : kW12, c)) : 0.0;
+  } else {
+    A.cur = add_(A.cur, mul_(kNu ? s5[5 * k + 3] : 0.5, c));
+    if (k + 1 < m0) A.next = add_(A.next, mul_(kNu ? s5[5 * (k + 1) + 1] : 0.5, c));
+    if (p < p_hi) {
+      A.prev = A.cur;
+      A.cur = A.next;
+      A.next = 0.0;
+    }
+  }
+  if (p == n0 - 1 && k >= i0 && k < i1) f0col[k * ld] = A.cur;
+}
+
+// k_coef_load0 for rank 2.  Each thread owns a column pair (2k, 2k+1) so
+// every branch is uniform across a warp (a per-column mapping alternates
+// the parity case lane by lane) and the corner loads are shared between the
+// pair.  Arithmetic is predict<T, kNu, 2>'s written out per case.
+template <typename T, bool kRec, bool kNu>
+__global__ void __launch_bounds__(256) k2_coef_load0(const T* __restrict__ blk, T* __restrict__ shell,
+                                                     T* __restrict__ coarse, double* __restrict__ f0,
+                                                     const LevelGeom g, const NuLevel nu, int chunk) {
+  const int64_t n0 = g.n[0], m0 = g.m[0], n1 = g.n[1], m1 = g.m[1];
+  const int64_t total = ((m0 + chunk - 1) / chunk) * m1;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const double* s5 = kNu ? nu.ax[0].s : nullptr;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total; q += stride) {
+    const int64_t ch = q / m1, k = q - ch * m1;
+    const int64_t i0 = ch * chunk, i1 = min(m0, i0 + chunk);
+    const int64_t t0 = 2 * k, t1 = t0 + 1;
+    const bool has1 = t1 < n1;
+    const int64_t t1r = (t1 + 1 < n1) ? t1 + 1 : t0;  // right corner column of t1
+    double a1l = 0.0, a1r = 0.0;
+    if (kNu && has1) a1l = nu.ax[1].wl[t1], a1r = nu.ax[1].wr[t1];
+    const int64_t p_lo = i0 > 0 ? 2 * i0 - 2 : 0;
+    const int64_t p_hi = min(n0 - 1, 2 * i1);
+    Roll0 A0, A1;
+    for (int64_t p = p_lo; p <= p_hi; ++p) {
+      const bool owned = p >= 2 * i0 && p < 2 * i1;
+      const int64_t r = p >> 1;
+      double c0, c1 = 0.0;
+      if (!(p & 1)) {
+        const int64_t sp = r * (n1 - m1) + k;  // (even row, odd column)
+        if (kRec) {
+          c0 = 0.0;
+          if (has1) c1 = double(blk[sp]);
+        } else {
+          const T x0 = blk[p * n1 + t0];
+          if (owned) coarse[r * m1 + k] = x0;
+          c0 = 0.0;
+          if (has1) {
+            const double v0 = double(x0), v1 = double(blk[p * n1 + t1r]);
+            const double pred = kNu ? add_(add_(0.0, mul_(a1l, v0)), mul_(a1r, v1))
+                                    : mul_(add_(add_(0.0, v0), v1), 0.5);
+            const T v = to_t<T>(sub_(double(blk[p * n1 + t1]), pred));
+            if (owned) shell[sp] = v;
+            c1 = double(v);
+          }
+        }
+      } else {
+        const int64_t sp = (m0 + r) * n1 - m0 * m1 + k;  // (odd row, even column); odd column at + m1
+        if (kRec) {
+          c0 = double(blk[sp]);
+          if (has1) c1 = double(blk[sp + m1]);
+        } else {
+          const int64_t pl = p - 1, pr = (p + 1 < n0) ? p + 1 : p - 1;
+          double a0l = 0.0, a0r = 0.0;
+          if (kNu) a0l = nu.ax[0].wl[p], a0r = nu.ax[0].wr[p];
+          const double u00 = double(blk[pl * n1 + t0]), u10 = double(blk[pr * n1 + t0]);
+          const double pred0 = kNu ? add_(add_(0.0, mul_(a0l, u00)), mul_(a0r, u10))
+                                   : mul_(add_(add_(0.0, u00), u10), 0.5);
+          const T v0 = to_t<T>(sub_(double(blk[p * n1 + t0]), pred0));
+          if (owned) shell[sp] = v0;
+          c0 = double(v0);
+          if (has1) {
+            const double u01 = double(blk[pl * n1 + t1r]), u11 = double(blk[pr * n1 + t1r]);
+            double pred1;
+            if (kNu) {
+              pred1 = add_(0.0, mul_(mul_(a0l, a1l), u00));
+              pred1 = add_(pred1, mul_(mul_(a0r, a1l), u10));
+              pred1 = add_(pred1, mul_(mul_(a0l, a1r), u01));
+              pred1 = add_(pred1, mul_(mul_(a0r, a1r), u11));
+            } else {
+              pred1 = mul_(add_(add_(add_(add_(0.0, u00), u10), u01), u11), 0.25);
+            }
+            const T v1 = to_t<T>(sub_(double(blk[p * n1 + t1]), pred1));
+            if (owned) shell[sp + m1] = v1;
+            c1 = double(v1);
+          }
+        }
+      }
+      roll0<kNu>(A0, c0, p, p_hi, n0, m0, i0, i1, s5, f0 + t0, n1);
+      if (has1) roll0<kNu>(A1, c1, p, p_hi, n0, m0, i0, i1, s5, f0 + t1, n1);
+    }
+  }
+}
+
+// k_rec_interp for rank 2 (32-bit node counts), one column pair (2k, 2k+1)
+// of one fine row per thread.
+template <typename T, bool kNu>
+__global__ void __launch_bounds__(256) k2_rec_interp(const T* __restrict__ shell, const T* __restrict__ coarse,
+                                                     T* __restrict__ fine, const LevelGeom g, const NuLevel nu) {
+  const uint32_t n0 = uint32_t(g.n[0]), m0 = uint32_t(g.m[0]), n1 = uint32_t(g.n[1]), m1 = uint32_t(g.m[1]);
+  const uint32_t total = n0 * m1;
+  const FastDiv dm1 = g.fn[0];  // set up by the caller as a divider by m1
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
+    const uint32_t p = dm1.div(q), k = q - p * m1, r = p >> 1;
+    const uint32_t t0 = 2 * k, t1 = t0 + 1;
+    const bool has1 = t1 < n1;
+    const uint32_t kr = (t1 + 1 < n1) ? k + 1 : k;
+    T* fr = fine + p * n1;
+    if (!(p & 1)) {
+      const T x0 = coarse[r * m1 + k];
+      fr[t0] = x0;
+      if (has1) {
+        const double v0 = double(x0), v1 = double(coarse[r * m1 + kr]);
+        const double pred = kNu ? add_(add_(0.0, mul_(nu.ax[1].wl[t1], v0)), mul_(nu.ax[1].wr[t1], v1))
+                                : mul_(add_(add_(0.0, v0), v1), 0.5);
+        fr[t1] = to_t<T>(add_(double(shell[r * (n1 - m1) + k]), pred));
+      }
+    } else {
+      const uint32_t rr = (p + 1 < n0) ? r + 1 : r;
+      const uint32_t sp = (m0 + r) * n1 - m0 * m1 + k;
+      double a0l = 0.0, a0r = 0.0;
+      if (kNu) a0l = nu.ax[0].wl[p], a0r = nu.ax[0].wr[p];
+      const double u00 = double(coarse[r * m1 + k]), u10 = double(coarse[rr * m1 + k]);
+      const double pred0 = kNu ? add_(add_(0.0, mul_(a0l, u00)), mul_(a0r, u10)) : mul_(add_(add_(0.0, u00), u10), 0.5);
+      fr[t0] = to_t<T>(add_(double(shell[sp]), pred0));
+      if (has1) {
+        const double u01 = double(coarse[r * m1 + kr]), u11 = double(coarse[rr * m1 + kr]);
+        double pred1;
+        if (kNu) {
+          const double a1l = nu.ax[1].wl[t1], a1r = nu.ax[1].wr[t1];
+          pred1 = add_(0.0, mul_(mul_(a0l, a1l), u00));
+          pred1 = add_(pred1, mul_(mul_(a0r, a1l), u10));
+          pred1 = add_(pred1, mul_(mul_(a0l, a1r), u01));
+          pred1 = add_(pred1, mul_(mul_(a0r, a1r), u11));
+        } else {
+          pred1 = mul_(add_(add_(add_(add_(0.0, u00), u10), u01), u11), 0.25);
+        }
+        fr[t1] = to_t<T>(add_(double(shell[sp + m1]), pred1));
+      }
+    }
+  }
+}
+
+// Serial Thomas along axis-0-style lines over a precomputed load vector, in
+// place: the same operations as k_sweep after its load (bit-identical).
+template <bool kNu>
+__global__ void __launch_bounds__(128) k_axis_thomas(double* __restrict__ y, int64_t lines, int64_t inner, int64_t m,
+                                                     const double* __restrict__ w, const double* __restrict__ inv_d,
+                                                     const NuAxis nu) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t t0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t0 < lines; t0 += stride) {
+    const int64_t o = t0 / inner, t = t0 - o * inner;
+    double* f = y + o * m * inner + t;
+    double prev = 0.0;
+    for (int64_t i = 0; i < m; ++i) {
+      double acc = f[i * inner];
+      if (i > 0) acc = sub_(acc, mul_(kNu ? nu.tw[i] : w[i], prev));
+      f[i * inner] = acc;
+      prev = acc;
+    }
+    double nxt = mul_(prev, kNu ? nu.tid[m - 1] : inv_d[m - 1]);
+    f[(m - 1) * inner] = nxt;
+    for (int64_t i = m - 2; i >= 0; --i) {
+      const double v = kNu ? mul_(sub_(f[i * inner], mul_(nu.off[i], nxt)), nu.tid[i])
+                           : mul_(sub_(f[i * inner], mul_(kOff, nxt)), inv_d[i]);
+      f[i * inner] = v;
+      nxt = v;
+    }
+  }
+}
+
 // Thomas (batched_solve, transform.hpp:116-130; nonuniform: super-diagonal
 // table `off`) along lines of m values at stride `inner`, in place.  16
 // lines per block, S = 2 blockDim.y segments per line; values stream from
@@ -284,16 +558,114 @@ __global__ void __launch_bounds__(1024) k_axis_solve(double* __restrict__ y, int
   }
 }
 
+// Tiled variant for strided lines (path "auto"): LB consecutive lines per
+// CTA staged whole in shared memory with the factor tables, so the four
+// segment passes of k_axis_solve touch HBM once (one read, one write).
+template <int LB>
+__global__ void __launch_bounds__(256) k_axis_solve_tile(double* __restrict__ y, int64_t nlines, int m, int64_t inner,
+                                                         const double* __restrict__ gw,
+                                                         const double* __restrict__ gid,
+                                                         const double* __restrict__ goff) {
+  extern __shared__ double ts[];
+  __shared__ double A[32][LB], B[32][LB];
+  double* w = ts;
+  double* inv_d = w + m;
+  double* off = goff ? inv_d + m : nullptr;
+  double* t = inv_d + (goff ? 2 : 1) * m;  // [m][LB]
+  const int c = threadIdx.x % LB, s = threadIdx.x / LB, S = blockDim.x / LB;
+  const int64_t line = int64_t(blockIdx.x) * LB + c;
+  const bool valid = line < nlines;
+  double* p = y + (valid ? (line / inner) * m * inner + line % inner : 0);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    w[i] = gw[i];
+    inv_d[i] = gid[i];
+    if (goff) off[i] = goff[i];
+  }
+  // asynchronous 8-byte copies: the whole tile in flight at once (a plain
+  // load loop keeps only a few rows per warp outstanding at 1 CTA per SM)
+  for (int i = s; i < m; i += S) {
+    if (valid) {
+      const uint32_t dst = uint32_t(__cvta_generic_to_shared(t + i * LB + c));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(p + i * inner) : "memory");
+    } else {
+      t[i * LB + c] = 0.0;
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  const int seg = (m + S - 1) / S;
+  const int s0 = min(m, s * seg), s1 = min(m, s0 + seg);
+  double ya = 0.0, yb = 1.0;
+  for (int i = s0; i < s1; ++i) {
+    const double wi = w[i];
+    ya = t[i * LB + c] - wi * ya;
+    yb = -wi * yb;
+  }
+  A[s][c] = ya;
+  B[s][c] = yb;
+  __syncthreads();
+  double cy = 0.0;
+  for (int q = 0; q < s; ++q) cy = A[q][c] + B[q][c] * cy;
+  __syncthreads();
+  for (int i = s0; i < s1; ++i) {
+    cy = t[i * LB + c] - w[i] * cy;
+    t[i * LB + c] = cy;
+  }
+  double za = 0.0, zb = 1.0;
+  for (int i = s1 - 1; i >= s0; --i) {
+    const double id = inv_d[i], oi = off ? off[i] : kOff;
+    za = (t[i * LB + c] - oi * za) * id;
+    zb = -oi * id * zb;
+  }
+  A[s][c] = za;
+  B[s][c] = zb;
+  __syncthreads();
+  double z = 0.0;
+  for (int q = S - 1; q > s; --q) z = A[q][c] + B[q][c] * z;
+  for (int i = s1 - 1; i >= s0; --i) {
+    z = (t[i * LB + c] - (off ? off[i] : kOff) * z) * inv_d[i];
+    t[i * LB + c] = z;
+  }
+  __syncthreads();
+  if (valid)
+    for (int i = s; i < m; i += S) p[i * inner] = t[i * LB + c];
+}
+
+// Strided-line solve dispatch: tiled when LB lines fit in shared memory.
+static void launch_axis_solve(double* y, int64_t lines, int64_t m, int64_t inner, const double* w, const double* id,
+                              const double* of, const Exec& ex) {
+  constexpr int LB = 8;
+  const size_t sm = size_t(LB + (of ? 3 : 2)) * size_t(m) * 8;
+  if (sm <= size_t(200) * 1024) {
+    cudaFuncSetAttribute(k_axis_solve_tile<LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    MGRX_LAUNCH(ex, "gen_solve", k_axis_solve_tile<LB><<<unsigned((lines + LB - 1) / LB), 256, sm, ex.s>>>(y, lines, int(m), inner, w, id, of));
+  } else {
+    const int SY = int(std::max<int64_t>(1, std::min<int64_t>(32, (m + 31) / 32)));
+    MGRX_LAUNCH(ex, "gen_solve", k_axis_solve<<<unsigned((lines + 15) / 16), dim3(32, SY), 0, ex.s>>>(y, lines, m, inner, w, id, of));
+  }
+}
+
 // Last-axis variant (contiguous lines): one warp per line, the line staged
 // in shared memory, lanes own contiguous segments (affine carries combined
 // with a warp shuffle scan, then exact reruns).
-__global__ void __launch_bounds__(128) k_axis_solve_rows(double* __restrict__ y, int64_t nlines, int m,
-                                                         const double* __restrict__ w,
-                                                         const double* __restrict__ inv_d,
-                                                         const double* __restrict__ off) {
+__global__ void __launch_bounds__(256) k_axis_solve_rows(double* __restrict__ y, int64_t nlines, int m,
+                                                         const double* __restrict__ gw,
+                                                         const double* __restrict__ gid,
+                                                         const double* __restrict__ goff) {
+  // the factor tables are staged too: lanes read them at a stride of one
+  // segment, which would split every global load into 32 transactions
   extern __shared__ double rowbuf[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  double* x = rowbuf + int64_t(warp) * m;
+  double* w = rowbuf;
+  double* inv_d = w + m;
+  double* off = goff ? inv_d + m : nullptr;
+  double* x = inv_d + (goff ? 2 : 1) * m + int64_t(warp) * m;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    w[i] = gw[i];
+    inv_d[i] = gid[i];
+    if (goff) off[i] = goff[i];
+  }
+  __syncthreads();
   const int seg = (m + 31) >> 5;
   const int s0 = min(m, lane * seg), s1 = min(m, s0 + seg);
   for (int64_t line = int64_t(blockIdx.x) * nw + warp; line < nlines; line += int64_t(gridDim.x) * nw) {
@@ -713,13 +1085,14 @@ static void launch_rec_interp(const T* shell, const T* coarse, T* fine, const Le
 
 // compute_correction sweeps on `comp` (natural fine extents); the result
 // (coarse extents, row-major) ends in *result, which points into comp or tmp.
+// a0 = 1: axis 0 is already done (comp holds its solved m0 x ... result).
 static void run_sweeps(double* comp, double* tmp, const LevelGeom& g, const ThomasLevel* th, const NuLevel* nu,
-                       double** result, const Exec& ex, bool fast) {
+                       double** result, const Exec& ex, bool fast, int a0 = 0) {
   int64_t cur[kMaxD];
-  for (int i = 0; i < g.d; ++i) cur[i] = g.n[i];
+  for (int i = 0; i < g.d; ++i) cur[i] = i < a0 ? g.m[i] : g.n[i];
   double* x = comp;
   double* y = tmp;
-  for (int a = 0; a < g.d; ++a) {
+  for (int a = a0; a < g.d; ++a) {
     int64_t outer = 1, inner = 1;
     for (int i = 0; i < a; ++i) outer *= cur[i];
     for (int i = a + 1; i < g.d; ++i) inner *= cur[i];
@@ -737,13 +1110,16 @@ static void run_sweeps(double* comp, double* tmp, const LevelGeom& g, const Thom
       const double* w = nu ? nu->ax[a].tw : th->w[a];
       const double* id = nu ? nu->ax[a].tid : th->inv_d[a];
       const double* of = nu ? nu->ax[a].off : nullptr;
-      const size_t row_smem = size_t(4) * size_t(g.m[a]) * 8;
+      (void)SY;
+      int nw = 8;
+      while (nw > 1 && size_t(nw + (of ? 3 : 2)) * size_t(g.m[a]) * 8 > size_t(200) * 1024) nw >>= 1;
+      const size_t row_smem = size_t(nw + (of ? 3 : 2)) * size_t(g.m[a]) * 8;
       if (inner == 1 && row_smem <= size_t(200) * 1024) {
         cudaFuncSetAttribute(k_axis_solve_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, int(row_smem));
-        const int64_t blocks = std::min<int64_t>((lines + 3) / 4, int64_t(kNumSMs) * 8);
-        MGRX_LAUNCH(ex, "gen_solve", k_axis_solve_rows<<<unsigned(blocks), 128, row_smem, ex.s>>>(y, lines, int(g.m[a]), w, id, of));
+        const int64_t blocks = std::min<int64_t>((lines + nw - 1) / nw, int64_t(kNumSMs) * 8);
+        MGRX_LAUNCH(ex, "gen_solve", k_axis_solve_rows<<<unsigned(blocks), 32 * nw, row_smem, ex.s>>>(y, lines, int(g.m[a]), w, id, of));
       } else {
-        MGRX_LAUNCH(ex, "gen_solve", k_axis_solve<<<unsigned((lines + 15) / 16), dim3(32, SY), 0, ex.s>>>(y, lines, g.m[a], inner, w, id, of));
+        launch_axis_solve(y, lines, g.m[a], inner, w, id, of, ex);
       }
     } else if (nu)
       MGRX_LAUNCH(ex, "gen_sweep", k_sweep<true><<<grid, 128, 0, ex.s>>>(x, y, outer, inner, g.n[a], g.m[a], nullptr, nullptr, nu->ax[a]));
@@ -757,12 +1133,59 @@ static void run_sweeps(double* comp, double* tmp, const LevelGeom& g, const Thom
   *result = x;
 }
 
+// Path "auto", rank >= 2: coefficients (kRec: the component) fused with the
+// axis-0 load into comp (m0 x inner), then the axis-0 solve in place.
+template <typename T, bool kRec>
+static void coef_load0_axis0(const T* src, T* shell, T* coarse, double* comp, const LevelGeom& g,
+                             const ThomasLevel* th, const NuLevel* nu, const Exec& ex) {
+  const int64_t inner = g.N / g.n[0], m0 = g.m[0];
+  const int chunk = int(std::max<int64_t>(1, std::min<int64_t>(64, m0 * inner / (int64_t(600) << 10))));
+  const int64_t work = ((m0 + chunk - 1) / chunk) * (g.d == 2 ? g.m[1] : inner);
+  const int grid = grid_for(work, 256);
+  const NuLevel z = nu ? *nu : NuLevel{};
+#define L_(NU, D)                                                                                         \
+  MGRX_LAUNCH(ex, kRec ? "gen_comp_load0" : "gen_coef_load0",                                             \
+              (k_coef_load0<T, kRec, NU, D><<<grid, 256, 0, ex.s>>>(src, shell, coarse, comp, g, z, inner, chunk)))
+#define R_(NU)                                                                                             \
+  if (g.d == 2)                                                                                            \
+    MGRX_LAUNCH(ex, kRec ? "gen_comp_load0" : "gen_coef_load0",                                            \
+                (k2_coef_load0<T, kRec, NU><<<grid, 256, 0, ex.s>>>(src, shell, coarse, comp, g, z, chunk))); \
+  else if (g.d == 3)    \
+    L_(NU, 3);          \
+  else if (g.d == 4)    \
+    L_(NU, 4);          \
+  else                  \
+    L_(NU, 0);
+  if (nu) {
+    R_(true)
+  } else {
+    R_(false)
+  }
+#undef R_
+#undef L_
+  const double* w = nu ? nu->ax[0].tw : th->w[0];
+  const double* id = nu ? nu->ax[0].tid : th->inv_d[0];
+  const double* of = nu ? nu->ax[0].off : nullptr;
+  if (inner < (int64_t(1) << 17)) {
+    launch_axis_solve(comp, inner, m0, inner, w, id, of, ex);
+  } else if (nu) {
+    MGRX_LAUNCH(ex, "gen_thomas", k_axis_thomas<true><<<grid_for(inner, 128, 32), 128, 0, ex.s>>>(comp, inner, inner, m0, nullptr, nullptr, nu->ax[0]));
+  } else {
+    MGRX_LAUNCH(ex, "gen_thomas", k_axis_thomas<false><<<grid_for(inner, 128, 32), 128, 0, ex.s>>>(comp, inner, inner, m0, w, id, NuAxis{}));
+  }
+}
+
 template <typename T>
 cudaError_t general_decompose_level(const T* blk, T* shell, T* coarse, double* comp, double* tmp, const LevelGeom& g,
                                     const ThomasLevel* th, const NuLevel* nu, const Exec& ex, bool fast) {
-  launch_dec_coef<T>(blk, shell, coarse, comp, g, nu, ex);
   double* z = nullptr;
-  run_sweeps(comp, tmp, g, th, nu, &z, ex, fast);
+  if (fast && g.d >= 2) {
+    coef_load0_axis0<T, false>(blk, shell, coarse, comp, g, th, nu, ex);
+    run_sweeps(comp, tmp, g, th, nu, &z, ex, fast, 1);
+  } else {
+    launch_dec_coef<T>(blk, shell, coarse, comp, g, nu, ex);
+    run_sweeps(comp, tmp, g, th, nu, &z, ex, fast);
+  }
   MGRX_LAUNCH(ex, "gen_apply", k_apply<T><<<grid_for(g.Nc, 256), 256, 0, ex.s>>>(coarse, z, g.Nc, 1.0));
   return cudaGetLastError();
 }
@@ -770,10 +1193,25 @@ cudaError_t general_decompose_level(const T* blk, T* shell, T* coarse, double* c
 template <typename T>
 cudaError_t general_recompose_level(const T* shell, T* coarse, T* fine, double* comp, double* tmp, const LevelGeom& g,
                                     const ThomasLevel* th, const NuLevel* nu, const Exec& ex, bool fast) {
-  launch_rec_comp<T>(shell, comp, g, ex);
   double* z = nullptr;
-  run_sweeps(comp, tmp, g, th, nu, &z, ex, fast);
+  if (fast && g.d >= 2) {
+    coef_load0_axis0<T, true>(shell, nullptr, nullptr, comp, g, th, nu, ex);
+    run_sweeps(comp, tmp, g, th, nu, &z, ex, fast, 1);
+  } else {
+    launch_rec_comp<T>(shell, comp, g, ex);
+    run_sweeps(comp, tmp, g, th, nu, &z, ex, fast);
+  }
   MGRX_LAUNCH(ex, "gen_apply", k_apply<T><<<grid_for(g.Nc, 256), 256, 0, ex.s>>>(coarse, z, g.Nc, -1.0));
+  if (fast && g.d == 2 && g.N < (int64_t(1) << 32)) {
+    LevelGeom g2 = g;
+    g2.fn[0] = FastDiv(uint32_t(g.m[1]));
+    const int grid = grid_for(g.n[0] * g.m[1], 256);
+    if (nu)
+      MGRX_LAUNCH(ex, "gen_rec_interp", k2_rec_interp<T, true><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, g2, *nu));
+    else
+      MGRX_LAUNCH(ex, "gen_rec_interp", k2_rec_interp<T, false><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, g2, NuLevel{}));
+    return cudaGetLastError();
+  }
   launch_rec_interp<T>(shell, coarse, fine, g, nu, ex);
   return cudaGetLastError();
 }
