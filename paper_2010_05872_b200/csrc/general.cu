@@ -476,6 +476,205 @@ __global__ void __launch_bounds__(256) k2_rec_interp(const T* __restrict__ shell
   }
 }
 
+// ---- rank 3-4 column-pair kernels (path "auto"): the last axis is walked
+// in pairs (2k, 2k+1), the leading axes' corner set is built once per pair
+// and shared: predict<T, kNu, D> enumerates corners in cmask order with the
+// last axis as the highest bit, so the odd column's corner sum is the even
+// column's sum continued over the right-hand corners (uniform case) —
+// bit-identical with far fewer instructions than the per-node corner loop.
+// The corner loop runs over all 2^(D-1) masks of the leading axes with the
+// masks touching an even axis predicated off: a mask's odd-axis bits in
+// ascending order are exactly predict's cmask, so the order is unchanged,
+// and control flow stays uniform across lanes of different parity classes
+// (a warp usually straddles two rows).  32-bit offsets (N < 2^32).
+// pred0 at column cl (meaningful unless the even node is nodal), pred1 at
+// the odd column between cl and cr (has1); w3l/w3r: nonuniform last-axis
+// weights of the odd column.  Returns the all-left corner offset.
+template <typename T, bool kNu, int D>
+__device__ __forceinline__ uint32_t pair_predict(const T* __restrict__ src, const LevelGeom& g, const NuLevel& nu,
+                                                 const int64_t* j, bool coarse, uint32_t cl, uint32_t cr, bool has1,
+                                                 double w3l, double w3r, double& pred0, double& pred1) {
+  constexpr int A = D - 1;
+  uint32_t base = 0, dl[A], evenmask = 0;
+  bool odd[A];
+  double wl[A], wr[A];
+  int nodd = 0;
+#pragma unroll
+  for (int i = 0; i < A; ++i) {
+    odd[i] = j[i] & 1;
+    const uint32_t ji = uint32_t(j[i]);
+    base += coarse ? (ji >> 1) * uint32_t(g.cst[i]) : (odd[i] ? ji - 1 : ji) * uint32_t(g.st[i]);
+    dl[i] = (odd[i] && j[i] + 1 < g.n[i]) ? (coarse ? uint32_t(g.cst[i]) : 2 * uint32_t(g.st[i])) : 0;
+    wl[i] = wr[i] = 1.0;
+    if (kNu && odd[i]) {
+      wl[i] = nu.ax[i].wl[ji];
+      wr[i] = nu.ax[i].wr[ji];
+    }
+    nodd += odd[i] ? 1 : 0;
+    evenmask |= odd[i] ? 0u : (1u << i);
+  }
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+  for (uint32_t fm = 0; fm < (1u << A); ++fm) {
+    if (fm & evenmask) continue;
+    uint32_t off = base;
+    double wp = 1.0;
+#pragma unroll
+    for (int i = 0; i < A; ++i) {
+      if ((fm >> i) & 1) off += dl[i];
+      if (kNu && odd[i]) wp = mul_(wp, ((fm >> i) & 1) ? wr[i] : wl[i]);
+    }
+    const double L = double(src[off + cl]);
+    if (kNu) {
+      s0 = add_(s0, mul_(wp, L));
+      s1 = add_(s1, mul_(mul_(wp, w3l), L));
+    } else {
+      s0 = add_(s0, L);
+    }
+  }
+  // 2^-nodd, exactly
+  const double sc0 = __longlong_as_double(int64_t(1023 - nodd) << 52);
+  pred0 = kNu ? s0 : mul_(s0, sc0);
+  if (has1) {
+    if (!kNu) s1 = s0;
+#pragma unroll
+    for (uint32_t fm = 0; fm < (1u << A); ++fm) {
+      if (fm & evenmask) continue;
+      uint32_t off = base;
+      double wp = 1.0;
+#pragma unroll
+      for (int i = 0; i < A; ++i) {
+        if ((fm >> i) & 1) off += dl[i];
+        if (kNu && odd[i]) wp = mul_(wp, ((fm >> i) & 1) ? wr[i] : wl[i]);
+      }
+      const double R = double(src[off + cr]);
+      s1 = kNu ? add_(s1, mul_(mul_(wp, w3r), R)) : add_(s1, R);
+    }
+    pred1 = kNu ? s1 : mul_(s1, 0.5 * sc0);
+  }
+  return base;
+}
+
+// k_coef_load0 for rank D = 3, 4: a thread owns a column pair of one row of
+// the middle axes and a chunk of coarse rows along axis 0.
+template <typename T, bool kRec, bool kNu, int D>
+__global__ void __launch_bounds__(256) kN_coef_load0(const T* __restrict__ blk, T* __restrict__ shell,
+                                                     T* __restrict__ coarse, double* __restrict__ f0,
+                                                     const LevelGeom g, const NuLevel nu, int64_t inner, int chunk) {
+  constexpr int E = D - 1;  // last axis
+  const int64_t n0 = g.n[0], m0 = g.m[0], nl = g.n[E], ml = g.m[E];
+  const int64_t rmid = inner / nl;
+  const int64_t total = ((m0 + chunk - 1) / chunk) * rmid * ml;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const double* s5 = kNu ? nu.ax[0].s : nullptr;
+  // 32-bit index decomposition (the caller guarantees < 2^32 work items):
+  // g.fn[E] divides by ml, g.fn[0] by rmid (neither is otherwise used here)
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total; q += stride) {
+    const uint32_t q32 = uint32_t(q);
+    const uint32_t rest = g.fn[E].div(q32);
+    const int64_t k = q32 - rest * uint32_t(ml);
+    const uint32_t ch32 = g.fn[0].div(rest);
+    const int64_t row = rest - ch32 * uint32_t(rmid), ch = ch32;
+    const int64_t i0 = ch * chunk, i1 = min(m0, i0 + chunk);
+    int64_t j[kMaxD];
+    bool mid_even = true;
+    int64_t cmid = 0;  // coarse offset of the middle axes
+    {
+      uint32_t r = uint32_t(row);
+#pragma unroll
+      for (int i = D - 2; i >= 1; --i) {
+        const uint32_t rq = g.fn[i].div(r);
+        j[i] = r - rq * uint32_t(g.n[i]);
+        r = rq;
+        mid_even &= !(j[i] & 1);
+        cmid += (j[i] >> 1) * g.cst[i];
+      }
+    }
+    const int64_t t0 = 2 * k, t1 = t0 + 1;
+    const bool has1 = t1 < nl;
+    const int64_t t1r = (t1 + 1 < nl) ? t1 + 1 : t0;
+    const int64_t tp0 = row * nl + t0;  // inner positions of the pair
+    double w3l = 0.0, w3r = 0.0;
+    if (kNu && has1) w3l = nu.ax[E].wl[t1], w3r = nu.ax[E].wr[t1];
+    const int64_t p_lo = i0 > 0 ? 2 * i0 - 2 : 0;
+    const int64_t p_hi = min(n0 - 1, 2 * i1);
+    Roll0 A0, A1;
+    for (int64_t p = p_lo; p <= p_hi; ++p) {
+      const bool owned = p >= 2 * i0 && p < 2 * i1;
+      const bool nodal0 = !(p & 1) && mid_even;
+      j[0] = p;
+      j[E] = t0;
+      const int64_t sp0 = shell_pos<D>(g, j);  // odd column at sp0 + ml
+      double c0 = 0.0, c1 = 0.0;
+      if (kRec) {
+        if (!nodal0) c0 = double(blk[sp0]);
+        if (has1) c1 = double(blk[sp0 + ml]);
+      } else {
+        const T* xr = blk + p * inner + tp0;
+        if (nodal0 && owned) coarse[(p >> 1) * g.cst[0] + cmid + k] = xr[0];
+        double pred0 = 0.0, pred1 = 0.0;
+        pair_predict<T, kNu, D>(blk, g, nu, j, false, uint32_t(t0), uint32_t(t1r), has1, w3l, w3r, pred0, pred1);
+        if (!nodal0) {
+          const T v = to_t<T>(sub_(double(xr[0]), pred0));
+          if (owned) shell[sp0] = v;
+          c0 = double(v);
+        }
+        if (has1) {
+          const T v = to_t<T>(sub_(double(xr[1]), pred1));
+          if (owned) shell[sp0 + ml] = v;
+          c1 = double(v);
+        }
+      }
+      roll0<kNu>(A0, c0, p, p_hi, n0, m0, i0, i1, s5, f0 + tp0, inner);
+      if (has1) roll0<kNu>(A1, c1, p, p_hi, n0, m0, i0, i1, s5, f0 + tp0 + 1, inner);
+    }
+  }
+}
+
+// k_rec_interp for rank D = 3, 4, one column pair per thread.
+template <typename T, bool kNu, int D>
+__global__ void __launch_bounds__(256) kN_rec_interp(const T* __restrict__ shell, const T* __restrict__ coarse,
+                                                     T* __restrict__ fine, const LevelGeom g, const NuLevel nu) {
+  constexpr int E = D - 1;
+  const int64_t nl = g.n[E], ml = g.m[E];
+  const int64_t rows = g.N / nl;
+  const int64_t total = rows * ml;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  // 32-bit index decomposition (N < 2^32); g.fn[E] divides by ml
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total; q += stride) {
+    const uint32_t q32 = uint32_t(q);
+    const uint32_t row32 = g.fn[E].div(q32);
+    const int64_t k = q32 - row32 * uint32_t(ml), row = row32;
+    int64_t j[kMaxD];
+    bool lead_even = true;
+    {
+      uint32_t r = row32;
+#pragma unroll
+      for (int i = D - 2; i >= 1; --i) {
+        const uint32_t rq = g.fn[i].div(r);
+        j[i] = r - rq * uint32_t(g.n[i]);
+        r = rq;
+        lead_even &= !(j[i] & 1);
+      }
+      j[0] = r;
+      lead_even &= !(r & 1);
+    }
+    const int64_t t0 = 2 * k, t1 = t0 + 1;
+    const bool has1 = t1 < nl;
+    const int64_t kr = (t1 + 1 < nl) ? k + 1 : k;
+    j[E] = t0;
+    const int64_t sp0 = shell_pos<D>(g, j);
+    double w3l = 0.0, w3r = 0.0;
+    if (kNu && has1) w3l = nu.ax[E].wl[t1], w3r = nu.ax[E].wr[t1];
+    double pred0 = 0.0, pred1 = 0.0;
+    const uint32_t cb =
+        pair_predict<T, kNu, D>(coarse, g, nu, j, true, uint32_t(k), uint32_t(kr), has1, w3l, w3r, pred0, pred1);
+    T* fr = fine + row * nl + t0;
+    fr[0] = lead_even ? coarse[cb + k] : to_t<T>(add_(double(shell[lead_even ? 0 : sp0]), pred0));
+    if (has1) fr[1] = to_t<T>(add_(double(shell[sp0 + ml]), pred1));
+  }
+}
+
 // Serial Thomas along axis-0-style lines over a precomputed load vector, in
 // place: the same operations as k_sweep after its load (bit-identical).
 template <bool kNu>
@@ -1140,9 +1339,12 @@ static void coef_load0_axis0(const T* src, T* shell, T* coarse, double* comp, co
                              const ThomasLevel* th, const NuLevel* nu, const Exec& ex) {
   const int64_t inner = g.N / g.n[0], m0 = g.m[0];
   const int chunk = int(std::max<int64_t>(1, std::min<int64_t>(64, m0 * inner / (int64_t(600) << 10))));
-  const int64_t work = ((m0 + chunk - 1) / chunk) * (g.d == 2 ? g.m[1] : inner);
+  const int64_t work = ((m0 + chunk - 1) / chunk) * (g.d <= 4 ? inner / g.n[g.d - 1] * g.m[g.d - 1] : inner);
   const int grid = grid_for(work, 256);
   const NuLevel z = nu ? *nu : NuLevel{};
+  LevelGeom gp = g;  // rank 3-4 pair kernels: dividers by m_last and by the middle row count
+  gp.fn[g.d - 1] = FastDiv(uint32_t(g.m[g.d - 1]));
+  gp.fn[0] = FastDiv(uint32_t(inner / g.n[g.d - 1]));
 #define L_(NU, D)                                                                                         \
   MGRX_LAUNCH(ex, kRec ? "gen_comp_load0" : "gen_coef_load0",                                             \
               (k_coef_load0<T, kRec, NU, D><<<grid, 256, 0, ex.s>>>(src, shell, coarse, comp, g, z, inner, chunk)))
@@ -1150,11 +1352,13 @@ static void coef_load0_axis0(const T* src, T* shell, T* coarse, double* comp, co
   if (g.d == 2)                                                                                            \
     MGRX_LAUNCH(ex, kRec ? "gen_comp_load0" : "gen_coef_load0",                                            \
                 (k2_coef_load0<T, kRec, NU><<<grid, 256, 0, ex.s>>>(src, shell, coarse, comp, g, z, chunk))); \
-  else if (g.d == 3)    \
-    L_(NU, 3);          \
-  else if (g.d == 4)    \
-    L_(NU, 4);          \
-  else                  \
+  else if (g.d == 3 && g.N < (int64_t(1) << 32))                                                          \
+    MGRX_LAUNCH(ex, kRec ? "gen_comp_load0" : "gen_coef_load0",                                            \
+                (kN_coef_load0<T, kRec, NU, 3><<<grid, 256, 0, ex.s>>>(src, shell, coarse, comp, gp, z, inner, chunk))); \
+  else if (g.d == 4 && g.N < (int64_t(1) << 32))                                                          \
+    MGRX_LAUNCH(ex, kRec ? "gen_comp_load0" : "gen_coef_load0",                                            \
+                (kN_coef_load0<T, kRec, NU, 4><<<grid, 256, 0, ex.s>>>(src, shell, coarse, comp, gp, z, inner, chunk))); \
+  else                                                                                                     \
     L_(NU, 0);
   if (nu) {
     R_(true)
@@ -1210,6 +1414,20 @@ cudaError_t general_recompose_level(const T* shell, T* coarse, T* fine, double* 
       MGRX_LAUNCH(ex, "gen_rec_interp", k2_rec_interp<T, true><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, g2, *nu));
     else
       MGRX_LAUNCH(ex, "gen_rec_interp", k2_rec_interp<T, false><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, g2, NuLevel{}));
+    return cudaGetLastError();
+  }
+  if (fast && (g.d == 3 || g.d == 4) && g.N < (int64_t(1) << 32)) {
+    const int grid = grid_for(g.N / g.n[g.d - 1] * g.m[g.d - 1], 256);
+    const NuLevel z = nu ? *nu : NuLevel{};
+    LevelGeom gp = g;
+    gp.fn[g.d - 1] = FastDiv(uint32_t(g.m[g.d - 1]));
+#define I_(NU, D) MGRX_LAUNCH(ex, "gen_rec_interp", (kN_rec_interp<T, NU, D><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, gp, z)))
+    if (g.d == 3) {
+      if (nu) I_(true, 3); else I_(false, 3);
+    } else {
+      if (nu) I_(true, 4); else I_(false, 4);
+    }
+#undef I_
     return cudaGetLastError();
   }
   launch_rec_interp<T>(shell, coarse, fine, g, nu, ex);
