@@ -195,6 +195,71 @@ __global__ void __launch_bounds__(128) k_sweep(const double* __restrict__ x, dou
   }
 }
 
+// k_sweep for contiguous lines (inner == 1): LINES consecutive lines are
+// staged in shared memory with coalesced copies (a thread walking its own
+// line directly would touch a different cache line per lane per step), each
+// thread runs k_sweep's exact per-line arithmetic on its line, and the
+// result lines go back coalesced.  Row strides are padded to odd lengths so
+// the per-thread walks hit distinct banks.
+template <bool kNu>
+__global__ void __launch_bounds__(128) k_sweep_rows(const double* __restrict__ x, double* __restrict__ y, int64_t lines,
+                                                    int n, int m, const double* __restrict__ w,
+                                                    const double* __restrict__ inv_d, const NuAxis nu) {
+  extern __shared__ double sw[];
+  const int L = blockDim.x;
+  const int ns = n | 1, ms = m | 1;
+  double* in = sw;
+  double* out = sw + int64_t(L) * ns;
+  const int64_t l0 = int64_t(blockIdx.x) * L;
+  const int nl = int(min(int64_t(L), lines - l0));
+  const double* xs = x + l0 * n;
+  for (int e = threadIdx.x; e < nl * n; e += L) {
+    const int r = e / n;
+    in[r * ns + (e - r * n)] = xs[e];
+  }
+  __syncthreads();
+  if (threadIdx.x < nl) {
+    const double* c = in + threadIdx.x * ns;
+    double* f = out + threadIdx.x * ms;
+    double prev = 0.0;
+    for (int i = 0; i < m; ++i) {
+      double acc = 0.0;
+      if (kNu) {
+        const double* sk = nu.s + 5 * i;
+        for (int k = 0; k < 5; ++k) {
+          const int jj = 2 * i + k - 2;
+          if (jj >= 0 && jj < n) acc = add_(acc, mul_(sk[k], c[jj]));
+        }
+        if (i > 0) acc = sub_(acc, mul_(nu.tw[i], prev));
+      } else {
+        if (i >= 1) {
+          acc = add_(acc, mul_(kW12, c[2 * i - 2]));
+          acc = add_(acc, mul_(0.5, c[2 * i - 1]));
+        }
+        acc = add_(acc, mul_((i == 0 || i + 1 == m) ? kW5_12 : kW5_6, c[2 * i]));
+        if (2 * i + 1 < n) acc = add_(acc, mul_(0.5, c[2 * i + 1]));
+        if (2 * i + 2 < n) acc = add_(acc, mul_(kW12, c[2 * i + 2]));
+        if (i > 0) acc = sub_(acc, mul_(w[i], prev));
+      }
+      f[i] = acc;
+      prev = acc;
+    }
+    double nxt = mul_(prev, kNu ? nu.tid[m - 1] : inv_d[m - 1]);
+    f[m - 1] = nxt;
+    for (int i = m - 2; i >= 0; --i) {
+      const double v = kNu ? mul_(sub_(f[i], mul_(nu.off[i], nxt)), nu.tid[i]) : mul_(sub_(f[i], mul_(kOff, nxt)), inv_d[i]);
+      f[i] = v;
+      nxt = v;
+    }
+  }
+  __syncthreads();
+  double* ys = y + l0 * m;
+  for (int e = threadIdx.x; e < nl * m; e += L) {
+    const int r = e / m;
+    ys[e] = out[r * ms + (e - r * m)];
+  }
+}
+
 // Parallel form of a sweep (path "auto"): the load vector as one fully
 // parallel stencil pass (same arithmetic and order as k_sweep, so the load
 // is bit-identical), then the Thomas solve split into segments per line
@@ -1319,6 +1384,17 @@ static void run_sweeps(double* comp, double* tmp, const LevelGeom& g, const Thom
         MGRX_LAUNCH(ex, "gen_solve", k_axis_solve_rows<<<unsigned(blocks), 32 * nw, row_smem, ex.s>>>(y, lines, int(g.m[a]), w, id, of));
       } else {
         launch_axis_solve(y, lines, g.m[a], inner, w, id, of, ex);
+      }
+    } else if (inner == 1 && size_t(128) * size_t((g.n[a] | 1) + (g.m[a] | 1)) * 8 <= size_t(160) * 1024) {
+      // contiguous lines: staged in shared memory (same arithmetic as k_sweep)
+      const size_t sm = size_t(128) * size_t((g.n[a] | 1) + (g.m[a] | 1)) * 8;
+      const unsigned blocks = unsigned((lines + 127) / 128);
+      if (nu) {
+        cudaFuncSetAttribute(k_sweep_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        MGRX_LAUNCH(ex, "gen_sweep", k_sweep_rows<true><<<blocks, 128, sm, ex.s>>>(x, y, lines, int(g.n[a]), int(g.m[a]), nullptr, nullptr, nu->ax[a]));
+      } else {
+        cudaFuncSetAttribute(k_sweep_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        MGRX_LAUNCH(ex, "gen_sweep", k_sweep_rows<false><<<blocks, 128, sm, ex.s>>>(x, y, lines, int(g.n[a]), int(g.m[a]), th->w[a], th->inv_d[a], NuAxis{}));
       }
     } else if (nu)
       MGRX_LAUNCH(ex, "gen_sweep", k_sweep<true><<<grid, 128, 0, ex.s>>>(x, y, outer, inner, g.n[a], g.m[a], nullptr, nullptr, nu->ax[a]));
