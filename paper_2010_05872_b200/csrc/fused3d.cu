@@ -1216,157 +1216,6 @@ __global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : (MAXT == kColT
   }
 }
 
-// Pipelined column pass: the same per-column arithmetic as k_f3_col, in a
-// persistent block that walks tiles of 16 columns.  The next tile's column
-// values are copied global -> shared with cp.async (8-byte chunks: the
-// column strides of G are odd multiples of 8 bytes) while the current tile
-// is solved, so HBM latency hides behind the solve instead of stalling the
-// block; with `coarse` set, the tile's coarse values are fetched the same way
-// alongside the next tile.
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <typename T>
-size_t colp_smem(int m, int S, bool apply) {
-  return size_t(2 * m + 2 * S * 16) * 8 + size_t(2) * m * 16 * 8 + (apply ? size_t(m) * 16 * sizeof(T) : 0);
-}
-
-template <typename T, int LS, bool APPLY, int MAXT, int MINB>
-__global__ void __launch_bounds__(MAXT, MINB)
-    k_f3_colp(double* __restrict__ G, T* __restrict__ coarse, double sign, int64_t ncols, int m, int64_t stride,
-              int64_t outer_stride, int64_t inner, const double* __restrict__ w, const double* __restrict__ inv_d) {
-  extern __shared__ double sc[];
-  const int lane = threadIdx.x, S = 2 * blockDim.y;
-  const int c16 = lane & 15, s = 2 * threadIdx.y + (lane >> 4);
-  const int t = threadIdx.y * 32 + lane, nthr = blockDim.y * 32;
-  double* tw = sc;
-  double* tid = sc + m;
-  double* A = tid + m;  // [S][16]
-  double* B = A + S * 16;
-  double* const buf0 = B + S * 16;  // two tile buffers of m x 16, then the coarse tile
-  T* cbuf = reinterpret_cast<T*>(buf0 + 2 * m * 16);
-  for (int i = t; i < m; i += nthr) {
-    tw[i] = w[i];
-    tid[i] = inv_d[i];
-  }
-  const int64_t ntiles = (ncols + 15) / 16;
-  const int seg = (m + S - 1) / S;
-  const int s0 = min(m, s * seg), s1 = min(m, s0 + seg);
-  const int len = s1 - s0;
-  auto colbase = [&](int64_t col) { return (col / inner) * outer_stride + (col % inner); };
-  // thread t always copies column t % 16 of a tile (nthr is a multiple of 16)
-  auto issue_g = [&](int64_t tile, double* dst) {
-    const int64_t col = tile * 16 + (t & 15);
-    if (col < ncols) {
-      const double* src = G + colbase(col);
-      for (int r = t >> 4; r < m; r += nthr >> 4) cp_async8(dst + r * 16 + (t & 15), src + int64_t(r) * stride);
-    }
-  };
-  auto issue_c = [&](int64_t tile) {
-    const int64_t col = tile * 16 + (t & 15);
-    if (col < ncols) {
-      const T* src = coarse + colbase(col);
-      for (int r = t >> 4; r < m; r += nthr >> 4) {
-        if (sizeof(T) == 8) cp_async8(cbuf + r * 16 + (t & 15), src + int64_t(r) * stride);
-        else cp_async4(cbuf + r * 16 + (t & 15), src + int64_t(r) * stride);
-      }
-    }
-  };
-  pdl_wait();
-  int64_t tile = blockIdx.x;
-  if (tile < ntiles) issue_g(tile, buf0);
-  cp_async_commit();
-  for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
-    double* cur = buf0 + (it & 1) * m * 16;
-    const int64_t nxt = tile + gridDim.x;
-    if (nxt < ntiles) issue_g(nxt, buf0 + ((it + 1) & 1) * m * 16);
-    if (APPLY) issue_c(tile);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();  // the tile (and, first time, the tables) visible to all
-    const int64_t col = tile * 16 + c16;
-    const bool valid = col < ncols;
-    double v[LS];
-#pragma unroll
-    for (int k = 0; k < LS; ++k) v[k] = (valid && k < len) ? cur[(s0 + k) * 16 + c16] : 0.0;
-    // forward y_i = f_i - w_i y_{i-1} (batched_solve, transform.hpp:117-120)
-    double ya = 0.0, yb = 1.0;
-#pragma unroll
-    for (int k = 0; k < LS; ++k)
-      if (k < len) {
-        const double wi = ld_volatile(tw + s0 + k);
-        ya = v[k] - wi * ya;
-        yb = -wi * yb;
-      }
-    A[s * 16 + c16] = ya;
-    B[s * 16 + c16] = yb;
-    __syncthreads();
-    double y = 0.0;
-    for (int q = 0; q < s; ++q) y = A[q * 16 + c16] + B[q * 16 + c16] * y;
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < LS; ++k)
-      if (k < len) {
-        y = v[k] - ld_volatile(tw + s0 + k) * y;
-        v[k] = y;
-      }
-    // back substitution z_i = (y_i - z_{i+1}/3) / d_i (transform.hpp:121-129)
-    double za = 0.0, zb = 1.0;
-#pragma unroll
-    for (int k = LS - 1; k >= 0; --k)
-      if (k < len) {
-        const double id = ld_volatile(tid + s0 + k);
-        za = (v[k] - kOff * za) * id;
-        zb = -kOff * id * zb;
-      }
-    A[s * 16 + c16] = za;
-    B[s * 16 + c16] = zb;
-    __syncthreads();
-    double z = 0.0;
-    for (int q = S - 1; q > s; --q) z = A[q * 16 + c16] + B[q * 16 + c16] * z;
-#pragma unroll
-    for (int k = LS - 1; k >= 0; --k)
-      if (k < len) {
-        z = (v[k] - kOff * z) * ld_volatile(tid + s0 + k);
-        v[k] = z;
-      }
-    if (APPLY) {
-      cp_async_wait<0>();
-      __syncthreads();  // the coarse tile visible
-    }
-    if (valid) {
-      const int64_t base = colbase(col) + int64_t(s0) * stride;
-      if (APPLY) {
-        T* c = coarse + base;
-#pragma unroll
-        for (int k = 0; k < LS; ++k) {
-          if (k < len) *c = to_t<T>(double(cbuf[(s0 + k) * 16 + c16]) + sign * v[k]);
-          c += stride;
-        }
-      } else {
-        double* gp = G + base;
-#pragma unroll
-        for (int k = 0; k < LS; ++k) {
-          if (k < len) *gp = v[k];
-          gp += stride;
-        }
-      }
-    }
-    __syncthreads();  // A/B, the tile buffer and cbuf free for the next issue
-  }
-  cp_async_wait<0>();
-  pdl_trigger();
-}
-
 // ------------------------------------------------------------ host side
 
 template <typename T, int TI1>
@@ -1432,30 +1281,6 @@ void launch_col(double* G, T* coarse, double sign, const F3Geom& g, int axis, co
                                     size_t(2 * m + 2 * 2 * SY * 16) * 8, ex.s, !ex.prof, G, coarse, sign, ncols, m,       \
                                     stride, outer_stride, inner, w, id));                                       \
   }
-  static const bool old_col = std::getenv("MGRX_COL_OLD") != nullptr;
-#define MGRX_COLP(LS, AP, MT, MINB)                                                                         \
-  {                                                                                                         \
-    const int SY = (m + 2 * LS - 1) / (2 * LS);                                                            \
-    const size_t sm = colp_smem<T>(m, 2 * SY, AP);                                                         \
-    auto kern = k_f3_colp<T, LS, AP, MT, MINB>;                                                             \
-    if (sm <= 227 * 1024 && !old_col) {                                                                     \
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));                     \
-      int nb = 0;                                                                                           \
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32 * SY, sm);                                \
-      nb = std::max(nb, 1);                                                                                 \
-      const unsigned pb = unsigned(std::min<int64_t>(blocks, int64_t(kNumSMs) * nb));                       \
-      MGRX_LAUNCH(ex, tag, pdl_launch(kern, dim3(pb), dim3(32, SY), sm, ex.s, !ex.prof, G, coarse, sign, ncols, m, \
-                                      stride, outer_stride, inner, w, id));                                 \
-      return;                                                                                               \
-    }                                                                                                       \
-  }
-  if (m <= 264) {
-    if (coarse) MGRX_COLP(12, true, kColThreads12, 2) else MGRX_COLP(12, false, kColThreads12, 3)
-  } else if (m <= 320) {
-    if (coarse) MGRX_COLP(16, true, kColThreads, 2) else MGRX_COLP(16, false, kColThreads, 2)
-  } else {
-    if (coarse) MGRX_COLP(16, true, 2 * kColThreads, 1) else MGRX_COLP(16, false, 2 * kColThreads, 1)
-  }
   if (m <= 264) {
     if (coarse) MGRX_COLL(12, true, kColThreads12) else MGRX_COLL(12, false, kColThreads12)
   } else if (m <= 320) {
@@ -1464,7 +1289,6 @@ void launch_col(double* G, T* coarse, double sign, const F3Geom& g, int axis, co
     if (coarse) MGRX_COL(true, 2 * kColThreads) else MGRX_COL(false, 2 * kColThreads)
   }
 #undef MGRX_COL
-#undef MGRX_COLP
 #undef MGRX_COLL
 }
 
