@@ -73,14 +73,18 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// try_wait suspends the waiting warp (up to this many ns) instead of
+// returning at once, so a waiting warp does not spin on issue slots.
+constexpr uint32_t kMbarSuspendNs = 100000;
+
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(kMbarSuspendNs)
       : "memory");
   return ok != 0;
 }
@@ -260,12 +264,43 @@ struct PlaneSmem {
 // Axis-2 load-vector restriction at column c from the pair values of this
 // lane and its neighbours: H(c) = w(c) e(c) + o(c)/2 + [e(c-1)/12 + o(c-1)/2]
 // + e(c+1)/12 (load_entry, transform.hpp:84-96; missing nodes carry 0).
+// The weights are per-lane constants (StripW): a lane outside the grid
+// (xe = 0) or without an odd node (xo = 0) contributes nothing, and the
+// right neighbour's even node only exists for c + 1 < m2 (er = 0), so the
+// lanes' values need no zeroing selects (they only have to be finite).
+struct StripW {
+  double wc, xe, xo, er;
+};
+__device__ __forceinline__ StripW strip_w(int c, int m2, bool valid, bool has_odd) {
+  StripW w;
+  w.wc = (c == 0 || c + 1 == m2) ? kW5_12 : kW5_6;
+  w.xe = valid ? kW12 : 0.0;
+  w.xo = has_odd ? 0.5 : 0.0;
+  w.er = (c + 1 < m2) ? kW12 : 0.0;
+  return w;
+}
+__device__ __forceinline__ double strip_restrict(double cE, double cO, const StripW& w) {
+  const double x = w.xe * cE + w.xo * cO;  // this column's share of H(c+1)
+  const double xl = __shfl_up_sync(0xffffffffu, x, 1);
+  const double er = __shfl_down_sync(0xffffffffu, cE, 1);
+  return w.wc * cE + w.xo * cO + xl + w.er * er;
+}
+
+// The same with the weights of column c (the recompose plane pass zeroes its
+// lanes' values instead: fewer live registers).
 __device__ __forceinline__ double strip_restrict(double cE, double cO, int c, int m2) {
   const double x = kW12 * cE + 0.5 * cO;  // this column's share of H(c+1)
   const double xl = __shfl_up_sync(0xffffffffu, x, 1);
   const double er = __shfl_down_sync(0xffffffffu, cE, 1);
   const double wc = (c == 0 || c + 1 == m2) ? kW5_12 : kW5_6;
   return wc * cE + 0.5 * cO + xl + kW12 * er;
+}
+
+// Shuffle source of the right neighbour's corner sum: a degenerate right
+// end (2c + 2 >= n2) uses its own (transform.hpp:231-266).
+__device__ __forceinline__ int right_src(bool right_degen) {
+  const int lane = threadIdx.x & 31;
+  return right_degen ? lane : min(lane + 1, 31);
 }
 
 // Thomas solve of one row x[0..m) in shared memory by one warp: lane
@@ -477,6 +512,9 @@ struct DecRows {
   bool own;           // owned lane and owned plane
   bool valid, has_odd, right_degen, has_right;
   int c;
+  int oi;      // offset of the odd node's raw value (0 without an odd node: a finite stand-in)
+  int rsrc;    // shuffle source of the right neighbour's corner sum
+  StripW sw;   // restriction weights of this lane
 };
 
 // Rows of one fine plane (decompose): for every fine row and this lane's
@@ -526,7 +564,7 @@ __device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const
     }
     const bool rdeg = !FULL && o1 && (j1 + 1 >= x.n1);
     const double rawE = double(rr[0]);
-    const double rawO = x.has_odd ? double(rr[1]) : 0.0;
+    const double rawO = double(rr[x.oi]);
     const double aL = aLc;
     const double bL = o1 ? (rdeg ? aL : aLn) : aL;
     double se;
@@ -544,15 +582,14 @@ __device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const
       }
       ke = o1 ? 2 : 1;
     }
-    double sn = __shfl_down_sync(0xffffffffu, se, 1);
-    if (x.right_degen) sn = se;
+    const double sn = __shfl_sync(0xffffffffu, se, x.rsrc);
     const double so = se + sn;
     const double sc_e = ke == 1 ? 0.5 : 0.25;
     const double sc_o = ke == 0 ? 0.5 : (ke == 1 ? 0.25 : 0.125);
     const T tE = to_t<T>(rawE - se * sc_e);
     const T tO = to_t<T>(rawO - so * sc_o);
-    const double cE = (ke == 0 || !x.valid) ? 0.0 : double(tE);
-    const double cO = x.has_odd ? double(tO) : 0.0;
+    const double cE = ke == 0 ? 0.0 : double(tE);  // finite on every lane (clamped columns)
+    const double cO = double(tO);
     const bool own_row = FULL ? (jr >= 2 && jr < 2 * TI1 + 2) : (j1 >= x.jlo_own && j1 < x.jhi_own);
     if (x.own && own_row) {
       if (o1) {
@@ -568,7 +605,7 @@ __device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const
         if (x.has_odd) sr[x.oofs] = tO;
       }
     }
-    const double h = strip_restrict(cE, cO, x.c, x.m2);
+    const double h = strip_restrict(cE, cO, x.sw);
 #pragma unroll
     for (int k = -2; k <= 2; ++k) {
       if (((jr - 2 - k) & 1) != 0) continue;
@@ -632,6 +669,9 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
   x.has_odd = S.valid && 2 * c + 1 < n2;
   x.right_degen = 2 * c + 2 >= n2;
   x.c = c;
+  x.oi = x.has_odd ? 1 : 0;
+  x.rsrc = right_src(x.right_degen);
+  x.sw = strip_w(c, m2, x.valid, x.has_odd);
   x.n2l = int(g.n2);
   const bool full = ur.b0 >= 1 && 2 * ur.b1 <= g.n1 - 1;
   const int cc = S.valid ? c : 0;  // clamp halo columns for addressing
@@ -903,6 +943,7 @@ template <typename T, int TRI, bool PODD, bool FULL>
 __device__ __forceinline__ void interp_rows(const T* ev, const T* od, int64_t st_e, int oofs, T* __restrict__ out,
                                             const double* CL, const double* CR, int j1lo, int n1, int64_t n2l,
                                             int m2, bool owned, bool has_odd, bool right_degen) {
+  const int rsrc = right_src(right_degen);
 #pragma unroll
   for (int jr = 0; jr < TRI; ++jr) {
     const int j1 = j1lo + jr;
@@ -928,8 +969,7 @@ __device__ __forceinline__ void interp_rows(const T* ev, const T* od, int64_t st
       }
       ke = o1 ? 2 : 1;
     }
-    double sn = __shfl_down_sync(0xffffffffu, se, 1);
-    if (right_degen) sn = se;
+    const double sn = __shfl_sync(0xffffffffu, se, rsrc);
     const double so = se + sn;
     if (owned) {
       const double sc_e = ke == 1 ? 0.5 : 0.25;
