@@ -296,6 +296,18 @@ __device__ __forceinline__ double strip_restrict(double cE, double cO, int c, in
   return wc * cE + 0.5 * cO + xl + kW12 * er;
 }
 
+// Predicated global store (no branch; the address is not dereferenced
+// when p is false).  No memory clobber: nothing in these kernels reads
+// what they store, so other accesses may move across it.
+__device__ __forceinline__ void st_if(float* a, float v, bool p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f32 [%0], %1;\n\t}" ::"l"(a), "f"(v),
+               "r"(int(p)));
+}
+__device__ __forceinline__ void st_if(double* a, double v, bool p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f64 [%0], %1;\n\t}" ::"l"(a), "d"(v),
+               "r"(int(p)));
+}
+
 // Shuffle source of the right neighbour's corner sum: a degenerate right
 // end (2c + 2 >= n2) uses its own (transform.hpp:231-266).
 __device__ __forceinline__ int right_src(bool right_degen) {
@@ -971,12 +983,12 @@ __device__ __forceinline__ void interp_rows(const T* ev, const T* od, int64_t st
     }
     const double sn = __shfl_sync(0xffffffffu, se, rsrc);
     const double so = se + sn;
-    if (owned) {
+    {  // predicated stores (owned lanes; the odd node where it exists)
       const double sc_e = ke == 1 ? 0.5 : 0.25;
       const double sc_o = ke == 0 ? 0.5 : (ke == 1 ? 0.25 : 0.125);
       T* o = out + int64_t(jr) * n2l;
-      o[0] = ke == 0 ? to_t<T>(aL) : to_t<T>(double(sr[0]) + se * sc_e);
-      if (has_odd) o[1] = to_t<T>(double(sr[o1 ? m2 : oofs]) + so * sc_o);
+      st_if(o, ke == 0 ? to_t<T>(aL) : to_t<T>(double(sr[0]) + se * sc_e), owned);
+      st_if(o + 1, to_t<T>(double(sr[o1 ? (has_odd ? m2 : 0) : (has_odd ? oofs : 0)]) + so * sc_o), owned && has_odd);
     }
   }
 }
