@@ -547,47 +547,49 @@ __global__ void __launch_bounds__(256) k2_rec_interp(const T* __restrict__ shell
 // last axis as the highest bit, so the odd column's corner sum is the even
 // column's sum continued over the right-hand corners (uniform case) —
 // bit-identical with far fewer instructions than the per-node corner loop.
-// The corner loop runs over all 2^(D-1) masks of the leading axes with the
-// masks touching an even axis predicated off: a mask's odd-axis bits in
-// ascending order are exactly predict's cmask, so the order is unchanged,
-// and control flow stays uniform across lanes of different parity classes
-// (a warp usually straddles two rows).  32-bit offsets (N < 2^32).
+// The corner loop is specialised on the parity pattern OM of the leading
+// axes (pair_predict dispatches; a lane's pattern is constant along a row):
+// only the subsets of the odd axes are enumerated, in ascending mask order —
+// a mask's odd-axis bits in ascending order are exactly predict's cmask, so
+// the order is unchanged.  32-bit offsets (N < 2^32).
 // pred0 at column cl (meaningful unless the even node is nodal), pred1 at
 // the odd column between cl and cr (has1); w3l/w3r: nonuniform last-axis
 // weights of the odd column.  Returns the all-left corner offset.
-template <typename T, bool kNu, int D>
-__device__ __forceinline__ uint32_t pair_predict(const T* __restrict__ src, const LevelGeom& g, const NuLevel& nu,
-                                                 const int64_t* j, bool coarse, uint32_t cl, uint32_t cr, bool has1,
-                                                 double w3l, double w3r, double& pred0, double& pred1) {
+template <typename T, bool kNu, int D, unsigned OM>
+__device__ __forceinline__ uint32_t pair_predict_m(const T* __restrict__ src, const LevelGeom& g, const NuLevel& nu,
+                                                   const int64_t* j, bool coarse, uint32_t cl, uint32_t cr, bool has1,
+                                                   double w3l, double w3r, double& pred0, double& pred1) {
+  // OM: the odd axes among 0..D-2 (compile time: only the corner subsets of
+  // the odd axes are enumerated, in ascending cmask order as before)
   constexpr int A = D - 1;
-  uint32_t base = 0, dl[A], evenmask = 0;
-  bool odd[A];
+  uint32_t base = 0, dl[A];
   double wl[A], wr[A];
   int nodd = 0;
 #pragma unroll
   for (int i = 0; i < A; ++i) {
-    odd[i] = j[i] & 1;
+    constexpr unsigned one = 1u;
+    const bool odd = (OM >> i) & one;
     const uint32_t ji = uint32_t(j[i]);
-    base += coarse ? (ji >> 1) * uint32_t(g.cst[i]) : (odd[i] ? ji - 1 : ji) * uint32_t(g.st[i]);
-    dl[i] = (odd[i] && j[i] + 1 < g.n[i]) ? (coarse ? uint32_t(g.cst[i]) : 2 * uint32_t(g.st[i])) : 0;
+    base += coarse ? (ji >> 1) * uint32_t(g.cst[i]) : (odd ? ji - 1 : ji) * uint32_t(g.st[i]);
+    dl[i] = (odd && j[i] + 1 < g.n[i]) ? (coarse ? uint32_t(g.cst[i]) : 2 * uint32_t(g.st[i])) : 0;
     wl[i] = wr[i] = 1.0;
-    if (kNu && odd[i]) {
+    if (kNu && odd) {
       wl[i] = nu.ax[i].wl[ji];
       wr[i] = nu.ax[i].wr[ji];
     }
-    nodd += odd[i] ? 1 : 0;
-    evenmask |= odd[i] ? 0u : (1u << i);
+    nodd += odd ? 1 : 0;
   }
   double s0 = 0.0, s1 = 0.0;
 #pragma unroll
   for (uint32_t fm = 0; fm < (1u << A); ++fm) {
-    if (fm & evenmask) continue;
+    if (fm & ~OM) continue;
     uint32_t off = base;
     double wp = 1.0;
 #pragma unroll
     for (int i = 0; i < A; ++i) {
+      if (!((OM >> i) & 1u)) continue;
       if ((fm >> i) & 1) off += dl[i];
-      if (kNu && odd[i]) wp = mul_(wp, ((fm >> i) & 1) ? wr[i] : wl[i]);
+      if (kNu) wp = mul_(wp, ((fm >> i) & 1) ? wr[i] : wl[i]);
     }
     const double L = double(src[off + cl]);
     if (kNu) {
@@ -604,13 +606,14 @@ __device__ __forceinline__ uint32_t pair_predict(const T* __restrict__ src, cons
     if (!kNu) s1 = s0;
 #pragma unroll
     for (uint32_t fm = 0; fm < (1u << A); ++fm) {
-      if (fm & evenmask) continue;
+      if (fm & ~OM) continue;
       uint32_t off = base;
       double wp = 1.0;
 #pragma unroll
       for (int i = 0; i < A; ++i) {
+        if (!((OM >> i) & 1u)) continue;
         if ((fm >> i) & 1) off += dl[i];
-        if (kNu && odd[i]) wp = mul_(wp, ((fm >> i) & 1) ? wr[i] : wl[i]);
+        if (kNu) wp = mul_(wp, ((fm >> i) & 1) ? wr[i] : wl[i]);
       }
       const double R = double(src[off + cr]);
       s1 = kNu ? add_(s1, mul_(mul_(wp, w3r), R)) : add_(s1, R);
@@ -618,6 +621,33 @@ __device__ __forceinline__ uint32_t pair_predict(const T* __restrict__ src, cons
     pred1 = kNu ? s1 : mul_(s1, 0.5 * sc0);
   }
   return base;
+}
+
+// Dispatch on the parity pattern of the leading axes (warp-uniform along a
+// row of the last axis).
+template <typename T, bool kNu, int D>
+__device__ __forceinline__ uint32_t pair_predict(const T* __restrict__ src, const LevelGeom& g, const NuLevel& nu,
+                                                 const int64_t* j, bool coarse, uint32_t cl, uint32_t cr, bool has1,
+                                                 double w3l, double w3r, double& pred0, double& pred1) {
+  unsigned om = 0;
+#pragma unroll
+  for (int i = 0; i < D - 1; ++i) om |= unsigned(j[i] & 1) << i;
+#define PP_(M) \
+  case M:      \
+    return pair_predict_m<T, kNu, D, (M) & ((1u << (D - 1)) - 1)>(src, g, nu, j, coarse, cl, cr, has1, w3l, w3r, pred0, pred1)
+  switch (om) {
+    PP_(0);
+    PP_(1);
+    PP_(2);
+    PP_(3);
+    PP_(4);
+    PP_(5);
+    PP_(6);
+    default:
+      return pair_predict_m<T, kNu, D, 7u & ((1u << (D - 1)) - 1)>(src, g, nu, j, coarse, cl, cr, has1, w3l, w3r, pred0,
+                                                                   pred1);
+  }
+#undef PP_
 }
 
 // k_coef_load0 for rank D = 3, 4: a thread owns a column pair of one row of
