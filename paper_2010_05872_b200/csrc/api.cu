@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -237,6 +238,8 @@ struct mgrx_gpu_ctx {
   static constexpr int kSide = 4;
   cudaStream_t side[kSide] = {};
   cudaStream_t chain = nullptr;  // high priority: the sequential recompose chain
+  cudaStream_t hi = nullptr;     // high priority: the finest level's correction (the critical path)
+  cudaStream_t chain_lo = nullptr;  // low priority variant of the chain (MGRX_REC_PRIO=2)
   cudaEvent_t fork = nullptr, join = nullptr;
   std::vector<cudaEvent_t> lvl_done;
 };
@@ -258,6 +261,8 @@ void ensure_side(mgrx_gpu_ctx* c, int levels) {
     for (int i = 0; i < mgrx_gpu_ctx::kSide; ++i)
       cuda_check(cudaStreamCreateWithPriority(&c->side[i], cudaStreamNonBlocking, least), "cudaStreamCreate(side)");
     cuda_check(cudaStreamCreateWithPriority(&c->chain, cudaStreamNonBlocking, greatest), "cudaStreamCreate(chain)");
+    cuda_check(cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, greatest), "cudaStreamCreate(hi)");
+    cuda_check(cudaStreamCreateWithPriority(&c->chain_lo, cudaStreamNonBlocking, least), "cudaStreamCreate(chain lo)");
     cuda_check(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming), "cudaEventCreate");
     cuda_check(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming), "cudaEventCreate");
   }
@@ -266,6 +271,14 @@ void ensure_side(mgrx_gpu_ctx* c, int levels) {
     cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     c->lvl_done.push_back(e);
   }
+}
+
+// Recompose stream priorities (MGRX_REC_PRIO, default 2): 0 = the chain high, every
+// correction low; 1 = also the finest level's correction high; 2 = that
+// correction high, the chain low.
+int rec_prio() {
+  static const int v = std::getenv("MGRX_REC_PRIO") ? std::atoi(std::getenv("MGRX_REC_PRIO")) : 2;
+  return v;
 }
 
 void set_device(mgrx_gpu_ctx* c) { cuda_check(cudaSetDevice(c->device), "cudaSetDevice"); }
@@ -591,6 +604,7 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
         const Fused3DPlan& fp = p.fused[l];
         if (!fp.enabled) continue;
         cudaStream_t sd = c->side[k++ % mgrx_gpu_ctx::kSide];
+        if (l == L && rec_prio() >= 1) sd = c->hi;
         cuda_check(cudaStreamWaitEvent(sd, c->fork, 0), "cudaStreamWaitEvent");
         cuda_check(fused3d_recompose_correction<T>(d_coeffs + h.node[l - 1], s + fp.scratch_off, fp, p.thomas[l],
                                                    exec_on(c, sd, l)),
@@ -598,7 +612,7 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
         cuda_check(cudaEventRecord(c->lvl_done[l], sd), "cudaEventRecord");
         forked[l] = 1;
       }
-      cs = c->chain;
+      cs = rec_prio() == 2 ? c->chain_lo : c->chain;
       cuda_check(cudaStreamWaitEvent(cs, c->fork, 0), "cudaStreamWaitEvent");
     }
   }
@@ -729,6 +743,8 @@ int mgrx_gpu_ctx_destroy(mgrx_gpu_ctx* c) {
   for (int i = 0; i < mgrx_gpu_ctx::kSide; ++i)
     if (c->side[i]) cudaStreamDestroy(c->side[i]);
   if (c->chain) cudaStreamDestroy(c->chain);
+  if (c->hi) cudaStreamDestroy(c->hi);
+  if (c->chain_lo) cudaStreamDestroy(c->chain_lo);
   if (c->fork) cudaEventDestroy(c->fork);
   if (c->join) cudaEventDestroy(c->join);
   for (cudaEvent_t e : c->lvl_done) cudaEventDestroy(e);
