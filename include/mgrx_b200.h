@@ -169,6 +169,48 @@ int mgrx_host_dequantize(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t
 int mgrx_gpu_workspace_size(int dtype, int ndims, const uint64_t* dims, int levels, int stop_level,
                             uint64_t* bytes);
 
+/* ---- slab mode (one 3-D field sharded by slabs of axis-0 planes) -------
+ * The reference has no distributed path; these are the per-pass pieces of
+ * decompose_with / recompose (transform.hpp:485-530) for ONE fused 3-D level
+ * restricted to a slab, so that a caller holding the slab on one GPU can run
+ * a level with its neighbours: it exchanges halo planes, and transposes the
+ * fp64 load-vector volume G (m0 x m1 x m2, row-major, global plane indexing)
+ * for the axis-0 solve (NCCL all-to-all in paper_2010_05872_b200/slab.py).
+ * All buffers are full-size and globally indexed (a rank touches its planes
+ * only): the level block `blk` / coarse block / level-centric `out` of the
+ * whole field.  `level` is the fine level l of the pass (1 <= l <= L).
+ *
+ * info[0..8] = n0, n1, n2 (level l), m0, m1, m2 (level l-1), fused (1 when
+ * the level runs on the fused 3-D path, which slab mode needs),
+ * node_count(l-1) (the level's shell offset), node_count(l). */
+int mgrx_gpu_slab_level(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels, int level,
+                        int64_t* info);
+/* Decompose plane pass for coarse planes [k0, k1): coefficients of the fine
+ * planes [2 k0, 2 k1) (and n0 - 1 when k1 = m0) into `out`'s shell, their
+ * nodal values into `coarse`, the axis-0/1/2 load vector into G[k0, k1).
+ * Reads fine planes [2 k0 - 2, 2 k1] of `blk`. */
+int mgrx_gpu_slab_dec_plane(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels, int level,
+                            uint64_t k0, uint64_t k1, const void* d_blk, void* d_out, void* d_coarse, double* d_G);
+/* Recompose plane pass: the load vector of the shell's coefficients (reads
+ * the shells of fine planes [2 k0 - 2, 2 k1]) into G[k0, k1). */
+int mgrx_gpu_slab_rec_plane(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels, int level,
+                            uint64_t k0, uint64_t k1, const void* d_coeffs, double* d_G);
+/* Axis-2 and axis-1 solves (batched_solve, transform.hpp:116-130) of G's
+ * planes [k0, k1), in place. */
+int mgrx_gpu_slab_inplane(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels, int level,
+                          uint64_t k0, uint64_t k1, double* d_G);
+/* Axis-0 solve of a transposed block Gt[m0][width] (full axis-0 columns),
+ * in place. */
+int mgrx_gpu_slab_axis0(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels, int level,
+                        uint64_t width, double* d_Gt);
+/* coarse[i] = T(double(coarse[i]) + sign * z[i]), i < n (apply_correction,
+ * transform.hpp:435-477). */
+int mgrx_gpu_slab_apply(mgrx_gpu_ctx* ctx, int dtype, void* d_coarse, const double* d_z, uint64_t n, double sign);
+/* Recompose interpolation of the fine planes [p0, p1) (p0 even) from the
+ * corrected coarse block (planes [p0 / 2, (p1 + 1) / 2]) and the shell. */
+int mgrx_gpu_slab_interp(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels, int level,
+                         uint64_t p0, uint64_t p1, const void* d_coeffs, const void* d_coarse, void* d_fine);
+
 #ifdef __cplusplus
 }
 #endif

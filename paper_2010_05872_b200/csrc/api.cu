@@ -1067,4 +1067,122 @@ int mgrx_host_recompose(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims
   return host_roundtrip(c, dtype, nd, dims, levels, stop, h_coeffs, h_field, false);
 }
 
+// ---- slab mode ------------------------------------------
+
+namespace {
+// The plan of the full field (stop 0) and its fused level `level`.
+Plan* slab_plan(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int level) {
+  if (!dims) fail(MGRX_INVALID_ARGUMENT, "null argument");
+  Plan* p = get_plan(c, dtype, nd, dims, levels, 0);
+  if (level < 1 || level > p->h.L) fail(MGRX_INVALID_LEVEL, "slab: level out of range");
+  if (!p->fused[level].enabled) fail(MGRX_INVALID_ARGUMENT, "slab: level is not on the fused 3-D path");
+  return p;
+}
+}  // namespace
+
+int mgrx_gpu_slab_level(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int level,
+                        int64_t* info) {
+  return guarded(c, [&] {
+    if (!dims || !info) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    Plan* p = get_plan(c, dtype, nd, dims, levels, 0);
+    if (level < 1 || level > p->h.L) fail(MGRX_INVALID_LEVEL, "slab: level out of range");
+    const Fused3DPlan& fp = p->fused[level];
+    const LevelGeom& g = p->geom[level];
+    for (int i = 0; i < 3; ++i) {
+      info[i] = i < g.d ? g.n[i] : 1;
+      info[3 + i] = i < g.d ? g.m[i] : 1;
+    }
+    info[6] = (fp.enabled && c->path == 0) ? 1 : 0;
+    info[7] = int64_t(p->h.node[level - 1]);
+    info[8] = int64_t(p->h.node[level]);
+  });
+}
+
+int mgrx_gpu_slab_dec_plane(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int level,
+                            uint64_t k0, uint64_t k1, const void* d_blk, void* d_out, void* d_coarse, double* d_G) {
+  return guarded(c, [&] {
+    if (!d_blk || !d_out || !d_coarse || !d_G) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    Plan* p = slab_plan(c, dtype, nd, dims, levels, level);
+    const size_t off = p->h.node[level - 1];
+    cudaError_t e;
+    if (dtype == MGRX_F32)
+      e = fused3d_slab_dec_plane<float>(static_cast<const float*>(d_blk), static_cast<float*>(d_out) + off,
+                                        static_cast<float*>(d_coarse), d_G, p->fused[level], int64_t(k0), int64_t(k1),
+                                        exec(c, level));
+    else
+      e = fused3d_slab_dec_plane<double>(static_cast<const double*>(d_blk), static_cast<double*>(d_out) + off,
+                                         static_cast<double*>(d_coarse), d_G, p->fused[level], int64_t(k0),
+                                         int64_t(k1), exec(c, level));
+    cuda_check(e, "slab dec plane");
+  });
+}
+
+int mgrx_gpu_slab_rec_plane(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int level,
+                            uint64_t k0, uint64_t k1, const void* d_coeffs, double* d_G) {
+  return guarded(c, [&] {
+    if (!d_coeffs || !d_G) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    Plan* p = slab_plan(c, dtype, nd, dims, levels, level);
+    const size_t off = p->h.node[level - 1];
+    cudaError_t e;
+    if (dtype == MGRX_F32)
+      e = fused3d_slab_rec_plane<float>(static_cast<const float*>(d_coeffs) + off, d_G, p->fused[level], int64_t(k0),
+                                        int64_t(k1), exec(c, level));
+    else
+      e = fused3d_slab_rec_plane<double>(static_cast<const double*>(d_coeffs) + off, d_G, p->fused[level],
+                                         int64_t(k0), int64_t(k1), exec(c, level));
+    cuda_check(e, "slab rec plane");
+  });
+}
+
+int mgrx_gpu_slab_inplane(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int level,
+                          uint64_t k0, uint64_t k1, double* d_G) {
+  return guarded(c, [&] {
+    if (!d_G) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    Plan* p = slab_plan(c, dtype, nd, dims, levels, level);
+    cuda_check(fused3d_slab_inplane(d_G, p->fused[level], p->thomas[level], int64_t(k0), int64_t(k1), exec(c, level)),
+               "slab in-plane solves");
+  });
+}
+
+int mgrx_gpu_slab_axis0(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int level,
+                        uint64_t width, double* d_Gt) {
+  return guarded(c, [&] {
+    if (!d_Gt) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    Plan* p = slab_plan(c, dtype, nd, dims, levels, level);
+    cuda_check(fused3d_slab_axis0(d_Gt, int64_t(width), p->fused[level], p->thomas[level], exec(c, level)),
+               "slab axis-0 solve");
+  });
+}
+
+int mgrx_gpu_slab_apply(mgrx_gpu_ctx* c, int dtype, void* d_coarse, const double* d_z, uint64_t n, double sign) {
+  return guarded(c, [&] {
+    if (!d_coarse || !d_z) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    cudaError_t e;
+    if (dtype == MGRX_F32)
+      e = apply_correction<float>(static_cast<float*>(d_coarse), d_z, int64_t(n), sign, exec(c));
+    else
+      e = apply_correction<double>(static_cast<double*>(d_coarse), d_z, int64_t(n), sign, exec(c));
+    cuda_check(e, "slab apply");
+  });
+}
+
+int mgrx_gpu_slab_interp(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int level,
+                         uint64_t p0, uint64_t p1, const void* d_coeffs, const void* d_coarse, void* d_fine) {
+  return guarded(c, [&] {
+    if (!d_coeffs || !d_coarse || !d_fine) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    Plan* p = slab_plan(c, dtype, nd, dims, levels, level);
+    const size_t off = p->h.node[level - 1];
+    cudaError_t e;
+    if (dtype == MGRX_F32)
+      e = fused3d_slab_interp<float>(static_cast<const float*>(d_coeffs) + off, static_cast<const float*>(d_coarse),
+                                     static_cast<float*>(d_fine), p->fused[level], int64_t(p0), int64_t(p1),
+                                     exec(c, level));
+    else
+      e = fused3d_slab_interp<double>(static_cast<const double*>(d_coeffs) + off, static_cast<const double*>(d_coarse),
+                                      static_cast<double*>(d_fine), p->fused[level], int64_t(p0), int64_t(p1),
+                                      exec(c, level));
+    cuda_check(e, "slab interpolation");
+  });
+}
+
 }  // extern "C"

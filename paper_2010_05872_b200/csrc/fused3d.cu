@@ -203,8 +203,8 @@ struct UnitRange {
 __device__ __forceinline__ UnitRange unit_range(const F3Geom& g, int u) {
   UnitRange r;
   const int chunk = u / g.ntile1, tile = u - chunk * g.ntile1;
-  r.a0 = int64_t(chunk) * g.chunk;
-  r.a1 = min(g.m0, r.a0 + g.chunk);
+  r.a0 = g.a_base + int64_t(chunk) * g.chunk;
+  r.a1 = min(g.a_end < 0 ? g.m0 : g.a_end, r.a0 + g.chunk);
   r.b0 = int64_t(tile) * g.tile_rows;
   r.b1 = min(g.m1, r.b0 + g.tile_rows);
   r.plo = max(int64_t(0), 2 * r.a0 - 2);
@@ -1009,8 +1009,8 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 3 : 1)
   const bool has_odd = S.valid && 2 * c + 1 < n2;
   const bool right_degen = 2 * c + 2 >= n2;
   const int chunk = int(blockIdx.x) / ntile, tile = int(blockIdx.x) - chunk * ntile;
-  const int64_t p0 = int64_t(chunk) * ich;  // even
-  const int D = int(min(g.n0, p0 + ich) - 1 - p0);
+  const int64_t p0 = g.p_base + int64_t(chunk) * ich;  // even
+  const int D = int(min(g.p_end < 0 ? g.n0 : g.p_end, p0 + ich) - 1 - p0);
   const int j1lo = tile * TRI;  // even
   const int nrows = min(TRI, n1 - j1lo);
   const int e0 = j1lo >> 1;
@@ -1426,9 +1426,10 @@ static cudaError_t launch_interp_t(const T* shell, const T* coarse, T* fine, con
   int64_t per_slot = 8;  // units per resident CTA slot (MGRX_INTERP_UNITS overrides)
   if (const char* env = std::getenv("MGRX_INTERP_UNITS")) per_slot = std::max(1, std::atoi(env));
   const int64_t want = int64_t(sms) * 3 * per_slot;
-  int64_t ich = (g.n0 * ntile) / want;
+  const int64_t np = (g.p_end < 0 ? g.n0 : g.p_end) - g.p_base;  // fine planes of this launch
+  int64_t ich = (np * ntile) / want;
   ich = std::max<int64_t>(2, std::min<int64_t>(32, ich & ~int64_t(1)));
-  const int64_t chunks = (g.n0 + ich - 1) / ich;
+  const int64_t chunks = (np + ich - 1) / ich;
   MGRX_LAUNCH(ex, "f3_rec_interp",
               pdl_launch(k_f3_rec_interp<T, TRI, MAXT>, dim3(unsigned(chunks * ntile)), dim3(g.threads), smem, ex.s, !ex.prof,
                          shell, coarse, fine, g, int(ich), ntile));
@@ -1533,6 +1534,106 @@ cudaError_t fused3d_recompose_level(const T* shell, T* coarse, T* fine, void* sc
   return fused3d_recompose_finish<T>(shell, coarse, fine, scratch, fp, th, ex);
 }
 
+// ------------------------------------------------------------ slab mode
+// Chunking of a slab of K coarse planes (the cost model of fused3d_plan).
+static F3Geom slab_geom(const F3Geom& g0, int64_t k0, int64_t k1) {
+  F3Geom g = g0;
+  g.a_base = k0;
+  g.a_end = k1;
+  const int64_t K = k1 - k0;
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (nsm <= 0) nsm = kNumSMs;
+  const int64_t ctas = int64_t(nsm) * g.ctas_per_sm;
+  int64_t chunk = 1;
+  double best = 1e300;
+  for (int64_t c = 1; c <= 32 && c <= K; ++c) {
+    const int64_t units = ((K + c - 1) / c) * g.ntile1;
+    const double cost = double((units + ctas - 1) / ctas) * double(2 * c + 6);
+    if (cost < best - 1e-9) {
+      best = cost;
+      chunk = c;
+    }
+  }
+  g.chunk = chunk;
+  g.units = int(((K + chunk - 1) / chunk) * g.ntile1);
+  g.grid = g.units;
+  return g;
+}
+
+template <typename T>
+cudaError_t fused3d_slab_dec_plane(const T* blk, T* shell, T* coarse, double* G, const Fused3DPlan& fp, int64_t k0,
+                                   int64_t k1, const Exec& ex) {
+  if (k1 <= k0) return cudaSuccess;
+  const F3Geom g = slab_geom(fp.g, k0, k1);
+  size_t ds = 0;
+  cudaError_t e = set_attrs<T>(g, &ds);
+  if (e != cudaSuccess) return e;
+#define MGRX_DEC(TI, MT)                                                                               \
+  if (g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))                      \
+    MGRX_LAUNCH(ex, "f3_dec_plane", pdl_launch(k_f3_dec_plane<T, TI, MT>, dim3(g.grid), dim3(g.threads), ds, \
+                                               ex.s, !ex.prof, blk, shell, coarse, G, g));
+  MGRX_DEC(4, kPlaneMaxThreads)
+  MGRX_DEC(2, kPlaneMaxThreads)
+  MGRX_DEC(4, kWideBound)
+  MGRX_DEC(2, kWideBound)
+#undef MGRX_DEC
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t fused3d_slab_rec_plane(const T* shell, double* G, const Fused3DPlan& fp, int64_t k0, int64_t k1,
+                                   const Exec& ex) {
+  if (k1 <= k0) return cudaSuccess;
+  const F3Geom g = slab_geom(fp.g, k0, k1);
+  size_t ds = 0;
+  cudaError_t e = set_attrs<T>(g, &ds);
+  if (e != cudaSuccess) return e;
+#define MGRX_REC(TI, MT)                                                                               \
+  if (g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))                      \
+    MGRX_LAUNCH(ex, "f3_rec_plane", pdl_launch(k_f3_rec_plane<T, TI, MT>, dim3(g.grid), dim3(g.threads), ds, \
+                                               ex.s, !ex.prof, shell, G, g));
+  MGRX_REC(4, kPlaneMaxThreads)
+  MGRX_REC(2, kPlaneMaxThreads)
+  MGRX_REC(4, kWideBound)
+  MGRX_REC(2, kWideBound)
+#undef MGRX_REC
+  return cudaGetLastError();
+}
+
+cudaError_t fused3d_slab_inplane(double* G, const Fused3DPlan& fp, const ThomasLevel& th, int64_t k0, int64_t k1,
+                                 const Exec& ex) {
+  if (k1 <= k0) return cudaSuccess;
+  F3Geom gs = fp.g;
+  gs.m0 = k1 - k0;
+  double* Gs = G + k0 * fp.g.m1 * fp.g.m2;
+  launch_row(Gs, gs, th.w[2], th.inv_d[2], ex);
+  launch_col<float>(Gs, static_cast<float*>(nullptr), 0.0, gs, 1, th.w[1], th.inv_d[1], ex);
+  return cudaGetLastError();
+}
+
+cudaError_t fused3d_slab_axis0(double* Gt, int64_t width, const Fused3DPlan& fp, const ThomasLevel& th,
+                               const Exec& ex) {
+  if (width <= 0) return cudaSuccess;
+  // a [m0][width] block is the axis-0 layout of a volume with m1 = 1, m2 = width
+  F3Geom gs = fp.g;
+  gs.m1 = 1;
+  gs.m2 = width;
+  launch_col<float>(Gt, static_cast<float*>(nullptr), 0.0, gs, 0, th.w[0], th.inv_d[0], ex);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t fused3d_slab_interp(const T* shell, const T* coarse, T* fine, const Fused3DPlan& fp, int64_t p0, int64_t p1,
+                                const Exec& ex) {
+  if (p1 <= p0) return cudaSuccess;
+  F3Geom g = fp.g;
+  g.p_base = p0;
+  g.p_end = p1;
+  return launch_interp<T>(shell, coarse, fine, g, ex);
+}
+
 #define MGRX_INST(T)                                                                                     \
   template cudaError_t fused3d_decompose_level<T>(const T*, T*, T*, void*, const LevelGeom&, const Fused3DPlan&, \
                                                   const ThomasLevel&, const Exec&);                      \
@@ -1544,6 +1645,15 @@ cudaError_t fused3d_recompose_level(const T* shell, T* coarse, T* fine, void* sc
                                                    const Exec&);
 MGRX_INST(float)
 MGRX_INST(double)
+#define MGRX_INST_SLAB(T)                                                                                        \
+  template cudaError_t fused3d_slab_dec_plane<T>(const T*, T*, T*, double*, const Fused3DPlan&, int64_t, int64_t, \
+                                                 const Exec&);                                                   \
+  template cudaError_t fused3d_slab_rec_plane<T>(const T*, double*, const Fused3DPlan&, int64_t, int64_t,         \
+                                                 const Exec&);                                                   \
+  template cudaError_t fused3d_slab_interp<T>(const T*, const T*, T*, const Fused3DPlan&, int64_t, int64_t, const Exec&);
+MGRX_INST_SLAB(float)
+MGRX_INST_SLAB(double)
+#undef MGRX_INST_SLAB
 #undef MGRX_INST
 
 }  // namespace mgrx_b200

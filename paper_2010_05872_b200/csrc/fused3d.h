@@ -20,6 +20,9 @@ struct F3Geom {
   int threads = 0;                 // plane-pass CTA size (strips of 30 coarse columns)
   int ctas_per_sm = 1;             // plane-pass CTAs resident per SM
   int grid = 0;                    // persistent plane-pass CTAs
+  // slab mode: the plane passes cover coarse planes
+  // [a_base, a_end), the interpolation fine planes [p_base, p_end)
+  int64_t a_base = 0, a_end = -1, p_base = 0, p_end = -1;
 };
 
 struct Fused3DPlan {
@@ -44,5 +47,23 @@ cudaError_t fused3d_recompose_correction(const T* shell, void* scratch, const Fu
 template <typename T>
 cudaError_t fused3d_recompose_finish(const T* shell, T* coarse, T* fine, void* scratch, const Fused3DPlan& fp,
                                      const ThomasLevel& th, const Exec& ex);
+
+// Slab mode: the passes of one fused level restricted to a slab of coarse
+// planes [k0, k1) (fine planes [p0, p1) for the interpolation), on the
+// caller's G (m0 x m1 x m2 fp64, global plane indexing).
+template <typename T>
+cudaError_t fused3d_slab_dec_plane(const T* blk, T* shell, T* coarse, double* G, const Fused3DPlan& fp, int64_t k0,
+                                   int64_t k1, const Exec& ex);
+template <typename T>
+cudaError_t fused3d_slab_rec_plane(const T* shell, double* G, const Fused3DPlan& fp, int64_t k0, int64_t k1,
+                                   const Exec& ex);
+cudaError_t fused3d_slab_inplane(double* G, const Fused3DPlan& fp, const ThomasLevel& th, int64_t k0, int64_t k1,
+                                 const Exec& ex);
+// axis-0 solve of a [m0][width] column block of G (transposed), in place
+cudaError_t fused3d_slab_axis0(double* Gt, int64_t width, const Fused3DPlan& fp, const ThomasLevel& th,
+                               const Exec& ex);
+template <typename T>
+cudaError_t fused3d_slab_interp(const T* shell, const T* coarse, T* fine, const Fused3DPlan& fp, int64_t p0, int64_t p1,
+                                const Exec& ex);
 
 }  // namespace mgrx_b200

@@ -1549,6 +1549,17 @@ MGRX_INST(float)
 MGRX_INST(double)
 #undef MGRX_INST
 
+// coarse[p] <- T(double(coarse[p]) + sign z[p]) over n values (slab mode's
+// apply after the axis-0 transpose back; apply_correction, transform.hpp:435-477).
+template <typename T>
+cudaError_t apply_correction(T* coarse, const double* z, int64_t n, double sign, const Exec& ex) {
+  if (n <= 0) return cudaSuccess;
+  MGRX_LAUNCH(ex, "gen_apply", k_apply<T><<<grid_for(n, 256), 256, 0, ex.s>>>(coarse, z, n, sign));
+  return cudaGetLastError();
+}
+template cudaError_t apply_correction<float>(float*, const double*, int64_t, double, const Exec&);
+template cudaError_t apply_correction<double>(double*, const double*, int64_t, double, const Exec&);
+
 template cudaError_t tail_decompose<float>(const float*, float*, float*, const void*, const void*, int, int64_t, int,
                                            const Exec&);
 template cudaError_t tail_decompose<double>(const double*, double*, double*, const void*, const void*, int, int64_t,

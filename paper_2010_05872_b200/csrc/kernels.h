@@ -21,6 +21,9 @@ cudaError_t general_recompose_level(const T* shell, T* coarse, T* fine, double* 
                                     const LevelGeom& g, const ThomasLevel* th, const NuLevel* nu, const Exec& ex,
                                     bool fast);
 
+template <typename T>
+cudaError_t apply_correction(T* coarse, const double* z, int64_t n, double sign, const Exec& ex);
+
 // ---- tail: all small levels in one CTA (general.cu) -------------------------
 size_t tail_smem_bytes(int64_t nmax, int esize);
 size_t tail_level_bytes();
