@@ -543,6 +543,68 @@ def e2e_measure(mg, wsp, field, h, args, workers=2):
                     "with one context each (copies of consecutive steps overlap)"}
 
 
+def run_slab(args, ws, rank, local):
+    """Slab mode: ONE field split into axis-0 slabs over the ws
+    ranks (paper_2010_05872_b200/slab.py: halo exchange + NCCL all-to-all
+    transposes for the axis-0 solve).  Strong scaling: value = the whole
+    field's bytes / the slowest rank's step time.  With ws == 1 and
+    --slab-emulate R > 1, all R ranks run on this one GPU with device copies
+    for the exchanges (a correctness / overhead check: the time is the SUM
+    over the emulated ranks, not a multi-GPU number)."""
+    import torch
+
+    import paper_2010_05872_b200 as mg
+    from paper_2010_05872_b200.fields import config2_field
+    from paper_2010_05872_b200.slab import LocalExchange, TorchExchange, max_slab_levels, slab_bounds, \
+        slab_decompose, slab_recompose
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    field = config2_field(DIMS, seed=0, device=dev)
+    h = mg.GridHierarchy.create(DIMS)
+    emul = ws == 1 and args.slab_emulate > 1
+    ex = LocalExchange(args.slab_emulate) if emul else (TorchExchange() if ws > 1 else LocalExchange(1))
+    R = ex.world
+    S = max_slab_levels(h, R)
+    P = slab_bounds(DIMS[0], R, S)
+    fields = [field.clone() for _ in ex.local]
+    wss = [mg.SolverWorkspace(device=local) for _ in ex.local]
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        outs = slab_decompose(fields, h, ex, wss, S)
+        return slab_recompose(outs, h, ex, wss, S)
+
+    for _ in range(max(args.warmup, 1)):
+        backs = step()
+    torch.cuda.synchronize()
+    err = 0.0
+    for i, r in enumerate(ex.local):
+        hi = P[r + 1] if r + 1 < R else DIMS[0]
+        d = (backs[i][P[r]:hi] - field[P[r]:hi]).abs()
+        err = max(err, float("inf") if bool(torch.isnan(d).any()) else float(d.max().item()))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws, device=dev)
+    nbytes = field.numel() * 4
+    if rank == 0:
+        line = {"metric": METRIC, "value": nbytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": WORKLOAD + " -- slab mode (one field split along axis 0)",
+                           "field": list(DIMS), "field_dtype": "f32", "ranks": R, "slab_levels": S,
+                           "slab_bounds": P, "emulated_on_one_gpu": emul,
+                           "parallelism": f"slab{R}" + (" (emulated: time is the sum over ranks)" if emul else "")},
+                "roundtrip_linf": err}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -557,6 +619,10 @@ def main():
                     help="field extents (config-2 generator); 1025,1025,1025 is BASELINE config 5b")
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--warmup-ref", type=int, default=0, help="untimed reference steps (CPU code needs none)")
+    ap.add_argument("--slab", action="store_true",
+                    help="slab mode: one field split along axis 0 over the ranks (NCCL transposes); strong scaling")
+    ap.add_argument("--slab-emulate", type=int, default=1,
+                    help="with --slab on one GPU: emulate this many ranks in-process (correctness/overhead check)")
     args = ap.parse_args()
     global DIMS, WORKLOAD
     dims = tuple(int(x) for x in args.dims.split(","))
@@ -570,7 +636,10 @@ def main():
         run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
         return
     ws, rank, local = dist_init()
-    run_ours(args, ws, rank, local)
+    if args.slab:
+        run_slab(args, ws, rank, local)
+    else:
+        run_ours(args, ws, rank, local)
     if ws > 1:
         import torch.distributed as dist
 

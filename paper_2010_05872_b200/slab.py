@@ -53,6 +53,17 @@ def slab_bounds(n0: int, ranks: int, slab_levels: int) -> List[int]:
     return [(r * units // ranks) * unit for r in range(ranks)] + [n0 - 1]
 
 
+def shell_plane_range(p: int, info) -> tuple:
+    """[start, end) of fine plane p's shell entries in the level-centric
+    buffer (pack_level_centric, reorder.hpp:180-215: reordered planes in
+    order, an even plane's nodal rows omitted): one contiguous run."""
+    n0, n1, n2, m0, m1, m2, _, off = info[:8]
+    full, short = n1 * n2, n1 * n2 - m1 * m2
+    r0 = p // 2 if p % 2 == 0 else m0 + p // 2
+    start = r0 * short if r0 < m0 else m0 * short + (r0 - m0) * full
+    return off + start, off + start + (short if r0 < m0 else full)
+
+
 def column_bounds(ncols: int, ranks: int) -> List[int]:
     return [r * ncols // ranks for r in range(ranks + 1)]
 
@@ -89,6 +100,18 @@ class LocalExchange:
             if r + 1 < R and right:
                 b = bounds[r + 1]
                 bufs[r][b:b + right] = bufs[r + 1][b:b + right]
+
+    def halo_ranges(self, bufs, left, right):
+        """1-D bufs: rank r receives the element ranges left(r) from rank
+        r - 1 and right(r) from rank r + 1 (lists of (start, end))."""
+        R = self.world
+        for r in range(R):
+            if r > 0:
+                for a, b in left(r):
+                    bufs[r][a:b] = bufs[r - 1][a:b]
+            if r + 1 < R:
+                for a, b in right(r):
+                    bufs[r][a:b] = bufs[r + 1][a:b]
 
     def transpose(self, G, K, Cb):
         """G[r]: (m0, ncols) with rank r's planes [K[r], K[r+1]) set ->
@@ -155,6 +178,35 @@ class TorchExchange:
                 req.wait()
         for sl, t in recv:
             buf[sl] = t
+
+    def halo_ranges(self, bufs, left, right):
+        import torch
+
+        dist, r, R = self.dist, self.rank, self.world
+        buf = bufs[0]
+        ops, recv = [], []
+        if r + 1 < R:  # what rank r + 1 wants from its left neighbour
+            ops.append(dist.P2POp(dist.isend, torch.cat([buf[a:b] for a, b in left(r + 1)]), r + 1, self.group))
+        if r > 0:  # what rank r - 1 wants from its right neighbour
+            ops.append(dist.P2POp(dist.isend, torch.cat([buf[a:b] for a, b in right(r - 1)]), r - 1, self.group))
+        if r > 0:
+            rl = left(r)
+            t = buf.new_empty(sum(b - a for a, b in rl))
+            ops.append(dist.P2POp(dist.irecv, t, r - 1, self.group))
+            recv.append((rl, t))
+        if r + 1 < R:
+            rr = right(r)
+            t = buf.new_empty(sum(b - a for a, b in rr))
+            ops.append(dist.P2POp(dist.irecv, t, r + 1, self.group))
+            recv.append((rr, t))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        for rng, t in recv:
+            o = 0
+            for a, b in rng:
+                buf[a:b] = t[o:o + b - a]
+                o += b - a
 
     def transpose(self, G, K, Cb):
         import torch
@@ -289,8 +341,10 @@ def slab_decompose(fields: Sequence, hierarchy: GridHierarchy, exch, workspaces:
 
 def slab_recompose(coeffs: Sequence, hierarchy: GridHierarchy, exch, workspaces: Sequence[SolverWorkspace],
                    slab_levels: Optional[int] = None):
-    """recompose into a slab-sharded field.  coeffs[i]: the full level-centric
-    buffer on local rank exch.local[i].  Returns full-size fields (one per
+    """recompose into a slab-sharded field.  coeffs[i]: the level-centric
+    buffer on local rank exch.local[i] holding the coarse levels and the
+    shells of its own planes (what slab_decompose returns); the shells of
+    the halo planes are exchanged here (the buffers are updated in place).  Returns full-size fields (one per
     local rank) holding its planes [P_r, P_{r+1}) (the last rank also n0 - 1)."""
     import torch
 
@@ -322,6 +376,9 @@ def slab_recompose(coeffs: Sequence, hierarchy: GridHierarchy, exch, workspaces:
         Pf[R] = n0
         K = [p >> (j + 1) for p in P]
         K[R] = m0
+        # the plane pass reads the shells of fine planes [2 K_r - 2, 2 K_{r+1}]
+        exch.halo_ranges(coeffs, lambda r: [shell_plane_range(p, info) for p in (Pf[r] - 2, Pf[r] - 1)],
+                         lambda r: [shell_plane_range(Pf[r + 1], info)])
         G = [torch.empty((m0, m1 * m2), dtype=torch.float64, device=dev) for _ in exch.local]
         for i, r in enumerate(exch.local):
             ws = workspaces[i]

@@ -11,7 +11,16 @@ import os
 
 import pytest
 
-from paper_2010_05872_b200.slab import LocalExchange, TorchExchange, column_bounds, max_slab_levels, slab_bounds
+from paper_2010_05872_b200.slab import LocalExchange, TorchExchange, column_bounds, max_slab_levels, \
+    shell_plane_range, slab_bounds
+
+
+def test_shell_plane_ranges_tile_the_level():
+    # level 9 of 513^3: fine 513^3, coarse 257^3, shell offset 257^3
+    info = [513, 513, 513, 257, 257, 257, 1, 257 ** 3]
+    rngs = sorted(shell_plane_range(p, info) for p in range(513))
+    assert rngs[0][0] == 257 ** 3 and rngs[-1][1] == 513 ** 3
+    assert all(a[1] == b[0] for a, b in zip(rngs, rngs[1:]))
 
 
 def test_bounds():
@@ -59,8 +68,9 @@ def test_slab_emulated_matches_single_gpu(shape, dtype, ranks):
     torch.cuda.synchronize()
     assert not torch.isnan(got).any()
     assert torch.equal(got, want)
-    # recompose from the full coefficients on every rank
-    backs = slab_recompose([want.clone() for _ in range(ranks)], h, ex, wss, S)
+    # recompose from each rank's own coefficients (its shells + the coarse
+    # levels; the halo planes' shells are exchanged inside)
+    backs = slab_recompose(outs, h, ex, wss, S)
     back = torch.empty_like(f)
     for r in range(ranks):
         hi = P[r + 1] if r + 1 < ranks else shape[0]
@@ -90,6 +100,15 @@ def _gloo_worker(rank, world, port, q):
         T_buf = [base[rank].clone()]
         te.halo(T_buf, None, K, 2, 1)
         ok = torch.equal(T_buf[0], L_bufs[rank])
+        # halo of element ranges
+        flat = [b.reshape(-1).clone() for b in base]
+        left = lambda r: [(r * 7, r * 7 + 3), (40, 42)]  # noqa: E731
+        right = lambda r: [(100 + r, 103 + r)]  # noqa: E731
+        L_fl = [f.clone() for f in flat]
+        loc.halo_ranges(L_fl, left, right)
+        T_fl = [flat[rank].clone()]
+        te.halo_ranges(T_fl, left, right)
+        ok &= torch.equal(T_fl[0], L_fl[rank])
         # transposes
         Gt_l = loc.transpose(base, K, Cb)
         Gt_t = te.transpose([base[rank]], K, Cb)
