@@ -169,6 +169,19 @@ int mgrx_host_dequantize(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t
 int mgrx_gpu_workspace_size(int dtype, int ndims, const uint64_t* dims, int levels, int stop_level,
                             uint64_t* bytes);
 
+/* ---- adaptive stop decision ---------------------------------------------
+ * choose_stop (adaptive.hpp:99-104; anchor_step 8, choose_stop_full: 2) on a
+ * level block already in device memory (natural row-major order,
+ * level_dims extents): per sampled 3^d block estimate_block_errors
+ * (src/adaptive.cpp:74-138) on the GPU, the blocks summed in anchor order on
+ * the host.  interp_penalty[k - 1] (k = 1..ndims) and lorenzo_penalty are
+ * the PenaltyModel's (adaptive.hpp:16-21); e the level's error bound.
+ * *stop = 1 when the Lorenzo estimate is lower (or the block is too small to
+ * sample), else 0; totals (optional) = {lorenzo, interp}.  Synchronous. */
+int mgrx_gpu_choose_stop(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* level_dims, const void* d_block,
+                         double e, const double* interp_penalty, double lorenzo_penalty, int anchor_step,
+                         double* totals, int* stop);
+
 /* ---- slab mode (one 3-D field sharded by slabs of axis-0 planes) -------
  * The reference has no distributed path; these are the per-pass pieces of
  * decompose_with / recompose (transform.hpp:485-530) for ONE fused 3-D level

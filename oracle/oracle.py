@@ -230,6 +230,20 @@ class Reference(_Lib):
         self._check(fn(len(d), dp, level, _ptr(field), corr.ctypes.data_as(_dp)))
         return field, corr.reshape(ld[level - 1])
 
+    def choose_stop(self, block, e, interp_penalty, lorenzo_penalty, step=8):
+        """The reference's accumulate_block_errors + choose_stop decision
+        (adaptive.hpp:51-104) on a natural-order level block: returns
+        (stop, lorenzo_total, interp_total)."""
+        block = np.ascontiguousarray(block)
+        d, dp = _dims(block.shape)
+        pen = np.ascontiguousarray(np.asarray(interp_penalty, dtype=np.float64))
+        tot = np.zeros(2)
+        stop = C.c_int(0)
+        fn = self._fn("choose_stop_" + self._sfx(block))
+        self._check(fn(len(d), dp, _ptr(block), C.c_double(e), pen.ctypes.data_as(_dp), C.c_double(lorenzo_penalty),
+                       int(step), tot.ctypes.data_as(_dp), C.byref(stop)))
+        return bool(stop.value), float(tot[0]), float(tot[1])
+
     def reorder_pack(self, field, stop=0):
         field = np.ascontiguousarray(field, dtype=np.float64)
         d, dp = _dims(field.shape)

@@ -15,6 +15,7 @@
 #include <span>
 #include <vector>
 
+#include "mgrx/adaptive.hpp"
 #include "mgrx/grid.hpp"
 #include "mgrx/quantize.hpp"
 #include "mgrx/reference.hpp"
@@ -172,9 +173,37 @@ int level_step_t(int nd, const uint64_t* dims, int level, T* field, double* corr
   });
 }
 
+// The adaptive stop decision's sampled totals (accumulate_block_errors,
+// adaptive.hpp:51-94) and decision (choose_stop, :99-104).
+template <typename T>
+int choose_stop_t(int nd, const uint64_t* dims, const T* data, double e, const double* interp_pen,
+                  double lorenzo_pen, int step, double* totals, int* stop) {
+  return guarded([&] {
+    const mgrx::Dims dl = to_dims(nd, dims);
+    mgrx::BlockView<const T> v{data, dl, mgrx::row_major_strides(dl)};
+    mgrx::PenaltyModel m;
+    m.lorenzo = lorenzo_pen;
+    m.interp.assign(interp_pen, interp_pen + nd);
+    mgrx::BlockErrors total;
+    const bool any = mgrx::detail::accumulate_block_errors(v, static_cast<std::size_t>(step), e, m, total);
+    totals[0] = total.lorenzo;
+    totals[1] = total.interp;
+    *stop = any ? (total.lorenzo < total.interp ? 1 : 0) : 1;
+  });
+}
+
 } // namespace
 
 extern "C" {
+
+int ref_choose_stop_f32(int nd, const uint64_t* dims, const float* data, double e, const double* interp_pen,
+                        double lorenzo_pen, int step, double* totals, int* stop) {
+  return choose_stop_t<float>(nd, dims, data, e, interp_pen, lorenzo_pen, step, totals, stop);
+}
+int ref_choose_stop_f64(int nd, const uint64_t* dims, const double* data, double e, const double* interp_pen,
+                        double lorenzo_pen, int step, double* totals, int* stop) {
+  return choose_stop_t<double>(nd, dims, data, e, interp_pen, lorenzo_pen, step, totals, stop);
+}
 
 const char* ref_last_error() { return g_msg; }
 

@@ -341,6 +341,42 @@ def recompose_nonuniform(coeffs: MultilevelCoefficients, coords, ws: Optional[So
 
 # -------------------------------------------------------------- quantize
 
+# ------------------------------------------------------ adaptive stop
+
+@dataclass
+class PenaltyModel:
+    """adaptive.hpp:16-21 (the calibrated 3-D constants by default; other
+    ranks take the reference's estimate_penalty_factors values)."""
+
+    lorenzo: float = 1.22
+    interp: tuple = (0.518, 0.366, 0.259)
+
+
+def choose_stop(level_block, e: float, model: Optional[PenaltyModel] = None, anchor_step: int = 8,
+                ws: Optional[SolverWorkspace] = None, return_totals: bool = False):
+    """choose_stop (adaptive.hpp:99-104) on a level block in device memory
+    (CUDA tensor, natural order): True = stop here (the Lorenzo estimate is
+    lower).  anchor_step 2 is choose_stop_full.  The sampled blocks'
+    estimates run on the GPU; the totals are bit-identical to the
+    reference's."""
+    ws = _ws(ws)
+    model = model or PenaltyModel()
+    _require_cuda(level_block, "level_block")
+    d = level_block.dim()
+    if len(model.interp) < d:
+        raise Error(15, "penalty model rank too small")
+    pen = (C.c_double * d)(*[float(x) for x in model.interp[:d]])
+    tot = (C.c_double * 2)()
+    stop = C.c_int(0)
+    ws._bind_stream()
+    _check(lib.mgrx_gpu_choose_stop(ws.handle, _dtype_code(level_block), d, _dims_arr(level_block.shape),
+                                    C.c_void_p(level_block.data_ptr()), float(e), pen, float(model.lorenzo),
+                                    int(anchor_step), tot, C.byref(stop)), ws.handle)
+    if return_totals:
+        return bool(stop.value), float(tot[0]), float(tot[1])
+    return bool(stop.value)
+
+
 class QuantMode(enum.IntEnum):  # quantize.hpp:14
     uniform = 0
     levelwise = 1

@@ -242,6 +242,11 @@ struct mgrx_gpu_ctx {
   cudaStream_t chain_lo = nullptr;  // low priority variant of the chain (MGRX_REC_PRIO=2)
   cudaEvent_t fork = nullptr, join = nullptr;
   std::vector<cudaEvent_t> lvl_done;
+  // adaptive stop decision: per-block sums (device) and their host copy
+  double* stop_dev = nullptr;
+  size_t stop_dev_bytes = 0;
+  double* stop_host = nullptr;
+  size_t stop_host_bytes = 0;
 };
 
 namespace {
@@ -748,6 +753,8 @@ int mgrx_gpu_ctx_destroy(mgrx_gpu_ctx* c) {
   if (c->fork) cudaEventDestroy(c->fork);
   if (c->join) cudaEventDestroy(c->join);
   for (cudaEvent_t e : c->lvl_done) cudaEventDestroy(e);
+  if (c->stop_dev) cudaFree(c->stop_dev);
+  if (c->stop_host) cudaFreeHost(c->stop_host);
   delete c;
   return MGRX_OK;
 }
@@ -1065,6 +1072,54 @@ int mgrx_host_decompose(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims
 int mgrx_host_recompose(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
                         const void* h_coeffs, void* h_field) {
   return host_roundtrip(c, dtype, nd, dims, levels, stop, h_coeffs, h_field, false);
+}
+
+// ---- adaptive stop decision ------------------------
+
+int mgrx_gpu_choose_stop(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* level_dims, const void* d_block,
+                         double e, const double* interp_penalty, double lorenzo_penalty, int anchor_step,
+                         double* totals, int* stop) {
+  return guarded(c, [&] {
+    if (!level_dims || !d_block || !interp_penalty || !stop) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    if (nd < 1 || nd > kMaxD) fail(MGRX_INVALID_DIMS, "choose_stop: rank out of range");
+    if (anchor_step < 1) fail(MGRX_INVALID_ARGUMENT, "choose_stop: anchor step must be positive");
+    int64_t ext[kMaxD];
+    for (int i = 0; i < nd; ++i) ext[i] = int64_t(level_dims[i]);
+    const int64_t nb = stop_blocks(nd, ext, anchor_step);
+    double tot[2] = {0.0, 0.0};
+    if (nb == 0) {  // too small to sample: stop (choose_stop, adaptive.hpp:101)
+      *stop = 1;
+    } else {
+      const size_t bytes = size_t(nb) * 2 * sizeof(double);
+      ensure(reinterpret_cast<void**>(&c->stop_dev), &c->stop_dev_bytes, bytes, c, "cudaMalloc(stop)");
+      if (c->stop_host_bytes < bytes) {
+        if (c->stop_host) cudaFreeHost(c->stop_host);
+        c->stop_host = nullptr;
+        c->stop_host_bytes = 0;
+        cuda_check(cudaMallocHost(reinterpret_cast<void**>(&c->stop_host), bytes), "cudaMallocHost(stop)");
+        c->stop_host_bytes = bytes;
+      }
+      cudaError_t err;
+      if (dtype == MGRX_F32)
+        err = block_errors<float>(static_cast<const float*>(d_block), nd, ext, anchor_step, e, interp_penalty,
+                                  lorenzo_penalty, c->stop_dev, exec(c));
+      else
+        err = block_errors<double>(static_cast<const double*>(d_block), nd, ext, anchor_step, e, interp_penalty,
+                                   lorenzo_penalty, c->stop_dev, exec(c));
+      cuda_check(err, "choose_stop");
+      cuda_check(cudaMemcpyAsync(c->stop_host, c->stop_dev, bytes, cudaMemcpyDeviceToHost, c->stream), "D2H");
+      cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+      for (int64_t b = 0; b < nb; ++b) {  // total += block, in anchor order (adaptive.hpp:77-79)
+        tot[0] += c->stop_host[2 * b];
+        tot[1] += c->stop_host[2 * b + 1];
+      }
+      *stop = tot[0] < tot[1] ? 1 : 0;
+    }
+    if (totals) {
+      totals[0] = tot[0];
+      totals[1] = tot[1];
+    }
+  });
 }
 
 // ---- slab mode ------------------------------------------

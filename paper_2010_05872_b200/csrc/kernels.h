@@ -24,6 +24,14 @@ cudaError_t general_recompose_level(const T* shell, T* coarse, T* fine, double* 
 template <typename T>
 cudaError_t apply_correction(T* coarse, const double* z, int64_t n, double sign, const Exec& ex);
 
+// ---- adaptive stop decision (adaptive.cu) -----------------------------------
+// Sampled 3^d blocks of a level block (anchor step `step`): their count, and
+// per block the (lorenzo, interp) sums of estimate_block_errors into out.
+int64_t stop_blocks(int d, const int64_t* ext, int step);
+template <typename T>
+cudaError_t block_errors(const T* blk, int d, const int64_t* ext, int step, double e, const double* interp_pen,
+                         double lorenzo_pen, double* out, const Exec& ex);
+
 // ---- tail: all small levels in one CTA (general.cu) -------------------------
 size_t tail_smem_bytes(int64_t nmax, int esize);
 size_t tail_level_bytes();
