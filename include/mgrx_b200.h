@@ -182,6 +182,19 @@ int mgrx_gpu_choose_stop(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t
                          double e, const double* interp_penalty, double lorenzo_penalty, int anchor_step,
                          double* totals, int* stop);
 
+/* decompose_with (transform.hpp:485-506) with the reference's adaptive
+ * decider — compress(adaptive) (pipeline.hpp:148-156) — on host buffers,
+ * the level blocks staying on the device: before level l (L..min_stop+1),
+ * mgrx_gpu_choose_stop with e_per_level[l], interp_penalty[l * ndims ..]
+ * and lorenzo_penalty[l] (arrays indexed by level, L + 1 entries; the
+ * caller evaluates penalty_model_for per level, adaptive.cpp:55-72) decides
+ * whether to stop there.  h_out receives the level-centric buffer of the
+ * whole field (coarse block of the stop level first), *stop_level the stop. */
+int mgrx_host_decompose_adaptive(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels,
+                                 const void* h_field, const double* e_per_level, const double* interp_penalty,
+                                 const double* lorenzo_penalty, int anchor_step, int min_stop_level, void* h_out,
+                                 int* stop_level);
+
 /* ---- slab mode (one 3-D field sharded by slabs of axis-0 planes) -------
  * The reference has no distributed path; these are the per-pass pieces of
  * decompose_with / recompose (transform.hpp:485-530) for ONE fused 3-D level

@@ -12,7 +12,8 @@
 //   mgrx::quantize_tail    (quantize.hpp:99)       mgrx::b200::quantize_tail
 //   mgrx::dequantize       (quantize.hpp:118)      mgrx::b200::dequantize
 //   mgrx::dequantize_tail  (quantize.hpp:137)      mgrx::b200::dequantize_tail
-//   mgrx::compress         (pipeline.hpp:130)      mgrx::b200::compress   (fixed, forced or adaptive stop)
+//   mgrx::compress         (pipeline.hpp:130)      mgrx::b200::compress   (fixed, forced or adaptive stop; the
+//                                                   adaptive decider runs on the GPU: decompose_adaptive)
 //   mgrx::decompress_field (pipeline.hpp:198)      mgrx::b200::decompress_field
 //   mgrx::SolverWorkspace  (transform.hpp:48)      mgrx::b200::Workspace  (owns the GPU context)
 //
@@ -212,9 +213,38 @@ void dequantize_tail(std::span<T> buffer, const LabelStream<T>& stream, const Gr
   detail::dequantize_impl<T>(buffer, stream, h, stop_level, plan, ws);
 }
 
+// decompose_with + the reference's adaptive decider (compress,
+// pipeline.hpp:148-156) with the level blocks kept on the GPU: the
+// per-level penalty models come from the reference's penalty_model_for
+// (adaptive.cpp:55-72, host, cached); choose_stop's sampled estimate runs on
+// the GPU (mgrx_host_decompose_adaptive, bit-identical totals).
+template <typename T>
+MultilevelCoefficients<T> decompose_adaptive(const TensorField<T>& field, const GridHierarchy& h,
+                                             const QuantizationPlan& plan, std::uint64_t seed, Workspace& ws) {
+  const int L = h.num_levels();
+  const int d = static_cast<int>(field.dims.size());
+  std::vector<double> e(L + 1, 0.0), pen(size_t(L + 1) * d, 0.0), lz(L + 1, 0.0);
+  for (int l = 1; l <= L; ++l) {
+    e[l] = plan.bin_widths[static_cast<std::size_t>(l)] / 2.0;
+    const double kappa = plan.bin_widths[static_cast<std::size_t>(l)] / plan.bin_widths[static_cast<std::size_t>(l - 1)];
+    const PenaltyModel& m = penalty_model_for(d, kappa, seed);
+    if (static_cast<int>(m.interp.size()) < d) fail(errc::invalid_input, "penalty model rank too small");
+    for (int i = 0; i < d; ++i) pen[size_t(l) * d + i] = m.interp[static_cast<std::size_t>(i)];
+    lz[l] = m.lorenzo;
+  }
+  const auto dd = detail::dims64(field.dims);
+  std::vector<T> out(h.total_count());
+  int stop = 0;
+  check(mgrx_host_decompose_adaptive(ws.get(), detail::dtype<T>(), d, dd.data(), L, field.data.data(), e.data(),
+                                     pen.data(), lz.data(), 8, 0, out.data(), &stop),
+        ws.get());
+  return MultilevelCoefficients<T>{std::move(out), h, stop};
+}
+
 // compress (pipeline.hpp:130-196) with the transform and quantizer on the
-// GPU.  The adaptive stop decision is the reference's own host heuristic
-// (choose_stop, adaptive.hpp:99-104) called through decompose_with.
+// GPU.  The adaptive stop decision is the reference's heuristic (choose_stop,
+// adaptive.hpp:99-104) evaluated on the GPU on the device-resident level
+// blocks (decompose_adaptive).
 template <typename T>
 std::vector<std::uint8_t> compress(const TensorField<T>& field, const CompressOptions& opt, Workspace& ws) {
   mgrx::detail::check_finite(field);
@@ -225,14 +255,7 @@ std::vector<std::uint8_t> compress(const TensorField<T>& field, const CompressOp
   if (stop < 0 || stop > L) fail(errc::invalid_level, "forced stop level out of range");
   std::optional<MultilevelCoefficients<T>> adaptive_coeffs;
   if (!opt.force_stop_level && opt.adaptive) {
-    const int d = static_cast<int>(field.dims.size());
-    StopDecider<T> decider = [&](int level, const BlockView<const T>& block) {
-      const double e_l = plan.bin_widths[static_cast<std::size_t>(level)] / 2.0;
-      const double kappa = plan.bin_widths[static_cast<std::size_t>(level)] /
-                           plan.bin_widths[static_cast<std::size_t>(level - 1)];
-      return choose_stop(block, e_l, penalty_model_for(d, kappa, opt.seed));
-    };
-    adaptive_coeffs = decompose_with(field, h, ws, decider);
+    adaptive_coeffs = decompose_adaptive(field, h, plan, opt.seed, ws);
     stop = adaptive_coeffs->stop_level;
   }
   Artifact a;

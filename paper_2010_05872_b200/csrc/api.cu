@@ -1074,6 +1074,83 @@ int mgrx_host_recompose(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims
   return host_roundtrip(c, dtype, nd, dims, levels, stop, h_coeffs, h_field, false);
 }
 
+}  // extern "C"
+
+namespace {
+// decompose_with (transform.hpp:485-506) with the reference's adaptive
+// decider (choose_stop, adaptive.hpp:99-104) evaluated on the GPU: the level
+// blocks never leave the device.  Each level step decomposes the level block
+// as a field of l levels stopped at l - 1 (the same arithmetic as the full
+// decompose, and as the host decompose_with of include/mgrx_b200.hpp).
+template <typename T>
+void decompose_adaptive_impl(mgrx_gpu_ctx* c, int nd, const uint64_t* dims, int levels, const T* h_field,
+                             const double* e_lvl, const double* pen_lvl, const double* lz_lvl, int step,
+                             int min_stop, T* h_out, int* stop_out) {
+  const Hierarchy h = make_hierarchy(nd, dims, levels);
+  const int L = h.L;
+  if (min_stop < 0 || min_stop > L) fail(MGRX_INVALID_LEVEL, "stop level out of range");
+  const int code = sizeof(T) == 4 ? MGRX_F32 : MGRX_F64;
+  const size_t N = size_t(h.node[L]);
+  T *blk = nullptr, *nxt = nullptr, *out = nullptr;
+  cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&blk), N * sizeof(T), c->stream), "cudaMalloc");
+  cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&nxt), N * sizeof(T), c->stream), "cudaMalloc");
+  cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&out), N * sizeof(T), c->stream), "cudaMalloc");
+  struct Free {
+    mgrx_gpu_ctx* c;
+    void* p[3];
+    ~Free() {
+      for (void* q : p)
+        if (q) cudaFreeAsync(q, c->stream);
+    }
+  } fr{c, {blk, nxt, out}};
+  cuda_check(cudaMemcpyAsync(blk, h_field, N * sizeof(T), cudaMemcpyHostToDevice, c->stream), "H2D");
+  int stop = min_stop;
+  for (int l = L; l > min_stop; --l) {
+    uint64_t dl[kMaxD];
+    for (int i = 0; i < nd; ++i) dl[i] = uint64_t(h.dims[l][i]);
+    int st = 0;
+    const int rc = mgrx_gpu_choose_stop(c, code, nd, dl, blk, e_lvl[l], pen_lvl + size_t(l) * nd, lz_lvl[l], step,
+                                        nullptr, &st);
+    if (rc != MGRX_OK) fail(rc, "%s", c->last_error.c_str());
+    if (st) {
+      stop = l;
+      break;
+    }
+    Plan* p = get_plan(c, code, nd, dl, l, l - 1);
+    decompose_impl<T>(c, *p, blk, nxt, nullptr);  // nxt = [coarse block of l - 1 | shell of level l]
+    const size_t nc = size_t(h.node[l - 1]), nl = size_t(h.node[l]);
+    cuda_check(cudaMemcpyAsync(out + nc, nxt + nc, (nl - nc) * sizeof(T), cudaMemcpyDeviceToDevice, c->stream),
+               "copy shell");
+    std::swap(blk, nxt);
+  }
+  cuda_check(cudaMemcpyAsync(out, blk, size_t(h.node[stop]) * sizeof(T), cudaMemcpyDeviceToDevice, c->stream),
+             "copy coarse");
+  cuda_check(cudaMemcpyAsync(h_out, out, N * sizeof(T), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  *stop_out = stop;
+}
+}  // namespace
+
+extern "C" {
+
+int mgrx_host_decompose_adaptive(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels,
+                                 const void* h_field, const double* e_per_level, const double* interp_penalty,
+                                 const double* lorenzo_penalty, int anchor_step, int min_stop_level, void* h_out,
+                                 int* stop_level) {
+  return guarded(c, [&] {
+    if (!dims || !h_field || !e_per_level || !interp_penalty || !lorenzo_penalty || !h_out || !stop_level)
+      fail(MGRX_INVALID_ARGUMENT, "null argument");
+    if (dtype == MGRX_F32)
+      decompose_adaptive_impl<float>(c, nd, dims, levels, static_cast<const float*>(h_field), e_per_level,
+                                     interp_penalty, lorenzo_penalty, anchor_step, min_stop_level,
+                                     static_cast<float*>(h_out), stop_level);
+    else
+      decompose_adaptive_impl<double>(c, nd, dims, levels, static_cast<const double*>(h_field), e_per_level,
+                                      interp_penalty, lorenzo_penalty, anchor_step, min_stop_level,
+                                      static_cast<double*>(h_out), stop_level);
+  });
+}
+
 // ---- adaptive stop decision ------------------------
 
 int mgrx_gpu_choose_stop(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* level_dims, const void* d_block,

@@ -129,6 +129,27 @@ void check_shape(const mgrx::Dims& dims, double tol) {
       ew = std::max(ew, std::fabs(double(rw.buffer[i]) - double(gw.buffer[i])));
     EXPECT(ew <= tol * range, "decompose_with (stop at %d) err %g", want, ew / range);
   }
+  // decompose_adaptive (choose_stop evaluated on the GPU on device-resident
+  // level blocks) against the reference's decompose_with + choose_stop
+  for (double rel : {1e-1, 1e-2, 1e-3, 1e-5}) {
+    const auto plan = mgrx::make_plan(mgrx::QuantMode::levelwise, rel * range, h);
+    const int d = int(dims.size());
+    std::vector<int> ref_levels;
+    mgrx::StopDecider<T> rdec = [&](int level, const mgrx::BlockView<const T>& b) {
+      const double e_l = plan.bin_widths[static_cast<size_t>(level)] / 2.0;
+      const double kappa = plan.bin_widths[static_cast<size_t>(level)] / plan.bin_widths[static_cast<size_t>(level - 1)];
+      return mgrx::choose_stop(b, e_l, mgrx::penalty_model_for(d, kappa, 0));
+    };
+    auto rw = mgrx::decompose_with(f, h, sws, rdec);
+    auto gw = mgrx::b200::decompose_adaptive(f, h, plan, 0, ws);
+    EXPECT(rw.stop_level == gw.stop_level, "decompose_adaptive stop %d vs reference %d (budget %g)", gw.stop_level,
+           rw.stop_level, rel);
+    double ea = 0.0;
+    for (size_t i = 0; i < rw.buffer.size(); ++i)
+      ea = std::max(ea, std::fabs(double(rw.buffer[i]) - double(gw.buffer[i])));
+    EXPECT(ea <= tol * range, "decompose_adaptive err %g (budget %g)", ea / range, rel);
+    std::printf("  adaptive budget %g: stop %d\n", rel, gw.stop_level);
+  }
   // adaptive compress (the reference's choose_stop decider) round trip
   mgrx::CompressOptions aopt;
   aopt.budget = 1e-3 * range / 4.0;
