@@ -350,7 +350,7 @@ def run_ours(args, ws, rank, local):
     # end-to-end through the host-buffer C-ABI entry points (pinned host
     # memory; H2D of the field + D2H of the coefficients for decompose, H2D
     # of the coefficients + D2H of the field for recompose, every step)
-    e2e = e2e_measure(mg, wsp, field, h, args)
+    e2e = e2e_measure(mg, wsp, field, h, args, workers=max(1, args.e2e_workers))
     quant = quant_measure(mg, wsp, field, h, args)
     batch = batch_measure(mg, field, h, args, dev)
 
@@ -619,6 +619,7 @@ def main():
                     help="field extents (config-2 generator); 1025,1025,1025 is BASELINE config 5b")
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--warmup-ref", type=int, default=0, help="untimed reference steps (CPU code needs none)")
+    ap.add_argument("--e2e-workers", type=int, default=2, help="host threads (contexts) of the e2e measurement")
     ap.add_argument("--slab", action="store_true",
                     help="slab mode: one field split along axis 0 over the ranks (NCCL transposes); strong scaling")
     ap.add_argument("--slab-emulate", type=int, default=1,
