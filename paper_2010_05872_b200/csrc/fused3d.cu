@@ -1120,7 +1120,10 @@ __global__ void __launch_bounds__(256, kRowCtas(NC)) k_f3_row(double* __restrict
   const int64_t step = int64_t(gridDim.x) * nw;
   int64_t r = int64_t(blockIdx.x) * nw + warp;
   double t[NC];
-  auto load = [&](int64_t row) {
+  // rows are walked from the last one down: the producer of G (plane pass)
+  // wrote the high planes last, so they are the likeliest L2 hits
+  auto load = [&](int64_t rr) {
+    const int64_t row = rows - 1 - rr;
     const double* gr = G + row * m + lane;
 #pragma unroll
     for (int k = 0; k < NC; ++k) t[k] = (lane + 32 * k < m) ? __ldcs(gr + 32 * k) : 0.0;
@@ -1133,7 +1136,7 @@ __global__ void __launch_bounds__(256, kRowCtas(NC)) k_f3_row(double* __restrict
     __syncwarp();
     if (r + step < rows) load(r + step);
     warp_row_thomas_reg<NC>(buf, m, tw, tid);
-    double* gr = G + r * m;
+    double* gr = G + (rows - 1 - r) * m;
 #pragma unroll
     for (int k = 0; k < NC; ++k)
       if (lane + 32 * k < m) gr[lane + 32 * k] = buf[lane + 32 * k];
@@ -1188,7 +1191,8 @@ __global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : (MAXT == kColT
     tw[i] = w[i];
     tid[i] = inv_d[i];
   }
-  const int64_t col = int64_t(blockIdx.x) * 16 + c16;
+  // tiles from the last one down (the previous pass wrote the high planes last)
+  const int64_t col = int64_t(gridDim.x - 1 - blockIdx.x) * 16 + c16;
   const bool valid = col < ncols;
   const int64_t base = valid ? (col / inner) * outer_stride + (col % inner) : 0;
   const int seg = (m + S - 1) / S;
