@@ -195,6 +195,16 @@ int mgrx_host_decompose_adaptive(mgrx_gpu_ctx* ctx, int dtype, int ndims, const 
                                  const double* lorenzo_penalty, int anchor_step, int min_stop_level, void* h_out,
                                  int* stop_level);
 
+/* ---- label entropy coding -------------------------------------------------
+ * encode_labels (src/huffman.cpp:209-255) of n device-resident labels: the
+ * reference's exact byte stream (min, range, code-length table, bit count,
+ * canonical Huffman codes bit-reversed and packed LSB-first) written to the
+ * host buffer h_out (capacity bytes; *out_size = the stream's size, also
+ * when it does not fit: MGRX_CAPACITY_EXCEEDED).  Histogram and bit packing
+ * run on the GPU, only the encoded bytes come back.  Synchronous. */
+int mgrx_gpu_encode_labels(mgrx_gpu_ctx* ctx, const int32_t* d_labels, uint64_t n, uint8_t* h_out, uint64_t capacity,
+                           uint64_t* out_size);
+
 /* ---- slab mode (one 3-D field sharded by slabs of axis-0 planes) -------
  * The reference has no distributed path; these are the per-pass pieces of
  * decompose_with / recompose (transform.hpp:485-530) for ONE fused 3-D level

@@ -230,6 +230,16 @@ class Reference(_Lib):
         self._check(fn(len(d), dp, level, _ptr(field), corr.ctypes.data_as(_dp)))
         return field, corr.reshape(ld[level - 1])
 
+    def encode_labels(self, labels):
+        """encode_labels (src/huffman.cpp:209-255) -> bytes."""
+        labels = np.ascontiguousarray(labels, dtype=np.int32)
+        cap = 32 + 4 * labels.size + (1 << 17) + 64
+        out = np.empty(cap, dtype=np.uint8)
+        size = C.c_uint64(0)
+        self._check(self._fn("encode_labels")(labels.ctypes.data_as(C.c_void_p), C.c_uint64(labels.size),
+                                              out.ctypes.data_as(C.c_void_p), C.c_uint64(cap), C.byref(size)))
+        return out[:size.value].tobytes()
+
     def choose_stop(self, block, e, interp_penalty, lorenzo_penalty, step=8):
         """The reference's accumulate_block_errors + choose_stop decision
         (adaptive.hpp:51-104) on a natural-order level block: returns

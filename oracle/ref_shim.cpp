@@ -17,6 +17,7 @@
 
 #include "mgrx/adaptive.hpp"
 #include "mgrx/grid.hpp"
+#include "mgrx/huffman.hpp"
 #include "mgrx/quantize.hpp"
 #include "mgrx/reference.hpp"
 #include "mgrx/reorder.hpp"
@@ -195,6 +196,16 @@ int choose_stop_t(int nd, const uint64_t* dims, const T* data, double e, const d
 } // namespace
 
 extern "C" {
+
+// encode_labels (huffman.hpp:14, src/huffman.cpp:209-255).
+int ref_encode_labels(const int32_t* labels, uint64_t n, uint8_t* out, uint64_t cap, uint64_t* size) {
+  return guarded([&] {
+    const std::vector<std::uint8_t> b = mgrx::encode_labels(std::span<const std::int32_t>(labels, n));
+    *size = b.size();
+    if (b.size() > cap) mgrx::fail(mgrx::errc::invalid_input, "capacity");
+    std::memcpy(out, b.data(), b.size());
+  });
+}
 
 int ref_choose_stop_f32(int nd, const uint64_t* dims, const float* data, double e, const double* interp_pen,
                         double lorenzo_pen, int step, double* totals, int* stop) {

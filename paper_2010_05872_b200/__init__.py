@@ -377,6 +377,26 @@ def choose_stop(level_block, e: float, model: Optional[PenaltyModel] = None, anc
     return bool(stop.value)
 
 
+def encode_labels(labels, ws: Optional[SolverWorkspace] = None) -> bytes:
+    """encode_labels (huffman.hpp:14): the reference's canonical-Huffman byte
+    stream of an int32 CUDA tensor of labels, histogram and bit packing on
+    the GPU (only the encoded bytes come to the host)."""
+    import torch
+
+    ws = _ws(ws)
+    _require_cuda(labels, "labels")
+    if labels.dtype != torch.int32:
+        raise Error(102, "labels must be int32")
+    n = labels.numel()
+    size = C.c_uint64(0)
+    cap = 16 + (1 << 17) + 4 * n + 64
+    buf = (C.c_uint8 * cap)()
+    ws._bind_stream()
+    _check(lib.mgrx_gpu_encode_labels(ws.handle, C.c_void_p(labels.data_ptr()), n, buf, cap, C.byref(size)),
+           ws.handle)
+    return bytes(buf[:size.value])
+
+
 class QuantMode(enum.IntEnum):  # quantize.hpp:14
     uniform = 0
     levelwise = 1

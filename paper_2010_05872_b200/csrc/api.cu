@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <queue>
 #include <memory>
 #include <string>
 #include <vector>
@@ -1196,6 +1197,167 @@ int mgrx_gpu_choose_stop(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* lev
       totals[0] = tot[0];
       totals[1] = tot[1];
     }
+  });
+}
+
+// ---- label entropy coding --------------------------
+
+}  // extern "C"
+
+namespace {
+// code_lengths (src/huffman.cpp:84-127): heap Huffman, the heap ordered by
+// (weight, node index) like the reference's priority_queue<pair, greater>.
+std::vector<int> huff_code_lengths(const std::vector<uint64_t>& freq) {
+  const size_t n = freq.size();
+  std::vector<int64_t> parent;
+  std::vector<int64_t> node_of(n, -1);
+  using Item = std::pair<uint64_t, size_t>;
+  std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
+  for (size_t s = 0; s < n; ++s)
+    if (freq[s]) {
+      node_of[s] = int64_t(parent.size());
+      heap.emplace(freq[s], parent.size());
+      parent.push_back(-1);
+    }
+  std::vector<int> lens(n, 0);
+  if (parent.empty()) return lens;
+  if (parent.size() == 1) {
+    for (size_t s = 0; s < n; ++s)
+      if (node_of[s] >= 0) lens[s] = 1;
+    return lens;
+  }
+  while (heap.size() > 1) {
+    const Item a = heap.top();
+    heap.pop();
+    const Item b = heap.top();
+    heap.pop();
+    const size_t node = parent.size();
+    parent.push_back(-1);
+    parent[a.second] = int64_t(node);
+    parent[b.second] = int64_t(node);
+    heap.emplace(a.first + b.first, node);
+  }
+  for (size_t s = 0; s < n; ++s) {
+    int64_t v = node_of[s];
+    if (v < 0) continue;
+    int len = 0;
+    while (parent[size_t(v)] >= 0) {
+      v = parent[size_t(v)];
+      ++len;
+    }
+    lens[s] = len;
+  }
+  return lens;
+}
+
+// canonicalize (:138-160) + the per-symbol reversed codes of encode_labels
+// (:228-236), packed as (reversed code << 6) | length.
+std::vector<unsigned long long> huff_codes(const std::vector<int>& lens) {
+  int max_len = 0;
+  for (int l : lens) max_len = std::max(max_len, l);
+  std::vector<unsigned long long> code(lens.size(), 0);
+  if (max_len == 0) return code;
+  if (max_len > 57) fail(MGRX_INVALID_INPUT, "code length too large");
+  std::vector<uint64_t> count(size_t(max_len) + 1, 0), first(size_t(max_len) + 1, 0);
+  for (int l : lens)
+    if (l > 0) ++count[size_t(l)];
+  uint64_t c = 0;
+  for (int l = 1; l <= max_len; ++l) {
+    c <<= 1;
+    first[size_t(l)] = c;
+    c += count[size_t(l)];
+  }
+  // canonical order: by length, then by symbol value
+  for (int l = 1; l <= max_len; ++l)
+    for (size_t s = 0; s < lens.size(); ++s)
+      if (lens[s] == l) {
+        const uint64_t cw = first[size_t(l)]++;
+        uint64_t r = 0;
+        for (int i = 0; i < l; ++i) r |= ((cw >> i) & 1ull) << (l - 1 - i);
+        code[s] = (r << 6) | uint64_t(l);
+      }
+  return code;
+}
+
+void put_le(uint8_t* p, uint64_t v, int bytes) {
+  for (int i = 0; i < bytes; ++i) p[i] = uint8_t(v >> (8 * i));
+}
+}  // namespace
+
+extern "C" {
+
+int mgrx_gpu_encode_labels(mgrx_gpu_ctx* c, const int32_t* d_labels, uint64_t n, uint8_t* h_out, uint64_t capacity,
+                           uint64_t* out_size) {
+  return guarded(c, [&] {
+    if (!out_size || (n && !d_labels)) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    if (n == 0) {  // min, range, bit count (huffman.cpp:211-216)
+      *out_size = 16;
+      if (capacity < 16 || !h_out) fail(MGRX_CAPACITY_EXCEEDED, "output capacity %llu < 16", (unsigned long long)capacity);
+      std::memset(h_out, 0, 16);
+      return;
+    }
+    const Exec ex = exec(c);
+    struct Dev {
+      mgrx_gpu_ctx* c;
+      std::vector<void*> p;
+      void* get(size_t bytes) {
+        void* q = nullptr;
+        cuda_check(cudaMallocAsync(&q, bytes, c->stream), "cudaMallocAsync");
+        p.push_back(q);
+        return q;
+      }
+      ~Dev() {
+        for (void* q : p) cudaFreeAsync(q, c->stream);
+      }
+    } dev{c, {}};
+    int* d_mm = static_cast<int*>(dev.get(8));
+    cuda_check(label_minmax(d_labels, int64_t(n), d_mm, ex), "label min/max");
+    int mm[2];
+    cuda_check(cudaMemcpyAsync(mm, d_mm, 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+    const int lo = mm[0];
+    const int64_t range = int64_t(mm[1]) - lo + 1;
+    if (range > (int64_t(1) << 17)) fail(MGRX_INVALID_INPUT, "label alphabet too large");
+    auto* d_freq = static_cast<unsigned long long*>(dev.get(size_t(range) * 8));
+    cuda_check(label_hist(d_labels, int64_t(n), lo, int(range), d_freq, ex), "label histogram");
+    std::vector<uint64_t> freq(static_cast<size_t>(range));
+    cuda_check(cudaMemcpyAsync(freq.data(), d_freq, size_t(range) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+    const std::vector<int> lens = huff_code_lengths(freq);
+    const std::vector<unsigned long long> code = huff_codes(lens);
+    uint64_t nbits = 0;
+    for (size_t s = 0; s < freq.size(); ++s) nbits += freq[s] * uint64_t(lens[s]);
+    const uint64_t hdr = 8 + uint64_t(range) + 8, payload = (nbits + 7) / 8;
+    *out_size = hdr + payload;
+    if (!h_out || capacity < *out_size)
+      fail(MGRX_CAPACITY_EXCEEDED, "output capacity %llu < %llu", (unsigned long long)capacity,
+           (unsigned long long)*out_size);
+    auto* d_code = static_cast<unsigned long long*>(dev.get(size_t(range) * 8));
+    cuda_check(cudaMemcpyAsync(d_code, code.data(), size_t(range) * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+    const int64_t nch = enc_chunks(int64_t(n));
+    auto* d_cb = static_cast<unsigned long long*>(dev.get(size_t(nch) * 8));
+    cuda_check(label_chunk_bits(d_labels, int64_t(n), lo, d_code, d_cb, ex), "chunk bits");
+    std::vector<unsigned long long> cb(static_cast<size_t>(nch));
+    cuda_check(cudaMemcpyAsync(cb.data(), d_cb, size_t(nch) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+    unsigned long long acc = 0;
+    for (auto& v : cb) {  // exclusive scan of the chunks' bits
+      const unsigned long long t = v;
+      v = acc;
+      acc += t;
+    }
+    if (acc != nbits) fail(MGRX_CUDA_ERROR, "encode: bit count mismatch");
+    cuda_check(cudaMemcpyAsync(d_cb, cb.data(), size_t(nch) * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+    const uint64_t nwords = nbits / 64 + 2;
+    auto* d_words = static_cast<unsigned long long*>(dev.get(size_t(nwords) * 8));
+    cuda_check(label_emit(d_labels, int64_t(n), lo, d_code, d_cb, d_words, nwords, ex), "emit");
+    put_le(h_out, uint32_t(lo), 4);
+    put_le(h_out + 4, uint64_t(range), 4);
+    for (int64_t s = 0; s < range; ++s) h_out[8 + s] = uint8_t(lens[size_t(s)]);
+    put_le(h_out + 8 + range, nbits, 8);
+    if (payload)
+      cuda_check(cudaMemcpyAsync(h_out + hdr, d_words, size_t(payload), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
   });
 }
 

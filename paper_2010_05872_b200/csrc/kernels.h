@@ -32,6 +32,17 @@ template <typename T>
 cudaError_t block_errors(const T* blk, int d, const int64_t* ext, int step, double e, const double* interp_pen,
                          double lorenzo_pen, double* out, const Exec& ex);
 
+// ---- label entropy coding (huffman.cu) ---------------------------------------
+cudaError_t label_minmax(const int32_t* x, int64_t n, int* d_mm, const Exec& ex);
+cudaError_t label_hist(const int32_t* x, int64_t n, int lo, int range, unsigned long long* d_freq, const Exec& ex);
+int64_t enc_chunks(int64_t n);
+// d_code[s] = (reversed code << 6) | length
+cudaError_t label_chunk_bits(const int32_t* x, int64_t n, int lo, const unsigned long long* d_code,
+                             unsigned long long* d_chunk_bits, const Exec& ex);
+cudaError_t label_emit(const int32_t* x, int64_t n, int lo, const unsigned long long* d_code,
+                       const unsigned long long* d_chunk_off, unsigned long long* d_words, uint64_t nwords,
+                       const Exec& ex);
+
 // ---- tail: all small levels in one CTA (general.cu) -------------------------
 size_t tail_smem_bytes(int64_t nmax, int esize);
 size_t tail_level_bytes();

@@ -1,0 +1,60 @@
+"""Label entropy coding on the GPU: encode_labels of
+device-resident labels must produce the reference's byte stream
+(src/huffman.cpp:209-255) exactly — same code lengths (heap order), same
+canonical codes, same bit packing."""
+import numpy as np
+import pytest
+
+from oracle.oracle import Reference
+
+
+@pytest.fixture(scope="module")
+def ref():
+    return Reference()
+
+
+def _labels(kind, n, seed):
+    rng = np.random.default_rng(seed)
+    if kind == "laplace":
+        return np.rint(rng.laplace(0, 3, n)).astype(np.int32)
+    if kind == "wide":
+        return rng.integers(-60000, 60000, n).astype(np.int32)
+    if kind == "single":
+        return np.full(n, -7, np.int32)
+    if kind == "two":
+        return rng.choice(np.array([5, 9], np.int32), n, p=[0.9, 0.1])
+    if kind == "skewed":  # long codes
+        return np.minimum(rng.geometric(0.5, n), 45).astype(np.int32) - 20
+    raise ValueError(kind)
+
+
+def test_reference_encode_binding(ref):
+    assert ref.encode_labels(np.zeros(0, np.int32)) == bytes(16)
+    b = ref.encode_labels(np.array([1, 1, 2, 3], np.int32))
+    assert b[:4] == (1).to_bytes(4, "little") and b[4:8] == (3).to_bytes(4, "little")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["laplace", "wide", "single", "two", "skewed"])
+@pytest.mark.parametrize("n", [1, 31, 4096, 4097, 100003, 3_000_001])
+def test_gpu_encode_labels_matches_reference(ref, kind, n):
+    import torch
+
+    import paper_2010_05872_b200 as mg
+
+    x = _labels(kind, n, n)
+    want = ref.encode_labels(x)
+    got = mg.encode_labels(torch.from_numpy(x).cuda())
+    assert got == want
+
+
+@pytest.mark.gpu
+def test_gpu_encode_empty_and_alphabet_limit(ref):
+    import torch
+
+    import paper_2010_05872_b200 as mg
+
+    assert mg.encode_labels(torch.zeros(0, dtype=torch.int32, device="cuda")) == bytes(16)
+    with pytest.raises(mg.Error) as e:
+        mg.encode_labels(torch.tensor([0, 1 << 17], dtype=torch.int32, device="cuda"))
+    assert e.value.status == 15  # 1 + errc::invalid_input (label alphabet too large)
