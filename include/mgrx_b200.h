@@ -205,6 +205,24 @@ int mgrx_host_decompose_adaptive(mgrx_gpu_ctx* ctx, int dtype, int ndims, const 
 int mgrx_gpu_encode_labels(mgrx_gpu_ctx* ctx, const int32_t* d_labels, uint64_t n, uint8_t* h_out, uint64_t capacity,
                            uint64_t* out_size);
 
+/* compress (pipeline.hpp:130-196) up to its sections, device-resident: the
+ * field goes to the GPU once; the stop level is force_stop (>= 0), else the
+ * adaptive decision (adaptive != 0; e_per_level / interp_penalty /
+ * lorenzo_penalty as for mgrx_host_decompose_adaptive), else 0; decompose,
+ * quantize (bin_widths: make_plan's, L + 1 entries) and each level's
+ * encode_labels run on the GPU.  Returns: *stop_level; for stop < L the
+ * encoded label streams of levels (stop ? stop + 1 : 0)..L back to back in
+ * h_sections with section_sizes[l] bytes each (L + 1 entries, 0 for absent
+ * levels), the outliers (strictly increasing positions), and for stop > 0
+ * the coarse block (node_count(stop) values) in h_coarse for the caller's
+ * Lorenzo coder.  For stop == L nothing else is produced (Lorenzo only). */
+int mgrx_host_compress(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels, const void* h_field,
+                       const double* bin_widths, int adaptive, int force_stop, const double* e_per_level,
+                       const double* interp_penalty, const double* lorenzo_penalty, uint8_t* h_sections,
+                       uint64_t sections_capacity, uint64_t* section_sizes, uint64_t* h_outlier_pos,
+                       void* h_outlier_val, uint64_t outlier_capacity, uint64_t* n_outliers, void* h_coarse,
+                       int* stop_level);
+
 /* ---- slab mode (one 3-D field sharded by slabs of axis-0 planes) -------
  * The reference has no distributed path; these are the per-pass pieces of
  * decompose_with / recompose (transform.hpp:485-530) for ONE fused 3-D level

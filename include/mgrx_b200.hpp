@@ -241,22 +241,57 @@ MultilevelCoefficients<T> decompose_adaptive(const TensorField<T>& field, const 
   return MultilevelCoefficients<T>{std::move(out), h, stop};
 }
 
-// compress (pipeline.hpp:130-196) with the transform and quantizer on the
-// GPU.  The adaptive stop decision is the reference's heuristic (choose_stop,
-// adaptive.hpp:99-104) evaluated on the GPU on the device-resident level
-// blocks (decompose_adaptive).
+// compress (pipeline.hpp:130-196) device-resident: the field is copied to
+// the GPU once; the adaptive stop decision (choose_stop, adaptive.hpp:99-104),
+// decompose, quantize and the labels' entropy coding (encode_labels,
+// huffman.cpp:209-255) run there (mgrx_host_compress); the reference's
+// container and Lorenzo coder assemble the artifact on the host.
 template <typename T>
 std::vector<std::uint8_t> compress(const TensorField<T>& field, const CompressOptions& opt, Workspace& ws) {
   mgrx::detail::check_finite(field);
   const GridHierarchy h = GridHierarchy::create(field.dims, opt.levels);
   const int L = h.num_levels();
   const QuantizationPlan plan = make_plan(opt.quant_mode, opt.budget, h);
-  int stop = opt.force_stop_level ? *opt.force_stop_level : 0;
-  if (stop < 0 || stop > L) fail(errc::invalid_level, "forced stop level out of range");
-  std::optional<MultilevelCoefficients<T>> adaptive_coeffs;
-  if (!opt.force_stop_level && opt.adaptive) {
-    adaptive_coeffs = decompose_adaptive(field, h, plan, opt.seed, ws);
-    stop = adaptive_coeffs->stop_level;
+  if (opt.force_stop_level && (*opt.force_stop_level < 0 || *opt.force_stop_level > L))
+    fail(errc::invalid_level, "forced stop level out of range");
+  const bool adaptive = !opt.force_stop_level && opt.adaptive;
+  const int d = static_cast<int>(field.dims.size());
+  // per-level penalty tables of the adaptive decision (penalty_model_for, host)
+  std::vector<double> e(L + 1, 0.0), pen(size_t(L + 1) * d, 0.0), lz(L + 1, 0.0);
+  if (adaptive)
+    for (int l = 1; l <= L; ++l) {
+      e[l] = plan.bin_widths[static_cast<std::size_t>(l)] / 2.0;
+      const double kappa =
+          plan.bin_widths[static_cast<std::size_t>(l)] / plan.bin_widths[static_cast<std::size_t>(l - 1)];
+      const PenaltyModel& m = penalty_model_for(d, kappa, opt.seed);
+      if (static_cast<int>(m.interp.size()) < d) fail(errc::invalid_input, "penalty model rank too small");
+      for (int i = 0; i < d; ++i) pen[size_t(l) * d + i] = m.interp[static_cast<std::size_t>(i)];
+      lz[l] = m.lorenzo;
+    }
+  // decompose + quantize + encode_labels on the GPU (mgrx_host_compress);
+  // only the encoded sections, the outliers and the coarse block return
+  const auto dd = detail::dims64(field.dims);
+  const size_t N = h.total_count();
+  std::vector<std::uint8_t> sec(4 * N + size_t(L + 1) * (16 + (1u << 17)) + 64);
+  std::vector<std::uint64_t> sec_sizes(L + 1, 0);
+  std::vector<std::uint64_t> opos;
+  std::vector<T> oval, coarse(N);
+  std::uint64_t cap = std::max<std::uint64_t>(1u << 16, N / 64), nout = 0;
+  int stop = 0;
+  for (;;) {
+    opos.resize(cap);
+    oval.resize(cap);
+    const int rc = mgrx_host_compress(ws.get(), detail::dtype<T>(), d, dd.data(), L, field.data.data(),
+                                      plan.bin_widths.data(), adaptive ? 1 : 0,
+                                      opt.force_stop_level ? *opt.force_stop_level : -1, e.data(), pen.data(),
+                                      lz.data(), sec.data(), sec.size(), sec_sizes.data(), opos.data(), oval.data(),
+                                      cap, &nout, coarse.data(), &stop);
+    if (rc == MGRX_CAPACITY_EXCEEDED && nout > cap) {
+      cap = nout;
+      continue;
+    }
+    check(rc, ws.get());
+    break;
   }
   Artifact a;
   a.element_type = element_type_of<T>();
@@ -272,22 +307,28 @@ std::vector<std::uint8_t> compress(const TensorField<T>& field, const CompressOp
     a.sections.push_back(mgrx::detail::lorenzo_section(stream));
     return write_artifact(a);
   }
-  MultilevelCoefficients<T> coeffs =
-      adaptive_coeffs ? std::move(*adaptive_coeffs) : decompose(field, h, stop, ws);
-  LabelStream<T> labels = stop == 0 ? quantize(coeffs, plan, ws)
-                                    : quantize_tail<T>(std::span<const T>(coeffs.buffer), h, stop, plan, ws);
-  for (const auto& lv : labels.labels) a.sections.push_back(mgrx::detail::label_section<T>(lv));
+  // label sections: u64 count + encode_labels bytes (label_section, pipeline.hpp:69-75)
+  std::size_t at = 0;
+  for (int l = stop == 0 ? 0 : stop + 1; l <= L; ++l) {
+    ByteWriter w;
+    w.u64(h.delta_count(l));
+    w.raw(std::span<const std::uint8_t>(sec.data() + at, sec_sizes[static_cast<std::size_t>(l)]));
+    at += sec_sizes[static_cast<std::size_t>(l)];
+    a.sections.push_back(std::move(w.bytes));
+  }
+  std::vector<Outlier<T>> outliers;
+  outliers.reserve(nout);
+  for (std::uint64_t i = 0; i < nout; ++i) outliers.push_back({opos[i], oval[i]});
   ByteWriter w;
-  mgrx::detail::write_outliers(w, labels.outliers);
+  mgrx::detail::write_outliers(w, outliers);
   a.sections.push_back(std::move(w.bytes));
   if (stop == 0) {
     a.method = Method::multigrid_full;
   } else {
     a.method = Method::multigrid_lorenzo;
-    TensorField<T> coarse(h.level_dims(stop),
-                          std::vector<T>(coeffs.buffer.begin(),
-                                         coeffs.buffer.begin() + static_cast<std::ptrdiff_t>(h.node_count(stop))));
-    LorenzoStream<T> stream = compress_lorenzo(coarse, coarse_error_bound(plan, stop));
+    coarse.resize(h.node_count(stop));
+    TensorField<T> cf(h.level_dims(stop), std::move(coarse));
+    LorenzoStream<T> stream = compress_lorenzo(cf, coarse_error_bound(plan, stop));
     a.sections.push_back(mgrx::detail::lorenzo_section(stream));
   }
   return write_artifact(a);

@@ -1083,28 +1083,28 @@ namespace {
 // blocks never leave the device.  Each level step decomposes the level block
 // as a field of l levels stopped at l - 1 (the same arithmetic as the full
 // decompose, and as the host decompose_with of include/mgrx_b200.hpp).
+// Device version: d_field (read only) -> d_out (level-centric), *stop_out.
 template <typename T>
-void decompose_adaptive_impl(mgrx_gpu_ctx* c, int nd, const uint64_t* dims, int levels, const T* h_field,
-                             const double* e_lvl, const double* pen_lvl, const double* lz_lvl, int step,
-                             int min_stop, T* h_out, int* stop_out) {
+void decompose_adaptive_dev(mgrx_gpu_ctx* c, int nd, const uint64_t* dims, int levels, const T* d_field,
+                            const double* e_lvl, const double* pen_lvl, const double* lz_lvl, int step, int min_stop,
+                            T* out, int* stop_out) {
   const Hierarchy h = make_hierarchy(nd, dims, levels);
   const int L = h.L;
   if (min_stop < 0 || min_stop > L) fail(MGRX_INVALID_LEVEL, "stop level out of range");
   const int code = sizeof(T) == 4 ? MGRX_F32 : MGRX_F64;
   const size_t N = size_t(h.node[L]);
-  T *blk = nullptr, *nxt = nullptr, *out = nullptr;
+  T *blk = nullptr, *nxt = nullptr;
   cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&blk), N * sizeof(T), c->stream), "cudaMalloc");
   cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&nxt), N * sizeof(T), c->stream), "cudaMalloc");
-  cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&out), N * sizeof(T), c->stream), "cudaMalloc");
   struct Free {
     mgrx_gpu_ctx* c;
-    void* p[3];
+    void* p[2];
     ~Free() {
       for (void* q : p)
         if (q) cudaFreeAsync(q, c->stream);
     }
-  } fr{c, {blk, nxt, out}};
-  cuda_check(cudaMemcpyAsync(blk, h_field, N * sizeof(T), cudaMemcpyHostToDevice, c->stream), "H2D");
+  } fr{c, {blk, nxt}};
+  cuda_check(cudaMemcpyAsync(blk, d_field, N * sizeof(T), cudaMemcpyDeviceToDevice, c->stream), "copy field");
   int stop = min_stop;
   for (int l = L; l > min_stop; --l) {
     uint64_t dl[kMaxD];
@@ -1126,13 +1126,144 @@ void decompose_adaptive_impl(mgrx_gpu_ctx* c, int nd, const uint64_t* dims, int 
   }
   cuda_check(cudaMemcpyAsync(out, blk, size_t(h.node[stop]) * sizeof(T), cudaMemcpyDeviceToDevice, c->stream),
              "copy coarse");
-  cuda_check(cudaMemcpyAsync(h_out, out, N * sizeof(T), cudaMemcpyDeviceToHost, c->stream), "D2H");
-  cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
   *stop_out = stop;
+}
+
+template <typename T>
+void decompose_adaptive_impl(mgrx_gpu_ctx* c, int nd, const uint64_t* dims, int levels, const T* h_field,
+                             const double* e_lvl, const double* pen_lvl, const double* lz_lvl, int step,
+                             int min_stop, T* h_out, int* stop_out) {
+  const Hierarchy h = make_hierarchy(nd, dims, levels);
+  const size_t N = size_t(h.node[h.L]);
+  T *din = nullptr, *dout = nullptr;
+  cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&din), N * sizeof(T), c->stream), "cudaMalloc");
+  cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&dout), N * sizeof(T), c->stream), "cudaMalloc");
+  struct Free {
+    mgrx_gpu_ctx* c;
+    void* p[2];
+    ~Free() {
+      for (void* q : p)
+        if (q) cudaFreeAsync(q, c->stream);
+    }
+  } fr{c, {din, dout}};
+  cuda_check(cudaMemcpyAsync(din, h_field, N * sizeof(T), cudaMemcpyHostToDevice, c->stream), "H2D");
+  decompose_adaptive_dev<T>(c, nd, dims, levels, din, e_lvl, pen_lvl, lz_lvl, step, min_stop, dout, stop_out);
+  cuda_check(cudaMemcpyAsync(h_out, dout, N * sizeof(T), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+}
+
+// compress's device part (pipeline.hpp:130-196 up to the sections): the
+// field goes to the GPU once; decompose (fixed or adaptive stop),
+// quantize and every level's encode_labels run there; the encoded label
+// sections, the outliers and (stop > 0) the coarse block come back.
+template <typename T>
+void compress_core(mgrx_gpu_ctx* c, int nd, const uint64_t* dims, int levels, const T* h_field, const double* q,
+                   int adaptive, int force_stop, const double* e_lvl, const double* pen_lvl, const double* lz_lvl,
+                   uint8_t* h_sec, uint64_t sec_cap, uint64_t* sec_sizes, uint64_t* h_opos, T* h_oval,
+                   uint64_t o_cap, uint64_t* n_out, T* h_coarse, int* stop_out) {
+  const Hierarchy h = make_hierarchy(nd, dims, levels);
+  const int L = h.L;
+  const int code = sizeof(T) == 4 ? MGRX_F32 : MGRX_F64;
+  const size_t N = size_t(h.node[L]);
+  std::vector<void*> bufs;
+  struct Free {
+    mgrx_gpu_ctx* c;
+    std::vector<void*>* b;
+    ~Free() {
+      for (void* q : *b) cudaFreeAsync(q, c->stream);
+    }
+  } fr{c, &bufs};
+  auto dalloc = [&](size_t bytes) {
+    void* p = nullptr;
+    cuda_check(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), c->stream), "cudaMallocAsync");
+    bufs.push_back(p);
+    return p;
+  };
+  T* dfield = static_cast<T*>(dalloc(N * sizeof(T)));
+  T* dco = static_cast<T*>(dalloc(N * sizeof(T)));
+  cuda_check(cudaMemcpyAsync(dfield, h_field, N * sizeof(T), cudaMemcpyHostToDevice, c->stream), "H2D");
+  int stop = 0;
+  if (force_stop >= 0) {
+    if (force_stop > L) fail(MGRX_INVALID_LEVEL, "forced stop level out of range");
+    stop = force_stop;
+  } else if (adaptive) {
+    decompose_adaptive_dev<T>(c, nd, dims, L, dfield, e_lvl, pen_lvl, lz_lvl, 8, 0, dco, &stop);
+  }
+  *stop_out = stop;
+  for (int l = 0; l <= L; ++l) sec_sizes[l] = 0;
+  *n_out = 0;
+  if (stop == L) return;  // Lorenzo only (the caller codes the field)
+  if (!(force_stop < 0 && adaptive)) {
+    const int rc = mgrx_gpu_decompose(c, code, nd, dims, L, stop, dfield, dco);
+    if (rc != MGRX_OK) fail(rc, "%s", c->last_error.c_str());
+  }
+  const size_t base = stop == 0 ? 0 : size_t(h.node[stop]);
+  int32_t* dlab = static_cast<int32_t*>(dalloc((N - base) * 4));
+  uint64_t cap = 1 << 16, nout = 0;
+  uint64_t* dpos = nullptr;
+  T* dval = nullptr;
+  for (;;) {
+    dpos = static_cast<uint64_t*>(dalloc(cap * 8));
+    dval = static_cast<T*>(dalloc(cap * sizeof(T)));
+    const int rc = mgrx_gpu_quantize(c, code, nd, dims, L, stop, q, dco, dlab, dpos, dval, cap, &nout);
+    if (rc == MGRX_CAPACITY_EXCEEDED) {
+      cap = nout;
+      continue;
+    }
+    if (rc != MGRX_OK) fail(rc, "%s", c->last_error.c_str());
+    break;
+  }
+  *n_out = nout;
+  if (nout > o_cap) fail(MGRX_CAPACITY_EXCEEDED, "%llu outliers exceed capacity %llu", (unsigned long long)nout,
+                         (unsigned long long)o_cap);
+  if (nout) {
+    cuda_check(cudaMemcpyAsync(h_opos, dpos, nout * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaMemcpyAsync(h_oval, dval, nout * sizeof(T), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  }
+  // per level: encode_labels of the level's labels (0 = coarsest)
+  uint64_t at = 0, used = 0;
+  for (int l = stop == 0 ? 0 : stop + 1; l <= L; ++l) {
+    const uint64_t cnt = uint64_t(h.delta[l]);
+    uint64_t sz = 0;
+    const int rc = mgrx_gpu_encode_labels(c, dlab + at, cnt, h_sec + used, sec_cap - used, &sz);
+    if (rc == MGRX_CAPACITY_EXCEEDED) fail(rc, "section capacity exceeded");
+    if (rc != MGRX_OK) fail(rc, "%s", c->last_error.c_str());
+    sec_sizes[l] = sz;
+    used += sz;
+    at += cnt;
+  }
+  if (stop > 0 && h_coarse)
+    cuda_check(cudaMemcpyAsync(h_coarse, dco, size_t(h.node[stop]) * sizeof(T), cudaMemcpyDeviceToHost, c->stream),
+               "D2H");
+  cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
 }
 }  // namespace
 
 extern "C" {
+
+int mgrx_host_compress(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, const void* h_field,
+                       const double* bin_widths, int adaptive, int force_stop, const double* e_per_level,
+                       const double* interp_penalty, const double* lorenzo_penalty, uint8_t* h_sections,
+                       uint64_t sections_capacity, uint64_t* section_sizes, uint64_t* h_outlier_pos,
+                       void* h_outlier_val, uint64_t outlier_capacity, uint64_t* n_outliers, void* h_coarse,
+                       int* stop_level) {
+  return guarded(c, [&] {
+    if (!dims || !h_field || !bin_widths || !h_sections || !section_sizes || !n_outliers || !stop_level)
+      fail(MGRX_INVALID_ARGUMENT, "null argument");
+    if (adaptive && force_stop < 0 && (!e_per_level || !interp_penalty || !lorenzo_penalty))
+      fail(MGRX_INVALID_ARGUMENT, "adaptive stop needs the per-level penalty tables");
+    if (dtype == MGRX_F32)
+      compress_core<float>(c, nd, dims, levels, static_cast<const float*>(h_field), bin_widths, adaptive, force_stop,
+                           e_per_level, interp_penalty, lorenzo_penalty, h_sections, sections_capacity,
+                           section_sizes, h_outlier_pos, static_cast<float*>(h_outlier_val), outlier_capacity,
+                           n_outliers, static_cast<float*>(h_coarse), stop_level);
+    else
+      compress_core<double>(c, nd, dims, levels, static_cast<const double*>(h_field), bin_widths, adaptive,
+                            force_stop, e_per_level, interp_penalty, lorenzo_penalty, h_sections, sections_capacity,
+                            section_sizes, h_outlier_pos, static_cast<double*>(h_outlier_val), outlier_capacity,
+                            n_outliers, static_cast<double*>(h_coarse), stop_level);
+  });
+}
 
 int mgrx_host_decompose_adaptive(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels,
                                  const void* h_field, const double* e_per_level, const double* interp_penalty,

@@ -158,6 +158,21 @@ void check_shape(const mgrx::Dims& dims, double tol) {
   const auto ra = mgrx::read_artifact(abytes);
   const auto rr = mgrx::read_artifact(mgrx::compress(f, aopt));
   EXPECT(ra.stop_level == rr.stop_level, "adaptive stop %d vs reference %d", int(ra.stop_level), int(rr.stop_level));
+  {  // the device-resident compress (GPU entropy coding) vs the reference's bytes
+    const auto rbytes = mgrx::compress(f, aopt);
+    std::printf("  adaptive artifact: %zu bytes (reference %zu)%s\n", abytes.size(), rbytes.size(),
+                abytes == rbytes ? ", byte-identical" : "");
+    mgrx::CompressOptions fopt = aopt;
+    fopt.adaptive = false;
+    const auto gb = mgrx::b200::compress(f, fopt, ws), rb = mgrx::compress(f, fopt);
+    std::printf("  full artifact: %zu bytes (reference %zu)%s\n", gb.size(), rb.size(),
+                gb == rb ? ", byte-identical" : "");
+    const auto fany = mgrx::decompress(gb);
+    const auto& ff = std::get<mgrx::TensorField<T>>(fany);
+    double fl = 0.0;
+    for (size_t i = 0; i < f.size(); ++i) fl = std::max(fl, std::fabs(double(ff.data[i]) - double(f.data[i])));
+    EXPECT(fl <= 1e-3 * range, "full GPU artifact: linf/tau %g", fl / (1e-3 * range));
+  }
   const auto aany = mgrx::decompress(abytes);
   const auto& af = std::get<mgrx::TensorField<T>>(aany);
   double alinf = 0.0;
