@@ -205,8 +205,17 @@ int mgrx_host_decompose_adaptive(mgrx_gpu_ctx* ctx, int dtype, int ndims, const 
 int mgrx_gpu_encode_labels(mgrx_gpu_ctx* ctx, const int32_t* d_labels, uint64_t n, uint8_t* h_out, uint64_t capacity,
                            uint64_t* out_size);
 
+/* check_finite (pipeline.hpp:113-118) + the value range in one read of n
+ * device values: min / max of the finite values (+inf / -inf when none) and
+ * the offset of the first non-finite value (n when all are finite).
+ * Synchronous. */
+int mgrx_gpu_field_stats(mgrx_gpu_ctx* ctx, int dtype, uint64_t n, const void* d_field, double* min_value,
+                         double* max_value, uint64_t* first_nonfinite);
+
 /* compress (pipeline.hpp:130-196) up to its sections, device-resident: the
- * field goes to the GPU once; the stop level is force_stop (>= 0), else the
+ * field's check_finite runs on the device copy (MGRX_NONFINITE_DATA with the
+ * reference's message); the field goes to the GPU once; the stop level is
+ * force_stop (>= 0), else the
  * adaptive decision (adaptive != 0; e_per_level / interp_penalty /
  * lorenzo_penalty as for mgrx_host_decompose_adaptive), else 0; decompose,
  * quantize (bin_widths: make_plan's, L + 1 entries) and each level's

@@ -248,7 +248,7 @@ MultilevelCoefficients<T> decompose_adaptive(const TensorField<T>& field, const 
 // container and Lorenzo coder assemble the artifact on the host.
 template <typename T>
 std::vector<std::uint8_t> compress(const TensorField<T>& field, const CompressOptions& opt, Workspace& ws) {
-  mgrx::detail::check_finite(field);
+  // check_finite (pipeline.hpp:132) runs on the GPU inside mgrx_host_compress
   const GridHierarchy h = GridHierarchy::create(field.dims, opt.levels);
   const int L = h.num_levels();
   const QuantizationPlan plan = make_plan(opt.quant_mode, opt.budget, h);

@@ -377,6 +377,19 @@ def choose_stop(level_block, e: float, model: Optional[PenaltyModel] = None, anc
     return bool(stop.value)
 
 
+def field_stats(field, ws: Optional[SolverWorkspace] = None):
+    """check_finite (pipeline.hpp:113-118) + range in one device read:
+    (min, max) of the finite values and the first non-finite offset (numel
+    when all are finite)."""
+    ws = _ws(ws)
+    _require_cuda(field, "field")
+    lo, hi, bad = C.c_double(0), C.c_double(0), C.c_uint64(0)
+    ws._bind_stream()
+    _check(lib.mgrx_gpu_field_stats(ws.handle, _dtype_code(field), field.numel(), C.c_void_p(field.data_ptr()),
+                                    C.byref(lo), C.byref(hi), C.byref(bad)), ws.handle)
+    return lo.value, hi.value, bad.value
+
+
 def encode_labels(labels, ws: Optional[SolverWorkspace] = None) -> bytes:
     """encode_labels (huffman.hpp:14): the reference's canonical-Huffman byte
     stream of an int32 CUDA tensor of labels, histogram and bit packing on

@@ -127,3 +127,62 @@ template cudaError_t block_errors<double>(const double*, int, const int64_t*, in
                                           double*, const Exec&);
 
 }  // namespace mgrx_b200
+
+// ---- field statistics --------------------------------
+// check_finite (pipeline.hpp:113-118) and the value range in one read of the
+// field: per block the min / max of the finite values and the first
+// non-finite offset; the host folds the blocks.
+namespace mgrx_b200 {
+namespace {
+template <typename T>
+__global__ void __launch_bounds__(256) k_field_stats(const T* __restrict__ x, int64_t n, double* __restrict__ bmin,
+                                                     double* __restrict__ bmax, unsigned long long* __restrict__ bbad) {
+  double lo = INFINITY, hi = -INFINITY;
+  unsigned long long bad = ~0ull;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const double v = double(x[i]);
+    if (isfinite(v)) {
+      lo = fmin(lo, v);
+      hi = fmax(hi, v);
+    } else if (bad == ~0ull) {
+      bad = (unsigned long long)i;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    const unsigned long long b = __shfl_xor_sync(0xffffffffu, bad, o);
+    bad = b < bad ? b : bad;
+  }
+  __shared__ double slo[8], shi[8];
+  __shared__ unsigned long long sbad[8];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    slo[w] = lo;
+    shi[w] = hi;
+    sbad[w] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < int(blockDim.x >> 5); ++k) {
+      lo = fmin(lo, slo[k]);
+      hi = fmax(hi, shi[k]);
+      bad = sbad[k] < bad ? sbad[k] : bad;
+    }
+    bmin[blockIdx.x] = lo;
+    bmax[blockIdx.x] = hi;
+    bbad[blockIdx.x] = bad;
+  }
+}
+}  // namespace
+
+int field_stats_blocks(int64_t n) { return grid_for(n, 256, 4); }
+
+template <typename T>
+cudaError_t field_stats(const T* x, int64_t n, double* bmin, double* bmax, unsigned long long* bbad, const Exec& ex) {
+  MGRX_LAUNCH(ex, "field_stats", k_field_stats<T><<<field_stats_blocks(n), 256, 0, ex.s>>>(x, n, bmin, bmax, bbad));
+  return cudaGetLastError();
+}
+template cudaError_t field_stats<float>(const float*, int64_t, double*, double*, unsigned long long*, const Exec&);
+template cudaError_t field_stats<double>(const double*, int64_t, double*, double*, unsigned long long*, const Exec&);
+}  // namespace mgrx_b200

@@ -1152,6 +1152,34 @@ void decompose_adaptive_impl(mgrx_gpu_ctx* c, int nd, const uint64_t* dims, int 
   cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
 }
 
+// Range and finiteness of n device values (check_finite, pipeline.hpp:113-118).
+template <typename T>
+void field_stats_run(mgrx_gpu_ctx* c, const T* d, int64_t n, double* lo, double* hi, uint64_t* first_bad) {
+  *lo = INFINITY;
+  *hi = -INFINITY;
+  *first_bad = uint64_t(n);
+  if (n <= 0) return;
+  const int nb = field_stats_blocks(n);
+  void* p = nullptr;
+  cuda_check(cudaMallocAsync(&p, size_t(nb) * 24, c->stream), "cudaMallocAsync");
+  double* bmin = static_cast<double*>(p);
+  double* bmax = bmin + nb;
+  auto* bbad = reinterpret_cast<unsigned long long*>(bmax + nb);
+  cudaError_t e = field_stats<T>(d, n, bmin, bmax, bbad, exec(c));
+  std::vector<double> h(size_t(nb) * 3);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), p, size_t(nb) * 24, cudaMemcpyDeviceToHost, c->stream);
+  cudaFreeAsync(p, c->stream);
+  cuda_check(e, "field stats");
+  cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  for (int b = 0; b < nb; ++b) {
+    *lo = std::min(*lo, h[size_t(b)]);
+    *hi = std::max(*hi, h[size_t(nb + b)]);
+    uint64_t bad;
+    std::memcpy(&bad, &h[size_t(2 * nb + b)], 8);
+    *first_bad = std::min<uint64_t>(*first_bad, bad);
+  }
+}
+
 // compress's device part (pipeline.hpp:130-196 up to the sections): the
 // field goes to the GPU once; decompose (fixed or adaptive stop),
 // quantize and every level's encode_labels run there; the encoded label
@@ -1182,6 +1210,12 @@ void compress_core(mgrx_gpu_ctx* c, int nd, const uint64_t* dims, int levels, co
   T* dfield = static_cast<T*>(dalloc(N * sizeof(T)));
   T* dco = static_cast<T*>(dalloc(N * sizeof(T)));
   cuda_check(cudaMemcpyAsync(dfield, h_field, N * sizeof(T), cudaMemcpyHostToDevice, c->stream), "H2D");
+  {  // check_finite (pipeline.hpp:132) on the device copy
+    double lo, hi;
+    uint64_t bad;
+    field_stats_run<T>(c, dfield, int64_t(N), &lo, &hi, &bad);
+    if (bad < N) fail(MGRX_NONFINITE_DATA, "non-finite value at offset %llu", (unsigned long long)bad);
+  }
   int stop = 0;
   if (force_stop >= 0) {
     if (force_stop > L) fail(MGRX_INVALID_LEVEL, "forced stop level out of range");
@@ -1240,6 +1274,19 @@ void compress_core(mgrx_gpu_ctx* c, int nd, const uint64_t* dims, int levels, co
 }  // namespace
 
 extern "C" {
+
+int mgrx_gpu_field_stats(mgrx_gpu_ctx* c, int dtype, uint64_t n, const void* d_field, double* min_value,
+                         double* max_value, uint64_t* first_nonfinite) {
+  return guarded(c, [&] {
+    if ((n && !d_field) || !min_value || !max_value || !first_nonfinite) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    if (dtype == MGRX_F32)
+      field_stats_run<float>(c, static_cast<const float*>(d_field), int64_t(n), min_value, max_value,
+                             first_nonfinite);
+    else
+      field_stats_run<double>(c, static_cast<const double*>(d_field), int64_t(n), min_value, max_value,
+                              first_nonfinite);
+  });
+}
 
 int mgrx_host_compress(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, const void* h_field,
                        const double* bin_widths, int adaptive, int force_stop, const double* e_per_level,

@@ -32,6 +32,11 @@ template <typename T>
 cudaError_t block_errors(const T* blk, int d, const int64_t* ext, int step, double e, const double* interp_pen,
                          double lorenzo_pen, double* out, const Exec& ex);
 
+// ---- field statistics (adaptive.cu): per block min / max / first non-finite
+int field_stats_blocks(int64_t n);
+template <typename T>
+cudaError_t field_stats(const T* x, int64_t n, double* bmin, double* bmax, unsigned long long* bbad, const Exec& ex);
+
 // ---- label entropy coding (huffman.cu) ---------------------------------------
 cudaError_t label_minmax(const int32_t* x, int64_t n, int* d_mm, const Exec& ex);
 cudaError_t label_hist(const int32_t* x, int64_t n, int lo, int range, unsigned long long* d_freq, const Exec& ex);

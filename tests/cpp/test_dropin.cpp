@@ -5,6 +5,7 @@
 // and that errors come back as mgrx::Error with the reference's errc.
 #include <cmath>
 #include <cstdio>
+#include <limits>
 #include <random>
 
 #include "mgrx/pipeline.hpp"
@@ -149,6 +150,17 @@ void check_shape(const mgrx::Dims& dims, double tol) {
       ea = std::max(ea, std::fabs(double(rw.buffer[i]) - double(gw.buffer[i])));
     EXPECT(ea <= tol * range, "decompose_adaptive err %g (budget %g)", ea / range, rel);
     std::printf("  adaptive budget %g: stop %d\n", rel, gw.stop_level);
+  }
+  {  // check_finite (pipeline.hpp:132) on the GPU: same error code as the reference
+    mgrx::TensorField<T> bad = f;
+    bad.data[bad.size() / 3] = std::numeric_limits<T>::quiet_NaN();
+    bool threw = false;
+    try {
+      mgrx::b200::compress(bad, opt, ws);
+    } catch (const mgrx::Error& e) {
+      threw = e.code() == mgrx::errc::nonfinite_data;
+    }
+    EXPECT(threw, "non-finite field: expected nonfinite_data");
   }
   // adaptive compress (the reference's choose_stop decider) round trip
   mgrx::CompressOptions aopt;

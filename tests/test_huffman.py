@@ -58,3 +58,19 @@ def test_gpu_encode_empty_and_alphabet_limit(ref):
     with pytest.raises(mg.Error) as e:
         mg.encode_labels(torch.tensor([0, 1 << 17], dtype=torch.int32, device="cuda"))
     assert e.value.status == 15  # 1 + errc::invalid_input (label alphabet too large)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_gpu_field_stats(dtype):
+    import torch
+
+    import paper_2010_05872_b200 as mg
+
+    x = torch.randn(1_000_003, dtype=getattr(torch, dtype), device="cuda")
+    lo, hi, bad = mg.field_stats(x)
+    assert lo == float(x.min()) and hi == float(x.max()) and bad == x.numel()
+    x[777_777] = float("inf")
+    x[900_001] = float("nan")
+    lo2, hi2, bad2 = mg.field_stats(x)
+    assert bad2 == 777_777 and lo2 == lo
