@@ -238,11 +238,11 @@ __device__ __forceinline__ StripLane strip_lane(int m2) {
 // Shared memory of the plane passes.  Decompose: a 4-slot ring of tile
 // planes (2 TI1 + 3 fine rows; an odd plane reads its two even neighbours in
 // place).  Recompose: a 3-slot ring of shell runs (even + odd rows).
-template <typename T, int TI1>
+template <typename T, int TI1, int NSD = 4>
 struct PlaneSmem {
   static constexpr int kRows = 2 * TI1 + 3;
   static constexpr int kDecRows = 2 * TI1 + 3;
-  static constexpr int kDecSlots = 4, kRecSlots = 4;
+  static constexpr int kDecSlots = NSD, kRecSlots = 4;
   static __host__ __device__ size_t raw_bytes(int64_t n2) {
     return (size_t(kRows) * size_t(n2) * sizeof(T) + 256 + 127) / 128 * 128;
   }
@@ -251,7 +251,7 @@ struct PlaneSmem {
   }
   static __host__ __device__ size_t ring_bytes(int64_t n2) {
     const size_t d = kDecSlots * dec_raw_bytes(n2), r = kRecSlots * raw_bytes(n2);
-    return d > r ? d : r;
+    return NSD != 4 ? d : (d > r ? d : r);  // the 3-slot variant is decompose-only
   }
   static __host__ __device__ size_t bytes(int64_t n2, int64_t m2) {
     size_t b = ring_bytes(n2);      // TMA ring of fine plane tiles / shell runs
@@ -637,11 +637,12 @@ __device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const
 
 // Decompose plane pass: one CTA per (axis-0 chunk, axis-1 tile) unit; the
 // unit's fine planes stream through a 3-deep TMA ring.
-template <typename T, int TI1, int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
+// NB = 3: the 3-CTAs-per-SM variant with a 3-slot ring (F3Geom::dec3)
+template <typename T, int TI1, int MAXT, int NB = 0>
+__global__ void __launch_bounds__(MAXT, NB ? NB : (MAXT == kPlaneMaxThreads ? 2 : 1))
     k_f3_dec_plane(const T* __restrict__ blk, T* __restrict__ shell, T* __restrict__ coarse, double* __restrict__ G,
                    const F3Geom g) {
-  using SM = PlaneSmem<T, TI1>;
+  using SM = PlaneSmem<T, TI1, NB == 3 ? 3 : 4>;
   constexpr int RMAX = SM::kRows;
   constexpr int NS = SM::kDecSlots;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -1278,6 +1279,10 @@ template <typename T, int TI1>
 size_t plane_smem(const F3Geom& g) {
   return PlaneSmem<T, TI1>::bytes(g.n2, g.m2);
 }
+template <typename T>
+size_t plane_smem3(const F3Geom& g) {
+  return PlaneSmem<T, 4, 3>::bytes(g.n2, g.m2);
+}
 
 // Row tile of the plane passes: maximise resident warps x useful-row
 // fraction (2 TI1 owned rows of 2 TI1 + 3 computed) within shared memory and
@@ -1304,6 +1309,12 @@ bool pick_tile(F3Geom& g, size_t optin, size_t per_sm) {
       g.ctas_per_sm = ctas;
     }
   }
+  // wide levels (8-9 warps per CTA, 4 coarse rows per tile): the decompose
+  // plane pass runs 3 CTAs per SM on a 3-slot ring (72 registers) — more
+  // independent plane streams per SM (MGRX_NO_DEC3 disables)
+  g.dec3 = 0;
+  static const bool no3 = std::getenv("MGRX_NO_DEC3") != nullptr;
+  if (!no3 && g.tile_rows == 4 && warps >= 8 && warps <= 9 && 3 * (plane_smem3<T>(g) + 1024) <= per_sm) g.dec3 = 1;
   return best > 0.0;
 }
 
@@ -1391,19 +1402,24 @@ Fused3DPlan fused3d_plan(const LevelGeom& lg, int esize) {
   // axis-0 chunk of a unit: a unit of c coarse planes streams 2c + 3 fine
   // planes (two halo planes are recomputed by the neighbour) plus a fixed
   // pipeline fill; pick c minimising waves x per-unit time.
-  int64_t chunk = 1;
-  double best = 1e300;
   double fill_planes = 3.0;  // pipeline fill of a unit, in plane-times (MGRX_FILL_PLANES overrides)
   if (const char* env = std::getenv("MGRX_FILL_PLANES")) fill_planes = std::atof(env);
-  for (int64_t c = 1; c <= 32 && c <= g.m0; ++c) {
-    const int64_t units = ((g.m0 + c - 1) / c) * g.ntile1;
-    const int64_t waves = (units + ctas - 1) / ctas;
-    const double cost = double(waves) * double(2 * c + 3 + fill_planes);
-    if (cost < best - 1e-9) {
-      best = cost;
-      chunk = c;
+  auto pick_chunk = [&](int64_t slots) {
+    int64_t ch = 1;
+    double best = 1e300;
+    for (int64_t c = 1; c <= 32 && c <= g.m0; ++c) {
+      const int64_t units = ((g.m0 + c - 1) / c) * g.ntile1;
+      const int64_t waves = (units + slots - 1) / slots;
+      const double cost = double(waves) * double(2 * c + 3 + fill_planes);
+      if (cost < best - 1e-9) {
+        best = cost;
+        ch = c;
+      }
     }
-  }
+    return ch;
+  };
+  int64_t chunk = pick_chunk(ctas);
+  if (g.dec3) g.dec_chunk = pick_chunk(int64_t(nsm) * 3);
   if (const char* env = std::getenv("MGRX_CHUNK")) chunk = std::max<int64_t>(1, std::min<int64_t>(g.m0, std::atoll(env)));
   const int64_t nchunk = (g.m0 + chunk - 1) / chunk;
   g.chunk = chunk;
@@ -1450,6 +1466,17 @@ static cudaError_t launch_interp(const T* shell, const T* coarse, T* fine, const
   return launch_interp_t<T, 4, kPlaneMaxThreads>(shell, coarse, fine, g, ex);
 }
 
+// The decompose plane pass's chunking for its 3-CTA variant.
+static F3Geom dec3_geom(const F3Geom& g) {
+  F3Geom gd = g;
+  if (g.dec_chunk > 0 && g.a_end < 0) {
+    gd.chunk = g.dec_chunk;
+    gd.units = int(((g.m0 + gd.chunk - 1) / gd.chunk) * g.ntile1);
+    gd.grid = gd.units;
+  }
+  return gd;
+}
+
 template <typename T>
 static cudaError_t set_attrs(const F3Geom& g, size_t* smem) {
   cudaError_t e = cudaSuccess;
@@ -1466,6 +1493,9 @@ static cudaError_t set_attrs(const F3Geom& g, size_t* smem) {
   MGRX_ATTR(4, kWideBound)
   MGRX_ATTR(2, kWideBound)
 #undef MGRX_ATTR
+  if (e == cudaSuccess && g.dec3)
+    e = cudaFuncSetAttribute(k_f3_dec_plane<T, 4, kPlaneMaxThreads, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(plane_smem3<T>(g)));
   return e;
 }
 
@@ -1478,7 +1508,7 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
   cudaError_t e = set_attrs<T>(g, &ds);
   if (e != cudaSuccess) return e;
 #define MGRX_DEC(TI, MT)                                                                               \
-  if (g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))                      \
+  if (!g.dec3 && g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))          \
     MGRX_LAUNCH(ex, "f3_dec_plane", pdl_launch(k_f3_dec_plane<T, TI, MT>, dim3(g.grid), dim3(g.threads), ds, \
                                                ex.s, !ex.prof, blk, shell, coarse, G, g));
   MGRX_DEC(4, kPlaneMaxThreads)
@@ -1486,6 +1516,11 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
   MGRX_DEC(4, kWideBound)
   MGRX_DEC(2, kWideBound)
 #undef MGRX_DEC
+  if (g.dec3) {
+    const F3Geom gd = dec3_geom(g);
+    MGRX_LAUNCH(ex, "f3_dec_plane", pdl_launch(k_f3_dec_plane<T, 4, kPlaneMaxThreads, 3>, dim3(gd.grid), dim3(gd.threads),
+                                               plane_smem3<T>(gd), ex.s, !ex.prof, blk, shell, coarse, G, gd));
+  }
   launch_row(G, g, th.w[2], th.inv_d[2], ex);
   launch_col<T>(G, nullptr, 0.0, g, 1, th.w[1], th.inv_d[1], ex);
   launch_col<T>(G, coarse, 1.0, g, 0, th.w[0], th.inv_d[0], ex);
@@ -1575,7 +1610,7 @@ cudaError_t fused3d_slab_dec_plane(const T* blk, T* shell, T* coarse, double* G,
   cudaError_t e = set_attrs<T>(g, &ds);
   if (e != cudaSuccess) return e;
 #define MGRX_DEC(TI, MT)                                                                               \
-  if (g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))                      \
+  if (!g.dec3 && g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))          \
     MGRX_LAUNCH(ex, "f3_dec_plane", pdl_launch(k_f3_dec_plane<T, TI, MT>, dim3(g.grid), dim3(g.threads), ds, \
                                                ex.s, !ex.prof, blk, shell, coarse, G, g));
   MGRX_DEC(4, kPlaneMaxThreads)
@@ -1583,6 +1618,9 @@ cudaError_t fused3d_slab_dec_plane(const T* blk, T* shell, T* coarse, double* G,
   MGRX_DEC(4, kWideBound)
   MGRX_DEC(2, kWideBound)
 #undef MGRX_DEC
+  if (g.dec3)
+    MGRX_LAUNCH(ex, "f3_dec_plane", pdl_launch(k_f3_dec_plane<T, 4, kPlaneMaxThreads, 3>, dim3(g.grid), dim3(g.threads),
+                                               plane_smem3<T>(g), ex.s, !ex.prof, blk, shell, coarse, G, g));
   return cudaGetLastError();
 }
 

@@ -19,6 +19,8 @@ struct F3Geom {
   int units = 0;                   // work units = chunks * ntile1
   int threads = 0;                 // plane-pass CTA size (strips of 30 coarse columns)
   int ctas_per_sm = 1;             // plane-pass CTAs resident per SM
+  int dec3 = 0;                    // decompose plane pass: the 3-CTA / 3-slot variant
+  int64_t dec_chunk = 0;           // its axis-0 chunk (units sized for 3 CTAs per SM)
   int grid = 0;                    // persistent plane-pass CTAs
   // slab mode: the plane passes cover coarse planes
   // [a_base, a_end), the interpolation fine planes [p_base, p_end)
