@@ -205,6 +205,16 @@ int mgrx_host_decompose_adaptive(mgrx_gpu_ctx* ctx, int dtype, int ndims, const 
 int mgrx_gpu_encode_labels(mgrx_gpu_ctx* ctx, const int32_t* d_labels, uint64_t n, uint8_t* h_out, uint64_t capacity,
                            uint64_t* out_size);
 
+/* compress_lorenzo (lorenzo.hpp:87-128) of a row-major block (host buffer,
+ * dims extents) with error bound e, on the GPU (hyperplane wavefront): the
+ * labels come back already entropy-coded (encode_labels' byte stream in
+ * h_enc, *enc_size bytes), the outliers in position order.  Bit-identical to
+ * the reference.  MGRX_CAPACITY_EXCEEDED (with the needed size / count set)
+ * when a buffer is too small.  Synchronous. */
+int mgrx_host_lorenzo(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, const void* h_block, double e,
+                      uint8_t* h_enc, uint64_t enc_capacity, uint64_t* enc_size, uint64_t* h_outlier_pos,
+                      void* h_outlier_val, uint64_t outlier_capacity, uint64_t* n_outliers);
+
 /* check_finite (pipeline.hpp:113-118) + the value range in one read of n
  * device values: min / max of the finite values (+inf / -inf when none) and
  * the offset of the first non-finite value (n when all are finite).

@@ -244,8 +244,46 @@ MultilevelCoefficients<T> decompose_adaptive(const TensorField<T>& field, const 
 // compress (pipeline.hpp:130-196) device-resident: the field is copied to
 // the GPU once; the adaptive stop decision (choose_stop, adaptive.hpp:99-104),
 // decompose, quantize and the labels' entropy coding (encode_labels,
-// huffman.cpp:209-255) run there (mgrx_host_compress); the reference's
-// container and Lorenzo coder assemble the artifact on the host.
+// huffman.cpp:209-255) run there (mgrx_host_compress), and the Lorenzo coder
+// of the coarse block too (lorenzo_section_gpu); the reference's container
+// assembles the artifact on the host.
+// lorenzo_section (pipeline.hpp:86-96) of compress_lorenzo(block, e)
+// (lorenzo.hpp:87-128) with the coder and its label entropy coding on the
+// GPU (mgrx_host_lorenzo, bit-identical); large blocks (> 2^24 values, the
+// one-CTA wavefront's limit of usefulness) use the reference's host coder.
+template <typename T>
+std::vector<std::uint8_t> lorenzo_section_gpu(const TensorField<T>& block, double e, Workspace& ws) {
+  const std::size_t N = block.size();
+  if (N > (std::size_t(1) << 24)) return mgrx::detail::lorenzo_section(compress_lorenzo(block, e));
+  const auto dd = detail::dims64(block.dims);
+  std::vector<std::uint8_t> enc(16 + (1u << 17) + 4 * N + 64);
+  std::uint64_t enc_size = 0, cap = std::max<std::uint64_t>(1u << 12, N / 64), nout = 0;
+  std::vector<std::uint64_t> pos;
+  std::vector<T> val;
+  for (;;) {
+    pos.resize(cap);
+    val.resize(cap);
+    const int rc = mgrx_host_lorenzo(ws.get(), detail::dtype<T>(), int(dd.size()), dd.data(), block.data.data(), e,
+                                     enc.data(), enc.size(), &enc_size, pos.data(), val.data(), cap, &nout);
+    if (rc == MGRX_CAPACITY_EXCEEDED && nout > cap) {
+      cap = nout;
+      continue;
+    }
+    check(rc, ws.get());
+    break;
+  }
+  ByteWriter w;
+  w.f64(e);
+  w.u64(N);
+  w.u64(enc_size);
+  w.raw(std::span<const std::uint8_t>(enc.data(), enc_size));
+  std::vector<Outlier<T>> outliers;
+  outliers.reserve(nout);
+  for (std::uint64_t i = 0; i < nout; ++i) outliers.push_back({pos[i], val[i]});
+  mgrx::detail::write_outliers(w, outliers);
+  return std::move(w.bytes);
+}
+
 template <typename T>
 std::vector<std::uint8_t> compress(const TensorField<T>& field, const CompressOptions& opt, Workspace& ws) {
   // check_finite (pipeline.hpp:132) runs on the GPU inside mgrx_host_compress
@@ -303,8 +341,7 @@ std::vector<std::uint8_t> compress(const TensorField<T>& field, const CompressOp
   a.bin_widths = plan.bin_widths;
   if (stop == L) {
     a.method = Method::lorenzo_only;
-    LorenzoStream<T> stream = compress_lorenzo(field, opt.budget);
-    a.sections.push_back(mgrx::detail::lorenzo_section(stream));
+    a.sections.push_back(lorenzo_section_gpu(field, opt.budget, ws));
     return write_artifact(a);
   }
   // label sections: u64 count + encode_labels bytes (label_section, pipeline.hpp:69-75)
@@ -328,8 +365,7 @@ std::vector<std::uint8_t> compress(const TensorField<T>& field, const CompressOp
     a.method = Method::multigrid_lorenzo;
     coarse.resize(h.node_count(stop));
     TensorField<T> cf(h.level_dims(stop), std::move(coarse));
-    LorenzoStream<T> stream = compress_lorenzo(cf, coarse_error_bound(plan, stop));
-    a.sections.push_back(mgrx::detail::lorenzo_section(stream));
+    a.sections.push_back(lorenzo_section_gpu(cf, coarse_error_bound(plan, stop), ws));
   }
   return write_artifact(a);
 }

@@ -230,6 +230,20 @@ class Reference(_Lib):
         self._check(fn(len(d), dp, level, _ptr(field), corr.ctypes.data_as(_dp)))
         return field, corr.reshape(ld[level - 1])
 
+    def lorenzo(self, block, e):
+        """compress_lorenzo (lorenzo.hpp:87-128) -> (labels, outlier positions, outlier values)."""
+        block = np.ascontiguousarray(block)
+        d, dp = _dims(block.shape)
+        labels = np.empty(block.size, np.int32)
+        cap = block.size
+        opos = np.empty(cap, np.uint64)
+        oval = np.empty(cap, block.dtype)
+        n = C.c_uint64(0)
+        fn = self._fn("lorenzo_" + self._sfx(block))
+        self._check(fn(len(d), dp, _ptr(block), C.c_double(e), labels.ctypes.data_as(C.c_void_p),
+                       opos.ctypes.data_as(C.c_void_p), _ptr(oval), C.c_uint64(cap), C.byref(n)))
+        return labels, opos[:n.value], oval[:n.value]
+
     def encode_labels(self, labels):
         """encode_labels (src/huffman.cpp:209-255) -> bytes."""
         labels = np.ascontiguousarray(labels, dtype=np.int32)

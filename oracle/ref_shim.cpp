@@ -18,6 +18,7 @@
 #include "mgrx/adaptive.hpp"
 #include "mgrx/grid.hpp"
 #include "mgrx/huffman.hpp"
+#include "mgrx/lorenzo.hpp"
 #include "mgrx/quantize.hpp"
 #include "mgrx/reference.hpp"
 #include "mgrx/reorder.hpp"
@@ -193,6 +194,24 @@ int choose_stop_t(int nd, const uint64_t* dims, const T* data, double e, const d
   });
 }
 
+// compress_lorenzo (lorenzo.hpp:87-128): labels, outliers.
+template <typename T>
+int lorenzo_t(int nd, const uint64_t* dims, const T* data, double e, int32_t* labels, uint64_t* opos, T* oval,
+              uint64_t cap, uint64_t* n_out) {
+  return guarded([&] {
+    mgrx::TensorField<T> f(to_dims(nd, dims));
+    std::memcpy(f.data.data(), data, f.size() * sizeof(T));
+    const mgrx::LorenzoStream<T> s = mgrx::compress_lorenzo(f, e);
+    std::memcpy(labels, s.labels.data(), s.labels.size() * 4);
+    *n_out = s.outliers.size();
+    if (s.outliers.size() > cap) mgrx::fail(mgrx::errc::invalid_input, "capacity");
+    for (std::size_t i = 0; i < s.outliers.size(); ++i) {
+      opos[i] = s.outliers[i].position;
+      oval[i] = s.outliers[i].value;
+    }
+  });
+}
+
 } // namespace
 
 extern "C" {
@@ -205,6 +224,15 @@ int ref_encode_labels(const int32_t* labels, uint64_t n, uint8_t* out, uint64_t 
     if (b.size() > cap) mgrx::fail(mgrx::errc::invalid_input, "capacity");
     std::memcpy(out, b.data(), b.size());
   });
+}
+
+int ref_lorenzo_f32(int nd, const uint64_t* dims, const float* data, double e, int32_t* labels, uint64_t* opos,
+                    float* oval, uint64_t cap, uint64_t* n_out) {
+  return lorenzo_t<float>(nd, dims, data, e, labels, opos, oval, cap, n_out);
+}
+int ref_lorenzo_f64(int nd, const uint64_t* dims, const double* data, double e, int32_t* labels, uint64_t* opos,
+                    double* oval, uint64_t cap, uint64_t* n_out) {
+  return lorenzo_t<double>(nd, dims, data, e, labels, opos, oval, cap, n_out);
 }
 
 int ref_choose_stop_f32(int nd, const uint64_t* dims, const float* data, double e, const double* interp_pen,

@@ -390,6 +390,27 @@ def field_stats(field, ws: Optional[SolverWorkspace] = None):
     return lo.value, hi.value, bad.value
 
 
+def lorenzo_encode(block, e: float, ws: Optional[SolverWorkspace] = None):
+    """compress_lorenzo (lorenzo.hpp:87-128) of a host numpy block on the GPU:
+    (encode_labels bytes of the labels, outlier positions, outlier values)."""
+    import numpy as np
+
+    ws = _ws(ws)
+    block = np.ascontiguousarray(block)
+    code = {np.dtype(np.float32): 0, np.dtype(np.float64): 1}[block.dtype]
+    n = block.size
+    enc = np.empty(16 + (1 << 17) + 4 * n + 64, np.uint8)
+    cap = max(n, 1)
+    opos = np.empty(cap, np.uint64)
+    oval = np.empty(cap, block.dtype)
+    esz, nout = C.c_uint64(0), C.c_uint64(0)
+    _check(lib.mgrx_host_lorenzo(ws.handle, code, block.ndim, _dims_arr(block.shape),
+                                 block.ctypes.data_as(C.c_void_p), float(e), enc.ctypes.data_as(C.c_void_p),
+                                 enc.size, C.byref(esz), opos.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                 oval.ctypes.data_as(C.c_void_p), cap, C.byref(nout)), ws.handle)
+    return enc[:esz.value].tobytes(), opos[:nout.value], oval[:nout.value]
+
+
 def encode_labels(labels, ws: Optional[SolverWorkspace] = None) -> bytes:
     """encode_labels (huffman.hpp:14): the reference's canonical-Huffman byte
     stream of an int32 CUDA tensor of labels, histogram and bit packing on

@@ -1275,6 +1275,94 @@ void compress_core(mgrx_gpu_ctx* c, int nd, const uint64_t* dims, int levels, co
 
 extern "C" {
 
+int mgrx_host_lorenzo(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, const void* h_block, double e,
+                      uint8_t* h_enc, uint64_t enc_capacity, uint64_t* enc_size, uint64_t* h_outlier_pos,
+                      void* h_outlier_val, uint64_t outlier_capacity, uint64_t* n_outliers) {
+  return guarded(c, [&] {
+    if (!dims || !h_block || !enc_size || !n_outliers) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    if (nd < 1 || nd > kMaxD) fail(MGRX_INVALID_DIMS, "lorenzo: rank out of range");
+    if (!(e > 0.0) || !std::isfinite(e)) fail(MGRX_INVALID_BUDGET, "error bound must be positive");
+    const size_t es = dtype == MGRX_F32 ? 4 : 8;
+    int64_t n[kMaxD], N = 1, H = 1;
+    for (int i = 0; i < nd; ++i) {
+      n[i] = int64_t(dims[i]);
+      if (n[i] < 1) fail(MGRX_INVALID_DIMS, "lorenzo: empty extent");
+      N *= n[i];
+      H += n[i] - 1;
+    }
+    if (N > int64_t(0xffffffffu)) fail(MGRX_INVALID_DIMS, "lorenzo: block too large");
+    // positions grouped by hyperplane sum(index) (counting sort, position order within)
+    std::vector<uint32_t> hs(size_t(H) + 1, 0), order(static_cast<size_t>(N));
+    {
+      std::vector<uint32_t> hof(static_cast<size_t>(N));
+      int64_t idx[kMaxD] = {0};
+      int64_t h = 0;
+      for (int64_t p = 0; p < N; ++p) {
+        hof[size_t(p)] = uint32_t(h);
+        ++hs[size_t(h) + 1];
+        for (int i = nd - 1; i >= 0; --i) {  // odometer, h tracks sum(index)
+          if (++idx[i] < n[i]) {
+            ++h;
+            break;
+          }
+          h -= idx[i] - 1;
+          idx[i] = 0;
+        }
+      }
+      for (int64_t k = 0; k < H; ++k) hs[size_t(k) + 1] += hs[size_t(k)];
+      std::vector<uint32_t> next(hs.begin(), hs.end() - 1);
+      for (int64_t p = 0; p < N; ++p) order[next[hof[size_t(p)]]++] = uint32_t(p);
+    }
+    std::vector<void*> bufs;
+    struct Free {
+      mgrx_gpu_ctx* c;
+      std::vector<void*>* b;
+      ~Free() {
+        for (void* q : *b) cudaFreeAsync(q, c->stream);
+      }
+    } fr{c, &bufs};
+    auto dalloc = [&](size_t bytes) {
+      void* q = nullptr;
+      cuda_check(cudaMallocAsync(&q, std::max<size_t>(bytes, 16), c->stream), "cudaMallocAsync");
+      bufs.push_back(q);
+      return q;
+    };
+    void* dx = dalloc(size_t(N) * es);
+    void* drec = dalloc(size_t(N) * es);
+    auto* dord = static_cast<uint32_t*>(dalloc(size_t(N) * 4));
+    auto* dhs = static_cast<uint32_t*>(dalloc((size_t(H) + 1) * 4));
+    auto* dlab = static_cast<int32_t*>(dalloc(size_t(N) * 4));
+    auto* dfl = static_cast<uint8_t*>(dalloc(size_t(N)));
+    const uint64_t cap = std::max<uint64_t>(outlier_capacity, 1);
+    auto* dpos = static_cast<uint64_t*>(dalloc(cap * 8));
+    void* dval = dalloc(cap * es);
+    auto* dcnt = static_cast<unsigned long long*>(dalloc(8));
+    cuda_check(cudaMemcpyAsync(dx, h_block, size_t(N) * es, cudaMemcpyHostToDevice, c->stream), "H2D");
+    cuda_check(cudaMemcpyAsync(dord, order.data(), size_t(N) * 4, cudaMemcpyHostToDevice, c->stream), "H2D");
+    cuda_check(cudaMemcpyAsync(dhs, hs.data(), (size_t(H) + 1) * 4, cudaMemcpyHostToDevice, c->stream), "H2D");
+    cudaError_t err;
+    if (dtype == MGRX_F32)
+      err = lorenzo_run<float>(static_cast<const float*>(dx), nd, n, dord, dhs, int(H), e, dlab, dfl,
+                               static_cast<float*>(drec), dpos, static_cast<float*>(dval), cap, dcnt, exec(c));
+    else
+      err = lorenzo_run<double>(static_cast<const double*>(dx), nd, n, dord, dhs, int(H), e, dlab, dfl,
+                                static_cast<double*>(drec), dpos, static_cast<double*>(dval), cap, dcnt, exec(c));
+    cuda_check(err, "lorenzo");
+    unsigned long long cnt = 0;
+    cuda_check(cudaMemcpyAsync(&cnt, dcnt, 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    *n_outliers = cnt;
+    if (cnt > outlier_capacity) fail(MGRX_CAPACITY_EXCEEDED, "%llu outliers exceed capacity %llu", cnt,
+                                     (unsigned long long)outlier_capacity);
+    if (cnt) {
+      cuda_check(cudaMemcpyAsync(h_outlier_pos, dpos, cnt * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+      cuda_check(cudaMemcpyAsync(h_outlier_val, dval, cnt * es, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    }
+    const int rc = mgrx_gpu_encode_labels(c, dlab, uint64_t(N), h_enc, enc_capacity, enc_size);
+    if (rc != MGRX_OK) fail(rc, "%s", c->last_error.c_str());
+  });
+}
+
 int mgrx_gpu_field_stats(mgrx_gpu_ctx* c, int dtype, uint64_t n, const void* d_field, double* min_value,
                          double* max_value, uint64_t* first_nonfinite) {
   return guarded(c, [&] {

@@ -37,6 +37,12 @@ int field_stats_blocks(int64_t n);
 template <typename T>
 cudaError_t field_stats(const T* x, int64_t n, double* bmin, double* bmax, unsigned long long* bbad, const Exec& ex);
 
+// ---- Lorenzo coder (lorenzo.cu): hyperplane wavefront in one CTA -------------
+template <typename T>
+cudaError_t lorenzo_run(const T* x, int d, const int64_t* n, const uint32_t* order, const uint32_t* hs, int H,
+                        double e, int32_t* labels, uint8_t* outl, T* recon, uint64_t* opos, T* oval, uint64_t cap,
+                        unsigned long long* count, const Exec& ex);
+
 // ---- label entropy coding (huffman.cu) ---------------------------------------
 cudaError_t label_minmax(const int32_t* x, int64_t n, int* d_mm, const Exec& ex);
 cudaError_t label_hist(const int32_t* x, int64_t n, int lo, int range, unsigned long long* d_freq, const Exec& ex);

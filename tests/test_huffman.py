@@ -74,3 +74,22 @@ def test_gpu_field_stats(dtype):
     x[900_001] = float("nan")
     lo2, hi2, bad2 = mg.field_stats(x)
     assert bad2 == 777_777 and lo2 == lo
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,dtype", [((33, 33, 33), np.float32), ((40, 17, 9), np.float64), ((129, 65), np.float32),
+                                         ((9, 7, 11, 5), np.float64), ((1000,), np.float32)])
+@pytest.mark.parametrize("e", [1e-1, 1e-4, 1e-9])
+def test_gpu_lorenzo_matches_reference(ref, shape, dtype, e):
+    """compress_lorenzo on the GPU (hyperplane wavefront): labels (as their
+    encode_labels bytes) and outliers identical to the reference's; the
+    tight bound forces outliers and the label-range cut-off."""
+    import paper_2010_05872_b200 as mg
+
+    rng = np.random.default_rng(len(shape))
+    axes = np.meshgrid(*[np.linspace(0, 1, n) for n in shape], indexing="ij")
+    x = (sum(np.sin(3 * a + i) for i, a in enumerate(axes)) + rng.normal(0, 1e-2, shape)).astype(dtype)
+    labels, opos, oval = ref.lorenzo(x, e)
+    enc, gpos, gval = mg.lorenzo_encode(x, e)
+    assert enc == ref.encode_labels(labels)
+    assert np.array_equal(gpos, opos) and np.array_equal(gval, oval)
