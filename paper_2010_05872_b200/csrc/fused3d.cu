@@ -238,11 +238,11 @@ __device__ __forceinline__ StripLane strip_lane(int m2) {
 // Shared memory of the plane passes.  Decompose: a 4-slot ring of tile
 // planes (2 TI1 + 3 fine rows; an odd plane reads its two even neighbours in
 // place).  Recompose: a 3-slot ring of shell runs (even + odd rows).
-template <typename T, int TI1, int NSD = 4>
+template <typename T, int TI1, int NSD = 4, int NSR = 4>
 struct PlaneSmem {
   static constexpr int kRows = 2 * TI1 + 3;
   static constexpr int kDecRows = 2 * TI1 + 3;
-  static constexpr int kDecSlots = NSD, kRecSlots = 4;
+  static constexpr int kDecSlots = NSD, kRecSlots = NSR;
   static __host__ __device__ size_t raw_bytes(int64_t n2) {
     return (size_t(kRows) * size_t(n2) * sizeof(T) + 256 + 127) / 128 * 128;
   }
@@ -251,7 +251,7 @@ struct PlaneSmem {
   }
   static __host__ __device__ size_t ring_bytes(int64_t n2) {
     const size_t d = kDecSlots * dec_raw_bytes(n2), r = kRecSlots * raw_bytes(n2);
-    return NSD != 4 ? d : (d > r ? d : r);  // the 3-slot variant is decompose-only
+    return d > r ? d : r;  // the 3-CTA variants size one direction only (the other's slots = 0)
   }
   static __host__ __device__ size_t bytes(int64_t n2, int64_t m2) {
     size_t b = ring_bytes(n2);      // TMA ring of fine plane tiles / shell runs
@@ -642,7 +642,7 @@ template <typename T, int TI1, int MAXT, int NB = 0>
 __global__ void __launch_bounds__(MAXT, NB ? NB : (MAXT == kPlaneMaxThreads ? 2 : 1))
     k_f3_dec_plane(const T* __restrict__ blk, T* __restrict__ shell, T* __restrict__ coarse, double* __restrict__ G,
                    const F3Geom g) {
-  using SM = PlaneSmem<T, TI1, NB == 3 ? 3 : 4>;
+  using SM = PlaneSmem<T, TI1, NB == 3 ? 3 : 4, NB == 3 ? 0 : 4>;
   constexpr int RMAX = SM::kRows;
   constexpr int NS = SM::kDecSlots;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -819,10 +819,10 @@ __device__ __forceinline__ void rec_rows(const T* ev, const T* od, int st_e, int
 // component read from the level's shell.  Per fine plane the tile's shell
 // rows form two contiguous runs (even fine rows, odd fine rows), fetched
 // with two bulk copies into one ring slot.
-template <typename T, int TI1, int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 2 : 1)
+template <typename T, int TI1, int MAXT, int NB = 0>
+__global__ void __launch_bounds__(MAXT, NB ? NB : (MAXT == kPlaneMaxThreads ? 2 : 1))
     k_f3_rec_plane(const T* __restrict__ shell, double* __restrict__ G, const F3Geom g) {
-  using SM = PlaneSmem<T, TI1>;
+  using SM = PlaneSmem<T, TI1, NB == 3 ? 0 : 4, NB == 3 ? 3 : 4>;
   constexpr int RMAX = SM::kRows;
   extern __shared__ __align__(128) unsigned char smem[];
   const int m2 = int(g.m2), n2 = int(g.n2), m1 = int(g.m1);
@@ -1280,8 +1280,12 @@ size_t plane_smem(const F3Geom& g) {
   return PlaneSmem<T, TI1>::bytes(g.n2, g.m2);
 }
 template <typename T>
+size_t plane_smem3r(const F3Geom& g) {
+  return PlaneSmem<T, 4, 0, 3>::bytes(g.n2, g.m2);
+}
+template <typename T>
 size_t plane_smem3(const F3Geom& g) {
-  return PlaneSmem<T, 4, 3>::bytes(g.n2, g.m2);
+  return PlaneSmem<T, 4, 3, 0>::bytes(g.n2, g.m2);
 }
 
 // Row tile of the plane passes: maximise resident warps x useful-row
@@ -1466,6 +1470,13 @@ static cudaError_t launch_interp(const T* shell, const T* coarse, T* fine, const
   return launch_interp_t<T, 4, kPlaneMaxThreads>(shell, coarse, fine, g, ex);
 }
 
+// The recompose plane pass's 3-CTA / 3-slot variant on the levels that use
+// the decompose one (MGRX_NO_REC3 disables; ~5 us per recompose at 513^3).
+static bool rec3_enabled() {
+  static const bool on = std::getenv("MGRX_NO_REC3") == nullptr;
+  return on;
+}
+
 // The decompose plane pass's chunking for its 3-CTA variant.
 static F3Geom dec3_geom(const F3Geom& g) {
   F3Geom gd = g;
@@ -1496,6 +1507,9 @@ static cudaError_t set_attrs(const F3Geom& g, size_t* smem) {
   if (e == cudaSuccess && g.dec3)
     e = cudaFuncSetAttribute(k_f3_dec_plane<T, 4, kPlaneMaxThreads, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(plane_smem3<T>(g)));
+  if (e == cudaSuccess && g.dec3 && rec3_enabled())
+    e = cudaFuncSetAttribute(k_f3_rec_plane<T, 4, kPlaneMaxThreads, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(plane_smem3r<T>(g)));
   return e;
 }
 
@@ -1539,8 +1553,9 @@ cudaError_t fused3d_recompose_correction(const T* shell, void* scratch, const Fu
   size_t ds = 0;
   cudaError_t e = set_attrs<T>(g, &ds);
   if (e != cudaSuccess) return e;
+  const bool r3 = g.dec3 && rec3_enabled();
 #define MGRX_REC(TI, MT)                                                                               \
-  if (g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))                      \
+  if (!r3 && g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))              \
     MGRX_LAUNCH(ex, "f3_rec_plane", pdl_launch(k_f3_rec_plane<T, TI, MT>, dim3(g.grid), dim3(g.threads), ds, \
                                                ex.s, !ex.prof, shell, G, g));
   MGRX_REC(4, kPlaneMaxThreads)
@@ -1548,6 +1563,11 @@ cudaError_t fused3d_recompose_correction(const T* shell, void* scratch, const Fu
   MGRX_REC(4, kWideBound)
   MGRX_REC(2, kWideBound)
 #undef MGRX_REC
+  if (r3) {
+    const F3Geom gd = dec3_geom(g);
+    MGRX_LAUNCH(ex, "f3_rec_plane", pdl_launch(k_f3_rec_plane<T, 4, kPlaneMaxThreads, 3>, dim3(gd.grid),
+                                               dim3(gd.threads), plane_smem3r<T>(gd), ex.s, !ex.prof, shell, G, gd));
+  }
   launch_row(G, g, th.w[2], th.inv_d[2], ex);
   launch_col<T>(G, static_cast<T*>(nullptr), 0.0, g, 1, th.w[1], th.inv_d[1], ex);
   return cudaGetLastError();
