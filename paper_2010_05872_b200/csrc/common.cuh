@@ -39,7 +39,7 @@ template <> __device__ __forceinline__ double to_t<double>(double v) { return v;
 // exact for every 32-bit dividend.
 struct FastDiv {
   uint32_t d, mul, shift;  // shift == 0 encodes d == 1
-  __host__ FastDiv() : d(1), mul(0), shift(0) {}
+  __host__ __device__ FastDiv() : d(1), mul(0), shift(0) {}
   __host__ explicit FastDiv(uint32_t div) : d(div), mul(0), shift(0) {
     if (div <= 1) return;
     uint32_t l = 0;

@@ -1074,6 +1074,109 @@ struct TailLevel {
   int64_t shell_off;  // node_count(l-1): shell position in the level-centric buffer
 };
 
+// The tail's level geometry in registers with 32-bit indices (a tail level
+// fits in shared memory): loaded once per level instead of re-reading the
+// 64-bit LevelGeom from global memory for every node.  Same index maps as
+// unravel / shell_pos / predict above.
+template <int D>
+struct TailGeo {
+  static constexpr int R = D > 0 ? D : kMaxD;
+  int d, N, Nc;
+  int n[R], m[R], st[R], cst[R], pm[R];
+  FastDiv fn[R];
+};
+#define TAIL_ND(G) (D > 0 ? D : (G).d)
+
+template <int D>
+__device__ __forceinline__ TailGeo<D> tail_geo(const LevelGeom& g) {
+  TailGeo<D> G;
+  G.d = g.d;
+  G.N = int(g.N);
+  G.Nc = int(g.Nc);
+#pragma unroll
+  for (int i = 0; i < TailGeo<D>::R; ++i) {
+    if (i < TAIL_ND(G)) {
+      G.n[i] = int(g.n[i]);
+      G.m[i] = int(g.m[i]);
+      G.st[i] = int(g.st[i]);
+      G.cst[i] = int(g.cst[i]);
+      G.pm[i] = int(g.pm[i]);
+      G.fn[i] = g.fn[i];
+    }
+  }
+  return G;
+}
+
+template <int D>
+__device__ __forceinline__ void tail_unravel(int p, const TailGeo<D>& G, int* j) {
+  uint32_t q = uint32_t(p);
+#pragma unroll
+  for (int i = TAIL_ND(G) - 1; i > 0; --i) {
+    const uint32_t qq = G.fn[i].div(q);
+    j[i] = int(q - qq * uint32_t(G.n[i]));
+    q = qq;
+  }
+  j[0] = int(q);
+}
+
+template <int D>
+__device__ __forceinline__ int tail_shell_pos(const TailGeo<D>& G, const int* j) {
+  const int d = TAIL_ND(G);
+  int row = 0, before = 0;
+  bool inside = true;
+#pragma unroll
+  for (int i = 0; i + 1 < d; ++i) {
+    const int r = (j[i] & 1) ? G.m[i] + (j[i] >> 1) : (j[i] >> 1);
+    row = row * G.n[i] + r;
+    if (inside) {
+      if (r < G.m[i]) {
+        before += r * G.pm[i];
+      } else {
+        before += G.m[i] * G.pm[i];
+        inside = false;
+      }
+    }
+  }
+  const int jl = j[d - 1];
+  const int rl = (jl & 1) ? G.m[d - 1] + (jl >> 1) : (jl >> 1);
+  return row * G.n[d - 1] - before * G.m[d - 1] + (inside ? rl - G.m[d - 1] : rl);
+}
+
+// predict<T, kNu, D>: corners in cmask order, summed in that order.
+template <typename T, bool kNu, int D>
+__device__ __forceinline__ double tail_predict(const T* __restrict__ src, bool coarse, const TailGeo<D>& G,
+                                               const NuLevel& nu, const int* j) {
+  int k = 0, base = 0;
+  int dl[TailGeo<D>::R];
+  int bit[TailGeo<D>::R];
+#pragma unroll
+  for (int i = 0; i < TAIL_ND(G); ++i) {
+    const int stride = coarse ? G.cst[i] : G.st[i];
+    const bool odd = j[i] & 1;
+    dl[i] = (odd && j[i] + 1 < G.n[i]) ? (coarse ? G.cst[i] : 2 * G.st[i]) : 0;
+    bit[i] = odd ? k : -1;
+    k += odd ? 1 : 0;
+    base += (coarse ? (odd ? (j[i] - 1) >> 1 : j[i] >> 1) : (odd ? j[i] - 1 : j[i])) * stride;
+  }
+  double sum = 0.0;
+#pragma unroll
+  for (unsigned cm = 0; cm < (D > 0 ? (1u << D) : (1u << kMaxD)); ++cm) {
+    if (cm >= (1u << k)) break;
+    int off = base;
+    double wprod = 1.0;
+#pragma unroll
+    for (int i = 0; i < TAIL_ND(G); ++i) {
+      if (bit[i] < 0) continue;
+      const bool right = (cm >> bit[i]) & 1u;
+      if (right) off += dl[i];
+      if (kNu) wprod = mul_(wprod, right ? nu.ax[i].wr[j[i]] : nu.ax[i].wl[j[i]]);
+    }
+    const double v = double(src[off]);
+    sum = kNu ? add_(sum, mul_(wprod, v)) : add_(sum, v);
+  }
+  return kNu ? sum : mul_(sum, 1.0 / double(1u << k));
+}
+
 template <int D, bool kNu>
 __device__ __forceinline__ void tail_sweeps(double* comp, double* tmp, const LevelGeom& g, const ThomasLevel& th,
                                             const NuLevel& nu, double** result) {
@@ -1093,35 +1196,45 @@ __device__ __forceinline__ void tail_sweeps(double* comp, double* tmp, const Lev
     const int n = int(g.n[a]), m = int(g.m[a]);
     const double* w = th.w[a];
     const double* inv_d = th.inv_d[a];
+    // (1) the restriction value of every (line, i), block-wide: y is laid out
+    // [outer][m][inner], so e walks y in order.
+    const int mi = m * inner;
+    for (int e = threadIdx.x; e < outer * mi; e += blockDim.x) {
+      const int o = e / mi, r = e - o * mi;
+      const int i = r / inner, t = r - i * inner;
+      const double* c = x + o * n * inner + t;
+      double acc = 0.0;
+      if (kNu) {  // same arithmetic as k_sweep<true>
+        const double* sk = nu.ax[a].s + 5 * i;
+        for (int k = 0; k < 5; ++k) {
+          const int jj = 2 * i + k - 2;
+          if (jj >= 0 && jj < n) acc = add_(acc, mul_(sk[k], c[jj * inner]));
+        }
+      } else {
+        if (i >= 1) {
+          acc = add_(acc, mul_(kW12, c[(2 * i - 2) * inner]));
+          acc = add_(acc, mul_(0.5, c[(2 * i - 1) * inner]));
+        }
+        acc = add_(acc, mul_((i == 0 || i + 1 == m) ? kW5_12 : kW5_6, c[(2 * i) * inner]));
+        if (2 * i + 1 < n) acc = add_(acc, mul_(0.5, c[(2 * i + 1) * inner]));
+        if (2 * i + 2 < n) acc = add_(acc, mul_(kW12, c[(2 * i + 2) * inner]));
+      }
+      y[e] = acc;
+    }
+    __syncthreads();
+    // (2) the two Thomas recurrences, one thread per line (the only serial part)
     for (int t0 = threadIdx.x; t0 < outer * inner; t0 += blockDim.x) {
       const int o = t0 / inner, t = t0 - o * inner;
-      const double* c = x + o * n * inner + t;
-      double* f = y + o * m * inner + t;
-      double prev = 0.0;
-      for (int i = 0; i < m; ++i) {
-        double acc = 0.0;
-        if (kNu) {  // same arithmetic as k_sweep<true>
-          const double* sk = nu.ax[a].s + 5 * i;
-          for (int k = 0; k < 5; ++k) {
-            const int jj = 2 * i + k - 2;
-            if (jj >= 0 && jj < n) acc = add_(acc, mul_(sk[k], c[jj * inner]));
-          }
-          if (i > 0) acc = sub_(acc, mul_(nu.ax[a].tw[i], prev));
-        } else {
-          if (i >= 1) {
-            acc = add_(acc, mul_(kW12, c[(2 * i - 2) * inner]));
-            acc = add_(acc, mul_(0.5, c[(2 * i - 1) * inner]));
-          }
-          acc = add_(acc, mul_((i == 0 || i + 1 == m) ? kW5_12 : kW5_6, c[(2 * i) * inner]));
-          if (2 * i + 1 < n) acc = add_(acc, mul_(0.5, c[(2 * i + 1) * inner]));
-          if (2 * i + 2 < n) acc = add_(acc, mul_(kW12, c[(2 * i + 2) * inner]));
-          if (i > 0) acc = sub_(acc, mul_(w[i], prev));
-        }
-        f[i * inner] = acc;
-        prev = acc;
+      double* f = y + o * mi + t;
+      double prev = f[0];
+#pragma unroll 4
+      for (int i = 1; i < m; ++i) {
+        prev = sub_(f[i * inner], mul_(kNu ? nu.ax[a].tw[i] : w[i], prev));
+        f[i * inner] = prev;
       }
       double nxt = mul_(prev, kNu ? nu.ax[a].tid[m - 1] : inv_d[m - 1]);
       f[(m - 1) * inner] = nxt;
+#pragma unroll 4
       for (int i = m - 2; i >= 0; --i) {
         const double v = kNu ? mul_(sub_(f[i * inner], mul_(nu.ax[a].off[i], nxt)), nu.ax[a].tid[i])
                              : mul_(sub_(f[i * inner], mul_(kOff, nxt)), inv_d[i]);
@@ -1158,27 +1271,30 @@ __global__ void __launch_bounds__(1024) k_tail_decompose(const T* __restrict__ b
     const LevelGeom& g = lv[k].g;
     const NuLevel nu = kNu ? nul[k] : NuLevel{};
     T* shell = out + lv[k].shell_off;
-    for (int64_t p = threadIdx.x; p < g.N; p += blockDim.x) {
-      int64_t j[kMaxD];
-      unravel<true, D>(p, g, j);
+    const TailGeo<D> G = tail_geo<D>(g);
+    for (int p = threadIdx.x; p < G.N; p += blockDim.x) {
+      int j[TailGeo<D>::R];
+      tail_unravel<D>(p, G, j);
       bool nodal = true;
-      for (int i = 0; i < MGRX_ND(g); ++i) nodal &= !(j[i] & 1);
+#pragma unroll
+      for (int i = 0; i < TAIL_ND(G); ++i) nodal &= !(j[i] & 1);
       if (nodal) {
-        int64_t cc = 0;
-        for (int i = 0; i < MGRX_ND(g); ++i) cc += (j[i] >> 1) * g.cst[i];
+        int cc = 0;
+#pragma unroll
+        for (int i = 0; i < TAIL_ND(G); ++i) cc += (j[i] >> 1) * G.cst[i];
         nxt[cc] = cur[p];
         comp[p] = 0.0;
       } else {
-        const double pred = predict<T, kNu, D>(cur, false, g, nu, j);
+        const double pred = tail_predict<T, kNu, D>(cur, false, G, nu, j);
         const T v = to_t<T>(sub_(double(cur[p]), pred));
         comp[p] = double(v);
-        shell[shell_pos<D>(g, j)] = v;
+        shell[tail_shell_pos<D>(G, j)] = v;
       }
     }
     __syncthreads();
     double* z = nullptr;
     tail_sweeps<D, kNu>(comp, tmp, g, lv[k].th, nu, &z);
-    for (int64_t p = threadIdx.x; p < g.Nc; p += blockDim.x) nxt[p] = to_t<T>(add_(double(nxt[p]), mul_(1.0, z[p])));
+    for (int p = threadIdx.x; p < G.Nc; p += blockDim.x) nxt[p] = to_t<T>(add_(double(nxt[p]), mul_(1.0, z[p])));
     __syncthreads();
     T* t = cur;
     cur = nxt;
@@ -1208,31 +1324,35 @@ __global__ void __launch_bounds__(1024) k_tail_recompose(const T* __restrict__ c
     const LevelGeom& g = lv[k].g;
     const NuLevel nu = kNu ? nul[k] : NuLevel{};
     const T* shell = coeffs + lv[k].shell_off;
-    for (int64_t p = threadIdx.x; p < g.N; p += blockDim.x) {
-      int64_t j[kMaxD];
-      unravel<true, D>(p, g, j);
+    const TailGeo<D> G = tail_geo<D>(g);
+    for (int p = threadIdx.x; p < G.N; p += blockDim.x) {
+      int j[TailGeo<D>::R];
+      tail_unravel<D>(p, G, j);
       bool nodal = true;
-      for (int i = 0; i < MGRX_ND(g); ++i) nodal &= !(j[i] & 1);
-      comp[p] = nodal ? 0.0 : double(shell[shell_pos<D>(g, j)]);
+#pragma unroll
+      for (int i = 0; i < TAIL_ND(G); ++i) nodal &= !(j[i] & 1);
+      comp[p] = nodal ? 0.0 : double(shell[tail_shell_pos<D>(G, j)]);
     }
     __syncthreads();
     double* z = nullptr;
     tail_sweeps<D, kNu>(comp, tmp, g, lv[k].th, nu, &z);
-    for (int64_t p = threadIdx.x; p < g.Nc; p += blockDim.x) cur[p] = to_t<T>(add_(double(cur[p]), mul_(-1.0, z[p])));
+    for (int p = threadIdx.x; p < G.Nc; p += blockDim.x) cur[p] = to_t<T>(add_(double(cur[p]), mul_(-1.0, z[p])));
     __syncthreads();
     T* dst = (k == nlev - 1) ? fine_out : fin;
-    for (int64_t p = threadIdx.x; p < g.N; p += blockDim.x) {
-      int64_t j[kMaxD];
-      unravel<true, D>(p, g, j);
+    for (int p = threadIdx.x; p < G.N; p += blockDim.x) {
+      int j[TailGeo<D>::R];
+      tail_unravel<D>(p, G, j);
       bool nodal = true;
-      for (int i = 0; i < MGRX_ND(g); ++i) nodal &= !(j[i] & 1);
+#pragma unroll
+      for (int i = 0; i < TAIL_ND(G); ++i) nodal &= !(j[i] & 1);
       if (nodal) {
-        int64_t cc = 0;
-        for (int i = 0; i < MGRX_ND(g); ++i) cc += (j[i] >> 1) * g.cst[i];
+        int cc = 0;
+#pragma unroll
+        for (int i = 0; i < TAIL_ND(G); ++i) cc += (j[i] >> 1) * G.cst[i];
         dst[p] = cur[cc];
       } else {
-        const double pred = predict<T, kNu, D>(cur, true, g, nu, j);
-        dst[p] = to_t<T>(add_(double(shell[shell_pos<D>(g, j)]), pred));
+        const double pred = tail_predict<T, kNu, D>(cur, true, G, nu, j);
+        dst[p] = to_t<T>(add_(double(shell[tail_shell_pos<D>(G, j)]), pred));
       }
     }
     __syncthreads();
