@@ -343,3 +343,25 @@ def test_rank_above_limit_is_rejected(mg):
     with pytest.raises(mg.Error) as e:
         mg.GridHierarchy.create((2,) * 9)
     assert e.value.code == "invalid_dims"
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_tail_kernel_bitwise(torch, mg, dtype):
+    """Hierarchies small enough to run entirely in the one-CTA tail kernels
+    (k_tail_decompose / k_tail_recompose: block-wide restriction, serial
+    Thomas recurrences, 32-bit register geometry) on every rank 1-5 and every
+    stop level: bit-identical to the oracle in both directions."""
+    from oracle.oracle import Oracle
+
+    o = Oracle()
+    rng = np.random.default_rng(11)
+    ws = mg.SolverWorkspace(path="auto")
+    for shape in [(257,), (40,), (33, 17), (17, 17, 17), (9, 16, 5), (5, 9, 3, 6), (3, 4, 5, 3, 3)]:
+        x = rng.uniform(-3, 3, shape).astype(dtype)
+        h = mg.GridHierarchy.create(shape)
+        for stop in range(h.num_levels() + 1):
+            got = mg.decompose(to_dev(torch, x), h, stop, ws).buffer.cpu().numpy()
+            want = o.decompose(x, stop).astype(dtype)
+            assert bits(got) == bits(want), (shape, stop, "decompose")
+            back = mg.recompose(mg.MultilevelCoefficients(to_dev(torch, want), h, stop), ws).cpu().numpy()
+            assert bits(back) == bits(o.recompose(want, shape, stop).astype(dtype)), (shape, stop, "recompose")
