@@ -859,7 +859,11 @@ void thomas(int m, double* w, double* id) {
 
 P2Plan p2_plan(const LevelGeom& lg, int esize) {
   P2Plan p;
-  if (std::getenv("MGRX_NO_P2")) return p;
+  // opt-in until it beats the fused3d passes (MGRX_P2=1)
+  {
+    const char* e = std::getenv("MGRX_P2");
+    if (!e || std::atoi(e) == 0) return p;
+  }
   if (lg.d != 3 || esize != 4) return p;
   P2Geom& g = p.g;
   g.n0 = int(lg.n[0]);

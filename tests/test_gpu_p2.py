@@ -14,8 +14,8 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-P2_SHAPES = [(65, 65, 65), (129, 129, 129), (17, 33, 129), (257, 17, 65), (41, 49, 65), (33, 257, 65),
-             (21, 9, 65), (9, 17, 513)]
+P2_SHAPES = [(65, 65, 65), (129, 129, 129), (17, 65, 129), (257, 65, 65), (41, 65, 65), (33, 257, 65),
+             (21, 9, 65), (9, 65, 513)]
 
 
 @pytest.fixture(scope="module")
@@ -42,16 +42,13 @@ def o():
 def _ws(mg, chunk=None, p2=True):
     """A workspace whose plans are built under the given p2 settings (the
     environment is read when a plan is first built)."""
-    old = {k: os.environ.get(k) for k in ("MGRX_P2_CHUNK", "MGRX_NO_P2")}
+    old = {k: os.environ.get(k) for k in ("MGRX_P2_CHUNK", "MGRX_P2")}
     try:
         if chunk is None:
             os.environ.pop("MGRX_P2_CHUNK", None)
         else:
             os.environ["MGRX_P2_CHUNK"] = str(chunk)
-        if p2:
-            os.environ.pop("MGRX_NO_P2", None)
-        else:
-            os.environ["MGRX_NO_P2"] = "1"
+        os.environ["MGRX_P2"] = "1" if p2 else "0"
         ws = mg.SolverWorkspace()
         return ws, old
     except Exception:
