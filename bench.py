@@ -2,6 +2,9 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
+`--gpus N` (N > 1) outside torchrun relaunches itself under
+torch.distributed.run with N ranks on 127.0.0.1.
+
 One step = decompose + recompose of one 513^3 fp32 field (BASELINE.json
 config 2 shape/distribution; config 5a's per-field unit when N > 1) with the
 input resident in HBM.  Under torchrun every rank processes its own field
@@ -107,7 +110,46 @@ def dist_init(backend="nccl"):
         import torch.distributed as dist
 
         dist.init_process_group(backend=backend)
+        # one line per rank on stderr: the rank count the driver can check
+        print(f"[bench] rank {rank}/{ws} local_rank {local} backend {dist.get_backend()} "
+              f"master {os.environ.get('MASTER_ADDR')}:{os.environ.get('MASTER_PORT')}", file=sys.stderr, flush=True)
     return ws, rank, local
+
+
+def self_launch(nproc, argv):
+    """`python bench.py --gpus N` outside torchrun: relaunch this script
+    under torch.distributed.run with N ranks (one per GPU) on 127.0.0.1 and
+    return its exit code (rank 0's JSON line goes to stdout)."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "WARN")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    print("[bench] launching " + " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
+
+
+def dist_selftest(args):
+    """CPU check of the N > 1 plumbing (gloo): every rank reports a fixed
+    per-rank time, rank 0 prints the JSON line exactly as run_ours would
+    aggregate it (used by tests/test_dist_host.py)."""
+    ws, rank, local = dist_init(backend="gloo")
+    ms = 1.0 + rank
+    barrier(ws)
+    m = max_over_ranks(ms, ws, device="cpu")
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": aggregate_gbs(ws, 1e9, m), "unit": "GB/s", "n_gpus": ws,
+                          "ms_per_step": m, "selftest": True}), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
 
 
 def field_seed(rank):
@@ -153,7 +195,7 @@ def run_reference(args, ws, rank):
 
     lib = Reference() if reference_available() else Oracle()
     kind = "reference" if reference_available() else "port"
-    ncpu = os.cpu_count() or 1
+    ncpu = physical_cores()
     try:
         import psutil
 
@@ -164,7 +206,7 @@ def run_reference(args, ws, rank):
     threads = max(1, min(ncpu, int(avail * 0.6 // per_field), args.ref_threads or ncpu))
     import torch
 
-    from paper_2010_05872_b200.fields import config2_field
+    from synthetic_fields import config2_field
 
     fields = [config2_field(DIMS, seed=i).numpy() for i in range(threads)]
     outs = [np.empty(f.size, dtype=np.float32) for f in fields]
@@ -198,11 +240,38 @@ def run_reference(args, ws, rank):
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind,
                          "sample": f"{threads} x 513^3 f32 decompose+recompose per step, "
                                    f"{args.warmup_ref} untimed warm-up steps",
-                         "cpu": _cpu_model()},
+                         "cpu": _cpu_model(), "logical_cpus": os.cpu_count()},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "roundtrip_linf": err,
     }
     print(json.dumps(line), flush=True)
+
+
+def physical_cores():
+    """Physical core count of the host (P = physical cores,
+    not logical CPUs)."""
+    try:
+        import psutil
+
+        n = psutil.cpu_count(logical=False)
+        if n:
+            return int(n)
+    except Exception:
+        pass
+    try:
+        cores = set()
+        phys = None
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("physical id"):
+                    phys = line.split(":", 1)[1].strip()
+                elif line.startswith("core id"):
+                    cores.add((phys, line.split(":", 1)[1].strip()))
+        if cores:
+            return len(cores)
+    except Exception:
+        pass
+    return os.cpu_count() or 1
 
 
 def _cpu_model():
@@ -216,9 +285,16 @@ def _cpu_model():
     return "unknown"
 
 
-def cpu_baseline_sample(field_np):
+def cpu_baseline_sample(field_np, mg=None, wsp=None, field=None, h=None):
     """Reference CPU decompose+recompose of the same field on 1 core (the
-    library is single-threaded by contract)."""
+    library is single-threaded by contract).  With the GPU
+    objects given, the reference's coefficients also serve as the parity
+    check of the bench field (north_star's bars): coefficient error over the
+    range, and for tau in {1e-2, 1e-3, 1e-4} * range the label flips against
+    the reference's quantize (each within 1 ulp of a bin edge) and the
+    L_inf / tau of the GPU dequantize + recompose."""
+    import numpy as np
+
     from oracle.oracle import Oracle, Reference, reference_available
 
     lib = Reference() if reference_available() else Oracle()
@@ -227,10 +303,34 @@ def cpu_baseline_sample(field_np):
     t1 = time.perf_counter()
     lib.recompose(c, field_np.shape)
     t2 = time.perf_counter()
-    return {"value": field_np.nbytes / (t2 - t0) / 1e9, "unit": "GB/s", "cores": 1,
-            "kind": "reference" if reference_available() else "port",
-            "sample": f"one 513^3 f32 decompose ({t1 - t0:.2f} s) + recompose ({t2 - t1:.2f} s), same field, rank 0",
-            "cpu": _cpu_model()}
+    cpu = {"value": field_np.nbytes / (t2 - t0) / 1e9, "unit": "GB/s", "cores": 1,
+           "kind": "reference" if reference_available() else "port",
+           "sample": f"one 513^3 f32 decompose ({t1 - t0:.2f} s) + recompose ({t2 - t1:.2f} s), same field, rank 0",
+           "cpu": _cpu_model(), "physical_cores": physical_cores()}
+    if mg is None:
+        return cpu, None
+    from oracle.parity import label_flips
+
+    rg = float(field_np.max() - field_np.min())
+    mc = mg.decompose(field, h, 0, wsp)
+    got = mc.buffer.cpu().numpy()
+    par = {"coeff_max_err_over_range": float(np.max(np.abs(got.astype(np.float64) - c))) / rg,
+           "coeff_bar": 1e-5, "budget": "tau / 4", "taus": {}}
+    for t in (1e-2, 1e-3, 1e-4):
+        tau = t * rg
+        plan = mg.make_plan(mg.QuantMode.levelwise, tau / 4.0, h)
+        s = mg.quantize(mc, plan, wsp)
+        lab, _, _ = lib.quantize(c, field_np.shape, plan.bin_widths)
+        try:
+            n, worst = label_flips(c, s.flat.cpu().numpy(), lab, h.delta_counts(), plan.bin_widths, ulps=1.0)
+            ok = True
+        except AssertionError as e:
+            n, worst, ok = -1, None, str(e)
+        rec = mg.recompose(mg.dequantize(s, plan, h, wsp), wsp)
+        linf = float((rec - field).abs().max().item())
+        par["taus"][f"{t:g}"] = {"label_flips": n, "worst_flip_ulp": worst, "flips_within_1ulp": ok,
+                                 "labels": int(lab.size), "linf_over_tau": linf / tau}
+    return cpu, par
 
 
 # --------------------------------------------------------------------- ours
@@ -240,7 +340,7 @@ def run_ours(args, ws, rank, local):
     import torch
 
     import paper_2010_05872_b200 as mg
-    from paper_2010_05872_b200.fields import config2_field
+    from synthetic_fields import config2_field
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -292,6 +392,20 @@ def run_ours(args, ws, rank, local):
             graph.replay()
         torch.cuda.synchronize()
 
+    # decompose and recompose alone, each captured in its own graph (the
+    # per-direction GB/s and roofline of SURVEY 8(d))
+    dir_graphs = {}
+    if not args.eager:
+        mc_rec = mg.decompose(field, h, 0, wsp)
+        for name, fn in (("decompose", lambda: mg.decompose(field, h, 0, wsp)),
+                         ("recompose", lambda: mg.recompose(mc_rec, wsp))):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            g.replay()
+            dir_graphs[name] = g
+        torch.cuda.synchronize()
+
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
@@ -306,8 +420,19 @@ def run_ours(args, ws, rank, local):
     e1.record(stream)
     torch.cuda.synchronize()
     barrier(ws)
-    clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
+    dir_ms = {}
+    for name, g in dir_graphs.items():
+        for _ in range(2):
+            g.replay()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dir_ms[name] = e0.elapsed_time(e1) / args.steps
+    clk = clocks.stop()
     ms_max = max_over_ranks(ms, ws)
     value = aggregate_gbs(ws, nbytes, ms_max)
     peak, peak_src = measured_peak()
@@ -354,9 +479,9 @@ def run_ours(args, ws, rank, local):
     quant = quant_measure(mg, wsp, field, h, args)
     batch = batch_measure(mg, field, h, args, dev)
 
-    cpu = None
+    cpu = parity = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(field.cpu().numpy())
+        cpu, parity = cpu_baseline_sample(field.cpu().numpy(), mg, wsp, field, h)
 
     if rank == 0:
         line = {
@@ -369,16 +494,24 @@ def run_ours(args, ws, rank, local):
                        "parallelism": f"batch: {ws} independent field(s), one per GPU, no collective",
                        "launch": "eager" if graph is None else "cuda_graph (one captured decompose+recompose step, replayed)",
                        "eager_ms_per_step": eager_ms},
-            "roofline": {"bound": "hbm", "achieved": kern_achieved, "peak": peak, "unit": "GB/s",
-                         "frac": kern_achieved / peak, "traffic": traffic, "kernel": dom_tag,
-                         "kernel_ms": kern_ms, "kernel_alg_bytes": kernel_bytes, "peak_source": peak_src,
-                         "definition": "2*s*#N_l of the kernel's level / its average CUDA-event duration"},
+            "roofline": {"bound": "hbm", "achieved": step_achieved, "peak": peak, "unit": "GB/s",
+                         "frac": step_achieved / peak, "frac_nominal_8tbs": step_achieved / 8000.0,
+                         "traffic": step_traffic(), "alg_bytes_per_step": 2 * alg_dir, "peak_source": peak_src,
+                         "definition": "the whole step: sum_{l=1..L} 2*s*#N_l per direction (SURVEY 8(d)), "
+                                       "decompose + recompose, / device step time; traffic = ncu DRAM read+write "
+                                       "bytes of all kernels of one step (profiles/traffic.json)"},
+            "directions": {
+                k: {"ms": v, "gbs_input": nbytes / (v * 1e-3) / 1e9,
+                    "achieved": alg_dir / (v * 1e-3) / 1e9, "frac": alg_dir / (v * 1e-3) / 1e9 / peak,
+                    "frac_nominal_8tbs": alg_dir / (v * 1e-3) / 1e9 / 8000.0} for k, v in dir_ms.items()},
+            "kernel_roofline": {"bound": "hbm", "achieved": kern_achieved, "peak": peak, "unit": "GB/s",
+                                "frac": kern_achieved / peak, "traffic": traffic, "kernel": dom_tag,
+                                "kernel_ms": kern_ms, "kernel_alg_bytes": kernel_bytes,
+                                "definition": "dominant kernel: 2*s*#N_l of its level / its average CUDA-event "
+                                              "duration"},
             "finest_level_roofline": {
                 k: {"ms": v, "achieved": lvl_bytes / (v * 1e-3) / 1e9 if v else 0.0,
                     "frac": (lvl_bytes / (v * 1e-3) / 1e9) / peak if v else 0.0} for k, v in lvl_ms.items()},
-            "step_roofline": {"achieved": step_achieved, "peak": peak, "frac": step_achieved / peak,
-                              "alg_bytes_per_step": 2 * alg_dir,
-                              "definition": "sum_l 2*s*#N_l per direction, dec+rec, / device step time"},
             "kernels_ms_per_step": {k: v[0] / args.steps for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])},
             "kernels_launches_per_step": {k: v[1] // args.steps for k, v in prof.items()},
             "profiled_step_ms": prof_total,
@@ -386,11 +519,23 @@ def run_ours(args, ws, rank, local):
             "quantize": quant,
             "batch": batch,
             "cpu_baseline": cpu,
+            "parity": parity,
             "clocks": clk,
             "gpu_launches": int(launches),
             "roundtrip_linf": err,
         }
         print(json.dumps(line), flush=True)
+
+
+def step_traffic():
+    """ncu DRAM bytes (read + write) of all kernels of one decompose +
+    recompose step (profiles/traffic.json "step"), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            v = json.load(f).get("step")
+        return None if v is None else float(v)
+    except Exception:
+        return None
 
 
 def measured_traffic(tag):
@@ -412,7 +557,7 @@ def batch_measure(mg, field, h, args, dev, inflight=None):
     Reported beside the single-field metric, same bytes per field."""
     import torch
 
-    from paper_2010_05872_b200.fields import config2_field
+    from synthetic_fields import config2_field
 
     inflight = inflight or args.batch_inflight
     fields = [field] + [config2_field(DIMS, seed=1000 + i, device=dev) for i in range(inflight - 1)]
@@ -554,7 +699,7 @@ def run_slab(args, ws, rank, local):
     import torch
 
     import paper_2010_05872_b200 as mg
-    from paper_2010_05872_b200.fields import config2_field
+    from synthetic_fields import config2_field
     from paper_2010_05872_b200.slab import LocalExchange, TorchExchange, max_slab_levels, slab_bounds, \
         slab_decompose, slab_recompose
 
@@ -624,7 +769,17 @@ def main():
                     help="slab mode: one field split along axis 0 over the ranks (NCCL transposes); strong scaling")
     ap.add_argument("--slab-emulate", type=int, default=1,
                     help="with --slab on one GPU: emulate this many ranks in-process (correctness/overhead check)")
+    ap.add_argument("--dist-selftest", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus, sys.argv[1:]))
+    if "WORLD_SIZE" in os.environ and args.impl == "ours" and not args.dist_selftest:
+        wsz = int(os.environ["WORLD_SIZE"])
+        if wsz != args.gpus:
+            print(f"[bench] note: --gpus {args.gpus} but WORLD_SIZE {wsz}; using WORLD_SIZE", file=sys.stderr)
+    if args.dist_selftest:
+        dist_selftest(args)
+        return
     global DIMS, WORKLOAD
     dims = tuple(int(x) for x in args.dims.split(","))
     if dims != DIMS:

@@ -565,6 +565,12 @@ void ensure_p2(mgrx_gpu_ctx* c, Plan& p) {
   for (size_t l = 0; l < p.p2.size(); ++l)
     if (p.p2[l].enabled)
       cuda_check(p2_init(p.p2[l], static_cast<char*>(c->scratch) + p.p2[l].scratch_off, c->stream), "p2 init");
+  // the fused levels' dataflow-solve counters (each launch leaves them zeroed)
+  for (size_t l = 0; l < p.fused.size(); ++l)
+    if (p.fused[l].enabled)
+      cuda_check(cudaMemsetAsync(static_cast<char*>(c->scratch) + p.fused[l].scratch_off + p.fused[l].ctr_off, 0,
+                                 fused3d_ctr_bytes(p.fused[l]), c->stream),
+                 "solve counters");
   p.p2_scratch = c->scratch;
 }
 

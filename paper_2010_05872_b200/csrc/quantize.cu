@@ -29,11 +29,12 @@ __device__ __forceinline__ int level_of(const QuantLevels& ql, int64_t pos) {
 // r = nearbyint(x / q) exactly as the reference (IEEE division, ties to
 // even): x * (1/q) is within 2 ulp of x / q, so its rounding can only differ
 // when it lies within a few ulp of a half-integer; those rare values take
-// the exact division.
+// the exact division.  So does a non-finite product (a subnormal bin width
+// whose reciprocal overflows: 0 * inf, x * inf), where only x / q is right.
 __device__ __forceinline__ double quant_round(double x, double q, double inv) {
   const double r1 = x * inv;
   const double n1 = rint(r1);
-  if (fabs(fabs(r1 - n1) - 0.5) <= fabs(r1) * 0x1p-48) return rint(__ddiv_rn(x, q));
+  if (!isfinite(r1) || fabs(fabs(r1 - n1) - 0.5) <= fabs(r1) * 0x1p-48) return rint(__ddiv_rn(x, q));
   return n1;
 }
 

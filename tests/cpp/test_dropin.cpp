@@ -55,7 +55,11 @@ mgrx::TensorField<T> bumps(const mgrx::Dims& dims, unsigned seed) {
 }
 
 template <typename T>
-void check_shape(const mgrx::Dims& dims, double tol) {
+// exact_bytes: the device-resident compress must produce the reference's
+// artifact byte for byte.  Off only for the fp64 fused-path case, whose
+// coefficients differ from the reference's at the 1e-16 level (different
+// rounding of the reordered sweeps); there the artifact size must match.
+void check_shape(const mgrx::Dims& dims, double tol, bool exact_bytes = true) {
   mgrx::b200::Workspace ws;
   auto f = bumps<T>(dims, 7);
   double lo = f.data[0], hi = f.data[0];
@@ -174,11 +178,19 @@ void check_shape(const mgrx::Dims& dims, double tol) {
     const auto rbytes = mgrx::compress(f, aopt);
     std::printf("  adaptive artifact: %zu bytes (reference %zu)%s\n", abytes.size(), rbytes.size(),
                 abytes == rbytes ? ", byte-identical" : "");
+    if (exact_bytes)
+      EXPECT(abytes == rbytes, "adaptive artifact differs from the reference's bytes");
+    else
+      EXPECT(abytes.size() == rbytes.size(), "adaptive artifact size %zu vs %zu", abytes.size(), rbytes.size());
     mgrx::CompressOptions fopt = aopt;
     fopt.adaptive = false;
     const auto gb = mgrx::b200::compress(f, fopt, ws), rb = mgrx::compress(f, fopt);
     std::printf("  full artifact: %zu bytes (reference %zu)%s\n", gb.size(), rb.size(),
                 gb == rb ? ", byte-identical" : "");
+    if (exact_bytes)
+      EXPECT(gb == rb, "full artifact differs from the reference's bytes");
+    else
+      EXPECT(gb.size() == rb.size(), "full artifact size %zu vs %zu", gb.size(), rb.size());
     const auto fany = mgrx::decompress(gb);
     const auto& ff = std::get<mgrx::TensorField<T>>(fany);
     double fl = 0.0;
@@ -195,7 +207,7 @@ void check_shape(const mgrx::Dims& dims, double tol) {
 }
 
 int main() {
-  check_shape<double>({33, 33, 33}, 1e-12);
+  check_shape<double>({33, 33, 33}, 1e-12, /*exact_bytes=*/false);
   check_shape<float>({65, 65, 65}, 1e-5);
   check_shape<float>({40, 36, 66}, 1e-5);
   check_shape<double>({17, 12}, 1e-12);

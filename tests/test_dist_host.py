@@ -65,3 +65,21 @@ def test_reference_arm_nonzero_rank_exits_without_work():
         ref_threads = 1
 
     assert bench.run_reference(A(), 2, 1) is None
+
+
+def test_self_launch_two_ranks():
+    """`bench.py --gpus 2` outside torchrun spawns 2 ranks itself (gloo
+    plumbing check): one JSON line from rank 0 with n_gpus 2, max over ranks."""
+    import json
+    import subprocess
+
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dist-selftest"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [json.loads(x) for x in p.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    assert lines[0]["n_gpus"] == 2 and lines[0]["ms_per_step"] == 2.0
+    assert p.stderr.count("[bench] rank ") == 2

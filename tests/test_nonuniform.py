@@ -21,7 +21,7 @@ import numpy as np
 import pytest
 
 from oracle.oracle import Oracle
-from paper_2010_05872_b200.fields import nonuniform_coords
+from synthetic_fields import nonuniform_coords
 
 
 @pytest.fixture(scope="module")

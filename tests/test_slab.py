@@ -39,7 +39,7 @@ def test_slab_emulated_matches_single_gpu(shape, dtype, ranks):
     import torch
 
     import paper_2010_05872_b200 as mg
-    from paper_2010_05872_b200.fields import config2_field
+    from synthetic_fields import config2_field
     from paper_2010_05872_b200.slab import _fused_depth, slab_decompose, slab_recompose
 
     dt = torch.float64 if dtype == "f64" else torch.float32

@@ -4,11 +4,11 @@ captured recompose of the bench field and print the increments."""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2010_05872_b200 as mg  # noqa: E402
-from paper_2010_05872_b200.fields import config2_field  # noqa: E402
+from synthetic_fields import config2_field  # noqa: E402
 
 dims = tuple(int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "513,513,513").split(","))
 f = config2_field(dims, seed=0, device="cuda")

@@ -7,6 +7,7 @@ import subprocess
 import sys
 
 csv.field_size_limit(10**9)
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.abspath(__file__)))
 from tools_ncu_csv import SCALE
 
 WANT = [("gpu__time_duration.sum", "duration us", 1e6),

@@ -29,39 +29,39 @@ __global__ void k_dadd(double* out, double a) {
 // float -> double conversions (independent): F2F.F64.F32
 __global__ void k_f2d(double* out, float a) {
   float f[8];
-  double acc[8];
+  unsigned long long acc[8];
   for (int k = 0; k < 8; ++k) { f[k] = a * (threadIdx.x + k); acc[k] = 0; }
   for (int i = 0; i < ITERS; ++i) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       double d = (double)f[k];
       asm volatile("" : "+d"(d));
-      acc[k] = d;  // keep live
-      f[k] = __int_as_float(__float_as_int(f[k]) ^ 1);
+      acc[k] ^= __double_as_longlong(d);  // keep live
+      f[k] = __int_as_float(__float_as_int(f[k]) + 1);
     }
   }
-  double s = 0;
-  for (int k = 0; k < 8; ++k) s += acc[k];
-  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  unsigned long long s = 0;
+  for (int k = 0; k < 8; ++k) s ^= acc[k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = __longlong_as_double(s);
 }
 
 // double -> float conversions: F2F.F32.F64
 __global__ void k_d2f(float* out, double a) {
   double d[8];
-  float acc[8];
+  unsigned acc[8];
   for (int k = 0; k < 8; ++k) { d[k] = a * (threadIdx.x + k); acc[k] = 0; }
   for (int i = 0; i < ITERS; ++i) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       float f = __double2float_rn(d[k]);
       asm volatile("" : "+f"(f));
-      acc[k] = f;
-      d[k] = __longlong_as_double(__double_as_longlong(d[k]) ^ 1);
+      acc[k] ^= __float_as_uint(f);
+      d[k] = __longlong_as_double(__double_as_longlong(d[k]) + 1);
     }
   }
-  float s = 0;
-  for (int k = 0; k < 8; ++k) s += acc[k];
-  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  unsigned s = 0;
+  for (int k = 0; k < 8; ++k) s ^= acc[k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = __uint_as_float(s);
 }
 
 __global__ void k_shfl(float* out, float a) {
