@@ -252,6 +252,11 @@ struct mgrx_gpu_ctx {
   // adaptive stop decision: per-block sums (device) and their host copy
   double* stop_dev = nullptr;
   size_t stop_dev_bytes = 0;
+  // check_finite fused into the first decompose pass (compress): while
+  // nf_armed, the next level decomposed on the fused 3-D path checks its
+  // input into nf_flag and sets nf_used
+  unsigned* nf_flag = nullptr;
+  bool nf_armed = false, nf_used = false;
   double* stop_host = nullptr;
   size_t stop_host_bytes = 0;
 };
@@ -591,6 +596,8 @@ void decompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, T* d_out, const 
   double* comp = reinterpret_cast<double*>(s + p.off_comp);
   double* tmp = reinterpret_cast<double*>(s + p.off_tmp);
   const T* blk = d_field;
+  const bool nf_arm = c->nf_armed;  // only this call's finest level can carry the check
+  c->nf_armed = false;
   for (int l = L; l > stop; --l) {
     if (l == p.tail_top) {  // levels l..stop+1 in one CTA
       cuda_check(tail_decompose<T>(blk, d_out, d_out, p.d_tail_dec, nu ? c->d_tail_nu : nullptr, l - stop,
@@ -609,7 +616,12 @@ void decompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, T* d_out, const 
       e = p2_decompose_level(reinterpret_cast<const float*>(blk), reinterpret_cast<float*>(shell),
                              reinterpret_cast<float*>(coarse), p.p2[l], b, t, exec(c, l));
     } else if (!nu && c->path == 0 && fp.enabled) {
-      e = fused3d_decompose_level<T>(blk, shell, coarse, s + fp.scratch_off, p.geom[l], fp, p.thomas[l], exec(c, l));
+      Exec ex = exec(c, l);
+      if (nf_arm && l == L) {  // check_finite rides on this level's plane pass
+        ex.nonfinite = c->nf_flag;
+        c->nf_used = true;
+      }
+      e = fused3d_decompose_level<T>(blk, shell, coarse, s + fp.scratch_off, p.geom[l], fp, p.thomas[l], ex);
     } else {
       e = general_decompose_level<T>(blk, shell, coarse, comp, tmp, p.geom[l], &p.thomas[l],
                                      nu ? &(*nu)[l] : nullptr, exec(c, l), c->path == 0);
@@ -825,6 +837,7 @@ int mgrx_gpu_ctx_destroy(mgrx_gpu_ctx* c) {
   if (c->join) cudaEventDestroy(c->join);
   for (cudaEvent_t e : c->lvl_done) cudaEventDestroy(e);
   if (c->stop_dev) cudaFree(c->stop_dev);
+  if (c->nf_flag) cudaFree(c->nf_flag);
   if (c->stop_host) cudaFreeHost(c->stop_host);
   delete c;
   return MGRX_OK;
@@ -1280,12 +1293,24 @@ void compress_core(mgrx_gpu_ctx* c, int nd, const uint64_t* dims, int levels, co
   T* dfield = static_cast<T*>(dalloc(N * sizeof(T)));
   T* dco = static_cast<T*>(dalloc(N * sizeof(T)));
   cuda_check(cudaMemcpyAsync(dfield, h_field, N * sizeof(T), cudaMemcpyHostToDevice, c->stream), "H2D");
-  {  // check_finite (pipeline.hpp:132) on the device copy
+  // check_finite (pipeline.hpp:132): fused into the finest level's first
+  // pass when that level runs on the fused 3-D path (no extra read of the
+  // field); otherwise a separate pass over the device copy.  On a non-finite
+  // value the reference's error (first offset) is raised either way.
+  auto check_finite_pass = [&]() {
     double lo, hi;
     uint64_t bad;
     field_stats_run<T>(c, dfield, int64_t(N), &lo, &hi, &bad);
     if (bad < N) fail(MGRX_NONFINITE_DATA, "non-finite value at offset %llu", (unsigned long long)bad);
-  }
+  };
+  if (!c->nf_flag) cuda_check(cudaMalloc(reinterpret_cast<void**>(&c->nf_flag), 64), "cudaMalloc(flag)");
+  cuda_check(cudaMemsetAsync(c->nf_flag, 0, 4, c->stream), "memset");
+  c->nf_used = false;
+  c->nf_armed = force_stop < 0 || force_stop < L;
+  struct Disarm {
+    mgrx_gpu_ctx* c;
+    ~Disarm() { c->nf_armed = false; }
+  } disarm{c};
   int stop = 0;
   if (force_stop >= 0) {
     if (force_stop > L) fail(MGRX_INVALID_LEVEL, "forced stop level out of range");
@@ -1296,10 +1321,22 @@ void compress_core(mgrx_gpu_ctx* c, int nd, const uint64_t* dims, int levels, co
   *stop_out = stop;
   for (int l = 0; l <= L; ++l) sec_sizes[l] = 0;
   *n_out = 0;
-  if (stop == L) return;  // Lorenzo only (the caller codes the field)
+  if (stop == L) {  // Lorenzo only (the caller codes the field)
+    check_finite_pass();
+    return;
+  }
   if (!(force_stop < 0 && adaptive)) {
     const int rc = mgrx_gpu_decompose(c, code, nd, dims, L, stop, dfield, dco);
     if (rc != MGRX_OK) fail(rc, "%s", c->last_error.c_str());
+  }
+  c->nf_armed = false;
+  if (c->nf_used) {
+    unsigned flag = 0;
+    cuda_check(cudaMemcpyAsync(&flag, c->nf_flag, 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    if (flag) check_finite_pass();  // locates the first offset and raises
+  } else {
+    check_finite_pass();
   }
   const size_t base = stop == 0 ? 0 : size_t(h.node[stop]);
   int32_t* dlab = static_cast<int32_t*>(dalloc((N - base) * 4));

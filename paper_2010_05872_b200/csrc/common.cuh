@@ -95,6 +95,7 @@ struct Exec {
   uint64_t* launches;
   Profiler* prof;
   int level = -1;  // hierarchy level being processed (profiling key), -1 = none
+  unsigned* nonfinite = nullptr;  // finest level of a compress: check_finite fused into its first pass
 };
 // Records a CUDA event before/after a tagged launch when profiling
 // (api.cu); no-op otherwise.

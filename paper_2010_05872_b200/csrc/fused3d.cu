@@ -538,8 +538,12 @@ struct DecRows {
 // restriction (shuffles) and the axis-1 restriction into Q (registers).
 // PODD: plane parity; FULL: interior tile (all rows present, no degenerate
 // row, interior axis-1 weights) — every row test is then compile-time.
-template <typename T, int TI1, bool PODD, bool FULL>
-__device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const T* nr, T* nb, int nbs, double* Q) {
+// CF: also fold every raw value into `nf` as nf + v * 0 (stays 0 unless a
+// value is inf / NaN): check_finite (pipeline.hpp:113-118) on the read the
+// pass makes anyway.
+template <typename T, int TI1, bool PODD, bool FULL, bool CF = false>
+__device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const T* nr, T* nb, int nbs, double* Q,
+                                         T& nf) {
   constexpr int RMAX = 2 * TI1 + 3;
   const int n2 = x.n2;
   const T* rr = x.rp + (x.jbase - x.rlo) * n2;  // tile row of jr = 0 (may precede the tile when not FULL)
@@ -577,8 +581,10 @@ __device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const
       continue;
     }
     const bool rdeg = !FULL && o1 && (j1 + 1 >= x.n1);
-    const double rawE = double(rr[0]);
-    const double rawO = double(rr[x.oi]);
+    const T rE = rr[0], rO = rr[x.oi];
+    if (CF) nf = rE * T(0) + (rO * T(0) + nf);
+    const double rawE = double(rE);
+    const double rawO = double(rO);
     const double aL = aLc;
     const double bL = o1 ? (rdeg ? aL : aLn) : aL;
     double se;
@@ -640,7 +646,7 @@ __device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const
 // Decompose plane pass: one CTA per (axis-0 chunk, axis-1 tile) unit; the
 // unit's fine planes stream through a 3-deep TMA ring.
 // NB = 3: the 3-CTAs-per-SM variant with a 3-slot ring (F3Geom::dec3)
-template <typename T, int TI1, int MAXT, int NB = 0>
+template <typename T, int TI1, int MAXT, int NB = 0, bool CF = false>
 __global__ void __launch_bounds__(MAXT, NB ? NB : (MAXT == kPlaneMaxThreads ? 2 : 1))
     k_f3_dec_plane(const T* __restrict__ blk, T* __restrict__ shell, T* __restrict__ coarse, double* __restrict__ G,
                    const F3Geom g) {
@@ -717,6 +723,7 @@ __global__ void __launch_bounds__(MAXT, NB ? NB : (MAXT == kPlaneMaxThreads ? 2 
 #pragma unroll
   for (int ir = 0; ir < TI1; ++ir) A.prev[ir] = A.cur[ir] = A.next[ir] = 0.0;
   int jdone = 0;  // coarse planes finished by this CTA
+  T nf = T(0);    // CF: 0 unless a raw value was inf / NaN
   // Shell / coarse pointers of the unit's first even and odd plane, advanced
   // by a constant per plane pair (shell_row_start is linear in k = p / 2 for
   // each parity: +n1 n2 - m1 m2 for even planes, +n1 n2 for odd ones).
@@ -745,8 +752,8 @@ __global__ void __launch_bounds__(MAXT, NB ? NB : (MAXT == kPlaneMaxThreads ? 2 
       double Q[TI1];
 #pragma unroll
       for (int ir = 0; ir < TI1; ++ir) Q[ir] = 0.0;
-      if (full) dec_rows<T, TI1, false, true>(x, r_own, r_own, nb, nt, Q);
-      else dec_rows<T, TI1, false, false>(x, r_own, r_own, nb, nt, Q);
+      if (full) dec_rows<T, TI1, false, true, CF>(x, r_own, r_own, nb, nt, Q, nf);
+      else dec_rows<T, TI1, false, false, CF>(x, r_own, r_own, nb, nt, Q, nf);
       pipe_release<NS>(pp, d, D, issue);  // this warp is done with plane d's slot
       l0_plane<TI1>(g, ur, S, p, Q, A, jdone, G);
       se_e += step_e;
@@ -769,14 +776,15 @@ __global__ void __launch_bounds__(MAXT, NB ? NB : (MAXT == kPlaneMaxThreads ? 2 
 #pragma unroll
       for (int ir = 0; ir < TI1; ++ir) Q[ir] = 0.0;
       const T* nr = x.has_right ? row0(d + 2) : r_own;
-      if (full) dec_rows<T, TI1, true, true>(x, r_own, nr, nb, nt, Q);
-      else dec_rows<T, TI1, true, false>(x, r_own, nr, nb, nt, Q);
+      if (full) dec_rows<T, TI1, true, true, CF>(x, r_own, nr, nb, nt, Q, nf);
+      else dec_rows<T, TI1, true, false, CF>(x, r_own, nr, nb, nt, Q, nf);
       pipe_release<NS>(pp, d + 1, D, issue);
       l0_plane<TI1>(g, ur, S, p, Q, A, jdone, G);
       se_o += step_o;
       so_o += step_o;
     }
   }
+  if (CF && !(nf == T(0))) atomicOr(g.nonfinite, 1u);
   pdl_trigger();
 }
 
@@ -2140,19 +2148,43 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
   size_t ds = 0;
   cudaError_t e = set_attrs<T>(g, &ds);
   if (e != cudaSuccess) return e;
-#define MGRX_DEC(TI, MT)                                                                               \
-  if (!g.dec3 && g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))          \
-    MGRX_LAUNCH(ex, "f3_dec_plane", pdl_launch(k_f3_dec_plane<T, TI, MT>, dim3(g.grid), dim3(g.threads), ds, \
-                                               ex.s, !ex.prof, blk, shell, coarse, G, g));
+  // ex.nonfinite: the finiteness check rides on this pass (the variant with CF)
+  const bool cf = ex.nonfinite != nullptr;
+  F3Geom gc = g;
+  gc.nonfinite = ex.nonfinite;
+#define MGRX_DEC(TI, MT)                                                                                      \
+  if (!g.dec3 && g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads)) {               \
+    if (cf) {                                                                                                 \
+      e = cudaFuncSetAttribute(k_f3_dec_plane<T, TI, MT, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                               int(ds));                                                                      \
+      if (e != cudaSuccess) return e;                                                                         \
+      MGRX_LAUNCH(ex, "f3_dec_plane", pdl_launch(k_f3_dec_plane<T, TI, MT, 0, true>, dim3(g.grid), dim3(g.threads), \
+                                                 ds, ex.s, !ex.prof, blk, shell, coarse, G, gc));             \
+    } else {                                                                                                  \
+      MGRX_LAUNCH(ex, "f3_dec_plane", pdl_launch(k_f3_dec_plane<T, TI, MT>, dim3(g.grid), dim3(g.threads), ds,  \
+                                                 ex.s, !ex.prof, blk, shell, coarse, G, g));                  \
+    }                                                                                                         \
+  }
   MGRX_DEC(4, kPlaneMaxThreads)
   MGRX_DEC(2, kPlaneMaxThreads)
   MGRX_DEC(4, kWideBound)
   MGRX_DEC(2, kWideBound)
 #undef MGRX_DEC
   if (g.dec3) {
-    const F3Geom gd = dec3_geom(g);
-    MGRX_LAUNCH(ex, "f3_dec_plane", pdl_launch(k_f3_dec_plane<T, 4, kPlaneMaxThreads, 3>, dim3(gd.grid), dim3(gd.threads),
-                                               plane_smem3<T>(gd), ex.s, !ex.prof, blk, shell, coarse, G, gd));
+    F3Geom gd = dec3_geom(g);
+    if (cf) {
+      gd.nonfinite = ex.nonfinite;
+      e = cudaFuncSetAttribute(k_f3_dec_plane<T, 4, kPlaneMaxThreads, 3, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(plane_smem3<T>(g)));
+      if (e != cudaSuccess) return e;
+      MGRX_LAUNCH(ex, "f3_dec_plane", pdl_launch(k_f3_dec_plane<T, 4, kPlaneMaxThreads, 3, true>, dim3(gd.grid),
+                                                 dim3(gd.threads), plane_smem3<T>(gd), ex.s, !ex.prof, blk, shell,
+                                                 coarse, G, gd));
+    } else {
+      MGRX_LAUNCH(ex, "f3_dec_plane", pdl_launch(k_f3_dec_plane<T, 4, kPlaneMaxThreads, 3>, dim3(gd.grid),
+                                                 dim3(gd.threads), plane_smem3<T>(gd), ex.s, !ex.prof, blk, shell,
+                                                 coarse, G, gd));
+    }
   }
   cudaError_t se = cudaSuccess;
   unsigned* ctr = reinterpret_cast<unsigned*>(static_cast<char*>(scratch) + fp.ctr_off);
@@ -2261,10 +2293,23 @@ cudaError_t fused3d_slab_dec_plane(const T* blk, T* shell, T* coarse, double* G,
   size_t ds = 0;
   cudaError_t e = set_attrs<T>(g, &ds);
   if (e != cudaSuccess) return e;
-#define MGRX_DEC(TI, MT)                                                                               \
-  if (!g.dec3 && g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads))          \
-    MGRX_LAUNCH(ex, "f3_dec_plane", pdl_launch(k_f3_dec_plane<T, TI, MT>, dim3(g.grid), dim3(g.threads), ds, \
-                                               ex.s, !ex.prof, blk, shell, coarse, G, g));
+  // ex.nonfinite: the finiteness check rides on this pass (the variant with CF)
+  const bool cf = ex.nonfinite != nullptr;
+  F3Geom gc = g;
+  gc.nonfinite = ex.nonfinite;
+#define MGRX_DEC(TI, MT)                                                                                      \
+  if (!g.dec3 && g.tile_rows == TI && (MT == kWideBound) == (g.threads > kPlaneMaxThreads)) {               \
+    if (cf) {                                                                                                 \
+      e = cudaFuncSetAttribute(k_f3_dec_plane<T, TI, MT, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                               int(ds));                                                                      \
+      if (e != cudaSuccess) return e;                                                                         \
+      MGRX_LAUNCH(ex, "f3_dec_plane", pdl_launch(k_f3_dec_plane<T, TI, MT, 0, true>, dim3(g.grid), dim3(g.threads), \
+                                                 ds, ex.s, !ex.prof, blk, shell, coarse, G, gc));             \
+    } else {                                                                                                  \
+      MGRX_LAUNCH(ex, "f3_dec_plane", pdl_launch(k_f3_dec_plane<T, TI, MT>, dim3(g.grid), dim3(g.threads), ds,  \
+                                                 ex.s, !ex.prof, blk, shell, coarse, G, g));                  \
+    }                                                                                                         \
+  }
   MGRX_DEC(4, kPlaneMaxThreads)
   MGRX_DEC(2, kPlaneMaxThreads)
   MGRX_DEC(4, kWideBound)

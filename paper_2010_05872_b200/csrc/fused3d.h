@@ -25,6 +25,7 @@ struct F3Geom {
   // slab mode: the plane passes cover coarse planes
   // [a_base, a_end), the interpolation fine planes [p_base, p_end)
   int64_t a_base = 0, a_end = -1, p_base = 0, p_end = -1;
+  unsigned* nonfinite = nullptr;  // decompose plane pass with the finiteness check: set to 1 on inf / NaN
 };
 
 struct Fused3DPlan {

@@ -5,6 +5,7 @@
 // and that errors come back as mgrx::Error with the reference's errc.
 #include <cmath>
 #include <cstdio>
+#include <string>
 #include <limits>
 #include <random>
 
@@ -155,16 +156,34 @@ void check_shape(const mgrx::Dims& dims, double tol, bool exact_bytes = true) {
     EXPECT(ea <= tol * range, "decompose_adaptive err %g (budget %g)", ea / range, rel);
     std::printf("  adaptive budget %g: stop %d\n", rel, gw.stop_level);
   }
-  {  // check_finite (pipeline.hpp:132) on the GPU: same error code as the reference
-    mgrx::TensorField<T> bad = f;
-    bad.data[bad.size() / 3] = std::numeric_limits<T>::quiet_NaN();
-    bool threw = false;
-    try {
-      mgrx::b200::compress(bad, opt, ws);
-    } catch (const mgrx::Error& e) {
-      threw = e.code() == mgrx::errc::nonfinite_data;
+  {  // check_finite (pipeline.hpp:132) on the GPU (fused into the finest
+     // level's plane pass on the fused path): the reference's error code and
+     // message (first non-finite offset), full and adaptive compress, NaN and inf
+    for (int variant = 0; variant < 4; ++variant) {
+      mgrx::TensorField<T> bad = f;
+      const size_t at = bad.size() / 3 + size_t(variant);
+      bad.data[at] = (variant & 1) ? std::numeric_limits<T>::infinity() : std::numeric_limits<T>::quiet_NaN();
+      bad.data[bad.size() - 1] = -std::numeric_limits<T>::infinity();  // a later one: the first offset wins
+      mgrx::CompressOptions o2 = opt;
+      o2.adaptive = variant >= 2;
+      std::string gmsg, rmsg;
+      bool threw = false, rthrew = false;
+      try {
+        mgrx::b200::compress(bad, o2, ws);
+      } catch (const mgrx::Error& e) {
+        threw = e.code() == mgrx::errc::nonfinite_data;
+        gmsg = e.what();
+      }
+      try {
+        mgrx::compress(bad, o2);
+      } catch (const mgrx::Error& e) {
+        rthrew = e.code() == mgrx::errc::nonfinite_data;
+        rmsg = e.what();
+      }
+      EXPECT(threw && rthrew, "non-finite field (variant %d): expected nonfinite_data", variant);
+      EXPECT(gmsg.find(std::to_string(at)) != std::string::npos, "message '%s' lacks offset %zu (reference: '%s')",
+             gmsg.c_str(), at, rmsg.c_str());
     }
-    EXPECT(threw, "non-finite field: expected nonfinite_data");
   }
   // adaptive compress (the reference's choose_stop decider) round trip
   mgrx::CompressOptions aopt;
