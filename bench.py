@@ -625,10 +625,24 @@ def quant_measure(mg, wsp, field, h, args):
     nb = field.numel() * (field.element_size() + 4)
     back = mg.recompose(d, wsp)
     linf = float((back - field).abs().max().item())
+    # kernel-level device times (library profiler) of one quantize + dequantize
+    wsp.profile_begin()
+    s = mg.quantize(mc, plan, wsp)
+    mg.dequantize(s, plan, h, wsp)
+    prof = {kk: v[0] * 1e3 for kk, v in wsp.profile_end().items()}
+    peak, _ = measured_peak()
+    kern = {}
+    for name in ("quant_labels", "dequant"):
+        us = prof.get(name)
+        if us:
+            kern[name] = {"us": us, "achieved_gbs": nb / (us * 1e-6) / 1e9, "frac": nb / (us * 1e-6) / 1e9 / peak}
     return {"quantize_ms": q_ms, "dequantize_ms": d_ms, "quantize_gbs": nb / (q_ms * 1e-3) / 1e9,
-            "dequantize_gbs": nb / (d_ms * 1e-3) / 1e9, "outliers": int(s.outlier_positions.numel()),
+            "dequantize_gbs": nb / (d_ms * 1e-3) / 1e9, "quantize_frac": nb / (q_ms * 1e-3) / 1e9 / peak,
+            "dequantize_frac": nb / (d_ms * 1e-3) / 1e9 / peak, "kernels_us": prof, "kernel_roofline": kern,
+            "alg_bytes": nb, "outliers": int(s.outlier_positions.numel()),
             "linf_over_tau": linf / (1e-3 * rg), "tau": "1e-3 * range, budget tau/4",
-            "note": "quantize includes the outlier-count readback (synchronous, as the reference's API)"}
+            "note": "whole calls include the outlier-count readback (synchronous, as the reference's API); "
+                    "bytes N*s + 4N each way (SURVEY 8(d))"}
 
 
 def e2e_measure(mg, wsp, field, h, args, workers=2):

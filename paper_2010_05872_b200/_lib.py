@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmgrx_b200.so")
+LIB_PATH = os.environ.get("MGRX_LIB_PATH") or os.path.join(HERE, "libmgrx_b200.so")  # override: A/B builds (development)
 
 # Every symbol include/mgrx_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = (

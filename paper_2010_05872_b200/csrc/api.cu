@@ -1020,6 +1020,18 @@ int mgrx_gpu_quantize(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, 
       e = quantize_pass1<double>(static_cast<const double*>(d_coeffs), d_labels, counts, offsets, flags, ql,
                                  exec(c));
     cuda_check(e, "quantize");
+    // the ordered outlier pass runs without waiting for the total: it
+    // writes the outliers that fit the capacity; one readback then gives the
+    // count (capacity exceeded: the caller retries with the exact count)
+    if (d_opos && d_oval && capacity > 0) {
+      if (dtype == MGRX_F32)
+        e = quantize_pass2<float>(static_cast<const float*>(d_coeffs), counts, offsets, d_opos,
+                                  static_cast<float*>(d_oval), capacity, ql, exec(c));
+      else
+        e = quantize_pass2<double>(static_cast<const double*>(d_coeffs), counts, offsets, d_opos,
+                                   static_cast<double*>(d_oval), capacity, ql, exec(c));
+      cuda_check(e, "quantize outliers");
+    }
     uint64_t* hp = static_cast<uint64_t*>(c->pinned);
     cuda_check(cudaMemcpyAsync(hp, offsets + nch, 8, cudaMemcpyDeviceToHost, c->stream), "readback");
     cuda_check(cudaMemcpyAsync(hp + 1, flags, 4, cudaMemcpyDeviceToHost, c->stream), "readback");
@@ -1030,17 +1042,7 @@ int mgrx_gpu_quantize(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, 
     if (flag) fail(MGRX_NONFINITE_DATA, "non-finite value in quantizer input");
     if (total > capacity) fail(MGRX_CAPACITY_EXCEEDED, "%llu outliers exceed capacity %llu",
                                (unsigned long long)total, (unsigned long long)capacity);
-    if (total > 0) {
-      if (!d_opos || !d_oval) fail(MGRX_INVALID_ARGUMENT, "null outlier buffers");
-      if (dtype == MGRX_F32)
-        e = quantize_pass2<float>(static_cast<const float*>(d_coeffs), counts, offsets, d_opos,
-                                  static_cast<float*>(d_oval), capacity, ql, exec(c));
-      else
-        e = quantize_pass2<double>(static_cast<const double*>(d_coeffs), counts, offsets, d_opos,
-                                   static_cast<double*>(d_oval), capacity, ql, exec(c));
-      cuda_check(e, "quantize outliers");
-      cuda_check(cudaStreamSynchronize(c->stream), "quantize sync");
-    }
+    if (total > 0 && (!d_opos || !d_oval)) fail(MGRX_INVALID_ARGUMENT, "null outlier buffers");
   });
 }
 

@@ -91,6 +91,9 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+#ifndef MGRX_WAIT_MODE
+#define MGRX_WAIT_MODE 0
+#endif
 #ifndef MGRX_MBAR_SPIN_LIMIT
 #define MGRX_MBAR_SPIN_LIMIT 0  // > 0: trap with a message after that many failed polls (debug)
 #endif
@@ -111,6 +114,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (t0 == 0) t0 = global_ns();
     if (global_ns() - t0 > uint64_t(MGRX_MBAR_SPIN_LIMIT)) asm volatile("trap;");
   }
+#elif MGRX_WAIT_MODE == 1
+  // plain try_wait (no suspend-time hint)
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) break;
+  }
+#elif MGRX_WAIT_MODE == 2
+  while (!mbar_try(bar, parity)) __nanosleep(200);
 #else
   while (!mbar_try(bar, parity)) {
   }
@@ -123,6 +141,46 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+
+// L2 residency hints for the fp64 volume G (136 MB at 513^3, next to a
+// 126 MB L2): its producer stores it with evict_last so the row / column
+// passes that follow find it in L2, while the streamed field reads are
+// marked evict_first.  g_l2hint = 0 (MGRX_NO_L2HINT) turns the policies
+// into evict_normal.
+__device__ int g_l2hint = 1;
+__device__ __forceinline__ uint64_t pol_keep() {
+  uint64_t p;
+  if (g_l2hint)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_stream() {
+  uint64_t p;
+  if (g_l2hint)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_pol(double* a, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ double ld_pol(const double* a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+// bulk copy global -> shared with an L2 policy
+__device__ __forceinline__ void bulk_g2s_pol(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
 
@@ -450,9 +508,10 @@ __device__ __forceinline__ void l0_complete(const F3Geom& g, const UnitRange& ur
   const int TR = int(ur.b1 - ur.b0);
   if (S.owned) {
     double* gp = G + (i0 * g.m1 + ur.b0) * g.m2 + S.c;
+    const uint64_t pol = pol_keep();
 #pragma unroll
     for (int ir = 0; ir < TI1; ++ir)
-      if (ir < TR) gp[int64_t(ir) * g.m2] = v[ir];
+      if (ir < TR) st_pol(gp + int64_t(ir) * g.m2, v[ir], pol);
   }
   ++j;
 }
@@ -706,7 +765,7 @@ __global__ void __launch_bounds__(MAXT, NB ? NB : (MAXT == kPlaneMaxThreads ? 2 
     bulk_span<T>(tile_src(d), 0, int64_t(R) * n2, &src, &bytes, &ld);
     fence_proxy_async();
     mbar_expect_tx(&pp->full[sl], bytes);
-    bulk_g2s(raw + size_t(sl) * rawb, src, bytes, &pp->full[sl]);
+    bulk_g2s_pol(raw + size_t(sl) * rawb, src, bytes, &pp->full[sl], pol_stream());
   };
   // tile row jbase of plane d, column 2 cc (the row may precede the slot
   // when not FULL; never read then); the 16-byte lead of a plane's bulk copy
@@ -1130,6 +1189,7 @@ __global__ void __launch_bounds__(256, kRowCtas(NC)) k_f3_row(double* __restrict
   pdl_wait();
   const int64_t step = int64_t(gridDim.x) * nw;
   int64_t r = int64_t(blockIdx.x) * nw + warp;
+  const uint64_t pkeep = pol_keep(), pstream = pol_stream();
   double t[NC];
   // rows are walked from the last one down: the producer of G (plane pass)
   // wrote the high planes last, so they are the likeliest L2 hits
@@ -1137,7 +1197,7 @@ __global__ void __launch_bounds__(256, kRowCtas(NC)) k_f3_row(double* __restrict
     const int64_t row = rows - 1 - rr;
     const double* gr = G + row * m + lane;
 #pragma unroll
-    for (int k = 0; k < NC; ++k) t[k] = (lane + 32 * k < m) ? __ldcs(gr + 32 * k) : 0.0;
+    for (int k = 0; k < NC; ++k) t[k] = (lane + 32 * k < m) ? ld_pol(gr + 32 * k, pstream) : 0.0;
   };
   if (r < rows) load(r);
   for (; r < rows; r += step) {
@@ -1150,7 +1210,7 @@ __global__ void __launch_bounds__(256, kRowCtas(NC)) k_f3_row(double* __restrict
     double* gr = G + (rows - 1 - r) * m;
 #pragma unroll
     for (int k = 0; k < NC; ++k)
-      if (lane + 32 * k < m) gr[lane + 32 * k] = buf[lane + 32 * k];
+      if (lane + 32 * k < m) st_pol(gr + lane + 32 * k, buf[lane + 32 * k], pkeep);
     __syncwarp();
   }
 }
@@ -1213,9 +1273,11 @@ __global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : (MAXT == kColT
   pdl_wait();
   {
     const double* gp = G + base + int64_t(s0) * stride;
+    // the axis-0 pass reads G for the last time (evict first); axis 1 keeps it
+    const uint64_t pol = APPLY ? pol_stream() : pol_keep();
 #pragma unroll
     for (int k = 0; k < LS; ++k) {
-      v[k] = (valid && k < len) ? *gp : 0.0;
+      v[k] = (valid && k < len) ? ld_pol(gp, pol) : 0.0;
       gp += stride;
     }
   }
@@ -1275,9 +1337,10 @@ __global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : (MAXT == kColT
     }
   } else {
     double* gp = G + base + int64_t(s0) * stride;
+    const uint64_t pol = pol_keep();
 #pragma unroll
     for (int k = 0; k < LS; ++k) {
-      if (k < len) *gp = v[k];
+      if (k < len) st_pol(gp, v[k], pol);
       gp += stride;
     }
   }
@@ -1993,6 +2056,11 @@ static void row_col1(double* G, const F3Geom& g, const ThomasLevel& th, const Ex
 
 Fused3DPlan fused3d_plan(const LevelGeom& lg, int esize) {
   Fused3DPlan fp;
+  {
+    static const int hint = std::getenv("MGRX_NO_L2HINT") ? 0 : 1;
+    cudaMemcpyToSymbol(g_l2hint, &hint, sizeof(int));
+
+  }
   if (lg.d != 3) return fp;
   F3Geom& g = fp.g;
   g.n0 = lg.n[0];
