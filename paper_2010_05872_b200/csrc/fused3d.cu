@@ -8,22 +8,26 @@
 // of the level block:
 //
 //   decompose  f3_dec_plane  streams fine planes (TMA bulk copies into a
-//                            3-deep shared-memory ring), computes every
+//                            3- or 4-slot shared-memory ring), computes every
 //                            coefficient (same corner order as
 //                            update_coefficients), writes the shell straight
 //                            into its level-centric position and the nodal
 //                            values into the compact coarse block, and
 //                            accumulates the load vector L0 L1 L2 c of the
-//                            fp64 component in registers/shared memory; once
-//                            a coarse plane is complete its rows are solved
-//                            along axis 2 (warp-parallel Thomas) and written
-//                            to the fp64 volume G.
+//                            fp64 component in registers; a finished coarse
+//                            plane's rows go to the fp64 volume G (optionally
+//                            also check_finite of every value it reads).
+//              f3_row        Thomas along axis 2 on G, in place (a warp per row).
 //              f3_col (axis 1)  Thomas along axis 1 on G, in place.
 //              f3_col (axis 0)  Thomas along axis 0 + coarse += z.
 //   recompose  f3_rec_plane  same load-vector accumulation, reading the
 //                            component from the shell;
-//              f3_col x2     as above, coarse -= z;
+//              f3_row, f3_col x2  as above, coarse -= z;
 //              f3_rec_interp fine block = coarse nodes + shell + prediction.
+//
+// Measured and kept opt-in (slower at 513^3): the in-plane
+// cluster solve f3_s12 (axes 2 + 1 in one pass over G through DSMEM,
+// MGRX_S12=1) and the one-launch dataflow solve f3_solveq (MGRX_SOLVEQ=1).
 //
 // The tensor-product correction z = S2 S1 S0 c (S_a = Thomas_a o Load_a,
 // transform.hpp:392-428) is evaluated as (T0 T1 T2)(L0 L1 L2) c: the
