@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "fused2d.h"
 #include "fused3d.h"
 #include "p2.h"
 #include "kernels.h"
@@ -161,6 +162,7 @@ struct Plan {
   size_t off_comp = 0, off_tmp = 0, off_blk = 0, bytes = 0;
   std::vector<size_t> blk_off;     // level block offsets (levels stop..L-1)
   std::vector<Fused3DPlan> fused;  // index l; .enabled false when not applicable
+  std::vector<Fused2DPlan> f2;     // index l; fused 2-D passes of nonuniform-coordinate calls
   std::vector<P2Plan> p2;          // index l; second-generation fused passes (fp32)
   double* d_p2tabs = nullptr;      // their tables
   const void* p2_scratch = nullptr;  // scratch the p2 counters were zeroed for
@@ -420,6 +422,14 @@ Plan* get_plan(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int lev
       off = align_up(off + p->fused[l].scratch_bytes);
     }
   }
+  p->f2.resize(L + 1);
+  for (int l = stop + 1; l <= L; ++l) {
+    p->f2[l] = fused2d_plan(p->geom[l]);
+    if (p->f2[l].enabled) {
+      p->f2[l].scratch_off = off;
+      off = align_up(off + p->f2[l].scratch_bytes);
+    }
+  }
   if (!p2host.empty()) {
     cuda_check(cudaMalloc(&p->d_p2tabs, p2host.size() * sizeof(double)), "cudaMalloc(p2 tables)");
     cuda_check(cudaMemcpy(p->d_p2tabs, p2host.data(), p2host.size() * sizeof(double), cudaMemcpyHostToDevice),
@@ -615,6 +625,8 @@ void decompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, T* d_out, const 
       p2_bind(p.p2[l], s + p.p2[l].scratch_off, p.d_p2tabs, &b, &t);
       e = p2_decompose_level(reinterpret_cast<const float*>(blk), reinterpret_cast<float*>(shell),
                              reinterpret_cast<float*>(coarse), p.p2[l], b, t, exec(c, l));
+    } else if (nu && c->path == 0 && p.f2[l].enabled) {
+      e = fused2d_decompose_level<T>(blk, shell, coarse, s + p.f2[l].scratch_off, p.f2[l], (*nu)[l], exec(c, l));
     } else if (!nu && c->path == 0 && fp.enabled) {
       Exec ex = exec(c, l);
       if (nf_arm && l == L) {  // check_finite rides on this level's plane pass
@@ -728,6 +740,9 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
       } else {
         e = fused3d_recompose_finish<T>(shell, coarse, fine, s + fp.scratch_off, fp, p.thomas[l], exec_on(c, cs, l));
       }
+    } else if (nu && c->path == 0 && p.f2[l].enabled) {
+      e = fused2d_recompose_level<T>(shell, coarse, fine, s + p.f2[l].scratch_off, p.f2[l], (*nu)[l],
+                                     exec_on(c, cs, l));
     } else if (!nu && c->path == 0 && fp.enabled) {
       e = fused3d_recompose_level<T>(shell, coarse, fine, s + fp.scratch_off, p.geom[l], fp, p.thomas[l],
                                      exec_on(c, cs, l));
