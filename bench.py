@@ -714,8 +714,8 @@ def run_slab(args, ws, rank, local):
 
     import paper_2010_05872_b200 as mg
     from synthetic_fields import config2_field
-    from paper_2010_05872_b200.slab import LocalExchange, TorchExchange, max_slab_levels, slab_bounds, \
-        slab_decompose, slab_recompose
+    from paper_2010_05872_b200.slab import LocalExchange, PlaneSlab, TorchExchange, max_slab_levels, \
+        owned_planes, slab_bounds, slab_decompose, slab_recompose
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -726,22 +726,30 @@ def run_slab(args, ws, rank, local):
     R = ex.world
     S = max_slab_levels(h, R)
     P = slab_bounds(DIMS[0], R, S)
-    fields = [field.clone() for _ in ex.local]
+    plane = DIMS[1] * DIMS[2]
+    fields = []
+    for r in ex.local:  # each rank holds only its own planes
+        lo, hi = owned_planes(P, r, DIMS[0])
+        s = PlaneSlab(lo, hi, plane, field.dtype, dev)
+        s.t.copy_(field.reshape(DIMS[0], -1)[lo:hi])
+        fields.append(s)
     wss = [mg.SolverWorkspace(device=local) for _ in ex.local]
     stream = torch.cuda.current_stream(dev)
 
     def step():
         outs = slab_decompose(fields, h, ex, wss, S)
-        return slab_recompose(outs, h, ex, wss, S)
+        return slab_recompose(outs, h, ex, wss), outs
 
     for _ in range(max(args.warmup, 1)):
-        backs = step()
+        backs, outs = step()
     torch.cuda.synchronize()
     err = 0.0
+    fv = field.reshape(DIMS[0], -1)
     for i, r in enumerate(ex.local):
-        hi = P[r + 1] if r + 1 < R else DIMS[0]
-        d = (backs[i][P[r]:hi] - field[P[r]:hi]).abs()
+        lo, hi = owned_planes(P, r, DIMS[0])
+        d = (backs[i].planes(lo, hi) - fv[lo:hi]).abs()
         err = max(err, float("inf") if bool(torch.isnan(d).any()) else float(d.max().item()))
+    rank_bytes = max(o.nbytes() for o in outs)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier(ws)
     torch.cuda.synchronize()
@@ -759,6 +767,7 @@ def run_slab(args, ws, rank, local):
                 "config": {"workload": WORKLOAD + " -- slab mode (one field split along axis 0)",
                            "field": list(DIMS), "field_dtype": "f32", "ranks": R, "slab_levels": S,
                            "slab_bounds": P, "emulated_on_one_gpu": emul,
+                           "coefficient_bytes_per_rank": rank_bytes,
                            "parallelism": f"slab{R}" + (" (emulated: time is the sum over ranks)" if emul else "")},
                 "roundtrip_linf": err}
         print(json.dumps(line), flush=True)

@@ -261,13 +261,21 @@ int mgrx_gpu_slab_level(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t*
 /* Decompose plane pass for coarse planes [k0, k1): coefficients of the fine
  * planes [2 k0, 2 k1) (and n0 - 1 when k1 = m0) into `out`'s shell, their
  * nodal values into `coarse`, the axis-0/1/2 load vector into G[k0, k1).
- * Reads fine planes [2 k0 - 2, 2 k1] of `blk`. */
+ * Reads fine planes [2 k0 - 2, 2 k1] of `blk`.
+ *
+ * All buffers are indexed globally (plane p of blk at p * n1 * n2, shell
+ * entries at their level-centric position).  A rank may hold only its slab:
+ * pass base pointers shifted back by the global offset of its first element
+ * (only the planes named above are touched), and keep the shells of its even
+ * and odd fine planes as two runs — odd_shift (elements) is added to the
+ * position of every odd plane's shell entry (0 for one global buffer). */
 int mgrx_gpu_slab_dec_plane(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels, int level,
-                            uint64_t k0, uint64_t k1, const void* d_blk, void* d_out, void* d_coarse, double* d_G);
+                            uint64_t k0, uint64_t k1, const void* d_blk, void* d_out, void* d_coarse, double* d_G,
+                            int64_t odd_shift);
 /* Recompose plane pass: the load vector of the shell's coefficients (reads
  * the shells of fine planes [2 k0 - 2, 2 k1]) into G[k0, k1). */
 int mgrx_gpu_slab_rec_plane(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels, int level,
-                            uint64_t k0, uint64_t k1, const void* d_coeffs, double* d_G);
+                            uint64_t k0, uint64_t k1, const void* d_coeffs, double* d_G, int64_t odd_shift);
 /* Axis-2 and axis-1 solves (batched_solve, transform.hpp:116-130) of G's
  * planes [k0, k1), in place. */
 int mgrx_gpu_slab_inplane(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels, int level,
@@ -282,7 +290,15 @@ int mgrx_gpu_slab_apply(mgrx_gpu_ctx* ctx, int dtype, void* d_coarse, const doub
 /* Recompose interpolation of the fine planes [p0, p1) (p0 even) from the
  * corrected coarse block (planes [p0 / 2, (p1 + 1) / 2]) and the shell. */
 int mgrx_gpu_slab_interp(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels, int level,
-                         uint64_t p0, uint64_t p1, const void* d_coeffs, const void* d_coarse, void* d_fine);
+                         uint64_t p0, uint64_t p1, const void* d_coeffs, const void* d_coarse, void* d_fine,
+                         int64_t odd_shift);
+/* K-pack for the all-to-all of slab mode: dst[q] = the rows x (c1 - c0)
+ * block of src (row pitch `pitch` doubles) at columns [cb[q], cb[q+1]) for
+ * q < nparts, packed back to back (unpack: the inverse scatter). */
+int mgrx_gpu_slab_pack(mgrx_gpu_ctx* ctx, const double* d_src, uint64_t rows, uint64_t pitch, const uint64_t* cb,
+                       int nparts, double* d_dst);
+int mgrx_gpu_slab_unpack(mgrx_gpu_ctx* ctx, const double* d_src, uint64_t rows, uint64_t pitch, const uint64_t* cb,
+                         int nparts, double* d_dst);
 
 #ifdef __cplusplus
 }

@@ -21,7 +21,7 @@ EXPORTS = (
     "mgrx_gpu_workspace_size",
     "mgrx_gpu_choose_stop", "mgrx_host_decompose_adaptive", "mgrx_gpu_encode_labels", "mgrx_host_compress", "mgrx_gpu_field_stats", "mgrx_host_lorenzo",
     "mgrx_gpu_slab_level", "mgrx_gpu_slab_dec_plane", "mgrx_gpu_slab_rec_plane", "mgrx_gpu_slab_inplane",
-    "mgrx_gpu_slab_axis0", "mgrx_gpu_slab_apply", "mgrx_gpu_slab_interp",
+    "mgrx_gpu_slab_axis0", "mgrx_gpu_slab_apply", "mgrx_gpu_slab_interp", "mgrx_gpu_slab_pack", "mgrx_gpu_slab_unpack",
 )
 
 u64p = C.POINTER(C.c_uint64)
@@ -70,12 +70,14 @@ def _load() -> C.CDLL:
         "mgrx_host_lorenzo": (i, [vp, i, i, u64p, vp, C.c_double, vp, C.c_uint64, u64p, u64p, vp, C.c_uint64, u64p]),
         # slab mode (paper_2010_05872_b200/slab.py)
         "mgrx_gpu_slab_level": (i, [vp, i, i, u64p, i, i, C.POINTER(C.c_int64)]),
-        "mgrx_gpu_slab_dec_plane": (i, [vp, i, i, u64p, i, i, C.c_uint64, C.c_uint64, vp, vp, vp, vp]),
-        "mgrx_gpu_slab_rec_plane": (i, [vp, i, i, u64p, i, i, C.c_uint64, C.c_uint64, vp, vp]),
+        "mgrx_gpu_slab_dec_plane": (i, [vp, i, i, u64p, i, i, C.c_uint64, C.c_uint64, vp, vp, vp, vp, C.c_int64]),
+        "mgrx_gpu_slab_rec_plane": (i, [vp, i, i, u64p, i, i, C.c_uint64, C.c_uint64, vp, vp, C.c_int64]),
         "mgrx_gpu_slab_inplane": (i, [vp, i, i, u64p, i, i, C.c_uint64, C.c_uint64, vp]),
         "mgrx_gpu_slab_axis0": (i, [vp, i, i, u64p, i, i, C.c_uint64, vp]),
         "mgrx_gpu_slab_apply": (i, [vp, i, vp, vp, C.c_uint64, C.c_double]),
-        "mgrx_gpu_slab_interp": (i, [vp, i, i, u64p, i, i, C.c_uint64, C.c_uint64, vp, vp, vp]),
+        "mgrx_gpu_slab_interp": (i, [vp, i, i, u64p, i, i, C.c_uint64, C.c_uint64, vp, vp, vp, C.c_int64]),
+        "mgrx_gpu_slab_pack": (i, [vp, vp, C.c_uint64, C.c_uint64, u64p, i, vp]),
+        "mgrx_gpu_slab_unpack": (i, [vp, vp, C.c_uint64, C.c_uint64, u64p, i, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -1783,36 +1783,41 @@ int mgrx_gpu_slab_level(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims
 }
 
 int mgrx_gpu_slab_dec_plane(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int level,
-                            uint64_t k0, uint64_t k1, const void* d_blk, void* d_out, void* d_coarse, double* d_G) {
+                            uint64_t k0, uint64_t k1, const void* d_blk, void* d_out, void* d_coarse, double* d_G,
+                            int64_t odd_shift) {
   return guarded(c, [&] {
     if (!d_blk || !d_out || !d_coarse || !d_G) fail(MGRX_INVALID_ARGUMENT, "null argument");
     Plan* p = slab_plan(c, dtype, nd, dims, levels, level);
     const size_t off = p->h.node[level - 1];
+    Fused3DPlan fp = p->fused[level];
+    fp.g.odd_shift = odd_shift;
     cudaError_t e;
     if (dtype == MGRX_F32)
       e = fused3d_slab_dec_plane<float>(static_cast<const float*>(d_blk), static_cast<float*>(d_out) + off,
-                                        static_cast<float*>(d_coarse), d_G, p->fused[level], int64_t(k0), int64_t(k1),
+                                        static_cast<float*>(d_coarse), d_G, fp, int64_t(k0), int64_t(k1),
                                         exec(c, level));
     else
       e = fused3d_slab_dec_plane<double>(static_cast<const double*>(d_blk), static_cast<double*>(d_out) + off,
-                                         static_cast<double*>(d_coarse), d_G, p->fused[level], int64_t(k0),
+                                         static_cast<double*>(d_coarse), d_G, fp, int64_t(k0),
                                          int64_t(k1), exec(c, level));
     cuda_check(e, "slab dec plane");
   });
 }
 
 int mgrx_gpu_slab_rec_plane(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int level,
-                            uint64_t k0, uint64_t k1, const void* d_coeffs, double* d_G) {
+                            uint64_t k0, uint64_t k1, const void* d_coeffs, double* d_G, int64_t odd_shift) {
   return guarded(c, [&] {
     if (!d_coeffs || !d_G) fail(MGRX_INVALID_ARGUMENT, "null argument");
     Plan* p = slab_plan(c, dtype, nd, dims, levels, level);
     const size_t off = p->h.node[level - 1];
+    Fused3DPlan fp = p->fused[level];
+    fp.g.odd_shift = odd_shift;
     cudaError_t e;
     if (dtype == MGRX_F32)
-      e = fused3d_slab_rec_plane<float>(static_cast<const float*>(d_coeffs) + off, d_G, p->fused[level], int64_t(k0),
+      e = fused3d_slab_rec_plane<float>(static_cast<const float*>(d_coeffs) + off, d_G, fp, int64_t(k0),
                                         int64_t(k1), exec(c, level));
     else
-      e = fused3d_slab_rec_plane<double>(static_cast<const double*>(d_coeffs) + off, d_G, p->fused[level],
+      e = fused3d_slab_rec_plane<double>(static_cast<const double*>(d_coeffs) + off, d_G, fp,
                                          int64_t(k0), int64_t(k1), exec(c, level));
     cuda_check(e, "slab rec plane");
   });
@@ -1851,21 +1856,40 @@ int mgrx_gpu_slab_apply(mgrx_gpu_ctx* c, int dtype, void* d_coarse, const double
 }
 
 int mgrx_gpu_slab_interp(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int level,
-                         uint64_t p0, uint64_t p1, const void* d_coeffs, const void* d_coarse, void* d_fine) {
+                         uint64_t p0, uint64_t p1, const void* d_coeffs, const void* d_coarse, void* d_fine,
+                         int64_t odd_shift) {
   return guarded(c, [&] {
     if (!d_coeffs || !d_coarse || !d_fine) fail(MGRX_INVALID_ARGUMENT, "null argument");
     Plan* p = slab_plan(c, dtype, nd, dims, levels, level);
     const size_t off = p->h.node[level - 1];
+    Fused3DPlan fp = p->fused[level];
+    fp.g.odd_shift = odd_shift;
     cudaError_t e;
     if (dtype == MGRX_F32)
       e = fused3d_slab_interp<float>(static_cast<const float*>(d_coeffs) + off, static_cast<const float*>(d_coarse),
-                                     static_cast<float*>(d_fine), p->fused[level], int64_t(p0), int64_t(p1),
+                                     static_cast<float*>(d_fine), fp, int64_t(p0), int64_t(p1),
                                      exec(c, level));
     else
       e = fused3d_slab_interp<double>(static_cast<const double*>(d_coeffs) + off, static_cast<const double*>(d_coarse),
-                                      static_cast<double*>(d_fine), p->fused[level], int64_t(p0), int64_t(p1),
+                                      static_cast<double*>(d_fine), fp, int64_t(p0), int64_t(p1),
                                       exec(c, level));
     cuda_check(e, "slab interpolation");
+  });
+}
+
+int mgrx_gpu_slab_pack(mgrx_gpu_ctx* c, const double* d_src, uint64_t rows, uint64_t pitch, const uint64_t* cb,
+                       int nparts, double* d_dst) {
+  return guarded(c, [&] {
+    if (!d_src || !d_dst || !cb || nparts <= 0 || nparts > 256) fail(MGRX_INVALID_ARGUMENT, "bad pack arguments");
+    cuda_check(slab_pack(d_src, int64_t(rows), int64_t(pitch), cb, nparts, d_dst, false, exec(c)), "slab pack");
+  });
+}
+
+int mgrx_gpu_slab_unpack(mgrx_gpu_ctx* c, const double* d_src, uint64_t rows, uint64_t pitch, const uint64_t* cb,
+                         int nparts, double* d_dst) {
+  return guarded(c, [&] {
+    if (!d_src || !d_dst || !cb || nparts <= 0 || nparts > 256) fail(MGRX_INVALID_ARGUMENT, "bad unpack arguments");
+    cuda_check(slab_pack(d_src, int64_t(rows), int64_t(pitch), cb, nparts, d_dst, true, exec(c)), "slab unpack");
   });
 }
 

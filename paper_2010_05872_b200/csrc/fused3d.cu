@@ -247,7 +247,7 @@ __device__ __forceinline__ ShellLin shell_lin(const F3Geom& g, int64_t r1) {
   ShellLin l;
   l.b[0] = shell_row_start(g, 0, r1);
   l.s[0] = g.n1 * g.n2 - g.m1 * g.m2;  // r0 = k < m0: one more nodal row of m1 entries per plane
-  l.b[1] = shell_row_start(g, g.m0, r1);
+  l.b[1] = shell_row_start(g, g.m0, r1) + g.odd_shift;
   l.s[1] = g.n1 * g.n2;
   return l;
 }
@@ -794,8 +794,8 @@ __global__ void __launch_bounds__(MAXT, NB ? NB : (MAXT == kPlaneMaxThreads ? 2 
   const int64_t k0 = ur.plo >> 1;
   T* se_e = shell + (shell_row_start(g, k0, e0 + 1) - (g.n2 - g.m2)) + cc;
   T* so_e = shell + (shell_row_start(g, k0, g.m1 + e0 + 1) - g.n2) + cc;
-  T* se_o = shell + (shell_row_start(g, g.m0 + k0, e0 + 1) - g.n2) + cc;
-  T* so_o = shell + (shell_row_start(g, g.m0 + k0, g.m1 + e0 + 1) - g.n2) + cc;
+  T* se_o = shell + (shell_row_start(g, g.m0 + k0, e0 + 1) - g.n2 + g.odd_shift) + cc;
+  T* so_o = shell + (shell_row_start(g, g.m0 + k0, g.m1 + e0 + 1) - g.n2 + g.odd_shift) + cc;
   T* cpe = coarse + (k0 * g.m1 + e0) * g.m2 + cc;
   const int64_t step_e = g.n1 * g.n2 - g.m1 * g.m2, step_o = g.n1 * g.n2, step_c = g.m1 * g.m2;
   const int plo = int(ur.plo), n0 = int(g.n0), a0x2 = int(2 * ur.a0), a1x2 = int(2 * ur.a1);
@@ -1109,6 +1109,10 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 3 : 1)
     x.le = shell_row_start(g, r0, e0 + ne) - x.se;
     x.so = shell_row_start(g, r0, g.m1 + e0);
     x.lo = shell_row_start(g, r0, g.m1 + e0 + no) - x.so;
+    if (p & 1) {  // slab-sized buffers: the odd planes' region
+      x.se += g.odd_shift;
+      x.so += g.odd_shift;
+    }
     const int64_t k = ((p & 1) && p + 1 < g.n0) ? (p >> 1) + 1 : (p >> 1);
     x.cs = (k * g.m1 + e0) * g.m2;
     return x;
@@ -2443,6 +2447,48 @@ cudaError_t fused3d_slab_interp(const T* shell, const T* coarse, T* fine, const 
   g.p_base = p0;
   g.p_end = p1;
   return launch_interp<T>(shell, coarse, fine, g, ex);
+}
+
+
+// ------------------------------------------------------------- slab K-pack
+// Column blocks of a rows x pitch fp64 array, back to back (block q is rows
+// x (cb[q+1] - cb[q]) row-major at rows * (cb[q] - cb[0])): the send buffer
+// of slab mode's transpose (all-to-all), and its inverse for the way back.
+struct PackParts {
+  int64_t cb[257];
+  int n;
+};
+template <bool UNPACK>
+__global__ void __launch_bounds__(256) k_slab_pack(const double* __restrict__ src, double* __restrict__ dst,
+                                                   int64_t rows, int64_t pitch, const PackParts pp) {
+  const int64_t c0 = pp.cb[0], width = pp.cb[pp.n] - c0;
+  const int64_t total = rows * width;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / width, c = c0 + (i - r * width);  // (row, column) of the strided array
+    int q = 0;
+    while (c >= pp.cb[q + 1]) ++q;
+    const int64_t w = pp.cb[q + 1] - pp.cb[q];
+    const int64_t pk = rows * (pp.cb[q] - c0) + r * w + (c - pp.cb[q]);
+    if (UNPACK)
+      dst[r * pitch + c] = src[pk];
+    else
+      dst[pk] = src[r * pitch + c];
+  }
+}
+
+cudaError_t slab_pack(const double* src, int64_t rows, int64_t pitch, const uint64_t* cb, int nparts, double* dst,
+                      bool unpack, const Exec& ex) {
+  PackParts pp;
+  pp.n = nparts;
+  for (int q = 0; q <= nparts; ++q) pp.cb[q] = int64_t(cb[q]);
+  const int64_t total = rows * (pp.cb[nparts] - pp.cb[0]);
+  if (total <= 0) return cudaSuccess;
+  const int grid = grid_for(total, 256, 8);
+  if (unpack)
+    MGRX_LAUNCH(ex, "slab_unpack", k_slab_pack<true><<<grid, 256, 0, ex.s>>>(src, dst, rows, pitch, pp));
+  else
+    MGRX_LAUNCH(ex, "slab_pack", k_slab_pack<false><<<grid, 256, 0, ex.s>>>(src, dst, rows, pitch, pp));
+  return cudaGetLastError();
 }
 
 #define MGRX_INST(T)                                                                                     \

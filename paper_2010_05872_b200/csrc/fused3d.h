@@ -26,6 +26,11 @@ struct F3Geom {
   // [a_base, a_end), the interpolation fine planes [p_base, p_end)
   int64_t a_base = 0, a_end = -1, p_base = 0, p_end = -1;
   unsigned* nonfinite = nullptr;  // decompose plane pass with the finiteness check: set to 1 on inf / NaN
+  // slab mode with slab-sized buffers: the shell entries of odd fine planes
+  // live at (global shell position + odd_shift) relative to the shell base
+  // (the even planes' region and the odd planes' region of a rank are two
+  // separate runs of the level-centric buffer); 0 = one global buffer
+  int64_t odd_shift = 0;
 };
 
 struct Fused3DPlan {
@@ -70,5 +75,10 @@ cudaError_t fused3d_slab_axis0(double* Gt, int64_t width, const Fused3DPlan& fp,
 template <typename T>
 cudaError_t fused3d_slab_interp(const T* shell, const T* coarse, T* fine, const Fused3DPlan& fp, int64_t p0, int64_t p1,
                                 const Exec& ex);
+
+// K-pack of slab mode's all-to-all: the column blocks [cb[q], cb[q+1]) of a
+// rows x pitch fp64 array packed back to back (unpack: the inverse).
+cudaError_t slab_pack(const double* src, int64_t rows, int64_t pitch, const uint64_t* cb, int nparts, double* dst,
+                      bool unpack, const Exec& ex);
 
 }  // namespace mgrx_b200

@@ -36,11 +36,24 @@ def test_bounds():
 @pytest.mark.parametrize("shape,dtype,ranks", [((129, 129, 129), "f64", 2), ((257, 129, 65), "f32", 3),
                                                ((513, 513, 513), "f32", 4)])
 def test_slab_emulated_matches_single_gpu(shape, dtype, ranks):
+    _slab_case(shape, dtype, ranks)
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_slab_1025_eight_ranks_slab_sized_buffers():
+    """Config 5b's field over 8 emulated ranks: bit-identical to one GPU,
+    every rank holding about 1/8 of the field plus halos."""
+    _slab_case((1025, 1025, 1025), "f32", 8, check_memory=True)
+
+
+def _slab_case(shape, dtype, ranks, check_memory=False):
     import torch
 
     import paper_2010_05872_b200 as mg
     from synthetic_fields import config2_field
-    from paper_2010_05872_b200.slab import _fused_depth, slab_decompose, slab_recompose
+    from paper_2010_05872_b200.slab import PlaneSlab, _fused_depth, assemble_coefficients, owned_planes, \
+        slab_decompose, slab_recompose
 
     dt = torch.float64 if dtype == "f64" else torch.float32
     f = config2_field(shape, seed=3, device="cuda").to(dt)
@@ -53,35 +66,39 @@ def test_slab_emulated_matches_single_gpu(shape, dtype, ranks):
     S = _fused_depth(ws1, 1 if dtype == "f64" else 0, shape, h.num_levels(), S)
     assert S >= 1
     P = slab_bounds(shape[0], ranks, S)
+    plane = shape[1] * shape[2]
     fields = []
-    for r in range(ranks):
-        x = torch.full_like(f, float("nan"))
-        hi = P[r + 1] if r + 1 < ranks else shape[0]
-        x[P[r]:hi] = f[P[r]:hi]
-        fields.append(x)
+    for r in range(ranks):  # each rank holds only its own planes (slab-sized)
+        lo, hi = owned_planes(P, r, shape[0])
+        s = PlaneSlab(lo, hi, plane, dt, f.device)
+        s.t.copy_(f.reshape(shape[0], -1)[lo:hi])
+        fields.append(s)
     ex = LocalExchange(ranks)
     wss = [mg.SolverWorkspace() for _ in range(ranks)]
     outs = slab_decompose(fields, h, ex, wss, S)
-    got = outs[0].clone()
-    for o in outs[1:]:
-        got = torch.where(torch.isnan(got), o, got)
+    got = assemble_coefficients(outs, h)
     torch.cuda.synchronize()
     assert not torch.isnan(got).any()
     assert torch.equal(got, want)
+    if check_memory:  # per-rank coefficient storage ~ 1/R of the buffer
+        for o in outs:
+            assert o.nbytes() < 1.5 * want.numel() * want.element_size() / ranks, o.nbytes()
+    del want
     # recompose from each rank's own coefficients (its shells + the coarse
     # levels; the halo planes' shells are exchanged inside)
-    backs = slab_recompose(outs, h, ex, wss, S)
-    back = torch.empty_like(f)
+    backs = slab_recompose(outs, h, ex, wss)
+    bw = back_want.reshape(shape[0], -1)
     for r in range(ranks):
-        hi = P[r + 1] if r + 1 < ranks else shape[0]
-        back[P[r]:hi] = backs[r][P[r]:hi]
+        lo, hi = owned_planes(P, r, shape[0])
+        assert torch.equal(backs[r].planes(lo, hi), bw[lo:hi]), r
     torch.cuda.synchronize()
-    assert torch.equal(back, back_want)
 
 
 def _gloo_worker(rank, world, port, q):
     import torch
     import torch.distributed as dist
+
+    from paper_2010_05872_b200.slab import PlaneSlab, ShellSlab
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -89,40 +106,57 @@ def _gloo_worker(rank, world, port, q):
     try:
         g = torch.Generator().manual_seed(7)
         m0, ncols = 12, 10
-        base = [torch.randn(m0, ncols, generator=g, dtype=torch.float64) for _ in range(world)]
+        base = torch.randn(m0, ncols, generator=g, dtype=torch.float64)
         K = [0, 5, 12]
         Cb = column_bounds(ncols, world)
         loc = LocalExchange(world)
         te = TorchExchange()
-        # halo
-        L_bufs = [b.clone() for b in base]
-        loc.halo(L_bufs, None, K, 2, 1)
-        T_buf = [base[rank].clone()]
-        te.halo(T_buf, None, K, 2, 1)
-        ok = torch.equal(T_buf[0], L_bufs[rank])
-        # halo of element ranges
-        flat = [b.reshape(-1).clone() for b in base]
-        left = lambda r: [(r * 7, r * 7 + 3), (40, 42)]  # noqa: E731
-        right = lambda r: [(100 + r, 103 + r)]  # noqa: E731
-        L_fl = [f.clone() for f in flat]
-        loc.halo_ranges(L_fl, left, right)
-        T_fl = [flat[rank].clone()]
-        te.halo_ranges(T_fl, left, right)
-        ok &= torch.equal(T_fl[0], L_fl[rank])
-        # transposes
-        Gt_l = loc.transpose(base, K, Cb)
-        Gt_t = te.transpose([base[rank]], K, Cb)
+
+        def slab(r, fill_own=True):  # rank r's planes with a 2-left / 1-right halo, halo NaN
+            lo, hi = K[r], K[r + 1]
+            s = PlaneSlab(max(0, lo - 2), min(m0, hi + 1), ncols, torch.float64, "cpu", fill=float("nan"))
+            s.planes(lo, hi).copy_(base[lo:hi])
+            return s
+
+        # plane halo
+        L_s = [slab(r) for r in range(world)]
+        loc.halo(L_s, K, 2, 1)
+        T_s = [slab(rank)]
+        te.halo(T_s, K, 2, 1)
+        ok = torch.equal(T_s[0].t.nan_to_num(-1), L_s[rank].t.nan_to_num(-1))
+        ok &= not bool(torch.isnan(L_s[rank].t).any())
+        # shell halo (level 12 x 10 x 10 -> shells of planes around the slab)
+        info = [12, 10, 10, 6, 5, 5, 1, 0, 1200]
+        Pf = [0, 6, 12]
+
+        def shells(r):
+            s = ShellSlab(info, Pf[r] - 2, Pf[r + 1], torch.float64, "cpu")
+            for p in range(Pf[r], min(Pf[r + 1], 12)):
+                x = s.run(p)
+                x.copy_(torch.arange(x.numel(), dtype=torch.float64) + 1000 * p)
+            return s
+
+        left = lambda r: [p for p in (Pf[r] - 2, Pf[r] - 1) if p >= 0]  # noqa: E731
+        right = lambda r: [Pf[r + 1]]  # noqa: E731
+        L_sh = [shells(r) for r in range(world)]
+        loc.halo_shells(L_sh, left, right)
+        T_sh = [shells(rank)]
+        te.halo_shells(T_sh, left, right)
+        ok &= torch.equal(T_sh[0].t.nan_to_num(-1), L_sh[rank].t.nan_to_num(-1))
+        # transposes (the torch K-pack on CPU tensors)
+        G = [base[K[r]:K[r + 1]].contiguous() for r in range(world)]
+        Gt_l = loc.transpose(G, K, Cb)
+        Gt_t = te.transpose([G[rank]], K, Cb)
         ok &= torch.equal(Gt_t[0], Gt_l[rank])
+        ok &= torch.equal(Gt_l[rank], base[:, Cb[rank]:Cb[rank + 1]])
         z_l = loc.transpose_back(Gt_l, K, Cb)
         z_t = te.transpose_back(Gt_t, K, Cb)
         ok &= torch.equal(z_t[0], z_l[rank])
-        ok &= torch.equal(z_l[rank], base[rank][K[rank]:K[rank + 1]])
+        ok &= torch.equal(z_l[rank], base[K[rank]:K[rank + 1]])
         # gather
-        G_l = [b.clone() for b in base]
-        loc.gather(G_l, K)
-        G_t = [base[rank].clone()]
-        te.gather(G_t, K)
-        ok &= torch.equal(G_t[0], G_l[rank])
+        G_l = loc.gather([slab(r) for r in range(world)], K, m0)
+        G_t = te.gather([slab(rank)], K, m0)
+        ok &= torch.equal(G_t[0], G_l[rank]) and torch.equal(G_l[rank], base)
         q.put((rank, bool(ok)))
     finally:
         dist.destroy_process_group()

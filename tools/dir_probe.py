@@ -10,12 +10,23 @@ import torch  # noqa: E402
 import paper_2010_05872_b200 as mg  # noqa: E402
 from synthetic_fields import config2_field  # noqa: E402
 
-dims = tuple(int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "513,513,513").split(","))
+arg = sys.argv[1] if len(sys.argv) > 1 else "513,513,513"
 stop = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-f = config2_field(dims, seed=0, device="cuda")
+coords = None
+if arg.startswith("config"):
+    import synthetic_fields as sf
+
+    f = getattr(sf, arg + "_field")(device="cuda")
+    if isinstance(f, tuple):
+        f, coords = f
+else:
+    f = config2_field(tuple(int(x) for x in arg.split(",")), seed=0, device="cuda")
 h = mg.GridHierarchy.create(f.shape)
 ws = mg.SolverWorkspace()
-mc = mg.decompose(f, h, stop, ws)
+if coords is None:
+    mc = mg.decompose(f, h, stop, ws)
+else:
+    mc = mg.decompose_nonuniform(f, h, coords, stop, ws)
 
 
 def timed(fn, reps=20, graph=True):
@@ -43,11 +54,19 @@ def timed(fn, reps=20, graph=True):
     return ts[len(ts) // 2]
 
 
-dec = lambda: mg.decompose(f, h, stop, ws)  # noqa: E731
-rec = lambda: mg.recompose(mc, ws)  # noqa: E731
+if coords is None:
+    dec = lambda: mg.decompose(f, h, stop, ws)  # noqa: E731
+    rec = lambda: mg.recompose(mc, ws)  # noqa: E731
+else:
+    dec = lambda: mg.decompose_nonuniform(f, h, coords, stop, ws)  # noqa: E731
+    rec = lambda: mg.recompose_nonuniform(mc, coords, ws)  # noqa: E731
+nbytes = sum(2 * f.element_size() * h.node_count(l) for l in range(stop + 1, h.num_levels() + 1))
 print(f"env {' '.join(k + '=' + v for k, v in os.environ.items() if k.startswith('MGRX'))}")
-print(f"decompose graph {timed(dec):.4f} eager {timed(dec, graph=False):.4f} ms")
-print(f"recompose graph {timed(rec):.4f} eager {timed(rec, graph=False):.4f} ms")
+td, tr = timed(dec), timed(rec)
+print(f"decompose graph {td:.4f} eager {timed(dec, graph=False):.4f} ms  ({nbytes / td / 1e6:.0f} GB/s alg, "
+      f"{nbytes / td / 1e6 / 6551.7:.3f} of peak)")
+print(f"recompose graph {tr:.4f} eager {timed(rec, graph=False):.4f} ms  ({nbytes / tr / 1e6:.0f} GB/s alg, "
+      f"{nbytes / tr / 1e6 / 6551.7:.3f} of peak)")
 for name, fn in (("dec", dec), ("rec", rec)):
     ws.profile_begin()
     for _ in range(5):

@@ -40,5 +40,14 @@ def last_step(items):
     if not dec:
         return items
     mx = max(nbytes(items[n][2]) for n in dec)
-    start = [n for n in dec if nbytes(items[n][2]) >= 0.5 * mx][-1]
-    return items[start:]
+    rec = [n for n, (i, k, m) in enumerate(items) if "rec_plane" in k or "rec_interp" in k or "k_tail_recompose" in k]
+    # the last finest-level decompose that a recompose follows, up to the
+    # first kernel after that step which belongs to neither (e.g. quantize)
+    starts = [n for n in dec if nbytes(items[n][2]) >= 0.5 * mx and rec and rec[-1] > n]
+    start = starts[-1] if starts else dec[-1]
+    end = len(items)
+    for n in range(start + 1, len(items)):
+        if "quant" in items[n][1] or (n in dec and nbytes(items[n][2]) >= 0.5 * mx):
+            end = n
+            break
+    return items[start:end]

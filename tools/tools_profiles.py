@@ -8,7 +8,10 @@ import csv
 import json
 import sys
 
-from tools_ncu_csv import last_step, read_launches, short
+import os
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from tools_ncu_csv import last_step, read_launches, short  # noqa: E402
 
 src, rnd = sys.argv[1], sys.argv[2]
 step = last_step(read_launches(src))
@@ -21,7 +24,8 @@ tot = sum(r[2] for r in out_rows)
 with open(f"profiles/{rnd}_launches.md", "w") as f:
     f.write(f"# {rnd}: ncu launch list, one decompose + recompose step of the 513^3 fp32 bench\n\n")
     f.write("Command: `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-            "--clock-control none python bench.py --steps 2 --warmup 1 --no-cpu-baseline` (tools_prof.sh).\n")
+            "--clock-control none --csv python tools/tools_step.py` (tools/tools_prof.sh: two eager decompose + "
+            "recompose steps of the bench field; the last step is listed).\n")
     f.write("ncu serialises launches and runs each cold: compare SHARES, not absolute times.\n\n")
     f.write("| id | kernel | us | DRAM read MB | DRAM write MB | GB/s |\n|---|---|---|---|---|---|\n")
     for i, name, t, rd, wr in out_rows:
@@ -36,7 +40,10 @@ for tag, rows_ in (("f3_dec_plane@9", dec), ("f3_rec_plane@9", rec), ("f3_rec_in
     if rows_:
         r = max(rows_, key=lambda r: r[3] + r[4])
         traffic[tag] = r[3] + r[4]
-json.dump({"round": rnd, "source": f"profiles/{rnd}_launches.md", "kernels": traffic}, open("profiles/traffic.json", "w"),
-          indent=1)
+step_bytes = sum(r[3] + r[4] for r in out_rows)
+with open(f"profiles/{rnd}_launches.md", "a") as f:
+    f.write(f"Step DRAM traffic (all kernels): {step_bytes / 1e9:.3f} GB (algorithmic 2.471 GB)\n")
+json.dump({"round": rnd, "source": f"profiles/{rnd}_launches.md", "kernels": traffic, "step": step_bytes},
+          open("profiles/traffic.json", "w"), indent=1)
 print(open(f"profiles/{rnd}_launches.md").read()[-1500:])
 print(traffic)

@@ -17,4 +17,8 @@ ws = mg.SolverWorkspace()
 for _ in range(2):
     out = mg.recompose(mg.decompose(f, h, 0, ws), ws)
 torch.cuda.synchronize()
+# one level-wise quantize of the coefficients (tau = 1e-3 * range, budget tau / 4)
+rg = float((f.max() - f.min()).item())
+mg.quantize(mg.decompose(f, h, 0, ws), mg.make_plan(mg.QuantMode.levelwise, 1e-3 * rg / 4.0, h), ws)
+torch.cuda.synchronize()
 print("roundtrip linf", float((out - f).abs().max()))
