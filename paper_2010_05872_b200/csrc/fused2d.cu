@@ -466,7 +466,7 @@ Fused2DPlan fused2d_plan(const LevelGeom& lg) {
   g.m1 = int(lg.m[1]);
   // long enough rows for the strips, columns that fit one axis-0 block, and
   // enough work to beat the per-step kernels
-  if (g.n0 < 5 || g.n1 < 5 || g.m0 > 128 * kColLS || int64_t(g.n0) * g.n1 < (int64_t(1) << 16)) return fp;
+  if (g.n0 < 5 || g.n1 < 5 || g.m0 > 128 * kColLS || int64_t(g.n0) * g.n1 < (int64_t(1) << 13)) return fp;
   g.strips = (g.m1 + kF2Strip - 1) / kF2Strip;
   // coarse rows per CTA: about two waves of 8 resident CTAs per SM (a CTA
   // streams its rows one after the other, latency bound), 2..32
