@@ -152,23 +152,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // L2 residency hints for the fp64 volume G (136 MB at 513^3, next to a
 // 126 MB L2): its producer stores it with evict_last so the row / column
 // passes that follow find it in L2, while the streamed field reads are
-// marked evict_first.  g_l2hint = 0 (MGRX_NO_L2HINT) turns the policies
-// into evict_normal.
-__device__ int g_l2hint = 1;
+// marked evict_first (A/B on the B200: decompose -10 us, recompose -7 us,
+// mostly the axis-0 pass).
 __device__ __forceinline__ uint64_t pol_keep() {
   uint64_t p;
-  if (g_l2hint)
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  else
-    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ uint64_t pol_stream() {
   uint64_t p;
-  if (g_l2hint)
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  else
-    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ void st_pol(double* a, double v, uint64_t pol) {
@@ -1281,11 +1274,10 @@ __global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : (MAXT == kColT
   pdl_wait();
   {
     const double* gp = G + base + int64_t(s0) * stride;
-    // the axis-0 pass reads G for the last time (evict first); axis 1 keeps it
-    const uint64_t pol = APPLY ? pol_stream() : pol_keep();
+    // the axis-0 pass reads G for the last time (evict first)
 #pragma unroll
     for (int k = 0; k < LS; ++k) {
-      v[k] = (valid && k < len) ? ld_pol(gp, pol) : 0.0;
+      v[k] = (valid && k < len) ? (APPLY ? __ldcs(gp) : *gp) : 0.0;
       gp += stride;
     }
   }
@@ -1333,15 +1325,16 @@ __global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : (MAXT == kColT
     }
   pdl_trigger();
   if (!valid) return;
-  if (APPLY) {  // coarse values loaded only now: fewer live registers, more resident warps
+  if (APPLY) {  // coarse values loaded only now, four at a time: fewer live registers
     T* c = coarse + base + int64_t(s0) * stride;
-    T cv[LS];
 #pragma unroll
-    for (int k = 0; k < LS; ++k) cv[k] = k < len ? c[int64_t(k) * stride] : T(0);
+    for (int k0 = 0; k0 < LS; k0 += 4) {
+      T cv[4];
 #pragma unroll
-    for (int k = 0; k < LS; ++k) {
-      if (k < len) *c = to_t<T>(double(cv[k]) + sign * v[k]);
-      c += stride;
+      for (int u = 0; u < 4; ++u) cv[u] = (k0 + u < LS && k0 + u < len) ? c[int64_t(k0 + u) * stride] : T(0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k0 + u < LS && k0 + u < len) c[int64_t(k0 + u) * stride] = to_t<T>(double(cv[u]) + sign * v[k0 + u]);
     }
   } else {
     double* gp = G + base + int64_t(s0) * stride;
@@ -2064,11 +2057,6 @@ static void row_col1(double* G, const F3Geom& g, const ThomasLevel& th, const Ex
 
 Fused3DPlan fused3d_plan(const LevelGeom& lg, int esize) {
   Fused3DPlan fp;
-  {
-    static const int hint = std::getenv("MGRX_NO_L2HINT") ? 0 : 1;
-    cudaMemcpyToSymbol(g_l2hint, &hint, sizeof(int));
-
-  }
   if (lg.d != 3) return fp;
   F3Geom& g = fp.g;
   g.n0 = lg.n[0];
