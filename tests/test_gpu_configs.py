@@ -152,7 +152,9 @@ def test_nonuniform_shapes(torch, mg, o, dtype):
     tol = 1e-12 if dtype == "f64" else 1e-5
     rng = np.random.default_rng(3)
     ws = mg.SolverWorkspace()
-    for shape in [(65,), (64,), (33, 20), (17, 9, 12), (40, 36, 66), (9, 8, 7, 6)]:
+    # (300, 258), (257, 130), (130, 301): the fused 2-D nonuniform passes
+    # (>= 2^13 nodes) with even / odd extents on either axis
+    for shape in [(65,), (64,), (33, 20), (17, 9, 12), (40, 36, 66), (9, 8, 7, 6), (300, 258), (257, 130), (130, 301)]:
         coords = [nonuniform_coords(n, seed=1, axis=a) for a, n in enumerate(shape)]
         x = rng.uniform(-5, 5, shape).astype(npdt)
         rg = float(x.max() - x.min())

@@ -47,6 +47,26 @@ def test_slab_1025_eight_ranks_slab_sized_buffers():
     _slab_case((1025, 1025, 1025), "f32", 8, check_memory=True)
 
 
+@pytest.mark.gpu
+def test_kpack_kernel_matches_torch():
+    """mgrx_gpu_slab_pack / _unpack (the all-to-all K-pack) against the torch
+    reference packing, on uneven column blocks."""
+    import torch
+
+    import paper_2010_05872_b200 as mg
+    from paper_2010_05872_b200.slab import KPack, _torch_pack, _torch_unpack
+
+    g = torch.Generator(device="cuda").manual_seed(5)
+    src = torch.randn(37, 1001, generator=g, dtype=torch.float64, device="cuda")
+    kp = KPack(mg.SolverWorkspace())
+    for cb in ([0, 1001], [0, 300, 301, 700, 1001], column_bounds(1001, 8)):
+        packed = kp.pack(src, cb)
+        torch.cuda.synchronize()
+        assert torch.equal(packed, _torch_pack(src, cb))
+        back = kp.unpack(packed, 37, cb)
+        assert torch.equal(back, _torch_unpack(packed, 37, cb)) and torch.equal(back, src)
+
+
 def _slab_case(shape, dtype, ranks, check_memory=False):
     import torch
 
