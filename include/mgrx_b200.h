@@ -222,6 +222,17 @@ int mgrx_host_lorenzo(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* d
 int mgrx_gpu_field_stats(mgrx_gpu_ctx* ctx, int dtype, uint64_t n, const void* d_field, double* min_value,
                          double* max_value, uint64_t* first_nonfinite);
 
+/* decompose (as mgrx_gpu_decompose) with check_finite and the range of the
+ * field (pipeline.hpp:113-118; the range gives the absolute bound of a
+ * relative tolerance) computed in the same read: on the fused 3-D path the
+ * finest level's plane pass folds them in; otherwise (or to locate the first
+ * non-finite value) a field_stats pass runs.  Outputs as
+ * mgrx_gpu_field_stats; MGRX_NONFINITE_DATA (the reference's message) when a
+ * value is inf / NaN.  Synchronous. */
+int mgrx_gpu_decompose_checked(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels,
+                               int stop_level, const void* d_field, void* d_out, double* min_value,
+                               double* max_value, uint64_t* first_nonfinite);
+
 /* compress (pipeline.hpp:130-196) up to its sections, device-resident: the
  * field's check_finite runs on the device copy (MGRX_NONFINITE_DATA with the
  * reference's message); the field goes to the GPU once; the stop level is

@@ -19,7 +19,7 @@ EXPORTS = (
     "mgrx_gpu_decompose_nonuniform", "mgrx_gpu_recompose_nonuniform", "mgrx_gpu_quantize",
     "mgrx_gpu_dequantize", "mgrx_host_decompose", "mgrx_host_recompose", "mgrx_host_quantize", "mgrx_host_dequantize",
     "mgrx_gpu_workspace_size",
-    "mgrx_gpu_choose_stop", "mgrx_host_decompose_adaptive", "mgrx_gpu_encode_labels", "mgrx_host_compress", "mgrx_gpu_field_stats", "mgrx_host_lorenzo",
+    "mgrx_gpu_choose_stop", "mgrx_host_decompose_adaptive", "mgrx_gpu_encode_labels", "mgrx_host_compress", "mgrx_gpu_field_stats", "mgrx_gpu_decompose_checked", "mgrx_host_lorenzo",
     "mgrx_gpu_slab_level", "mgrx_gpu_slab_dec_plane", "mgrx_gpu_slab_rec_plane", "mgrx_gpu_slab_inplane",
     "mgrx_gpu_slab_axis0", "mgrx_gpu_slab_apply", "mgrx_gpu_slab_interp", "mgrx_gpu_slab_pack", "mgrx_gpu_slab_unpack",
 )
@@ -67,6 +67,7 @@ def _load() -> C.CDLL:
         "mgrx_host_compress": (i, [vp, i, i, u64p, i, vp, dp, i, i, dp, dp, dp, vp, C.c_uint64, u64p, u64p, vp,
                                    C.c_uint64, u64p, vp, C.POINTER(i)]),
         "mgrx_gpu_field_stats": (i, [vp, i, C.c_uint64, vp, dp, dp, u64p]),
+        "mgrx_gpu_decompose_checked": (i, [vp, i, i, u64p, i, i, vp, vp, dp, dp, u64p]),
         "mgrx_host_lorenzo": (i, [vp, i, i, u64p, vp, C.c_double, vp, C.c_uint64, u64p, u64p, vp, C.c_uint64, u64p]),
         # slab mode (paper_2010_05872_b200/slab.py)
         "mgrx_gpu_slab_level": (i, [vp, i, i, u64p, i, i, C.POINTER(C.c_int64)]),

@@ -1280,6 +1280,41 @@ void field_stats_run(mgrx_gpu_ctx* c, const T* d, int64_t n, double* lo, double*
   }
 }
 
+// check_finite / range fused into the finest level's first plane pass:
+// nf_flag = {u32 non-finite flag, pad, u64 min, u64 max} (order-preserving
+// images of the fp64 values, see fused3d.cu ordered_bits).
+uint64_t ordered_bits_host(double x) {
+  uint64_t b;
+  std::memcpy(&b, &x, 8);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+double from_ordered_bits(uint64_t o) {
+  const uint64_t b = (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o;
+  double x;
+  std::memcpy(&x, &b, 8);
+  return x;
+}
+void nf_arm(mgrx_gpu_ctx* c) {
+  if (!c->nf_flag) cuda_check(cudaMalloc(reinterpret_cast<void**>(&c->nf_flag), 64), "cudaMalloc(flag)");
+  static const uint64_t init[3] = {0, ordered_bits_host(INFINITY), ordered_bits_host(-INFINITY)};
+  cuda_check(cudaMemcpyAsync(c->nf_flag, init, sizeof init, cudaMemcpyHostToDevice, c->stream), "init flag");
+  c->nf_used = false;
+  c->nf_armed = true;
+}
+// after the decompose: the fused stats when the finest level carried them
+// (true), else false (the caller runs field_stats)
+bool nf_read(mgrx_gpu_ctx* c, unsigned* flag, double* lo, double* hi) {
+  c->nf_armed = false;
+  if (!c->nf_used) return false;
+  uint64_t h[3];
+  cuda_check(cudaMemcpyAsync(h, c->nf_flag, sizeof h, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  *flag = unsigned(h[0] & 0xffffffffu);
+  *lo = from_ordered_bits(h[1]);
+  *hi = from_ordered_bits(h[2]);
+  return true;
+}
+
 // compress's device part (pipeline.hpp:130-196 up to the sections): the
 // field goes to the GPU once; decompose (fixed or adaptive stop),
 // quantize and every level's encode_labels run there; the encoded label
@@ -1320,9 +1355,7 @@ void compress_core(mgrx_gpu_ctx* c, int nd, const uint64_t* dims, int levels, co
     field_stats_run<T>(c, dfield, int64_t(N), &lo, &hi, &bad);
     if (bad < N) fail(MGRX_NONFINITE_DATA, "non-finite value at offset %llu", (unsigned long long)bad);
   };
-  if (!c->nf_flag) cuda_check(cudaMalloc(reinterpret_cast<void**>(&c->nf_flag), 64), "cudaMalloc(flag)");
-  cuda_check(cudaMemsetAsync(c->nf_flag, 0, 4, c->stream), "memset");
-  c->nf_used = false;
+  nf_arm(c);
   c->nf_armed = force_stop < 0 || force_stop < L;
   struct Disarm {
     mgrx_gpu_ctx* c;
@@ -1346,14 +1379,14 @@ void compress_core(mgrx_gpu_ctx* c, int nd, const uint64_t* dims, int levels, co
     const int rc = mgrx_gpu_decompose(c, code, nd, dims, L, stop, dfield, dco);
     if (rc != MGRX_OK) fail(rc, "%s", c->last_error.c_str());
   }
-  c->nf_armed = false;
-  if (c->nf_used) {
+  {
     unsigned flag = 0;
-    cuda_check(cudaMemcpyAsync(&flag, c->nf_flag, 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    cuda_check(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
-    if (flag) check_finite_pass();  // locates the first offset and raises
-  } else {
-    check_finite_pass();
+    double lo, hi;
+    if (nf_read(c, &flag, &lo, &hi)) {
+      if (flag) check_finite_pass();  // locates the first offset and raises
+    } else {
+      check_finite_pass();
+    }
   }
   const size_t base = stop == 0 ? 0 : size_t(h.node[stop]);
   int32_t* dlab = static_cast<int32_t*>(dalloc((N - base) * 4));
@@ -1497,6 +1530,40 @@ int mgrx_gpu_field_stats(mgrx_gpu_ctx* c, int dtype, uint64_t n, const void* d_f
     else
       field_stats_run<double>(c, static_cast<const double*>(d_field), int64_t(n), min_value, max_value,
                               first_nonfinite);
+  });
+}
+
+int mgrx_gpu_decompose_checked(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
+                               const void* d_field, void* d_out, double* min_value, double* max_value,
+                               uint64_t* first_nonfinite) {
+  return guarded(c, [&] {
+    if (!dims || !d_field || !d_out || !min_value || !max_value || !first_nonfinite)
+      fail(MGRX_INVALID_ARGUMENT, "null argument");
+    Plan* p = get_plan(c, dtype, nd, dims, levels, stop);
+    const int64_t N = p->h.node[p->h.L];
+    nf_arm(c);
+    struct Disarm {
+      mgrx_gpu_ctx* c;
+      ~Disarm() { c->nf_armed = false; }
+    } disarm{c};
+    if (dtype == MGRX_F32)
+      decompose_impl<float>(c, *p, static_cast<const float*>(d_field), static_cast<float*>(d_out), nullptr);
+    else
+      decompose_impl<double>(c, *p, static_cast<const double*>(d_field), static_cast<double*>(d_out), nullptr);
+    unsigned flag = 0;
+    double lo = INFINITY, hi = -INFINITY;
+    uint64_t bad = uint64_t(N);
+    if (!nf_read(c, &flag, &lo, &hi) || flag) {  // separate pass (or the exact first offset)
+      if (dtype == MGRX_F32)
+        field_stats_run<float>(c, static_cast<const float*>(d_field), N, &lo, &hi, &bad);
+      else
+        field_stats_run<double>(c, static_cast<const double*>(d_field), N, &lo, &hi, &bad);
+    }
+    *min_value = lo;
+    *max_value = hi;
+    *first_nonfinite = bad;
+    if (bad < uint64_t(N))
+      fail(MGRX_NONFINITE_DATA, "non-finite value at offset %llu", (unsigned long long)bad);
   });
 }
 

@@ -568,6 +568,13 @@ __device__ __forceinline__ void pipe_release(PlanePipe* pp, int d, int dmax, Iss
 }
 
 // Per-plane, per-thread context of the decompose row loop.
+// Order-preserving image of an fp64 value in 64-bit unsigned integers
+// (x < y  <=>  ordered_bits(x) < ordered_bits(y) for non-NaN values).
+__device__ __forceinline__ unsigned long long ordered_bits(double x) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
 template <typename T>
 struct DecRows {
   const T* rp;        // tile row 0 (= fine row rlo), at column 2c
@@ -599,7 +606,7 @@ struct DecRows {
 // pass makes anyway.
 template <typename T, int TI1, bool PODD, bool FULL, bool CF = false>
 __device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const T* nr, T* nb, int nbs, double* Q,
-                                         T& nf) {
+                                         T& nf, T& lo, T& hi) {
   constexpr int RMAX = 2 * TI1 + 3;
   const int n2 = x.n2;
   const T* rr = x.rp + (x.jbase - x.rlo) * n2;  // tile row of jr = 0 (may precede the tile when not FULL)
@@ -638,7 +645,11 @@ __device__ __forceinline__ void dec_rows(const DecRows<T>& x, const T* nl, const
     }
     const bool rdeg = !FULL && o1 && (j1 + 1 >= x.n1);
     const T rE = rr[0], rO = rr[x.oi];
-    if (CF) nf = rE * T(0) + (rO * T(0) + nf);
+    if (CF) {  // finiteness + range of every value read (NaN is ignored by fmin / fmax)
+      nf = rE * T(0) + (rO * T(0) + nf);
+      lo = fmin(lo, fmin(rE, rO));
+      hi = fmax(hi, fmax(rE, rO));
+    }
     const double rawE = double(rE);
     const double rawO = double(rO);
     const double aL = aLc;
@@ -780,6 +791,7 @@ __global__ void __launch_bounds__(MAXT, NB ? NB : (MAXT == kPlaneMaxThreads ? 2 
   for (int ir = 0; ir < TI1; ++ir) A.prev[ir] = A.cur[ir] = A.next[ir] = 0.0;
   int jdone = 0;  // coarse planes finished by this CTA
   T nf = T(0);    // CF: 0 unless a raw value was inf / NaN
+  T lo = T(INFINITY), hi = T(-INFINITY);  // CF: range of the values read
   // Shell / coarse pointers of the unit's first even and odd plane, advanced
   // by a constant per plane pair (shell_row_start is linear in k = p / 2 for
   // each parity: +n1 n2 - m1 m2 for even planes, +n1 n2 for odd ones).
@@ -808,8 +820,8 @@ __global__ void __launch_bounds__(MAXT, NB ? NB : (MAXT == kPlaneMaxThreads ? 2 
       double Q[TI1];
 #pragma unroll
       for (int ir = 0; ir < TI1; ++ir) Q[ir] = 0.0;
-      if (full) dec_rows<T, TI1, false, true, CF>(x, r_own, r_own, nb, nt, Q, nf);
-      else dec_rows<T, TI1, false, false, CF>(x, r_own, r_own, nb, nt, Q, nf);
+      if (full) dec_rows<T, TI1, false, true, CF>(x, r_own, r_own, nb, nt, Q, nf, lo, hi);
+      else dec_rows<T, TI1, false, false, CF>(x, r_own, r_own, nb, nt, Q, nf, lo, hi);
       pipe_release<NS>(pp, d, D, issue);  // this warp is done with plane d's slot
       l0_plane<TI1>(g, ur, S, p, Q, A, jdone, G);
       se_e += step_e;
@@ -832,15 +844,30 @@ __global__ void __launch_bounds__(MAXT, NB ? NB : (MAXT == kPlaneMaxThreads ? 2 
 #pragma unroll
       for (int ir = 0; ir < TI1; ++ir) Q[ir] = 0.0;
       const T* nr = x.has_right ? row0(d + 2) : r_own;
-      if (full) dec_rows<T, TI1, true, true, CF>(x, r_own, nr, nb, nt, Q, nf);
-      else dec_rows<T, TI1, true, false, CF>(x, r_own, nr, nb, nt, Q, nf);
+      if (full) dec_rows<T, TI1, true, true, CF>(x, r_own, nr, nb, nt, Q, nf, lo, hi);
+      else dec_rows<T, TI1, true, false, CF>(x, r_own, nr, nb, nt, Q, nf, lo, hi);
       pipe_release<NS>(pp, d + 1, D, issue);
       l0_plane<TI1>(g, ur, S, p, Q, A, jdone, G);
       se_o += step_o;
       so_o += step_o;
     }
   }
-  if (CF && !(nf == T(0))) atomicOr(g.nonfinite, 1u);
+  if (CF) {
+    if (!(nf == T(0))) atomicOr(g.nonfinite, 1u);
+    // range: warp minimum / maximum, one atomic per warp on the
+    // order-preserving 64-bit image of the fp64 value
+    double dl = double(lo), dh = double(hi);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      dl = fmin(dl, __shfl_xor_sync(0xffffffffu, dl, o));
+      dh = fmax(dh, __shfl_xor_sync(0xffffffffu, dh, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      unsigned long long* mm = reinterpret_cast<unsigned long long*>(g.nonfinite + 2);
+      atomicMin(mm, ordered_bits(dl));
+      atomicMax(mm + 1, ordered_bits(dh));
+    }
+  }
   pdl_trigger();
 }
 

@@ -77,6 +77,45 @@ def test_gpu_field_stats(dtype):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("shape,dt", [((65, 65, 65), "f32"), ((129, 65, 33), "f32"), ((33, 40, 70), "f64"),
+                                      ((9, 11, 700), "f32"), ((300, 258), "f64"), ((9, 8, 7, 6), "f32")])
+def test_gpu_decompose_checked(shape, dt):
+    """check_finite + range folded into the decompose's first plane pass
+    (mgrx_gpu_decompose_checked; the fused 3-D shapes) or a separate pass
+    (2-D / 4-D): the range equals the field's exact min / max, the output
+    equals decompose's, and a NaN / inf raises the reference's
+    nonfinite_data (MGRX_NONFINITE_DATA) with the first offset."""
+    import ctypes as C
+
+    import torch
+
+    import paper_2010_05872_b200 as mg
+    from paper_2010_05872_b200._lib import lib
+
+    dtype = torch.float32 if dt == "f32" else torch.float64
+    x = torch.randn(shape, dtype=dtype, device="cuda") * 3.0 + 1.0
+    h = mg.GridHierarchy.create(shape)
+    ws = mg.SolverWorkspace()
+    out = torch.empty(x.numel(), dtype=dtype, device="cuda")
+    dims = (C.c_uint64 * len(shape))(*shape)
+    lo, hi, bad = C.c_double(), C.c_double(), C.c_uint64()
+    code = 0 if dt == "f32" else 1
+    ws._bind_stream()
+    rc = lib.mgrx_gpu_decompose_checked(ws.handle, code, len(shape), dims, -1, 0, C.c_void_p(x.data_ptr()),
+                                        C.c_void_p(out.data_ptr()), C.byref(lo), C.byref(hi), C.byref(bad))
+    assert rc == 0, rc
+    assert lo.value == float(x.min()) and hi.value == float(x.max()) and bad.value == x.numel()
+    assert torch.equal(out, mg.decompose(x, h, 0, ws).buffer)
+    y = x.clone().reshape(-1)
+    y[y.numel() // 3] = float("nan")
+    y[y.numel() // 2] = float("-inf")
+    ws._bind_stream()
+    rc = lib.mgrx_gpu_decompose_checked(ws.handle, code, len(shape), dims, -1, 0, C.c_void_p(y.data_ptr()),
+                                        C.c_void_p(out.data_ptr()), C.byref(lo), C.byref(hi), C.byref(bad))
+    assert rc == 9 and bad.value == y.numel() // 3, (rc, bad.value)  # MGRX_NONFINITE_DATA
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("shape,dtype", [((33, 33, 33), np.float32), ((40, 17, 9), np.float64), ((129, 65), np.float32),
                                          ((9, 7, 11, 5), np.float64), ((1000,), np.float32)])
 @pytest.mark.parametrize("e", [1e-1, 1e-4, 1e-9])
