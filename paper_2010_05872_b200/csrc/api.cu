@@ -20,7 +20,6 @@
 #include "common.cuh"
 #include "fused2d.h"
 #include "fused3d.h"
-#include "p2.h"
 #include "kernels.h"
 
 using namespace mgrx_b200;
@@ -163,9 +162,6 @@ struct Plan {
   std::vector<size_t> blk_off;     // level block offsets (levels stop..L-1)
   std::vector<Fused3DPlan> fused;  // index l; .enabled false when not applicable
   std::vector<Fused2DPlan> f2;     // index l; fused 2-D passes of nonuniform-coordinate calls
-  std::vector<P2Plan> p2;          // index l; second-generation fused passes (fp32)
-  double* d_p2tabs = nullptr;      // their tables
-  const void* p2_scratch = nullptr;  // scratch the p2 counters were zeroed for
   // tail: levels stop+1..tail_top run in one CTA (uniform or nonuniform coordinates)
   int tail_top = -1;
   int64_t tail_nmax = 0;
@@ -173,7 +169,6 @@ struct Plan {
   void* d_tail_rec = nullptr;  // TailLevel[] coarsest first
   ~Plan() {
     if (d_tables) cudaFree(d_tables);
-    if (d_p2tabs) cudaFree(d_p2tabs);
     if (d_tail_dec) cudaFree(d_tail_dec);
     if (d_tail_rec) cudaFree(d_tail_rec);
   }
@@ -404,20 +399,10 @@ Plan* get_plan(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int lev
     p->blk_off[l] = off;
     off = align_up(off + size_t(h.node[l]) * es);
   }
-  // Fused 3-D plans (fused3d.cu) for the levels they cover; on fp32 levels
-  // with odd extents the second-generation passes (fused_p2.cu) replace the
-  // plane / row / column passes (the interpolation stays fused3d's).
-  p->p2.resize(L + 1);
-  std::vector<double> p2host;
+  // Fused 3-D plans (fused3d.cu) for the levels they cover.
   for (int l = stop + 1; l <= L; ++l) {
     p->fused[l] = fused3d_plan(p->geom[l], int(es));
-    if (p->fused[l].enabled) p->p2[l] = p2_plan(p->geom[l], int(es));
-    if (p->p2[l].enabled) {
-      p->p2[l].scratch_off = off;
-      off = align_up(off + p->p2[l].scratch_bytes);
-      p->p2[l].tab_off = p2host.size();
-      p2host.insert(p2host.end(), p->p2[l].tabs.begin(), p->p2[l].tabs.end());
-    } else if (p->fused[l].enabled) {
+    if (p->fused[l].enabled) {
       p->fused[l].scratch_off = off;
       off = align_up(off + p->fused[l].scratch_bytes);
     }
@@ -429,11 +414,6 @@ Plan* get_plan(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int lev
       p->f2[l].scratch_off = off;
       off = align_up(off + p->f2[l].scratch_bytes);
     }
-  }
-  if (!p2host.empty()) {
-    cuda_check(cudaMalloc(&p->d_p2tabs, p2host.size() * sizeof(double)), "cudaMalloc(p2 tables)");
-    cuda_check(cudaMemcpy(p->d_p2tabs, p2host.data(), p2host.size() * sizeof(double), cudaMemcpyHostToDevice),
-               "upload p2 tables");
   }
   p->bytes = off;
   Plan* raw = p.get();
@@ -573,24 +553,6 @@ std::vector<NuLevel> upload_nu(mgrx_gpu_ctx* c, const Plan& p, const double* con
 
 // ------------------------------------------------------------- transform
 
-// The p2 passes' completion counters live in the scratch: zero them whenever
-// the scratch was (re)allocated since they were last zeroed.
-void ensure_p2(mgrx_gpu_ctx* c, Plan& p) {
-  if (p.p2_scratch == c->scratch) return;
-  for (size_t l = 0; l < p.p2.size(); ++l)
-    if (p.p2[l].enabled)
-      cuda_check(p2_init(p.p2[l], static_cast<char*>(c->scratch) + p.p2[l].scratch_off, c->stream), "p2 init");
-  // the fused levels' dataflow-solve counters (each launch leaves them zeroed)
-  for (size_t l = 0; l < p.fused.size(); ++l)
-    if (p.fused[l].enabled)
-      cuda_check(cudaMemsetAsync(static_cast<char*>(c->scratch) + p.fused[l].scratch_off + p.fused[l].ctr_off, 0,
-                                 fused3d_ctr_bytes(p.fused[l]), c->stream),
-                 "solve counters");
-  p.p2_scratch = c->scratch;
-}
-
-bool use_p2(const mgrx_gpu_ctx* c, const Plan& p, int l, bool nu) { return !nu && c->path == 0 && p.p2[l].enabled; }
-
 template <typename T>
 void decompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, T* d_out, const std::vector<NuLevel>* nu) {
   const Hierarchy& h = p.h;
@@ -601,7 +563,6 @@ void decompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, T* d_out, const 
     return;
   }
   ensure(&c->scratch, &c->scratch_bytes, p.bytes, c, "cudaMalloc(scratch)");
-  ensure_p2(c, p);
   char* s = static_cast<char*>(c->scratch);
   double* comp = reinterpret_cast<double*>(s + p.off_comp);
   double* tmp = reinterpret_cast<double*>(s + p.off_tmp);
@@ -619,13 +580,7 @@ void decompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, T* d_out, const 
     T* coarse = (l - 1 == stop) ? d_out : reinterpret_cast<T*>(s + p.blk_off[l - 1]);
     const Fused3DPlan& fp = p.fused[l];
     cudaError_t e;
-    if (std::is_same<T, float>::value && use_p2(c, p, l, nu != nullptr)) {
-      P2Bufs b;
-      P2Tabs t;
-      p2_bind(p.p2[l], s + p.p2[l].scratch_off, p.d_p2tabs, &b, &t);
-      e = p2_decompose_level(reinterpret_cast<const float*>(blk), reinterpret_cast<float*>(shell),
-                             reinterpret_cast<float*>(coarse), p.p2[l], b, t, exec(c, l));
-    } else if (nu && c->path == 0 && p.f2[l].enabled) {
+    if (nu && c->path == 0 && p.f2[l].enabled) {
       e = fused2d_decompose_level<T>(blk, shell, coarse, s + p.f2[l].scratch_off, p.f2[l], (*nu)[l], exec(c, l));
     } else if (!nu && c->path == 0 && fp.enabled) {
       Exec ex = exec(c, l);
@@ -654,12 +609,9 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
     return;
   }
   ensure(&c->scratch, &c->scratch_bytes, p.bytes, c, "cudaMalloc(scratch)");
-  ensure_p2(c, p);
   char* s = static_cast<char*>(c->scratch);
   double* comp = reinterpret_cast<double*>(s + p.off_comp);
   double* tmp = reinterpret_cast<double*>(s + p.off_tmp);
-  const bool f32 = std::is_same<T, float>::value;
-  auto p2_bufs = [&](int l, P2Bufs* b, P2Tabs* t) { p2_bind(p.p2[l], s + p.p2[l].scratch_off, p.d_p2tabs, b, t); };
   // Corrections of the fused levels depend only on their shells
   // (transform.hpp:343-366: the component is zero on the coarse nodes): fork
   // them onto side streams at the start; the sequential chain (tail, then per
@@ -685,18 +637,9 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
         cudaStream_t sd = c->side[k++ % mgrx_gpu_ctx::kSide];
         if (l == L && rec_prio() >= 1) sd = c->hi;
         cuda_check(cudaStreamWaitEvent(sd, c->fork, 0), "cudaStreamWaitEvent");
-        if (f32 && use_p2(c, p, l, nu != nullptr)) {
-          P2Bufs b;
-          P2Tabs t;
-          p2_bufs(l, &b, &t);
-          cuda_check(p2_recompose_correction(reinterpret_cast<const float*>(d_coeffs + h.node[l - 1]), p.p2[l], b, t,
-                                             exec_on(c, sd, l)),
-                     "recompose correction");
-        } else {
-          cuda_check(fused3d_recompose_correction<T>(d_coeffs + h.node[l - 1], s + fp.scratch_off, fp, p.thomas[l],
-                                                     exec_on(c, sd, l)),
-                     "recompose correction");
-        }
+        cuda_check(fused3d_recompose_correction<T>(d_coeffs + h.node[l - 1], s + fp.scratch_off, fp, p.thomas[l],
+                                                   exec_on(c, sd, l)),
+                   "recompose correction");
         cuda_check(cudaEventRecord(c->lvl_done[l], sd), "cudaEventRecord");
         forked[l] = 1;
       }
@@ -725,21 +668,9 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
     T* fine = (l == L) ? d_field : reinterpret_cast<T*>(s + p.blk_off[l]);
     const Fused3DPlan& fp = p.fused[l];
     cudaError_t e;
-    const bool p2l = f32 && use_p2(c, p, l, nu != nullptr);
-    if (forked[l] || p2l) {
-      if (forked[l]) cuda_check(cudaStreamWaitEvent(cs, c->lvl_done[l], 0), "cudaStreamWaitEvent");
-      if (p2l) {
-        P2Bufs b;
-        P2Tabs t;
-        p2_bufs(l, &b, &t);
-        if (!forked[l])
-          cuda_check(p2_recompose_correction(reinterpret_cast<const float*>(shell), p.p2[l], b, t, exec_on(c, cs, l)),
-                     "recompose correction");
-        e = p2_recompose_apply(reinterpret_cast<float*>(coarse), p.p2[l], b, t, exec_on(c, cs, l));
-        if (e == cudaSuccess) e = fused3d_slab_interp<T>(shell, coarse, fine, fp, 0, fp.g.n0, exec_on(c, cs, l));
-      } else {
-        e = fused3d_recompose_finish<T>(shell, coarse, fine, s + fp.scratch_off, fp, p.thomas[l], exec_on(c, cs, l));
-      }
+    if (forked[l]) {
+      cuda_check(cudaStreamWaitEvent(cs, c->lvl_done[l], 0), "cudaStreamWaitEvent");
+      e = fused3d_recompose_finish<T>(shell, coarse, fine, s + fp.scratch_off, fp, p.thomas[l], exec_on(c, cs, l));
     } else if (nu && c->path == 0 && p.f2[l].enabled) {
       e = fused2d_recompose_level<T>(shell, coarse, fine, s + p.f2[l].scratch_off, p.f2[l], (*nu)[l],
                                      exec_on(c, cs, l));

@@ -25,9 +25,9 @@
 //              f3_row, f3_col x2  as above, coarse -= z;
 //              f3_rec_interp fine block = coarse nodes + shell + prediction.
 //
-// Measured and kept opt-in (slower at 513^3): the in-plane
-// cluster solve f3_s12 (axes 2 + 1 in one pass over G through DSMEM,
-// MGRX_S12=1) and the one-launch dataflow solve f3_solveq (MGRX_SOLVEQ=1).
+// Measured and removed (slower at 513^3; commit 48aabc0 has
+// them): an in-plane cluster solve of axes 2 + 1 through DSMEM and a
+// one-launch dataflow solve of all three axes.
 //
 // The tensor-product correction z = S2 S1 S0 c (S_a = Thomas_a o Load_a,
 // transform.hpp:392-428) is evaluated as (T0 T1 T2)(L0 L1 L2) c: the
@@ -1374,298 +1374,6 @@ __global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : (MAXT == kColT
   }
 }
 
-// ------------------------------------------------- in-plane cluster solve
-// Thomas along axis 2 and then axis 1 (batched_solve, transform.hpp:116-130,
-// the reference's axis sweeps :392-428 restricted to one coarse plane) of
-// every plane of G in ONE read and write of G.  A thread-block cluster of NC
-// CTAs holds a whole m1 x m2 plane in distributed shared memory: CTA rank r
-// owns the band of rows [r B, r B + B), loaded by one TMA bulk copy (the rows
-// of a band are contiguous in G).  Axis 2: one warp per row of the band
-// (segmented solve, warp_row_thomas_reg).  Axis 1: one thread per column;
-// the band's segment of the column runs the recurrence from a zero carry,
-// the segments' affine maps are published in shared memory and every CTA
-// folds the maps of the ranks before it (forward) / after it (backward)
-// through DSMEM, then reruns the exact recurrence from its true carry and
-// the backward pass stores z straight to G.  Two cluster barriers per plane.
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t cluster_size() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// (a, b) of `p` in the shared memory of cluster CTA `rank`
-__device__ __forceinline__ Aff ld_cluster_aff(const double2* p, uint32_t rank) {
-  uint32_t ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(rank));
-  double a, b;
-  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(ra) : "memory");
-  return Aff{a, b};
-}
-
-struct S12Smem {
-  size_t pub, tab, buf, total;
-};
-__host__ __device__ inline S12Smem s12_smem(int m2, int B) {
-  S12Smem L;
-  L.pub = 16;                                   // mbarrier
-  L.tab = L.pub + size_t(2) * m2 * 16;          // pubF, pubB: (a, b) per column
-  L.buf = (L.tab + size_t(2) * B * 8 + 15) / 16 * 16;  // band Thomas tables of axis 1
-  L.total = L.buf + size_t(B) * m2 * 8 + 16;    // the band (+ 16-byte lead of the bulk copy)
-  return L;
-}
-
-__host__ __device__ constexpr int s12_maxt(int seg) { return seg <= 9 ? 320 : 576; }
-constexpr int kS12Band = 17;  // rows per CTA band: a column's segment lives in registers
-
-// Fold the published affine maps of cluster ranks [q0, q1) (forward: in
-// increasing rank order) or (q1, q0] (backward), four DSMEM loads in flight.
-template <bool FWD>
-__device__ __forceinline__ double s12_fold(const double2* pub, uint32_t q0, uint32_t q1, double x) {
-  for (uint32_t q = q0; q < q1; q += 4) {
-    Aff p[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const uint32_t qq = FWD ? q + t : q1 - 1 - (q - q0) - t;
-      p[t] = (q + t < q1) ? ld_cluster_aff(pub, qq) : Aff{0.0, 1.0};
-    }
-#pragma unroll
-    for (int t = 0; t < 4; ++t) x = p[t].a + p[t].b * x;
-  }
-  return x;
-}
-
-template <int SEG>
-__global__ void __launch_bounds__(s12_maxt(SEG), SEG <= 9 ? 3 : 1) k_f3_solve12(double* __restrict__ G, int64_t m0, int m1, int m2, int B,
-                                                   const double* __restrict__ w1, const double* __restrict__ id1,
-                                                   const double* __restrict__ w2, const double* __restrict__ id2,
-                                                   unsigned long long* trace) {
-  constexpr int BM = kS12Band;
-  unsigned long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tlast = clock64();
-  auto tmark = [&](int ph) {
-    if (trace) {
-      const unsigned long long t = clock64();
-      tacc[ph] += t - tlast;
-      tlast = t;
-    }
-  };
-  extern __shared__ __align__(16) unsigned char smem[];
-  const S12Smem LY = s12_smem(m2, B);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-  double2* pubF = reinterpret_cast<double2*>(smem + LY.pub);
-  double2* pubB = pubF + m2;
-  double* tw1 = reinterpret_cast<double*>(smem + LY.tab);
-  double* tid1 = tw1 + B;
-  unsigned char* braw = smem + LY.buf;
-  const uint32_t rank = cluster_rank(), NC = cluster_size();
-  const int r0 = int(rank) * B, r1 = min(m1, r0 + B), nr = max(0, r1 - r0);
-  const int tid = threadIdx.x, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int64_t cid = blockIdx.x / NC, ncl = gridDim.x / NC;
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int i = tid; i < nr; i += blockDim.x) {
-    tw1[i] = w1[r0 + i];
-    tid1[i] = id1[r0 + i];
-  }
-  __syncthreads();
-  cluster_sync_all();  // every CTA of the cluster runs before any DSMEM access
-  pdl_wait();
-  auto band = [&](int64_t k) { return G + (k * m1 + r0) * int64_t(m2); };
-  auto issue = [&](int64_t k) {  // one thread: the band of plane k into the buffer
-    const uintptr_t a = reinterpret_cast<uintptr_t>(band(k));
-    const uintptr_t a0 = a & ~uintptr_t(15);
-    const uint32_t bytes = uint32_t(((a + uintptr_t(nr) * m2 * 8 + 15) & ~uintptr_t(15)) - a0);
-    fence_proxy_async();
-    mbar_expect_tx(bar, bytes);
-    for (uint32_t off = 0; off < bytes; off += 32768u)
-      bulk_g2s(braw + off, reinterpret_cast<const char*>(a0) + off, min(32768u, bytes - off), bar);
-  };
-  uint32_t phase = 0;
-  const int c = tid;
-  const bool act = c < m2;
-  if (tid == 0 && nr > 0 && cid < m0) issue(cid);
-  for (int64_t k = cid; k < m0; k += ncl) {
-    double* gband = band(k);
-    const int lead = int(reinterpret_cast<uintptr_t>(gband) & 15);
-    double v[BM];
-    if (nr > 0) {
-      tmark(7);
-      mbar_wait(bar, phase);
-      phase ^= 1u;
-      tmark(0);
-      double* buf = reinterpret_cast<double*>(braw + lead);
-      // axis 2: one warp per band row
-      for (int row = warp; row < nr; row += nw) warp_row_thomas_reg<SEG>(buf + int64_t(row) * m2, m2, w2, id2);
-      __syncthreads();
-      tmark(1);
-      // this thread's column segment into registers; the buffer is then free
-      // for the next plane's band, loaded while the axis-1 solve runs
-#pragma unroll
-      for (int i = 0; i < BM; ++i) v[i] = (act && i < nr) ? buf[i * m2 + c] : 0.0;
-      fence_proxy_async();
-      __syncthreads();
-      if (tid == 0 && k + ncl < m0) issue(k + ncl);
-      tmark(2);
-    }
-    // axis 1, forward: y_i = f_i - w_i y_{i-1} over the band from a zero carry
-    double fa = 0.0, fb = 1.0;
-#pragma unroll
-    for (int i = 0; i < BM; ++i)
-      if (i < nr) {
-        const double wi = tw1[i];
-        fa = v[i] - wi * fa;
-        fb = -wi * fb;
-      }
-    if (act) pubF[c] = make_double2(fa, fb);
-    tmark(3);
-    cluster_sync_all();
-    tmark(4);
-    double y = act ? s12_fold<true>(pubF + c, 0, rank, 0.0) : 0.0;
-#pragma unroll
-    for (int i = 0; i < BM; ++i)
-      if (i < nr) {
-        y = v[i] - tw1[i] * y;
-        v[i] = y;
-      }
-    // backward: z_i = (y_i - z_{i+1}/3) / d_i from a zero carry
-    double ba = 0.0, bb = 1.0;
-#pragma unroll
-    for (int i = BM - 1; i >= 0; --i)
-      if (i < nr) {
-        const double id = tid1[i];
-        ba = (v[i] - kOff * ba) * id;
-        bb = -kOff * id * bb;
-      }
-    if (act) pubB[c] = make_double2(ba, bb);
-    tmark(5);
-    cluster_sync_all();
-    tmark(6);
-    if (act) {
-      double z = s12_fold<false>(pubB + c, rank + 1, NC, 0.0);
-      double* gc = gband + c;
-#pragma unroll
-      for (int i = BM - 1; i >= 0; --i)
-        if (i < nr) {
-          z = (v[i] - kOff * z) * tid1[i];
-          gc[int64_t(i) * m2] = z;
-        }
-    }
-  }
-  tmark(7);
-  if (trace && tid == 0)
-    for (int i = 0; i < 8; ++i) atomicAdd(trace + i, tacc[i]);
-  pdl_trigger();
-  cluster_sync_all();  // no CTA leaves while a peer may still read its published maps
-}
-
-// Cluster shape of the in-plane solve: the smallest cluster whose bands fit
-// three CTAs per SM (then two, then one); 0 when the plane does not fit.
-struct S12Plan {
-  int nc = 0, B = 0, threads = 0, seg = 0;
-  size_t smem = 0;
-};
-static S12Plan s12_plan(int m1, int m2) {
-  S12Plan p;
-  if (!std::getenv("MGRX_S12")) return p;  // opt-in: slower than the dataflow solve (cluster barriers)
-  const int seg = (m2 + 31) / 32;
-  p.seg = seg <= 3 ? 3 : (seg <= 5 ? 5 : (seg <= 9 ? 9 : (seg <= 17 ? 17 : 0)));
-  if (p.seg == 0 || (m2 + 31) / 32 * 32 > s12_maxt(p.seg)) {
-    p.seg = 0;
-    return p;
-  }
-  // bands of <= kS12Band rows (register-resident column segments), as few
-  // cluster CTAs as that allows (<= 16)
-  const int nc = (m1 + kS12Band - 1) / kS12Band;
-  if (nc > 16) return p;
-  int B = (m1 + nc - 1) / nc;
-  const size_t bytes = s12_smem(m2, B).total;
-  if (bytes > 200 * 1024) return p;
-  p.nc = nc;
-  p.B = B;
-  p.smem = bytes;
-  p.threads = (m2 + 31) / 32 * 32;
-  return p;
-}
-
-// Launch the in-plane solve over planes [0, m0) of G; false when the plane
-// shape does not fit a cluster (the caller runs the row + column passes).
-static bool launch_solve12(double* G, int64_t m0, int m1, int m2, const ThomasLevel& th, const Exec& ex,
-                           cudaError_t* err) {
-  const S12Plan p = s12_plan(m1, m2);
-  if (p.nc == 0) return false;
-  void (*kern)(double*, int64_t, int, int, int, const double*, const double*, const double*, const double*,
-               unsigned long long*) =
-      p.seg == 3 ? k_f3_solve12<3> : (p.seg == 5 ? k_f3_solve12<5> : (p.seg == 9 ? k_f3_solve12<9> : k_f3_solve12<17>));
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem));
-  if (e == cudaSuccess && p.nc > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  if (e != cudaSuccess) {
-    *err = e;
-    return true;
-  }
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = unsigned(p.nc);
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(unsigned(p.threads));
-  cfg.dynamicSmemBytes = p.smem;
-  cfg.stream = ex.s;
-  cfg.attrs = attr;
-  cfg.numAttrs = ex.prof ? 1 : 2;
-  // resident clusters (cached per shape: the query is not free)
-  static thread_local int cache_key[4] = {-1, -1, -1, -1};
-  static thread_local int cache_val = 0;
-  const int key[4] = {p.nc, p.B, p.threads, m2};
-  if (std::memcmp(key, cache_key, sizeof key) != 0) {
-    cfg.gridDim = dim3(unsigned(p.nc * 64));
-    int ncl = 0;
-    if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess || ncl <= 0) {
-      cudaGetLastError();
-      ncl = std::max(1, kNumSMs / p.nc);
-    }
-    std::memcpy(cache_key, key, sizeof key);
-    cache_val = ncl;
-    if (std::getenv("MGRX_DEBUG"))
-      std::fprintf(stderr, "[mgrx] f3_s12 m1 %d m2 %d: cluster %d, band %d rows, %d threads, %zu B smem, %d clusters\n",
-                   m1, m2, p.nc, p.B, p.threads, p.smem, ncl);
-  }
-  const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>(m0, cache_val));
-  cfg.gridDim = dim3(unsigned(ncl * p.nc));
-  // MGRX_S12_TRACE: per-phase clock totals of every CTA's thread 0 (debug, eager only)
-  static const bool tr = std::getenv("MGRX_S12_TRACE") != nullptr;
-  unsigned long long* trace = nullptr;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(ex.s, &cs);
-  if (tr && cs == cudaStreamCaptureStatusNone) {
-    cudaMallocAsync(reinterpret_cast<void**>(&trace), 64, ex.s);
-    cudaMemsetAsync(trace, 0, 64, ex.s);
-  }
-  MGRX_LAUNCH(ex, "f3_s12", (*err = cudaLaunchKernelEx(&cfg, kern, G, m0, m1, m2, p.B, th.w[1], th.inv_d[1],
-                                                       th.w[2], th.inv_d[2], trace)));
-  if (trace) {
-    unsigned long long h[8];
-    cudaMemcpyAsync(h, trace, 64, cudaMemcpyDeviceToHost, ex.s);
-    cudaStreamSynchronize(ex.s);
-    cudaFreeAsync(trace, ex.s);
-    const double n = double(cfg.gridDim.x);
-    std::fprintf(stderr, "[mgrx] s12 m1 %d trace (kcycles per CTA): tma %.1f t2 %.1f regs %.1f fwd %.1f bar1 %.1f "
-                 "fold+bwd %.1f bar2 %.1f fold+store %.1f\n", m1, h[0] / n / 1e3, h[1] / n / 1e3, h[2] / n / 1e3,
-                 h[3] / n / 1e3, h[4] / n / 1e3, h[5] / n / 1e3, h[6] / n / 1e3, h[7] / n / 1e3);
-  }
-  return true;
-}
-
 // ------------------------------------------------------------ host side
 
 template <typename T, int TI1>
@@ -1756,328 +1464,10 @@ void launch_col(double* G, T* coarse, double sign, const F3Geom& g, int axis, co
 #undef MGRX_COLL
 }
 
-// ---------------------------------------------- dataflow solve (one launch)
-// The three Thomas sweeps of a fused level (axis 2, axis 1, axis 0 +
-// apply_correction; batched_solve transform.hpp:116-130, apply :435-477) as
-// ONE persistent launch instead of three: CTAs claim work items in order
-// from a global counter,
-//   R(k, g)   axis 2 of rows 11 g .. 11 g + 10 of plane k (a warp per row,
-//             warp_row_thomas_reg),
-//   C(k, g)   axis 1 of columns 16 g .. 16 g + 15 of plane k (the column
-//             pass's segmented solve), once every R item of plane k is done
-//             (a per-plane counter; the plane was just written, so it is read
-//             from L2),
-//   Z(j)      axis 0 + coarse +/- z of columns 16 j .. 16 j + 15 of the
-//             (row, column) grid, once every C item is done,
-// with the C items of plane k placed `lag` planes after its R items.  Items
-// are claimed in increasing order and depend only on smaller items, so the
-// smallest unfinished claimed item can always run: no deadlock, whatever
-// share of the GPU the launch gets.
-constexpr int kQThreads = 352;  // 11 warps: R items = 11 rows, C/Z items = 16 columns x 22 segments
-constexpr int kQWarps = kQThreads / 32;
-constexpr int kQLS = 12;        // values per column segment (m <= 264)
-constexpr int kQMaxM = 2 * kQWarps * kQLS;
-
-template <typename T>
-struct QArgs {
-  double* G;
-  T* coarse;  // null: no Z items (recompose correction)
-  double sign;
-  int m0, m1, m2;
-  int nrg, ncg;            // R / C items per plane
-  int64_t nzg;             // Z items
-  int lag;                 // planes between R(k) and C(k)
-  int64_t nsteps, total;   // (m0 + lag) steps of nrg + ncg items, then the Z items
-  unsigned* ctr;           // [0] item counter, [1] C items done, [2 + k] R items of plane k done,
-                           // [2 + m0] CTAs finished: the last one zeroes the counters for the next launch
-  const double *w0, *id0, *w1, *id1, *w2, *id2;
-  unsigned long long* trace;  // MGRX_Q_TRACE: clocks per item type (R, C wait, C, Z wait, Z) summed over CTAs
-};
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void q_wait(const unsigned* c, unsigned need) {
-  if (threadIdx.x == 0)
-    while (ld_acquire_u32(c) < need) __nanosleep(128);
-  __syncthreads();
-}
-__device__ __forceinline__ void q_done(unsigned* c) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(c, 1u);
-  }
-}
-
-// Segmented Thomas of 16 columns (column pass body, k_f3_col): column c16 at
-// G[base(c16) + i * stride], i < m; the CTA's 22 segments of <= kQLS values.
-template <typename T, bool APPLY>
-__device__ __forceinline__ void q_cols(double* __restrict__ G, T* __restrict__ coarse, double sign, int64_t base,
-                                       bool valid, int m, int64_t stride, const double* tw, const double* tid,
-                                       double* A, double* B) {
-  const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
-  const int SY = (m + 2 * kQLS - 1) / (2 * kQLS), S = 2 * SY;
-  const int c16 = lane & 15, s = 2 * wy + (lane >> 4);
-  const bool act = wy < SY;
-  const int seg = (m + S - 1) / S;
-  const int s0 = min(m, s * seg), len = act ? min(m, s0 + seg) - s0 : 0;
-  double v[kQLS];
-  {
-    const double* gp = G + base + int64_t(s0) * stride;
-#pragma unroll
-    for (int k = 0; k < kQLS; ++k) {
-      v[k] = (valid && k < len) ? __ldcg(gp) : 0.0;
-      gp += stride;
-    }
-  }
-  double ya = 0.0, yb = 1.0;
-#pragma unroll
-  for (int k = 0; k < kQLS; ++k)
-    if (k < len) {
-      const double wi = ld_volatile(tw + s0 + k);
-      ya = v[k] - wi * ya;
-      yb = -wi * yb;
-    }
-  if (act) {
-    A[s * 16 + c16] = ya;
-    B[s * 16 + c16] = yb;
-  }
-  __syncthreads();
-  double y = 0.0;
-  for (int q = 0; q < s && act; ++q) y = A[q * 16 + c16] + B[q * 16 + c16] * y;
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < kQLS; ++k)
-    if (k < len) {
-      y = v[k] - ld_volatile(tw + s0 + k) * y;
-      v[k] = y;
-    }
-  double za = 0.0, zb = 1.0;
-#pragma unroll
-  for (int k = kQLS - 1; k >= 0; --k)
-    if (k < len) {
-      const double id = ld_volatile(tid + s0 + k);
-      za = (v[k] - kOff * za) * id;
-      zb = -kOff * id * zb;
-    }
-  if (act) {
-    A[s * 16 + c16] = za;
-    B[s * 16 + c16] = zb;
-  }
-  __syncthreads();
-  double z = 0.0;
-  for (int q = S - 1; q > s && act; --q) z = A[q * 16 + c16] + B[q * 16 + c16] * z;
-#pragma unroll
-  for (int k = kQLS - 1; k >= 0; --k)
-    if (k < len) {
-      z = (v[k] - kOff * z) * ld_volatile(tid + s0 + k);
-      v[k] = z;
-    }
-  if (valid && len > 0) {
-    if (APPLY) {
-      T* c = coarse + base + int64_t(s0) * stride;
-      T cv[kQLS];
-#pragma unroll
-      for (int k = 0; k < kQLS; ++k) cv[k] = k < len ? c[int64_t(k) * stride] : T(0);
-#pragma unroll
-      for (int k = 0; k < kQLS; ++k) {
-        if (k < len) *c = to_t<T>(double(cv[k]) + sign * v[k]);
-        c += stride;
-      }
-    } else {
-      double* gp = G + base + int64_t(s0) * stride;
-#pragma unroll
-      for (int k = 0; k < kQLS; ++k) {
-        if (k < len) *gp = v[k];
-        gp += stride;
-      }
-    }
-  }
-  __syncthreads();  // A / B are reused by the next item
-}
-
-template <typename T, int SEG>
-__global__ void __launch_bounds__(kQThreads, 2) k_f3_solveq(const QArgs<T> q) {
-  extern __shared__ __align__(16) double qs[];
-  double* tw0 = qs;
-  double* tid0 = tw0 + q.m0;
-  double* tw1 = tid0 + q.m0;
-  double* tid1 = tw1 + q.m1;
-  double* tw2 = tid1 + q.m1;
-  double* tid2 = tw2 + q.m2;
-  double* A = tid2 + q.m2;  // [22][16]
-  double* B = A + 2 * kQWarps * 16;
-  double* rows = B + 2 * kQWarps * 16;  // [11][m2]
-  __shared__ int64_t next_item;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < q.m0; i += blockDim.x) {
-    tw0[i] = q.w0[i];
-    tid0[i] = q.id0[i];
-  }
-  for (int i = tid; i < q.m1; i += blockDim.x) {
-    tw1[i] = q.w1[i];
-    tid1[i] = q.id1[i];
-  }
-  for (int i = tid; i < q.m2; i += blockDim.x) {
-    tw2[i] = q.w2[i];
-    tid2[i] = q.id2[i];
-  }
-  pdl_wait();
-  if (tid == 0) next_item = atomicAdd(q.ctr, 1u);
-  __syncthreads();
-  int64_t it = next_item;
-  const int64_t per = int64_t(q.nrg) + q.ncg;
-  const int64_t nA = q.nsteps * per;
-  unsigned long long tr[6] = {0, 0, 0, 0, 0, 0};
-  unsigned long long t_0 = clock64();
-  auto mark = [&](int k) {
-    if (q.trace) {
-      const unsigned long long t = clock64();
-      tr[k] += t - t_0;
-      t_0 = t;
-    }
-  };
-  while (it < q.total) {
-    __syncthreads();  // everyone has read next_item
-    unsigned nx = 0;
-    if (tid == 0) nx = atomicAdd(q.ctr, 1u);  // claimed now (its latency hides behind this item), started after it
-    mark(5);
-    if (it < nA) {
-      const int64_t t = it / per;
-      const int sl = int(it - t * per);
-      if (sl < q.nrg) {
-        if (t < q.m0) {  // R(t, sl)
-          const int r = sl * kQWarps + warp;
-          if (r < q.m1) {
-            double* row = q.G + (t * q.m1 + r) * int64_t(q.m2);
-            double* buf = rows + warp * q.m2;
-            for (int e = lane; e < q.m2; e += 32) buf[e] = __ldcg(row + e);
-            __syncwarp();
-            warp_row_thomas_reg<SEG>(buf, q.m2, tw2, tid2);
-            for (int e = lane; e < q.m2; e += 32) row[e] = buf[e];
-          }
-          q_done(q.ctr + 2 + t);
-          mark(0);
-        }
-      } else if (t >= q.lag) {  // C(k, g)
-        const int64_t k = t - q.lag;
-        const int g = sl - q.nrg;
-        q_wait(q.ctr + 2 + k, unsigned(q.nrg));
-        mark(1);
-        const int i2 = g * 16 + (lane & 15);
-        q_cols<T, false>(q.G, static_cast<T*>(nullptr), 0.0, k * q.m1 * q.m2 + i2, i2 < q.m2, q.m1, q.m2, tw1,
-                         tid1, A, B);
-        q_done(q.ctr + 1);
-        mark(2);
-      }
-    } else {  // Z(j)
-      const int64_t j = it - nA;
-      q_wait(q.ctr + 1, unsigned(q.m0) * unsigned(q.ncg));
-      mark(3);
-      const int64_t col = j * 16 + (lane & 15);
-      q_cols<T, true>(q.G, q.coarse, q.sign, col, col < int64_t(q.m1) * q.m2, q.m0, int64_t(q.m1) * q.m2, tw0,
-                      tid0, A, B);
-      mark(4);
-    }
-    if (tid == 0) next_item = nx;
-    __syncthreads();
-    it = next_item;
-  }
-  if (q.trace && tid == 0)
-    for (int k = 0; k < 6; ++k) atomicAdd(q.trace + k, tr[k]);
-  pdl_trigger();
-  if (tid == 0) {
-    __threadfence();
-    if (atomicAdd(q.ctr + 2 + q.m0, 1u) == gridDim.x - 1) {
-      for (int i = 0; i < 3 + q.m0; ++i) q.ctr[i] = 0u;
-      __threadfence();
-    }
-  }
-}
-
-// Launch the dataflow solve (axis 2, axis 1 and, with `coarse`, axis 0 +
-// coarse += sign z) of a fused level; false when its extents do not fit the
-// item shapes (the caller runs the row and column passes).
-template <typename T>
-static bool launch_solveq(double* G, T* coarse, double sign, const F3Geom& g, const ThomasLevel& th,
-                          unsigned* ctr, const Exec& ex, cudaError_t* err) {
-  // opt-in (MGRX_SOLVEQ=1): measured slower than the three passes at 513^3
-  // (288 vs 215 us per decompose; items are latency-bound at 2 CTAs per SM)
-  static const bool on = std::getenv("MGRX_SOLVEQ") != nullptr;
-  if (!on || ctr == nullptr) return false;
-  const int seg = int((g.m2 + 31) / 32);
-  if (g.m1 > kQMaxM || g.m0 > kQMaxM || seg > 9) return false;
-  QArgs<T> a;
-  a.G = G;
-  a.coarse = coarse;
-  a.sign = sign;
-  a.m0 = int(g.m0);
-  a.m1 = int(g.m1);
-  a.m2 = int(g.m2);
-  a.nrg = (a.m1 + kQWarps - 1) / kQWarps;
-  a.ncg = (a.m2 + 15) / 16;
-  a.nzg = coarse ? (int64_t(a.m1) * a.m2 + 15) / 16 : 0;
-  const size_t smem = size_t(2 * (a.m0 + a.m1 + a.m2) + 4 * kQWarps * 16 + kQWarps * a.m2) * 8;
-  void (*kern)(const QArgs<T>) = seg <= 3 ? k_f3_solveq<T, 3> : (seg <= 5 ? k_f3_solveq<T, 5> : k_f3_solveq<T, 9>);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  int per_sm = 0;
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQThreads, smem);
-  if (e != cudaSuccess) {
-    *err = e;
-    return true;
-  }
-  const int grid = std::max(1, per_sm) * kNumSMs;
-  static const int lag_env = std::getenv("MGRX_QLAG") ? std::atoi(std::getenv("MGRX_QLAG")) : -1;
-  a.lag = lag_env >= 0 ? lag_env : 3 * int(grid / (a.nrg + a.ncg)) + 2;
-  a.nsteps = int64_t(a.m0) + a.lag;
-  a.total = a.nsteps * (a.nrg + a.ncg) + a.nzg;
-  a.ctr = ctr;
-  a.w0 = th.w[0];
-  a.id0 = th.inv_d[0];
-  a.w1 = th.w[1];
-  a.id1 = th.inv_d[1];
-  a.w2 = th.w[2];
-  a.id2 = th.inv_d[2];
-  static const bool tr = std::getenv("MGRX_Q_TRACE") != nullptr;
-  a.trace = nullptr;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(ex.s, &cs);
-  if (tr && cs == cudaStreamCaptureStatusNone) {
-    cudaMallocAsync(reinterpret_cast<void**>(&a.trace), 64, ex.s);
-    cudaMemsetAsync(a.trace, 0, 64, ex.s);
-  }
-  MGRX_LAUNCH(ex, coarse ? "f3_solveq" : "f3_solveq12",
-              (*err = pdl_launch(kern, dim3(unsigned(grid)), dim3(kQThreads), smem, ex.s, !ex.prof, a)));
-  if (a.trace) {
-    unsigned long long h[6];
-    cudaMemcpyAsync(h, a.trace, 48, cudaMemcpyDeviceToHost, ex.s);
-    cudaStreamSynchronize(ex.s);
-    cudaFreeAsync(a.trace, ex.s);
-    const double n = double(grid) * 1e3;
-    std::fprintf(stderr, "[mgrx] solveq m %d lag %d grid %d (kcycles per CTA): R %.1f Cwait %.1f C %.1f Zwait %.1f "
-                 "Z %.1f fetch %.1f\n", a.m1, a.lag, grid, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, h[5] / n);
-  }
-  return true;
-}
-
-// Axis-2 then axis-1 solves of G by the row and column passes; with
-// MGRX_SLABS = S > 1 the volume is processed in S slabs of planes (row pass
-// then column pass per slab, so the column pass reads the row pass's output
-// from L2).
+// Axis-2 then axis-1 solves of G: the row pass and the axis-1 column pass.
 static void row_col1(double* G, const F3Geom& g, const ThomasLevel& th, const Exec& ex) {
-  static const int slabs = std::getenv("MGRX_SLABS") ? std::max(1, std::atoi(std::getenv("MGRX_SLABS"))) : 1;
-  const int64_t S = std::min<int64_t>(slabs, g.m0);
-  for (int64_t s = 0; s < S; ++s) {
-    const int64_t k0 = g.m0 * s / S, k1 = g.m0 * (s + 1) / S;
-    F3Geom gs = g;
-    gs.m0 = k1 - k0;
-    double* Gs = G + k0 * g.m1 * g.m2;
-    launch_row(Gs, gs, th.w[2], th.inv_d[2], ex);
-    launch_col<float>(Gs, static_cast<float*>(nullptr), 0.0, gs, 1, th.w[1], th.inv_d[1], ex);
-  }
+  launch_row(G, g, th.w[2], th.inv_d[2], ex);
+  launch_col<float>(G, static_cast<float*>(nullptr), 0.0, g, 1, th.w[1], th.inv_d[1], ex);
 }
 
 }  // namespace
@@ -2147,8 +1537,7 @@ Fused3DPlan fused3d_plan(const LevelGeom& lg, int esize) {
   g.units = int(nchunk * g.ntile1);
   g.grid = g.units;  // one CTA per unit; the hardware scheduler balances
   fp.enabled = true;
-  fp.ctr_off = size_t(g.m0) * g.m1 * g.m2 * 8 + 256;
-  fp.scratch_bytes = fp.ctr_off + fused3d_ctr_bytes(fp);
+  fp.scratch_bytes = size_t(g.m0) * g.m1 * g.m2 * 8 + 256;
   return fp;
 }
 
@@ -2277,14 +1666,7 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
                                                  coarse, G, gd));
     }
   }
-  cudaError_t se = cudaSuccess;
-  unsigned* ctr = reinterpret_cast<unsigned*>(static_cast<char*>(scratch) + fp.ctr_off);
-  if (launch_solveq<T>(G, coarse, 1.0, g, th, ctr, ex, &se)) return se != cudaSuccess ? se : cudaGetLastError();
-  if (!launch_solve12(G, g.m0, int(g.m1), int(g.m2), th, ex, &se)) {
-    row_col1(G, g, th, ex);
-  } else if (se != cudaSuccess) {
-    return se;
-  }
+  row_col1(G, g, th, ex);
   launch_col<T>(G, coarse, 1.0, g, 0, th.w[0], th.inv_d[0], ex);
   return cudaGetLastError();
 }
@@ -2316,15 +1698,7 @@ cudaError_t fused3d_recompose_correction(const T* shell, void* scratch, const Fu
     MGRX_LAUNCH(ex, "f3_rec_plane", pdl_launch(k_f3_rec_plane<T, 4, kPlaneMaxThreads, 3>, dim3(gd.grid),
                                                dim3(gd.threads), plane_smem3r<T>(gd), ex.s, !ex.prof, shell, G, gd));
   }
-  cudaError_t se = cudaSuccess;
-  unsigned* ctr = reinterpret_cast<unsigned*>(static_cast<char*>(scratch) + fp.ctr_off);
-  if (launch_solveq<T>(G, static_cast<T*>(nullptr), 0.0, g, th, ctr, ex, &se))
-    return se != cudaSuccess ? se : cudaGetLastError();
-  if (!launch_solve12(G, g.m0, int(g.m1), int(g.m2), th, ex, &se)) {
-    row_col1(G, g, th, ex);
-  } else if (se != cudaSuccess) {
-    return se;
-  }
+  row_col1(G, g, th, ex);
   return cudaGetLastError();
 }
 

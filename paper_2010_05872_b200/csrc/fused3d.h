@@ -35,14 +35,12 @@ struct F3Geom {
 
 struct Fused3DPlan {
   bool enabled = false;
-  size_t ctr_off = 0;        // dataflow-solve counters (after G); zeroed once per scratch allocation
-  size_t scratch_bytes = 0;  // fp64 load-vector volume G + counters
+  size_t scratch_bytes = 0;  // fp64 load-vector volume G
   size_t scratch_off = 0;    // filled by the caller's scratch layout
   F3Geom g;
 };
 
 Fused3DPlan fused3d_plan(const LevelGeom& g, int esize);
-inline size_t fused3d_ctr_bytes(const Fused3DPlan& fp) { return size_t(fp.g.m0 + 8) * 4 + 252; }
 
 template <typename T>
 cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scratch, const LevelGeom& g,
