@@ -1817,6 +1817,41 @@ cudaError_t fused3d_slab_inplane(double* G, const Fused3DPlan& fp, const ThomasL
   return cudaGetLastError();
 }
 
+// Thomas (uniform ThomasAux) along the middle axis of a [outer][m][inner]
+// fp64 array (inner > 1: the segmented column pass) or along the rows of a
+// [outer][m] array (inner == 1: the row pass), in place.
+cudaError_t f3_axis_solve(double* y, int64_t outer, int64_t m, int64_t inner, const double* w, const double* id,
+                          const Exec& ex) {
+  if (m > kColMaxM || m < 2 || outer <= 0 || inner <= 0) return cudaErrorNotSupported;
+  F3Geom g;
+  if (inner == 1) {
+    g.m0 = outer;
+    g.m1 = 1;
+    g.m2 = m;
+    launch_row(y, g, w, id, ex);
+  } else {
+    g.m0 = outer;
+    g.m1 = m;
+    g.m2 = inner;
+    launch_col<float>(y, static_cast<float*>(nullptr), 0.0, g, 1, w, id, ex);
+  }
+  return cudaGetLastError();
+}
+
+// Axis-0 Thomas (uniform ThomasAux) of every column of a [m0][inner] fp64
+// array, in place, by the segmented column pass (general path, auto mode):
+// one read and one write instead of the per-line recurrence's two of each.
+cudaError_t f3_axis0_solve(double* y, int64_t m0, int64_t inner, const double* w, const double* id,
+                           const Exec& ex) {
+  if (m0 > kColMaxM || m0 < 2 || inner <= 0) return cudaErrorNotSupported;
+  F3Geom g;
+  g.m0 = m0;
+  g.m1 = 1;
+  g.m2 = inner;
+  launch_col<float>(y, static_cast<float*>(nullptr), 0.0, g, 0, w, id, ex);
+  return cudaGetLastError();
+}
+
 cudaError_t fused3d_slab_axis0(double* Gt, int64_t width, const Fused3DPlan& fp, const ThomasLevel& th,
                                const Exec& ex) {
   if (width <= 0) return cudaSuccess;

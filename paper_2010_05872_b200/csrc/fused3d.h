@@ -74,6 +74,14 @@ template <typename T>
 cudaError_t fused3d_slab_interp(const T* shell, const T* coarse, T* fine, const Fused3DPlan& fp, int64_t p0, int64_t p1,
                                 const Exec& ex);
 
+// Thomas along the middle axis of [outer][m][inner] (rows when inner == 1).
+cudaError_t f3_axis_solve(double* y, int64_t outer, int64_t m, int64_t inner, const double* w, const double* id,
+                          const Exec& ex);
+// Axis-0 Thomas of the columns of a [m0][inner] fp64 array (the segmented
+// column pass); cudaErrorNotSupported when m0 is outside its range.
+cudaError_t f3_axis0_solve(double* y, int64_t m0, int64_t inner, const double* w, const double* id,
+                           const Exec& ex);
+
 // K-pack of slab mode's all-to-all: the column blocks [cb[q], cb[q+1]) of a
 // rows x pitch fp64 array packed back to back (unpack: the inverse).
 cudaError_t slab_pack(const double* src, int64_t rows, int64_t pitch, const uint64_t* cb, int nparts, double* dst,

@@ -17,6 +17,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "fused3d.h"
 #include "kernels.h"
 
 namespace mgrx_b200 {
@@ -378,6 +379,29 @@ __global__ void __launch_bounds__(256) k_coef_load0(const T* __restrict__ blk, T
 // cmask order (axis 0 is bit 0 when odd); shell positions: an even row
 // holds only its odd-column tail, (r, k) -> r (n1 - m1) + k; odd row r of
 // the reordered block starts at (m0 + r) n1 - m0 m1.
+
+// k_axis_load (uniform weights) with 32-bit index math (total < 2^32):
+// y[o][i][t] = load_entry of x[o][.][t] at coarse i (transform.hpp:84-96,
+// the same operation order).
+__global__ void __launch_bounds__(256) k_axis_load32(const double* __restrict__ x, double* __restrict__ y,
+                                                     uint32_t total, uint32_t inner, uint32_t n, uint32_t m,
+                                                     const FastDiv div_inner, const FastDiv div_m) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += stride) {
+    const uint32_t oi = div_inner.div(q), t = q - oi * inner;
+    const uint32_t o = div_m.div(oi), i = oi - o * m;
+    const double* c = x + (uint64_t(o) * n) * inner + t;
+    double acc = 0.0;
+    if (i >= 1) {
+      acc = add_(acc, mul_(kW12, c[uint64_t(2 * i - 2) * inner]));
+      acc = add_(acc, mul_(0.5, c[uint64_t(2 * i - 1) * inner]));
+    }
+    acc = add_(acc, mul_((i == 0 || i + 1 == m) ? kW5_12 : kW5_6, c[uint64_t(2 * i) * inner]));
+    if (2 * i + 1 < n) acc = add_(acc, mul_(0.5, c[uint64_t(2 * i + 1) * inner]));
+    if (2 * i + 2 < n) acc = add_(acc, mul_(kW12, c[uint64_t(2 * i + 2) * inner]));
+    y[q] = acc;
+  }
+}
 
 // Rolling axis-0 load accumulators of one column (see k_coef_load0): rows
 // k-1, k, k+1 around fine row p, k = p >> 1; finished rows go to f0.
@@ -1514,7 +1538,15 @@ static void run_sweeps(double* comp, double* tmp, const LevelGeom& g, const Thom
     const int grid = grid_for(lines, 128, 32);
     // the serial per-line sweep saturates the GPU when there are many lines;
     // few long lines (2-D levels) need the segmented solve
-    if (fast && lines < (int64_t(1) << 17)) {
+    const int64_t outs_all = outer * g.m[a] * inner;
+    if (fast && !nu && lines >= (int64_t(1) << 17) && g.m[a] <= 640 && outs_all < (int64_t(1) << 32)) {
+      // many lines: the restriction (32-bit index math), then the segmented
+      // column pass (or the row pass for the contiguous axis) on y
+      MGRX_LAUNCH(ex, "gen_load", k_axis_load32<<<grid_for(outs_all, 256), 256, 0, ex.s>>>(
+                                      x, y, uint32_t(outs_all), uint32_t(inner), uint32_t(g.n[a]), uint32_t(g.m[a]),
+                                      FastDiv(uint32_t(inner)), FastDiv(uint32_t(g.m[a]))));
+      if (f3_axis_solve(y, outer, g.m[a], inner, th->w[a], th->inv_d[a], ex) != cudaSuccess) cudaGetLastError();
+    } else if (fast && lines < (int64_t(1) << 17)) {
       const int64_t outs = outer * g.m[a] * inner;
       if (nu)
         MGRX_LAUNCH(ex, "gen_load", k_axis_load<true><<<grid_for(outs, 256), 256, 0, ex.s>>>(x, y, outer, inner, g.n[a], g.m[a], nu->ax[a].s));
@@ -1600,7 +1632,8 @@ static void coef_load0_axis0(const T* src, T* shell, T* coarse, double* comp, co
     launch_axis_solve(comp, inner, m0, inner, w, id, of, ex);
   } else if (nu) {
     MGRX_LAUNCH(ex, "gen_thomas", k_axis_thomas<true><<<grid_for(inner, 128, 32), 128, 0, ex.s>>>(comp, inner, inner, m0, nullptr, nullptr, nu->ax[0]));
-  } else {
+  } else if (f3_axis0_solve(comp, m0, inner, w, id, ex) != cudaSuccess) {
+    cudaGetLastError();
     MGRX_LAUNCH(ex, "gen_thomas", k_axis_thomas<false><<<grid_for(inner, 128, 32), 128, 0, ex.s>>>(comp, inner, inner, m0, w, id, NuAxis{}));
   }
 }
