@@ -794,6 +794,408 @@ __global__ void __launch_bounds__(256) kN_rec_interp(const T* __restrict__ shell
   }
 }
 
+// ---- rank 3-4 axis-0 walkers (uniform weights, N < 2^32): a thread owns a
+// column pair (2k, 2k+1) of one row of the middle axes and walks a chunk of
+// fine planes along axis 0.  The corner values of the last even plane stay
+// in registers: an odd plane's corner set is the left even plane's (cached)
+// interleaved with the right one's (loaded once, then cached for the next
+// even plane), so every corner value is loaded once per plane pair instead
+// of three times.  Shell positions are linear in p for each parity (even
+// planes: +Nmid nl - pm0 ml per plane pair, odd: +Nmid nl), so the per-node
+// index math is a few additions.  Sums run in predict's cmask order (axis 0
+// lowest, then the middle axes ascending, the last axis highest) as in
+// pair_predict_m — bit-identical to kN_coef_load0 / kN_rec_interp.
+
+// Corner offsets (inside one plane, without the column) of the middle-axis
+// subsets of this row, and the row's parity pattern / odd count.
+#ifndef MGRX_WALK_MINB
+#define MGRX_WALK_MINB 2
+#endif
+#ifndef MGRX_WALK_MINB_I
+#define MGRX_WALK_MINB_I 3
+#endif
+template <int D>
+struct MidCorners {
+  static constexpr int NC = 1 << (D - 2);
+  uint32_t off[NC];  // fine (coarse = false) or coarse (coarse = true) offsets
+  unsigned M;        // odd middle axes (bit i-1 for axis i)
+  int nodd;
+};
+
+template <int D>
+__device__ __forceinline__ MidCorners<D> mid_corners(const LevelGeom& g, const int64_t* j, bool coarse) {
+  MidCorners<D> mc;
+  mc.M = 0;
+  mc.nodd = 0;
+  uint32_t base = 0, dl[D > 2 ? D - 2 : 1];
+#pragma unroll
+  for (int i = 1; i <= D - 2; ++i) {
+    const bool odd = j[i] & 1;
+    const uint32_t ji = uint32_t(j[i]);
+    base += coarse ? (ji >> 1) * uint32_t(g.cst[i]) : (odd ? ji - 1 : ji) * uint32_t(g.st[i]);
+    dl[i - 1] = (odd && j[i] + 1 < g.n[i]) ? (coarse ? uint32_t(g.cst[i]) : 2 * uint32_t(g.st[i])) : 0;
+    mc.M |= unsigned(odd) << (i - 1);
+    mc.nodd += odd ? 1 : 0;
+  }
+#pragma unroll
+  for (int fm = 0; fm < MidCorners<D>::NC; ++fm) {
+    uint32_t o = base;
+#pragma unroll
+    for (int i = 0; i < D - 2; ++i)
+      if ((fm >> i) & 1) o += dl[i];
+    mc.off[fm] = o;
+  }
+  return mc;
+}
+
+// Corner values of one plane at columns cl / cr (only the subsets of M are loaded).
+template <typename T, int D>
+__device__ __forceinline__ void load_corners(const T* __restrict__ pl, const MidCorners<D>& mc, uint32_t cl,
+                                             uint32_t cr, bool has1, double* vl, double* vr) {
+#pragma unroll
+  for (int fm = 0; fm < MidCorners<D>::NC; ++fm) {
+    vl[fm] = vr[fm] = 0.0;
+    if (fm & ~mc.M) continue;
+    vl[fm] = double(pl[mc.off[fm] + cl]);
+    if (has1) vr[fm] = double(pl[mc.off[fm] + cr]);
+  }
+}
+
+// Even plane: predict over the plane's own corners (scale 2^-nodd).
+template <int D>
+__device__ __forceinline__ void pred_even(const MidCorners<D>& mc, const double* el, const double* er, double& p0,
+                                          double& p1) {
+  double s = 0.0;
+#pragma unroll
+  for (int fm = 0; fm < MidCorners<D>::NC; ++fm)
+    if (!(fm & ~mc.M)) s = add_(s, el[fm]);
+  const double sc = __longlong_as_double(int64_t(1023 - mc.nodd) << 52);
+  p0 = mul_(s, sc);
+#pragma unroll
+  for (int fm = 0; fm < MidCorners<D>::NC; ++fm)
+    if (!(fm & ~mc.M)) s = add_(s, er[fm]);
+  p1 = mul_(s, 0.5 * sc);
+}
+
+// Odd plane: left / right planes interleaved per middle subset (scale 2^-(nodd+1)).
+template <int D>
+__device__ __forceinline__ void pred_odd(const MidCorners<D>& mc, const double* el, const double* er,
+                                         const double* nl_, const double* nr_, double& p0, double& p1) {
+  double s = 0.0;
+#pragma unroll
+  for (int fm = 0; fm < MidCorners<D>::NC; ++fm)
+    if (!(fm & ~mc.M)) {
+      s = add_(s, el[fm]);
+      s = add_(s, nl_[fm]);
+    }
+  const double sc = __longlong_as_double(int64_t(1023 - mc.nodd - 1) << 52);
+  p0 = mul_(s, sc);
+#pragma unroll
+  for (int fm = 0; fm < MidCorners<D>::NC; ++fm)
+    if (!(fm & ~mc.M)) {
+      s = add_(s, er[fm]);
+      s = add_(s, nr_[fm]);
+    }
+  p1 = mul_(s, 0.5 * sc);
+}
+
+// roll0 split by plane parity (the same arithmetic).
+__device__ __forceinline__ void roll_even(Roll0& A, double c, int k, int p, int n0, int m0, int i0, int i1,
+                                          double* __restrict__ f0col, int64_t ld) {
+  if (k >= 1) {
+    A.prev = add_(A.prev, mul_(kW12, c));
+    if (k - 1 >= i0 && k - 1 < i1) f0col[int64_t(k - 1) * ld] = A.prev;
+  }
+  A.cur = add_(A.cur, mul_((k == 0 || k + 1 == m0) ? kW5_12 : kW5_6, c));
+  A.next = (k + 1 < m0) ? add_(0.0, mul_(kW12, c)) : 0.0;
+  if (p == n0 - 1 && k >= i0 && k < i1) f0col[int64_t(k) * ld] = A.cur;
+}
+__device__ __forceinline__ void roll_odd(Roll0& A, double c, int k, int p, int p_hi, int n0, int m0, int i0, int i1,
+                                         double* __restrict__ f0col, int64_t ld) {
+  A.cur = add_(A.cur, mul_(0.5, c));
+  if (k + 1 < m0) A.next = add_(A.next, mul_(0.5, c));
+  if (p == n0 - 1 && k >= i0 && k < i1) f0col[int64_t(k) * ld] = A.cur;
+  if (p < p_hi) {
+    A.prev = A.cur;
+    A.cur = A.next;
+    A.next = 0.0;
+  }
+}
+
+// Row of the middle axes -> j[1..D-2], their even-ness and coarse offset.
+template <int D>
+__device__ __forceinline__ void mid_unravel(const LevelGeom& g, uint32_t row, int64_t* j, bool& even, int64_t& cmid) {
+  even = true;
+  cmid = 0;
+#pragma unroll
+  for (int i = D - 2; i >= 1; --i) {
+    const uint32_t rq = g.fn[i].div(row);
+    j[i] = row - rq * uint32_t(g.n[i]);
+    row = rq;
+    even &= !(j[i] & 1);
+    cmid += (j[i] >> 1) * g.cst[i];
+  }
+}
+
+// Raw values one plane pair ahead (registers): the loop body works on the
+// pair fetched one iteration earlier, so each thread keeps two pairs' loads
+// in flight instead of waiting a full memory latency per pair.
+template <typename T, int NC>
+struct PairRaw {
+  T e0, e1, o0, o1;   // even / odd plane values (coefficient walk: the node pair; kRec / interp: shell)
+  T cl[NC], cr[NC];   // corners of the next even plane at columns cl / cr
+};
+
+template <typename T, int D>
+__device__ __forceinline__ void fetch_corners(const T* __restrict__ pl, const MidCorners<D>& mc, uint32_t cl,
+                                              uint32_t cr, bool has1, T* vl, T* vr) {
+#pragma unroll
+  for (int fm = 0; fm < MidCorners<D>::NC; ++fm) {
+    vl[fm] = vr[fm] = T(0);
+    if (fm & ~mc.M) continue;
+    vl[fm] = pl[mc.off[fm] + cl];
+    if (has1) vr[fm] = pl[mc.off[fm] + cr];
+  }
+}
+
+// coefficients (kRec: the component read from the shell) + the axis-0 load
+// vector, as kN_coef_load0 (uniform weights).
+template <typename T, bool kRec, int D>
+__global__ void __launch_bounds__(256, MGRX_WALK_MINB) kN_coef_load0w(const T* __restrict__ blk, T* __restrict__ shell,
+                                                      T* __restrict__ coarse, double* __restrict__ f0,
+                                                      const LevelGeom g, int64_t inner, int chunk) {
+  constexpr int E = D - 1;
+  constexpr int NC = MidCorners<D>::NC;
+  const int n0 = int(g.n[0]), m0 = int(g.m[0]), nl = int(g.n[E]), ml = int(g.m[E]);
+  const int64_t rmid = inner / nl;
+  const int64_t total = ((m0 + chunk - 1) / chunk) * rmid * ml;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int64_t nmid = 1;
+#pragma unroll
+  for (int i = 1; i <= D - 2; ++i) nmid *= g.n[i];
+  const int64_t dsp_e = nmid * nl - g.pm[0] * ml, dsp_o = nmid * nl;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total; q += stride) {
+    const uint32_t q32 = uint32_t(q);
+    const uint32_t rest = g.fn[E].div(q32);
+    const int k = int(q32 - rest * uint32_t(ml));
+    const uint32_t ch = g.fn[0].div(rest);
+    const uint32_t row = rest - ch * uint32_t(rmid);
+    const int i0 = int(ch) * chunk, i1 = min(m0, i0 + chunk);
+    int64_t j[kMaxD];
+    bool mid_even;
+    int64_t cmid;
+    mid_unravel<D>(g, row, j, mid_even, cmid);
+    const int t0 = 2 * k, t1 = t0 + 1;
+    const bool has1 = t1 < nl;
+    const uint32_t cr = (t1 + 1 < nl) ? uint32_t(t1 + 1) : uint32_t(t0);
+    const int64_t tp0 = int64_t(row) * nl + t0;
+    const int p_lo = i0 > 0 ? 2 * i0 - 2 : 0;
+    const int p_hi = min(n0 - 1, 2 * i1);
+    j[E] = t0;
+    j[0] = p_lo;
+    int64_t sp_e = shell_pos<D>(g, j);
+    j[0] = p_lo + 1;
+    int64_t sp_o = shell_pos<D>(g, j);
+    MidCorners<D> mc;
+    if (!kRec) mc = mid_corners<D>(g, j, false);
+    // fetch(p): the raw values of the plane pair (p, p + 1) and the corners
+    // of the odd plane's right neighbour (p + 2, or p at a degenerate end)
+    auto fetch = [&](int p, int64_t spe, int64_t spo, PairRaw<T, NC>& r) {
+      const bool odd = p + 1 <= p_hi;
+      if (kRec) {
+        r.e0 = mid_even ? T(0) : blk[spe];
+        r.e1 = has1 ? blk[spe + ml] : T(0);
+        r.o0 = odd ? blk[spo] : T(0);
+        r.o1 = (odd && has1) ? blk[spo + ml] : T(0);
+      } else {
+        const T* pl = blk + int64_t(p) * inner + tp0;
+        r.e0 = pl[0];
+        r.e1 = has1 ? pl[1] : T(0);
+        r.o0 = odd ? pl[inner] : T(0);
+        r.o1 = (odd && has1) ? pl[inner + 1] : T(0);
+        if (odd) {
+          const T* prt = blk + int64_t(p + 2 < n0 ? p + 2 : p) * inner;
+          fetch_corners<T, D>(prt, mc, uint32_t(t0), cr, has1, r.cl, r.cr);
+        }
+      }
+    };
+    double el[NC], er[NC];
+    if (!kRec) {
+      T vl[NC], vr[NC];
+      fetch_corners<T, D>(blk + int64_t(p_lo) * inner, mc, uint32_t(t0), cr, has1, vl, vr);
+#pragma unroll
+      for (int fm = 0; fm < NC; ++fm) {
+        el[fm] = double(vl[fm]);
+        er[fm] = double(vr[fm]);
+      }
+    }
+    T* cp = coarse + int64_t(p_lo >> 1) * g.cst[0] + cmid + k;
+    Roll0 A0, A1;
+    double* f0c = f0 + tp0;
+    PairRaw<T, NC> cur;
+    fetch(p_lo, sp_e, sp_o, cur);
+    for (int p = p_lo; p <= p_hi; p += 2, sp_e += dsp_e, sp_o += dsp_o, cp += g.cst[0]) {
+      PairRaw<T, NC> nx;
+      if (p + 2 <= p_hi) fetch(p + 2, sp_e + dsp_e, sp_o + dsp_o, nx);
+      const int kk = p >> 1;
+      {  // even plane p
+        const bool owned = p >= 2 * i0 && p < 2 * i1;
+        double c0 = 0.0, c1 = 0.0;
+        if (kRec) {
+          c0 = double(cur.e0);
+          c1 = double(cur.e1);
+        } else {
+          double pred0, pred1;
+          pred_even<D>(mc, el, er, pred0, pred1);
+          if (mid_even) {
+            if (owned) *cp = cur.e0;
+          } else {
+            const T v = to_t<T>(sub_(double(cur.e0), pred0));
+            if (owned) shell[sp_e] = v;
+            c0 = double(v);
+          }
+          if (has1) {
+            const T v = to_t<T>(sub_(double(cur.e1), pred1));
+            if (owned) shell[sp_e + ml] = v;
+            c1 = double(v);
+          }
+        }
+        roll_even(A0, c0, kk, p, n0, m0, i0, i1, f0c, inner);
+        if (has1) roll_even(A1, c1, kk, p, n0, m0, i0, i1, f0c + 1, inner);
+      }
+      if (p + 1 <= p_hi) {  // odd plane p + 1
+        const int po = p + 1;
+        const bool owned = po >= 2 * i0 && po < 2 * i1;
+        double c0, c1 = 0.0;
+        if (kRec) {
+          c0 = double(cur.o0);
+          c1 = double(cur.o1);
+        } else {
+          double nl_[NC], nr_[NC];
+#pragma unroll
+          for (int fm = 0; fm < NC; ++fm) {
+            nl_[fm] = double(cur.cl[fm]);
+            nr_[fm] = double(cur.cr[fm]);
+          }
+          double pred0, pred1;
+          pred_odd<D>(mc, el, er, nl_, nr_, pred0, pred1);
+          {
+            const T v = to_t<T>(sub_(double(cur.o0), pred0));
+            if (owned) shell[sp_o] = v;
+            c0 = double(v);
+          }
+          if (has1) {
+            const T v = to_t<T>(sub_(double(cur.o1), pred1));
+            if (owned) shell[sp_o + ml] = v;
+            c1 = double(v);
+          }
+#pragma unroll
+          for (int fm = 0; fm < NC; ++fm) {
+            el[fm] = nl_[fm];
+            er[fm] = nr_[fm];
+          }
+        }
+        roll_odd(A0, c0, kk, po, p_hi, n0, m0, i0, i1, f0c, inner);
+        if (has1) roll_odd(A1, c1, kk, po, p_hi, n0, m0, i0, i1, f0c + 1, inner);
+      }
+      cur = nx;
+    }
+  }
+}
+
+// add_interpolant + unpack (kN_rec_interp, uniform weights) walking chunks
+// of `chunk` fine planes (even) along axis 0 with the coarse corner values
+// of the current coarse plane cached and the next pair's loads in flight.
+template <typename T, int D>
+__global__ void __launch_bounds__(256, MGRX_WALK_MINB_I) kN_rec_interpw(const T* __restrict__ shell, const T* __restrict__ coarse,
+                                                      T* __restrict__ fine, const LevelGeom g, int64_t inner,
+                                                      int chunk) {
+  constexpr int E = D - 1;
+  constexpr int NC = MidCorners<D>::NC;
+  const int n0 = int(g.n[0]), nl = int(g.n[E]), ml = int(g.m[E]);
+  const int64_t rmid = inner / nl;
+  const int64_t total = ((n0 + chunk - 1) / chunk) * rmid * ml;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int64_t nmid = 1;
+#pragma unroll
+  for (int i = 1; i <= D - 2; ++i) nmid *= g.n[i];
+  const int64_t dsp_e = nmid * nl - g.pm[0] * ml, dsp_o = nmid * nl;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total; q += stride) {
+    const uint32_t q32 = uint32_t(q);
+    const uint32_t rest = g.fn[E].div(q32);
+    const int k = int(q32 - rest * uint32_t(ml));
+    const uint32_t ch = g.fn[0].div(rest);
+    const uint32_t row = rest - ch * uint32_t(rmid);
+    const int pa = int(ch) * chunk, pb = min(n0, pa + chunk);  // fine planes [pa, pb), pa even
+    int64_t j[kMaxD];
+    bool mid_even;
+    int64_t cmid;
+    mid_unravel<D>(g, row, j, mid_even, cmid);
+    const int t0 = 2 * k, t1 = t0 + 1;
+    const bool has1 = t1 < nl;
+    const uint32_t kr = (t1 + 1 < nl) ? uint32_t(k + 1) : uint32_t(k);
+    j[E] = t0;
+    j[0] = pa;
+    int64_t sp_e = shell_pos<D>(g, j);
+    j[0] = pa + 1;
+    int64_t sp_o = shell_pos<D>(g, j);
+    const MidCorners<D> mc = mid_corners<D>(g, j, true);
+    auto fetch = [&](int p, int64_t spe, int64_t spo, PairRaw<T, NC>& r) {
+      const bool odd = p + 1 < pb;
+      r.e0 = mid_even ? T(0) : shell[spe];
+      r.e1 = has1 ? shell[spe + ml] : T(0);
+      r.o0 = odd ? shell[spo] : T(0);
+      r.o1 = (odd && has1) ? shell[spo + ml] : T(0);
+      if (odd) {
+        const int kc = (p + 2 < n0) ? (p >> 1) + 1 : (p >> 1);
+        fetch_corners<T, D>(coarse + int64_t(kc) * g.cst[0], mc, uint32_t(k), kr, has1, r.cl, r.cr);
+      }
+    };
+    double el[NC], er[NC];
+    {
+      T vl[NC], vr[NC];
+      fetch_corners<T, D>(coarse + int64_t(pa >> 1) * g.cst[0], mc, uint32_t(k), kr, has1, vl, vr);
+#pragma unroll
+      for (int fm = 0; fm < NC; ++fm) {
+        el[fm] = double(vl[fm]);
+        er[fm] = double(vr[fm]);
+      }
+    }
+    T* fr = fine + int64_t(pa) * inner + int64_t(row) * nl + t0;
+    PairRaw<T, NC> cur;
+    fetch(pa, sp_e, sp_o, cur);
+    for (int p = pa; p < pb; p += 2, fr += 2 * inner, sp_e += dsp_e, sp_o += dsp_o) {
+      PairRaw<T, NC> nx;
+      if (p + 2 < pb) fetch(p + 2, sp_e + dsp_e, sp_o + dsp_o, nx);
+      {  // even plane
+        double pred0, pred1;
+        pred_even<D>(mc, el, er, pred0, pred1);
+        fr[0] = mid_even ? T(el[0]) : to_t<T>(add_(double(cur.e0), pred0));
+        if (has1) fr[1] = to_t<T>(add_(double(cur.e1), pred1));
+      }
+      if (p + 1 < pb) {  // odd plane
+        double nl_[NC], nr_[NC];
+#pragma unroll
+        for (int fm = 0; fm < NC; ++fm) {
+          nl_[fm] = double(cur.cl[fm]);
+          nr_[fm] = double(cur.cr[fm]);
+        }
+        double pred0, pred1;
+        pred_odd<D>(mc, el, er, nl_, nr_, pred0, pred1);
+        T* fo = fr + inner;
+        fo[0] = to_t<T>(add_(double(cur.o0), pred0));
+        if (has1) fo[1] = to_t<T>(add_(double(cur.o1), pred1));
+#pragma unroll
+        for (int fm = 0; fm < NC; ++fm) {
+          el[fm] = nl_[fm];
+          er[fm] = nr_[fm];
+        }
+      }
+      cur = nx;
+    }
+  }
+}
+
 // Serial Thomas along axis-0-style lines over a precomputed load vector, in
 // place: the same operations as k_sweep after its load (bit-identical).
 template <bool kNu>
@@ -1590,6 +1992,12 @@ static void run_sweeps(double* comp, double* tmp, const LevelGeom& g, const Thom
   *result = x;
 }
 
+// MGRX_NO_WALK: the per-node rank 3-4 kernels instead of the axis-0 walkers (A/B).
+static bool walk_off() {
+  static const bool off = std::getenv("MGRX_NO_WALK") != nullptr;
+  return off;
+}
+
 // Path "auto", rank >= 2: coefficients (kRec: the component) fused with the
 // axis-0 load into comp (m0 x inner), then the axis-0 solve in place.
 template <typename T, bool kRec>
@@ -1620,6 +2028,13 @@ static void coef_load0_axis0(const T* src, T* shell, T* coarse, double* comp, co
     L_(NU, 0);
   if (nu) {
     R_(true)
+  } else if ((g.d == 3 || g.d == 4) && g.N < (int64_t(1) << 32) && !walk_off()) {
+    if (g.d == 3)
+      MGRX_LAUNCH(ex, kRec ? "gen_comp_load0" : "gen_coef_load0",
+                  (kN_coef_load0w<T, kRec, 3><<<grid, 256, 0, ex.s>>>(src, shell, coarse, comp, gp, inner, chunk)));
+    else
+      MGRX_LAUNCH(ex, kRec ? "gen_comp_load0" : "gen_coef_load0",
+                  (kN_coef_load0w<T, kRec, 4><<<grid, 256, 0, ex.s>>>(src, shell, coarse, comp, gp, inner, chunk)));
   } else {
     R_(false)
   }
@@ -1673,6 +2088,21 @@ cudaError_t general_recompose_level(const T* shell, T* coarse, T* fine, double* 
       MGRX_LAUNCH(ex, "gen_rec_interp", k2_rec_interp<T, true><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, g2, *nu));
     else
       MGRX_LAUNCH(ex, "gen_rec_interp", k2_rec_interp<T, false><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, g2, NuLevel{}));
+    return cudaGetLastError();
+  }
+  if (fast && !nu && (g.d == 3 || g.d == 4) && g.N < (int64_t(1) << 32) && !walk_off()) {
+    const int64_t inner = g.N / g.n[0];
+    const int64_t pairs = inner / g.n[g.d - 1] * g.m[g.d - 1];
+    int chunk = int(std::max<int64_t>(1, std::min<int64_t>(32, g.n[0] * pairs / (int64_t(600) << 10))));
+    chunk += chunk & 1;
+    LevelGeom gp = g;
+    gp.fn[g.d - 1] = FastDiv(uint32_t(g.m[g.d - 1]));
+    gp.fn[0] = FastDiv(uint32_t(inner / g.n[g.d - 1]));
+    const int grid = grid_for(((g.n[0] + chunk - 1) / chunk) * pairs, 256);
+    if (g.d == 3)
+      MGRX_LAUNCH(ex, "gen_rec_interp", (kN_rec_interpw<T, 3><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, gp, inner, chunk)));
+    else
+      MGRX_LAUNCH(ex, "gen_rec_interp", (kN_rec_interpw<T, 4><<<grid, 256, 0, ex.s>>>(shell, coarse, fine, gp, inner, chunk)));
     return cudaGetLastError();
   }
   if (fast && (g.d == 3 || g.d == 4) && g.N < (int64_t(1) << 32)) {
