@@ -1365,6 +1365,56 @@ static void launch_axis_solve(double* y, int64_t lines, int64_t m, int64_t inner
   }
 }
 
+// Short contiguous lines (m <= kShortRow): one thread per line, the
+// block's lines staged in shared memory with coalesced loads / stores; the
+// serial Thomas recurrences of k_sweep (transform.hpp:116-130 order,
+// bit-identical).
+constexpr int kShortRow = 64;
+constexpr int kShortRowThreads = 128;
+__global__ void __launch_bounds__(kShortRowThreads) k_rows_thomas(double* __restrict__ y, int64_t nlines, int m,
+                                                                  const double* __restrict__ w,
+                                                                  const double* __restrict__ inv_d) {
+  extern __shared__ double sb[];
+  double* tw = sb;
+  double* td = sb + kShortRow;
+  double* x = sb + 2 * kShortRow;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < m; i += kShortRowThreads) {
+    tw[i] = w[i];
+    td[i] = inv_d[i];
+  }
+  const int64_t l0 = int64_t(blockIdx.x) * kShortRowThreads;
+  const int nl = int(min(int64_t(kShortRowThreads), nlines - l0));
+  const int cnt = nl * m;
+  double* gl = y + l0 * m;
+  for (int e = tid; e < cnt; e += kShortRowThreads) x[e] = gl[e];
+  __syncthreads();
+  if (tid < nl) {
+    double* f = x + tid * m;
+    double prev = f[0];
+    for (int i = 1; i < m; ++i) {
+      prev = sub_(f[i], mul_(tw[i], prev));
+      f[i] = prev;
+    }
+    double nxt = mul_(prev, td[m - 1]);
+    f[m - 1] = nxt;
+    for (int i = m - 2; i >= 0; --i) {
+      const double v = mul_(sub_(f[i], mul_(kOff, nxt)), td[i]);
+      f[i] = v;
+      nxt = v;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < cnt; e += kShortRowThreads) gl[e] = x[e];
+}
+
+static void launch_rows_thomas(double* y, int64_t lines, int m, const double* w, const double* id, const Exec& ex) {
+  const size_t sm = size_t(2 * kShortRow + kShortRowThreads * m) * 8;
+  cudaFuncSetAttribute(k_rows_thomas, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  MGRX_LAUNCH(ex, "gen_rows", k_rows_thomas<<<unsigned((lines + kShortRowThreads - 1) / kShortRowThreads),
+                                              kShortRowThreads, sm, ex.s>>>(y, lines, m, w, id));
+}
+
 // Last-axis variant (contiguous lines): one warp per line, the line staged
 // in shared memory, lanes own contiguous segments (affine carries combined
 // with a warp shuffle scan, then exact reruns).
@@ -1947,7 +1997,10 @@ static void run_sweeps(double* comp, double* tmp, const LevelGeom& g, const Thom
       MGRX_LAUNCH(ex, "gen_load", k_axis_load32<<<grid_for(outs_all, 256), 256, 0, ex.s>>>(
                                       x, y, uint32_t(outs_all), uint32_t(inner), uint32_t(g.n[a]), uint32_t(g.m[a]),
                                       FastDiv(uint32_t(inner)), FastDiv(uint32_t(g.m[a]))));
-      if (f3_axis_solve(y, outer, g.m[a], inner, th->w[a], th->inv_d[a], ex) != cudaSuccess) cudaGetLastError();
+      if (inner == 1 && g.m[a] <= kShortRow)
+        launch_rows_thomas(y, outer, int(g.m[a]), th->w[a], th->inv_d[a], ex);
+      else if (f3_axis_solve(y, outer, g.m[a], inner, th->w[a], th->inv_d[a], ex) != cudaSuccess)
+        cudaGetLastError();
     } else if (fast && lines < (int64_t(1) << 17)) {
       const int64_t outs = outer * g.m[a] * inner;
       if (nu)
