@@ -1991,7 +1991,8 @@ static void run_sweeps(double* comp, double* tmp, const LevelGeom& g, const Thom
     // the serial per-line sweep saturates the GPU when there are many lines;
     // few long lines (2-D levels) need the segmented solve
     const int64_t outs_all = outer * g.m[a] * inner;
-    if (fast && !nu && lines >= (int64_t(1) << 17) && g.m[a] <= 640 && outs_all < (int64_t(1) << 32)) {
+    static const bool seg_all = std::getenv("MGRX_SEG_BIG_ONLY") == nullptr;
+    if (fast && !nu && (seg_all || lines >= (int64_t(1) << 17)) && g.m[a] <= 640 && outs_all < (int64_t(1) << 32)) {
       // many lines: the restriction (32-bit index math), then the segmented
       // column pass (or the row pass for the contiguous axis) on y
       MGRX_LAUNCH(ex, "gen_load", k_axis_load32<<<grid_for(outs_all, 256), 256, 0, ex.s>>>(
@@ -2096,7 +2097,11 @@ static void coef_load0_axis0(const T* src, T* shell, T* coarse, double* comp, co
   const double* w = nu ? nu->ax[0].tw : th->w[0];
   const double* id = nu ? nu->ax[0].tid : th->inv_d[0];
   const double* of = nu ? nu->ax[0].off : nullptr;
-  if (inner < (int64_t(1) << 17)) {
+  static const bool seg_all = std::getenv("MGRX_SEG_BIG_ONLY") == nullptr;
+  if (!nu && seg_all && f3_axis0_solve(comp, m0, inner, w, id, ex) == cudaSuccess) {
+    // segmented column pass (any number of columns)
+  } else if (inner < (int64_t(1) << 17)) {
+    cudaGetLastError();
     launch_axis_solve(comp, inner, m0, inner, w, id, of, ex);
   } else if (nu) {
     MGRX_LAUNCH(ex, "gen_thomas", k_axis_thomas<true><<<grid_for(inner, 128, 32), 128, 0, ex.s>>>(comp, inner, inner, m0, nullptr, nullptr, nu->ax[0]));
