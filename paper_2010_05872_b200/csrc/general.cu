@@ -1884,7 +1884,7 @@ static cudaError_t tail_rec_t(const T* coeffs, const T* coarse_in, T* fine_out, 
   return cudaGetLastError();
 }
 
-// Rank-specialised tails for 1-3 dimensions (the common cases), runtime
+// Rank-specialised tails for 1-4 dimensions (the common cases), runtime
 // rank otherwise; d_nu: per-level nonuniform tables (same order as the
 // levels) or null for uniform coordinates.
 template <typename T>
@@ -1894,6 +1894,7 @@ cudaError_t tail_decompose(const T* blk, T* out, T* coarse_out, const void* d_le
     case 1: return tail_dec_t<T, 1>(blk, out, coarse_out, d_levels, d_nu, nlev, nmax, ex);
     case 2: return tail_dec_t<T, 2>(blk, out, coarse_out, d_levels, d_nu, nlev, nmax, ex);
     case 3: return tail_dec_t<T, 3>(blk, out, coarse_out, d_levels, d_nu, nlev, nmax, ex);
+    case 4: return tail_dec_t<T, 4>(blk, out, coarse_out, d_levels, d_nu, nlev, nmax, ex);
     default: return tail_dec_t<T, 0>(blk, out, coarse_out, d_levels, d_nu, nlev, nmax, ex);
   }
 }
@@ -1905,6 +1906,7 @@ cudaError_t tail_recompose(const T* coeffs, const T* coarse_in, T* fine_out, con
     case 1: return tail_rec_t<T, 1>(coeffs, coarse_in, fine_out, d_levels, d_nu, nlev, nmax, ex);
     case 2: return tail_rec_t<T, 2>(coeffs, coarse_in, fine_out, d_levels, d_nu, nlev, nmax, ex);
     case 3: return tail_rec_t<T, 3>(coeffs, coarse_in, fine_out, d_levels, d_nu, nlev, nmax, ex);
+    case 4: return tail_rec_t<T, 4>(coeffs, coarse_in, fine_out, d_levels, d_nu, nlev, nmax, ex);
     default: return tail_rec_t<T, 0>(coeffs, coarse_in, fine_out, d_levels, d_nu, nlev, nmax, ex);
   }
 }
