@@ -149,6 +149,33 @@ int mgrx_gpu_dequantize(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t*
                         const uint64_t* d_outlier_pos, const void* d_outlier_val, uint64_t n_outliers,
                         void* d_coeffs);
 
+/* decompose (transform.hpp:485-506) followed by quantize / quantize_tail
+ * (quantize.hpp:79-114) of its output — the ★ pair compress_field runs back
+ * to back (pipeline.hpp:145-183) — as ONE call: d_coeffs receives decompose's
+ * buffer, d_labels / outliers quantize's output, results identical to the
+ * two calls.  The finest shell (7/8 of a 3-D field) is final after the first
+ * plane pass, so its labels are produced on a low-priority side stream under
+ * the rest of the decomposition (the solves and every coarser level), which
+ * runs on a high-priority stream: the quantizer's read of the coefficients
+ * leaves the critical path.  SYNCHRONOUS like mgrx_gpu_quantize (same
+ * errors). */
+int mgrx_gpu_decompose_quantize(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels,
+                                int stop_level, const void* d_field, const double* bin_widths, void* d_coeffs,
+                                int32_t* d_labels, uint64_t* d_outlier_pos, void* d_outlier_val,
+                                uint64_t outlier_capacity, uint64_t* n_outliers);
+
+/* dequantize / dequantize_tail (quantize.hpp:118-150) followed by recompose
+ * (transform.hpp:509-530) — the ★ pair of decompress_field
+ * (pipeline.hpp:235-260) — as one call: d_coeffs receives the dequantized
+ * buffer (for stop_level > 0 its coarse block must already hold the decoded
+ * coarse values), d_field the reconstruction; identical to the two calls.
+ * Without outliers the finest shell is dequantized on the stream of the finest
+ * level's correction while the coarser levels recompose beside it. */
+int mgrx_gpu_dequantize_recompose(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels,
+                                  int stop_level, const double* bin_widths, const int32_t* d_labels,
+                                  const uint64_t* d_outlier_pos, const void* d_outlier_val, uint64_t n_outliers,
+                                  void* d_coeffs, void* d_field);
+
 /* ---- host-buffer entry points (end-to-end: H2D + compute + D2H) ---------- */
 
 int mgrx_host_decompose(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels,

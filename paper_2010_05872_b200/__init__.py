@@ -34,7 +34,8 @@ from ._lib import LIB_PATH, lib, dp, u64p
 __all__ = [
     "Error", "GridHierarchy", "SolverWorkspace", "MultilevelCoefficients", "QuantMode", "QuantizationPlan",
     "LabelStream", "decompose", "recompose", "decompose_nonuniform", "recompose_nonuniform", "make_plan",
-    "quantize", "quantize_tail", "dequantize", "dequantize_tail", "LIB_PATH",
+    "quantize", "quantize_tail", "dequantize", "dequantize_tail", "decompose_quantize", "dequantize_recompose",
+    "LIB_PATH",
 ]
 
 ERRC = [
@@ -521,6 +522,94 @@ def quantize_tail(buffer, hierarchy: GridHierarchy, stop_level: int, plan: Quant
                   ws: Optional[SolverWorkspace] = None) -> LabelStream:
     """quantize_tail (quantize.hpp:99-114): levels above stop_level only."""
     return _quantize(buffer, hierarchy, int(stop_level), plan, ws)
+
+
+def decompose_quantize(field, hierarchy: GridHierarchy, plan: QuantizationPlan, stop_level: int = 0,
+                       ws: Optional[SolverWorkspace] = None):
+    """decompose (transform.hpp:485-506) + quantize / quantize_tail
+    (quantize.hpp:79-114) as compress_field runs them (pipeline.hpp:145-183),
+    in one call: the finest shell's labels are produced under the rest of the
+    decomposition.  Returns (MultilevelCoefficients, LabelStream), identical to
+    ``decompose`` followed by ``quantize`` / ``quantize_tail``."""
+    import torch
+
+    ws = _ws(ws)
+    h = hierarchy
+    _require_cuda(field, "field")
+    if tuple(field.shape) != h.level_dims(h.num_levels()):
+        raise Error(7, "field dims do not match hierarchy")
+    if stop_level < 0 or stop_level > h.num_levels():
+        raise Error(3, "stop level out of range")
+    if plan.num_levels() != h.num_levels():
+        raise Error(7, "plan does not match hierarchy")
+    stop = int(stop_level)
+    L = h.num_levels()
+    first = 0 if stop == 0 else stop + 1
+    base = 0 if stop == 0 else h.node_count(stop)
+    nlab = h.total_count() - base
+    out = torch.empty(field.numel(), dtype=field.dtype, device=field.device)
+    flat = torch.empty(nlab, dtype=torch.int32, device=field.device)
+    q = np.ascontiguousarray(plan.bin_widths, dtype=np.float64)
+    n_out = C.c_uint64()
+    cap = max(1, min(nlab, max(1 << 16, nlab >> 8)))
+    opos = torch.empty(cap, dtype=torch.int64, device=field.device)
+    oval = torch.empty(cap, dtype=field.dtype, device=field.device)
+    ws._bind_stream()
+    d = _dims_arr(field.shape)
+    rc = lib.mgrx_gpu_decompose_quantize(ws.handle, _dtype_code(field), field.dim(), d, L, stop,
+                                         C.c_void_p(field.data_ptr()), q.ctypes.data_as(dp),
+                                         C.c_void_p(out.data_ptr()), C.c_void_p(flat.data_ptr()),
+                                         C.c_void_p(opos.data_ptr()), C.c_void_p(oval.data_ptr()), C.c_uint64(cap),
+                                         C.byref(n_out))
+    mc = MultilevelCoefficients(out, h, stop)
+    if rc == 103:  # capacity exceeded: the coefficients are complete, redo the quantizer with the exact count
+        return mc, _quantize(out, h, stop, plan, ws)
+    _check(rc, ws.handle)
+    k = int(n_out.value)
+    labels, pos = [], 0
+    for l in range(first, L + 1):
+        labels.append(flat[pos:pos + h.delta_count(l)])
+        pos += h.delta_count(l)
+    return mc, LabelStream(flat, labels, opos[:k], oval[:k])
+
+
+def dequantize_recompose(stream: LabelStream, plan: QuantizationPlan, hierarchy: GridHierarchy,
+                         ws: Optional[SolverWorkspace] = None, dtype=None, stop_level: int = 0, buffer=None):
+    """dequantize / dequantize_tail (quantize.hpp:118-150) + recompose
+    (transform.hpp:509-530) as decompress_field runs them (pipeline.hpp:235-260),
+    in one call.  For ``stop_level`` > 0 pass ``buffer`` holding the decoded
+    coarse block (its shells are overwritten).  Returns the field."""
+    import torch
+
+    ws = _ws(ws)
+    h = hierarchy
+    stop = int(stop_level)
+    L = h.num_levels()
+    first = 0 if stop == 0 else stop + 1
+    if len(stream.labels) != L + 1 - first:
+        raise Error(7, "label stream does not match hierarchy")
+    for l, lv in zip(range(first, L + 1), stream.labels):
+        if lv.numel() != h.delta_count(l):
+            raise Error(7, "label count mismatch")
+    if stop > 0 and buffer is None:
+        raise Error(15, "a tail stream needs the buffer holding the coarse block")
+    dtype = dtype or (buffer.dtype if buffer is not None else stream.outlier_values.dtype)
+    if buffer is None:
+        buffer = torch.empty(h.total_count(), dtype=dtype, device=stream.flat.device)
+    _require_cuda(buffer, "buffer")
+    flat = stream.flat if stream.flat.numel() == sum(x.numel() for x in stream.labels) else torch.cat(stream.labels)
+    q = np.ascontiguousarray(plan.bin_widths, dtype=np.float64)
+    dims = h.level_dims(L)
+    out = torch.empty(dims, dtype=buffer.dtype, device=buffer.device)
+    n = int(stream.outlier_positions.numel())
+    ws._bind_stream()
+    _check(lib.mgrx_gpu_dequantize_recompose(ws.handle, _dtype_code(buffer), len(dims), _dims_arr(dims), L, stop,
+                                             q.ctypes.data_as(dp), C.c_void_p(flat.data_ptr()),
+                                             C.c_void_p(stream.outlier_positions.data_ptr() if n else 0),
+                                             C.c_void_p(stream.outlier_values.data_ptr() if n else 0),
+                                             C.c_uint64(n), C.c_void_p(buffer.data_ptr()),
+                                             C.c_void_p(out.data_ptr())), ws.handle)
+    return out
 
 
 def _dequantize(stream: LabelStream, plan: QuantizationPlan, h: GridHierarchy, stop: int, out, ws):

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <queue>
 #include <memory>
@@ -256,6 +257,9 @@ struct mgrx_gpu_ctx {
   bool nf_armed = false, nf_used = false;
   double* stop_host = nullptr;
   size_t stop_host_bytes = 0;
+  // dequantize + recompose: enqueued on the stream of the finest level's
+  // correction before it (the finest shell's dequantization)
+  std::function<void(cudaStream_t)> rec_pre_finest;
 };
 
 namespace {
@@ -553,8 +557,12 @@ std::vector<NuLevel> upload_nu(mgrx_gpu_ctx* c, const Plan& p, const double* con
 
 // ------------------------------------------------------------- transform
 
+// finest_shell_done: when given and the finest level runs on the fused 3-D
+// path, the event is recorded right after that level's plane pass (its shell
+// is final from then on) and *shell_event_used is set.
 template <typename T>
-void decompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, T* d_out, const std::vector<NuLevel>* nu) {
+void decompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, T* d_out, const std::vector<NuLevel>* nu,
+                    cudaEvent_t finest_shell_done = nullptr, bool* shell_event_used = nullptr) {
   const Hierarchy& h = p.h;
   const int L = h.L, stop = p.stop;
   if (stop == L) {  // identity (transform.hpp:494 loop does not run)
@@ -587,6 +595,10 @@ void decompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, T* d_out, const 
       if (nf_arm && l == L) {  // check_finite rides on this level's plane pass
         ex.nonfinite = c->nf_flag;
         c->nf_used = true;
+      }
+      if (finest_shell_done && l == L) {
+        ex.after_plane = finest_shell_done;
+        if (shell_event_used) *shell_event_used = true;
       }
       e = fused3d_decompose_level<T>(blk, shell, coarse, s + fp.scratch_off, p.geom[l], fp, p.thomas[l], ex);
     } else {
@@ -637,6 +649,7 @@ void recompose_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_coeffs, T* d_field, con
         cudaStream_t sd = c->side[k++ % mgrx_gpu_ctx::kSide];
         if (l == L && rec_prio() >= 1) sd = c->hi;
         cuda_check(cudaStreamWaitEvent(sd, c->fork, 0), "cudaStreamWaitEvent");
+        if (l == L && c->rec_pre_finest) c->rec_pre_finest(sd);
         cuda_check(fused3d_recompose_correction<T>(d_coeffs + h.node[l - 1], s + fp.scratch_off, fp, p.thomas[l],
                                                    exec_on(c, sd, l)),
                    "recompose correction");
@@ -1010,6 +1023,175 @@ int mgrx_gpu_dequantize(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims
     cuda_check(e, "dequantize");
   });
 }
+
+}  // extern "C"
+
+// Quantizer scratch of a call: per-chunk outlier counts, their scan, flags.
+struct QuantTmp {
+  uint32_t* counts;
+  uint64_t* offsets;
+  int* flags;
+  int64_t nch;
+};
+static QuantTmp quant_tmp(mgrx_gpu_ctx* c, const QuantLevels& ql) {
+  const int64_t nch = quant_num_chunks(ql);
+  const size_t need = align_up(size_t(nch + 1) * 4) + size_t(nch + 1) * 8 + 16;
+  ensure(&c->qtmp, &c->qtmp_bytes, need, c, "cudaMalloc(quant tmp)");
+  char* b = static_cast<char*>(c->qtmp);
+  QuantTmp t;
+  t.counts = reinterpret_cast<uint32_t*>(b);
+  t.offsets = reinterpret_cast<uint64_t*>(b + align_up(size_t(nch + 1) * 4));
+  t.flags = reinterpret_cast<int*>(t.offsets + nch + 1);
+  t.nch = nch;
+  return t;
+}
+
+// Runs the body with the context's stream switched to `s` (the level drivers
+// launch on c->stream).
+struct StreamSwap {
+  mgrx_gpu_ctx* c;
+  cudaStream_t saved;
+  StreamSwap(mgrx_gpu_ctx* c_, cudaStream_t s) : c(c_), saved(c_->stream) { c->stream = s; }
+  ~StreamSwap() { c->stream = saved; }
+};
+
+template <typename T>
+static void decompose_quantize_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, const double* q, T* d_coeffs,
+                                    int32_t* d_labels, uint64_t* d_opos, T* d_oval, uint64_t capacity,
+                                    uint64_t* n_outliers) {
+  const Hierarchy& h = p.h;
+  const int L = h.L;
+  QuantLevels ql = quant_levels(p, q);
+  QuantTmp qt = quant_tmp(c, ql);
+  cuda_check(cudaMemsetAsync(qt.flags, 0, sizeof(int), c->stream), "memset");
+  // chunks [split, nch) lie inside the finest shell: they are quantized on a
+  // low-priority side stream as soon as the finest level's plane pass has
+  // written that shell, under the rest of the decomposition (the finest
+  // level's solves and every coarser level: latency-bound, little HBM
+  // traffic), which runs on the high-priority chain stream
+  const bool overlap = L > p.stop && c->path == 0 && p.fused[L].enabled && !c->profiling;
+  int64_t split = qt.nch;
+  if (overlap) {
+    ensure_side(c, L + 1);
+    split = std::min(qt.nch, quant_chunk_of(ql, h.node[L - 1]));
+    cuda_check(cudaEventRecord(c->fork, c->stream), "cudaEventRecord(fork)");
+    cuda_check(cudaStreamWaitEvent(c->chain, c->fork, 0), "cudaStreamWaitEvent");
+    bool used = false;
+    {
+      StreamSwap sw(c, c->chain);
+      decompose_impl<T>(c, p, d_field, d_coeffs, nullptr, c->lvl_done[L], &used);
+    }
+    cuda_check(cudaEventRecord(c->join, c->chain), "cudaEventRecord(join)");
+    if (used) {
+      cudaStream_t sd = c->side[0];
+      cuda_check(cudaStreamWaitEvent(sd, c->lvl_done[L], 0), "cudaStreamWaitEvent");
+      static const int resident = std::getenv("MGRX_QOV_CTAS") ? std::atoi(std::getenv("MGRX_QOV_CTAS")) : 0;
+      cuda_check(quantize_labels_range<T>(d_coeffs, d_labels, qt.counts, qt.flags, ql, split, qt.nch,
+                                          exec_on(c, sd, L), resident),
+                 "quantize finest shell");
+      cuda_check(cudaEventRecord(c->lvl_done[0], sd), "cudaEventRecord");
+      cuda_check(cudaStreamWaitEvent(c->stream, c->lvl_done[0], 0), "cudaStreamWaitEvent");
+    } else {
+      split = qt.nch;
+    }
+    cuda_check(cudaStreamWaitEvent(c->stream, c->join, 0), "cudaStreamWaitEvent");
+  } else {
+    decompose_impl<T>(c, p, d_field, d_coeffs, nullptr);
+  }
+  cuda_check(quantize_labels_range<T>(d_coeffs, d_labels, qt.counts, qt.flags, ql, 0, split, exec(c)),
+             "quantize");
+  cuda_check(quantize_scan(qt.counts, qt.offsets, ql, exec(c)), "quantize scan");
+  if (d_opos && d_oval && capacity > 0)
+    cuda_check(quantize_pass2<T>(d_coeffs, qt.counts, qt.offsets, d_opos, d_oval, capacity, ql, exec(c)),
+               "quantize outliers");
+  uint64_t* hp = static_cast<uint64_t*>(c->pinned);
+  cuda_check(cudaMemcpyAsync(hp, qt.offsets + qt.nch, 8, cudaMemcpyDeviceToHost, c->stream), "readback");
+  cuda_check(cudaMemcpyAsync(hp + 1, qt.flags, 4, cudaMemcpyDeviceToHost, c->stream), "readback");
+  cuda_check(cudaStreamSynchronize(c->stream), "quantize sync");
+  const uint64_t total = hp[0];
+  const int flag = *reinterpret_cast<int*>(hp + 1);
+  *n_outliers = total;
+  if (flag) fail(MGRX_NONFINITE_DATA, "non-finite value in quantizer input");
+  if (total > capacity)
+    fail(MGRX_CAPACITY_EXCEEDED, "%llu outliers exceed capacity %llu", (unsigned long long)total,
+         (unsigned long long)capacity);
+  if (total > 0 && (!d_opos || !d_oval)) fail(MGRX_INVALID_ARGUMENT, "null outlier buffers");
+}
+
+template <typename T>
+static void dequantize_recompose_impl(mgrx_gpu_ctx* c, Plan& p, const double* q, const int32_t* d_labels,
+                                      const uint64_t* d_opos, const T* d_oval, uint64_t n_outliers, T* d_coeffs,
+                                      T* d_field) {
+  const Hierarchy& h = p.h;
+  const int L = h.L;
+  QuantLevels ql = quant_levels(p, q);
+  const int64_t nch = quant_num_chunks(ql);
+  // the finest shell's labels are dequantized (and its outliers restored) on
+  // the stream of the finest level's correction, which reads only that
+  // shell, after the coarser shells, whose levels' work then runs beside it
+  const bool overlap = L > p.stop && c->path == 0 && p.fused[L].enabled && !c->profiling;
+  if (!overlap) {
+    cuda_check(dequantize_run<T>(d_labels, d_opos, d_oval, n_outliers, d_coeffs, ql, exec(c)), "dequantize");
+    recompose_impl<T>(c, p, d_coeffs, d_field, nullptr);
+    return;
+  }
+  const int64_t split = std::min(nch, quant_chunk_of(ql, h.node[L - 1]));
+  cuda_check(dequantize_range<T>(d_labels, d_opos, d_oval, n_outliers, d_coeffs, ql, 0, split, exec(c)),
+             "dequantize");
+  c->rec_pre_finest = [&](cudaStream_t sd) {
+    cuda_check(dequantize_range<T>(d_labels, d_opos, d_oval, n_outliers, d_coeffs, ql, split, nch,
+                                   exec_on(c, sd, L)),
+               "dequantize finest shell");
+  };
+  try {
+    recompose_impl<T>(c, p, d_coeffs, d_field, nullptr);
+  } catch (...) {
+    c->rec_pre_finest = nullptr;
+    throw;
+  }
+  c->rec_pre_finest = nullptr;
+}
+
+extern "C" {
+
+int mgrx_gpu_decompose_quantize(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
+                                const void* d_field, const double* q, void* d_coeffs, int32_t* d_labels,
+                                uint64_t* d_opos, void* d_oval, uint64_t capacity, uint64_t* n_outliers) {
+  return guarded(c, [&] {
+    if (!dims || !q || !d_field || !d_coeffs || !d_labels || !n_outliers)
+      fail(MGRX_INVALID_ARGUMENT, "null argument");
+    Plan* p = get_plan(c, dtype, nd, dims, levels, stop);
+    for (int l = 0; l <= p->h.L; ++l)
+      if (!(q[l] > 0.0) || !std::isfinite(q[l])) fail(MGRX_INVALID_BUDGET, "bad bin width at level %d", l);
+    if (dtype == MGRX_F32)
+      decompose_quantize_impl<float>(c, *p, static_cast<const float*>(d_field), q, static_cast<float*>(d_coeffs),
+                                     d_labels, d_opos, static_cast<float*>(d_oval), capacity, n_outliers);
+    else
+      decompose_quantize_impl<double>(c, *p, static_cast<const double*>(d_field), q,
+                                      static_cast<double*>(d_coeffs), d_labels, d_opos,
+                                      static_cast<double*>(d_oval), capacity, n_outliers);
+  });
+}
+
+int mgrx_gpu_dequantize_recompose(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
+                                  const double* q, const int32_t* d_labels, const uint64_t* d_opos,
+                                  const void* d_oval, uint64_t n_outliers, void* d_coeffs, void* d_field) {
+  return guarded(c, [&] {
+    if (!dims || !q || !d_labels || !d_coeffs || !d_field) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    if (n_outliers && (!d_opos || !d_oval)) fail(MGRX_INVALID_ARGUMENT, "null outlier buffers");
+    Plan* p = get_plan(c, dtype, nd, dims, levels, stop);
+    if (dtype == MGRX_F32)
+      dequantize_recompose_impl<float>(c, *p, q, d_labels, d_opos, static_cast<const float*>(d_oval), n_outliers,
+                                       static_cast<float*>(d_coeffs), static_cast<float*>(d_field));
+    else
+      dequantize_recompose_impl<double>(c, *p, q, d_labels, d_opos, static_cast<const double*>(d_oval),
+                                        n_outliers, static_cast<double*>(d_coeffs), static_cast<double*>(d_field));
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
 
 static int host_roundtrip(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
                           const void* h_in, void* h_out, bool dec) {

@@ -96,6 +96,7 @@ struct Exec {
   Profiler* prof;
   int level = -1;  // hierarchy level being processed (profiling key), -1 = none
   unsigned* nonfinite = nullptr;  // finest level of a compress: check_finite fused into its first pass
+  cudaEvent_t after_plane = nullptr;  // recorded after a fused level's decompose plane pass (its shell is final)
 };
 // Records a CUDA event before/after a tagged launch when profiling
 // (api.cu); no-op otherwise.

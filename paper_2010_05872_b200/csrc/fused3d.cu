@@ -1666,6 +1666,10 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
                                                  coarse, G, gd));
     }
   }
+  if (ex.after_plane) {
+    e = cudaEventRecord(ex.after_plane, ex.s);
+    if (e != cudaSuccess) return e;
+  }
   row_col1(G, g, th, ex);
   launch_col<T>(G, coarse, 1.0, g, 0, th.w[0], th.inv_d[0], ex);
   return cudaGetLastError();

@@ -82,10 +82,10 @@ __device__ __forceinline__ bool quant_fast(double x, double inv, int32_t* lab, b
 // few) runs the fast path; a thread that met a value needing the exact
 // division (or a non-finite one) redoes its 16 values exactly.
 template <typename T>
-__global__ void __launch_bounds__(kQBlock, 4) k_quant_labels(const T* __restrict__ c, int32_t* __restrict__ labels,
-                                                             uint32_t* __restrict__ chunk_counts,
-                                                             int* __restrict__ flags, const QuantLevels ql) {
-  const int64_t chunk0 = ql.base + int64_t(blockIdx.x) * kQChunk;
+__device__ __forceinline__ void quant_chunk(const T* __restrict__ c, int32_t* __restrict__ labels,
+                                            uint32_t* __restrict__ chunk_counts, int* __restrict__ flags,
+                                            const QuantLevels& ql, const int64_t chunk, int* warp_sums) {
+  const int64_t chunk0 = ql.base + chunk * kQChunk;
   const int n = int(min(int64_t(kQChunk), ql.total - chunk0));  // positions in this chunk
   const T* cp = c + chunk0 + threadIdx.x;
   int32_t* lp = labels + (chunk0 - ql.base) + threadIdx.x;
@@ -133,7 +133,6 @@ __global__ void __launch_bounds__(kQBlock, 4) k_quant_labels(const T* __restrict
   }
   if (nonfinite) atomicOr(flags, 1);
   // block reduction of counts
-  __shared__ int warp_sums[kQBlock / 32];
   int wsum = count;
   for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
   if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = wsum;
@@ -141,7 +140,33 @@ __global__ void __launch_bounds__(kQBlock, 4) k_quant_labels(const T* __restrict
   if (threadIdx.x == 0) {
     int t = 0;
     for (int w = 0; w < kQBlock / 32; ++w) t += warp_sums[w];
-    chunk_counts[blockIdx.x] = uint32_t(t);
+    chunk_counts[chunk] = uint32_t(t);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kQBlock, 4) k_quant_labels(const T* __restrict__ c, int32_t* __restrict__ labels,
+                                                             uint32_t* __restrict__ chunk_counts,
+                                                             int* __restrict__ flags, const QuantLevels ql,
+                                                             const int64_t chunk_begin) {
+  __shared__ int warp_sums[kQBlock / 32];
+  quant_chunk<T>(c, labels, chunk_counts, flags, ql, chunk_begin + int64_t(blockIdx.x), warp_sums);
+}
+
+// The same over chunks chunk_begin + blockIdx.x, + gridDim.x, ... : a small
+// resident grid that trickles through the finest shell beside the
+// decomposition's remaining passes (decompose_quantize) instead of flooding
+// every SM.
+template <typename T>
+__global__ void __launch_bounds__(kQBlock, 4) k_quant_labels_loop(const T* __restrict__ c,
+                                                                  int32_t* __restrict__ labels,
+                                                                  uint32_t* __restrict__ chunk_counts,
+                                                                  int* __restrict__ flags, const QuantLevels ql,
+                                                                  const int64_t chunk_begin, const int64_t chunk_end) {
+  __shared__ int warp_sums[kQBlock / 32];
+  for (int64_t ch = chunk_begin + int64_t(blockIdx.x); ch < chunk_end; ch += gridDim.x) {
+    quant_chunk<T>(c, labels, chunk_counts, flags, ql, ch, warp_sums);
+    __syncthreads();  // warp_sums is reused
   }
 }
 
@@ -291,8 +316,8 @@ __global__ void __launch_bounds__(kQBlock) k_quant_outliers(const T* __restrict_
 // thread.
 template <typename T>
 __global__ void __launch_bounds__(kQBlock, 4) k_dequant(const int32_t* __restrict__ labels, T* __restrict__ c,
-                                                        const QuantLevels ql) {
-  const int64_t chunk0 = ql.base + int64_t(blockIdx.x) * kQChunk;
+                                                        const QuantLevels ql, const int64_t chunk_begin) {
+  const int64_t chunk0 = ql.base + (chunk_begin + int64_t(blockIdx.x)) * kQChunk;
   const int n = int(min(int64_t(kQChunk), ql.total - chunk0));
   const int32_t* lp = labels + (chunk0 - ql.base) + threadIdx.x;
   T* cp = c + chunk0 + threadIdx.x;
@@ -319,19 +344,50 @@ __global__ void __launch_bounds__(kQBlock, 4) k_dequant(const int32_t* __restric
 template <typename T>
 __global__ void __launch_bounds__(256) k_restore_outliers(const uint64_t* __restrict__ opos,
                                                           const T* __restrict__ oval, uint64_t n,
-                                                          T* __restrict__ c) {
+                                                          T* __restrict__ c, uint64_t lo, uint64_t hi) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) c[opos[i]] = oval[i];
+  if (i < n) {
+    const uint64_t p = opos[i];
+    if (p >= lo && p < hi) c[p] = oval[i];
+  }
 }
 
 int64_t quant_num_chunks(const QuantLevels& ql) { return (ql.total - ql.base + kQChunk - 1) / kQChunk; }
+
+int64_t quant_chunk_of(const QuantLevels& ql, int64_t pos) { return (pos - ql.base + kQChunk - 1) / kQChunk; }
+
+// Labels + outlier counts of chunks [chunk_begin, chunk_end) only (the
+// overlapped decompose + quantize launches the finest shell's chunks as soon
+// as that shell is final).
+template <typename T>
+cudaError_t quantize_labels_range(const T* c, int32_t* labels, uint32_t* chunk_counts, int* flags,
+                                  const QuantLevels& ql, int64_t chunk_begin, int64_t chunk_end, const Exec& ex,
+                                  int resident_ctas) {
+  if (chunk_end > chunk_begin) {
+    if (resident_ctas > 0 && chunk_end - chunk_begin > resident_ctas)
+      MGRX_LAUNCH(ex, "quant_labels", k_quant_labels_loop<T><<<unsigned(resident_ctas), kQBlock, 0, ex.s>>>(
+                                          c, labels, chunk_counts, flags, ql, chunk_begin, chunk_end));
+    else
+      MGRX_LAUNCH(ex, "quant_labels", k_quant_labels<T><<<unsigned(chunk_end - chunk_begin), kQBlock, 0, ex.s>>>(
+                                          c, labels, chunk_counts, flags, ql, chunk_begin));
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t quantize_scan(const uint32_t* chunk_counts, uint64_t* offsets, const QuantLevels& ql, const Exec& ex) {
+  const int64_t nch = quant_num_chunks(ql);
+  const size_t ssm = size_t(std::min<int64_t>(std::max<int64_t>(nch, 1), kScanMax)) * 4;
+  cudaFuncSetAttribute(k_scan_counts, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ssm));
+  MGRX_LAUNCH(ex, "quant_scan", k_scan_counts<<<1, kScanThreads, ssm, ex.s>>>(chunk_counts, offsets, nch));
+  return cudaGetLastError();
+}
 
 template <typename T>
 cudaError_t quantize_pass1(const T* c, int32_t* labels, uint32_t* chunk_counts, uint64_t* offsets, int* flags,
                            const QuantLevels& ql, const Exec& ex) {
   const int64_t nch = quant_num_chunks(ql);
   if (nch > 0)
-    MGRX_LAUNCH(ex, "quant_labels", k_quant_labels<T><<<unsigned(nch), kQBlock, 0, ex.s>>>(c, labels, chunk_counts, flags, ql));
+    MGRX_LAUNCH(ex, "quant_labels", k_quant_labels<T><<<unsigned(nch), kQBlock, 0, ex.s>>>(c, labels, chunk_counts, flags, ql, 0));
   const size_t ssm = size_t(std::min<int64_t>(std::max<int64_t>(nch, 1), kScanMax)) * 4;
   cudaFuncSetAttribute(k_scan_counts, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ssm));
   MGRX_LAUNCH(ex, "quant_scan", k_scan_counts<<<1, kScanThreads, ssm, ex.s>>>(chunk_counts, offsets, nch));
@@ -353,10 +409,28 @@ template <typename T>
 cudaError_t dequantize_run(const int32_t* labels, const uint64_t* opos, const T* oval, uint64_t n_out, T* c,
                            const QuantLevels& ql, const Exec& ex) {
   const int64_t nch = quant_num_chunks(ql);
-  if (nch > 0) MGRX_LAUNCH(ex, "dequant", k_dequant<T><<<unsigned(nch), kQBlock, 0, ex.s>>>(labels, c, ql));
+  if (nch > 0) MGRX_LAUNCH(ex, "dequant", k_dequant<T><<<unsigned(nch), kQBlock, 0, ex.s>>>(labels, c, ql, 0));
   if (n_out > 0)
     MGRX_LAUNCH(ex, "dequant_outliers",
-                k_restore_outliers<T><<<unsigned((n_out + 255) / 256), 256, 0, ex.s>>>(opos, oval, n_out, c));
+                k_restore_outliers<T><<<unsigned((n_out + 255) / 256), 256, 0, ex.s>>>(opos, oval, n_out, c, 0,
+                                                                                       ~uint64_t(0)));
+  return cudaGetLastError();
+}
+
+// Labels -> coefficients of chunks [chunk_begin, chunk_end) only (no outlier
+// restore): the overlapped dequantize + recompose.
+template <typename T>
+cudaError_t dequantize_range(const int32_t* labels, const uint64_t* opos, const T* oval, uint64_t n_out, T* c,
+                             const QuantLevels& ql, int64_t chunk_begin, int64_t chunk_end, const Exec& ex) {
+  if (chunk_end > chunk_begin)
+    MGRX_LAUNCH(ex, "dequant", k_dequant<T><<<unsigned(chunk_end - chunk_begin), kQBlock, 0, ex.s>>>(labels, c, ql,
+                                                                                                 chunk_begin));
+  if (n_out > 0 && chunk_end > chunk_begin) {  // outliers of this chunk range only
+    const uint64_t lo = uint64_t(ql.base + chunk_begin * kQChunk);
+    const uint64_t hi = uint64_t(std::min<int64_t>(ql.total, ql.base + chunk_end * kQChunk));
+    MGRX_LAUNCH(ex, "dequant_outliers",
+                k_restore_outliers<T><<<unsigned((n_out + 255) / 256), 256, 0, ex.s>>>(opos, oval, n_out, c, lo, hi));
+  }
   return cudaGetLastError();
 }
 
@@ -366,7 +440,11 @@ cudaError_t dequantize_run(const int32_t* labels, const uint64_t* opos, const T*
   template cudaError_t quantize_pass2<T>(const T*, const uint32_t*, const uint64_t*, uint64_t*, T*, uint64_t, \
                                          const QuantLevels&, const Exec&);                                  \
   template cudaError_t dequantize_run<T>(const int32_t*, const uint64_t*, const T*, uint64_t, T*,            \
-                                         const QuantLevels&, const Exec&);
+                                         const QuantLevels&, const Exec&);                                  \
+  template cudaError_t quantize_labels_range<T>(const T*, int32_t*, uint32_t*, int*, const QuantLevels&,     \
+                                                int64_t, int64_t, const Exec&, int);                           \
+  template cudaError_t dequantize_range<T>(const int32_t*, const uint64_t*, const T*, uint64_t, T*,          \
+                                           const QuantLevels&, int64_t, int64_t, const Exec&);
 MGRX_INST(float)
 MGRX_INST(double)
 #undef MGRX_INST
