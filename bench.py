@@ -630,6 +630,26 @@ def quant_measure(mg, wsp, field, h, args):
     s = mg.quantize(mc, plan, wsp)
     mg.dequantize(s, plan, h, wsp)
     prof = {kk: v[0] * 1e3 for kk, v in wsp.profile_end().items()}
+    # the one-call forms (decompose + quantize, dequantize + recompose) beside the two-call sequences
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(k):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / k
+
+    one_call = {
+        "decompose_then_quantize_ms": timed(lambda: mg.quantize(mg.decompose(field, h, 0, wsp), plan, wsp)),
+        "decompose_quantize_ms": timed(lambda: mg.decompose_quantize(field, h, plan, 0, wsp)),
+        "dequantize_then_recompose_ms": timed(lambda: mg.recompose(mg.dequantize(s, plan, h, wsp), wsp)),
+        "dequantize_recompose_ms": timed(lambda: mg.dequantize_recompose(s, plan, h, wsp)),
+        "note": "eager calls; decompose_quantize quantizes the finest shell on a side stream under the rest of "
+                "the decomposition",
+    }
     peak, _ = measured_peak()
     kern = {}
     for name in ("quant_labels", "dequant"):
@@ -639,7 +659,7 @@ def quant_measure(mg, wsp, field, h, args):
     return {"quantize_ms": q_ms, "dequantize_ms": d_ms, "quantize_gbs": nb / (q_ms * 1e-3) / 1e9,
             "dequantize_gbs": nb / (d_ms * 1e-3) / 1e9, "quantize_frac": nb / (q_ms * 1e-3) / 1e9 / peak,
             "dequantize_frac": nb / (d_ms * 1e-3) / 1e9 / peak, "kernels_us": prof, "kernel_roofline": kern,
-            "alg_bytes": nb, "outliers": int(s.outlier_positions.numel()),
+            "alg_bytes": nb, "outliers": int(s.outlier_positions.numel()), "one_call": one_call,
             "linf_over_tau": linf / (1e-3 * rg), "tau": "1e-3 * range, budget tau/4",
             "note": "whole calls include the outlier-count readback (synchronous, as the reference's API); "
                     "bytes N*s + 4N each way (SURVEY 8(d))"}

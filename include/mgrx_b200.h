@@ -178,6 +178,15 @@ int mgrx_gpu_dequantize_recompose(mgrx_gpu_ctx* ctx, int dtype, int ndims, const
 
 /* ---- host-buffer entry points (end-to-end: H2D + compute + D2H) ---------- */
 
+/* decompress_field's ★ pair (pipeline.hpp:235-260) from HOST buffers in one
+ * device-resident pass: labels (+ outliers, + for stop_level > 0 the decoded
+ * coarse block of node_count(stop) values, else NULL) go to the GPU,
+ * mgrx_gpu_dequantize_recompose runs there, only the field comes back. */
+int mgrx_host_decompress(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels,
+                         int stop_level, const double* bin_widths, const int32_t* h_labels,
+                         const uint64_t* h_outlier_pos, const void* h_outlier_val, uint64_t n_outliers,
+                         const void* h_coarse, void* h_field);
+
 int mgrx_host_decompose(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels,
                         int stop_level, const void* h_field, void* h_out);
 int mgrx_host_recompose(mgrx_gpu_ctx* ctx, int dtype, int ndims, const uint64_t* dims, int levels,

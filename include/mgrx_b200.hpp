@@ -185,6 +185,38 @@ void dequantize_impl(std::span<T> buffer, const LabelStream<T>& stream, const Gr
                              plan.bin_widths.data(), flat.data(), pos.data(), val.data(), pos.size(), buffer.data()),
         ws.get());
 }
+// dequantize (+ the decoded coarse block for a tail stream) + recompose in
+// one device-resident pass (mgrx_host_decompress): the coefficients never
+// come back to the host.
+template <typename T>
+TensorField<T> decompress_impl(const LabelStream<T>& stream, const GridHierarchy& h, int stop,
+                               const QuantizationPlan& plan, const T* coarse, Workspace& ws) {
+  const int first = stop == 0 ? 0 : stop + 1;
+  if (stream.labels.size() != size_t(h.num_levels() + 1 - first))
+    fail(errc::shape_error, "label stream does not match hierarchy");
+  std::vector<int32_t> flat;
+  flat.reserve(h.total_count());
+  for (int l = first; l <= h.num_levels(); ++l) {
+    const auto& lv = stream.labels[size_t(l - first)];
+    if (lv.size() != h.delta_count(l)) fail(errc::shape_error, "label count mismatch");
+    flat.insert(flat.end(), lv.begin(), lv.end());
+  }
+  std::vector<uint64_t> pos;
+  std::vector<T> val;
+  for (const auto& o : stream.outliers) {
+    pos.push_back(o.position);
+    val.push_back(o.value);
+  }
+  TensorField<T> out;
+  out.dims = h.level_dims(h.num_levels());
+  out.data.resize(h.total_count());
+  const auto d = dims64(out.dims);
+  check(mgrx_host_decompress(ws.get(), dtype<T>(), int(d.size()), d.data(), h.num_levels(), stop,
+                             plan.bin_widths.data(), flat.data(), pos.data(), val.data(), pos.size(), coarse,
+                             out.data.data()),
+        ws.get());
+  return out;
+}
 }  // namespace detail
 
 template <typename T>
@@ -395,12 +427,11 @@ TensorField<T> decompress_field(const Artifact& a, Workspace& ws) {
           mgrx::detail::parse_label_section(a.sections[static_cast<std::size_t>(l)], h.delta_count(l));
     ByteReader r{a.sections.back()};
     stream.outliers = mgrx::detail::read_outliers<T>(r, h.total_count());
-    return recompose(dequantize(stream, plan, h, ws), ws);
+    return detail::decompress_impl<T>(stream, h, 0, plan, nullptr, ws);
   }
   if (stop < 1 || stop > L) fail(errc::corrupt, "bad stop level");
   const std::size_t tail_levels = static_cast<std::size_t>(L - stop);
   if (a.sections.size() != tail_levels + 2) fail(errc::corrupt, "unexpected section count");
-  MultilevelCoefficients<T> coeffs{std::vector<T>(h.total_count()), h, stop};
   LabelStream<T> stream;
   stream.labels.resize(tail_levels);
   for (std::size_t i = 0; i < tail_levels; ++i)
@@ -412,11 +443,9 @@ TensorField<T> decompress_field(const Artifact& a, Workspace& ws) {
     for (const auto& o : stream.outliers)
       if (o.position < h.node_count(stop)) fail(errc::corrupt, "outlier inside coarse block");
   }
-  dequantize_tail<T>(coeffs.buffer, stream, h, stop, plan, ws);
   LorenzoStream<T> coarse_stream = mgrx::detail::parse_lorenzo_section<T>(a.sections.back(), h.node_count(stop));
   TensorField<T> coarse = decompress_lorenzo(coarse_stream, h.level_dims(stop));
-  std::copy(coarse.data.begin(), coarse.data.end(), coeffs.buffer.begin());
-  return recompose(coeffs, ws);
+  return detail::decompress_impl<T>(stream, h, stop, plan, coarse.data.data(), ws);
 }
 
 }  // namespace mgrx::b200

@@ -17,7 +17,7 @@ EXPORTS = (
     "mgrx_gpu_get_stream", "mgrx_gpu_synchronize", "mgrx_gpu_last_error", "mgrx_gpu_launch_count",
     "mgrx_gpu_set_path", "mgrx_gpu_profile_begin", "mgrx_gpu_profile_end", "mgrx_hierarchy", "mgrx_make_plan", "mgrx_gpu_decompose", "mgrx_gpu_recompose",
     "mgrx_gpu_decompose_nonuniform", "mgrx_gpu_recompose_nonuniform", "mgrx_gpu_quantize",
-    "mgrx_gpu_dequantize", "mgrx_gpu_decompose_quantize", "mgrx_gpu_dequantize_recompose", "mgrx_host_decompose", "mgrx_host_recompose", "mgrx_host_quantize", "mgrx_host_dequantize",
+    "mgrx_gpu_dequantize", "mgrx_gpu_decompose_quantize", "mgrx_gpu_dequantize_recompose", "mgrx_host_decompress", "mgrx_host_decompose", "mgrx_host_recompose", "mgrx_host_quantize", "mgrx_host_dequantize",
     "mgrx_gpu_workspace_size",
     "mgrx_gpu_choose_stop", "mgrx_host_decompose_adaptive", "mgrx_gpu_encode_labels", "mgrx_host_compress", "mgrx_gpu_field_stats", "mgrx_gpu_decompose_checked", "mgrx_host_lorenzo",
     "mgrx_gpu_slab_level", "mgrx_gpu_slab_dec_plane", "mgrx_gpu_slab_rec_plane", "mgrx_gpu_slab_inplane",
@@ -58,6 +58,7 @@ def _load() -> C.CDLL:
         "mgrx_gpu_dequantize": (i, [vp, i, i, u64p, i, i, dp, vp, vp, vp, C.c_uint64, vp]),
         "mgrx_gpu_decompose_quantize": (i, [vp, i, i, u64p, i, i, vp, dp, vp, vp, vp, vp, C.c_uint64, u64p]),
         "mgrx_gpu_dequantize_recompose": (i, [vp, i, i, u64p, i, i, dp, vp, vp, vp, C.c_uint64, vp, vp]),
+        "mgrx_host_decompress": (i, [vp, i, i, u64p, i, i, dp, vp, vp, vp, C.c_uint64, vp, vp]),
         "mgrx_host_decompose": (i, [vp, i, i, u64p, i, i, vp, vp]),
         "mgrx_host_recompose": (i, [vp, i, i, u64p, i, i, vp, vp]),
         "mgrx_host_quantize": (i, [vp, i, i, u64p, i, i, dp, vp, vp, vp, vp, C.c_uint64, u64p]),

@@ -1278,6 +1278,44 @@ int mgrx_host_dequantize(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dim
   });
 }
 
+// decompress_field's ★ pair from host buffers (pipeline.hpp:235-260): the
+// labels, the outliers and (stop > 0) the decoded coarse block go to the GPU,
+// dequantize + recompose run there back to back, only the field comes back
+// (the two host calls would move the N coefficients down and up again).
+int mgrx_host_decompress(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
+                         const double* q, const int32_t* h_labels, const uint64_t* h_opos, const void* h_oval,
+                         uint64_t n_outliers, const void* h_coarse, void* h_field) {
+  return guarded(c, [&] {
+    if (!dims || !q || !h_labels || !h_field) fail(MGRX_INVALID_ARGUMENT, "null argument");
+    if (n_outliers && (!h_opos || !h_oval)) fail(MGRX_INVALID_ARGUMENT, "null outlier buffers");
+    Plan* p = get_plan(c, dtype, nd, dims, levels, stop);
+    if (stop > 0 && !h_coarse) fail(MGRX_INVALID_ARGUMENT, "a tail stream needs the coarse block");
+    const size_t n = size_t(p->h.node[p->h.L]);
+    const size_t base = stop == 0 ? 0 : size_t(p->h.node[stop]);
+    const size_t es = p->esize;
+    const size_t no = size_t(n_outliers);
+    const size_t need =
+        2 * align_up(n * es) + align_up((n - base) * 4) + align_up(no * 8 + 8) + align_up(no * es + 8);
+    ensure(&c->io, &c->io_bytes, need, c, "cudaMalloc(io)");
+    char* b = static_cast<char*>(c->io);
+    char* dc = b;
+    char* df = b + align_up(n * es);
+    int32_t* dl = reinterpret_cast<int32_t*>(df + align_up(n * es));
+    uint64_t* dp = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(dl) + align_up((n - base) * 4));
+    char* dv = reinterpret_cast<char*>(dp) + align_up(no * 8 + 8);
+    if (base) cuda_check(cudaMemcpyAsync(dc, h_coarse, base * es, cudaMemcpyHostToDevice, c->stream), "H2D");
+    cuda_check(cudaMemcpyAsync(dl, h_labels, (n - base) * 4, cudaMemcpyHostToDevice, c->stream), "H2D");
+    if (no) {
+      cuda_check(cudaMemcpyAsync(dp, h_opos, no * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+      cuda_check(cudaMemcpyAsync(dv, h_oval, no * es, cudaMemcpyHostToDevice, c->stream), "H2D");
+    }
+    const int r = mgrx_gpu_dequantize_recompose(c, dtype, nd, dims, levels, stop, q, dl, dp, dv, n_outliers, dc, df);
+    if (r != MGRX_OK) throw Fail{r, c->last_error};
+    cuda_check(cudaMemcpyAsync(h_field, df, n * es, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
 int mgrx_host_decompose(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int levels, int stop,
                         const void* h_field, void* h_out) {
   return host_roundtrip(c, dtype, nd, dims, levels, stop, h_field, h_out, true);

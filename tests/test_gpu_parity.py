@@ -215,7 +215,7 @@ def test_level_step_intermediates_general(torch, mg, g, ws_general):
 
 def test_config1_against_reference(torch, mg):
     """BASELINE config 1 (129^3 f64, 16 bumps + noise), full decomposition,
-    recomposition and level-wise quantization at 1e-3 relative (budget = tau/2)."""
+    recomposition and level-wise quantization at 1e-3 relative (budget = tau/4)."""
     from oracle.oracle import Oracle, Reference, reference_available
     from synthetic_fields import config1_field
 
