@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(256) k_f2_rows(double* __restrict__ G, int row
     off[i] = goff[i];
   }
   __syncthreads();
-  const int seg = (m + 31) >> 5;
+  const int seg = ((m + 31) >> 5) | 1;  // odd: lanes' segments start in distinct shared-memory banks
   const int s0 = min(m, lane * seg), s1 = min(m, s0 + seg);
   pdl_wait();
   for (int r = blockIdx.x * nw + warp; r < rows; r += gridDim.x * nw) {

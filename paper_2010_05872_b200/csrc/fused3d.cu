@@ -379,7 +379,7 @@ __device__ __forceinline__ int right_src(bool right_degen) {
 __device__ __forceinline__ void warp_row_thomas(double* x, int m, const double* __restrict__ w,
                                                 const double* __restrict__ inv_d) {
   const int lane = threadIdx.x & 31;
-  const int seg = (m + 31) >> 5;
+  const int seg = ((m + 31) >> 5) | 1;  // odd: lanes' segments start in distinct shared-memory banks
   const int s0 = min(m, lane * seg), s1 = min(m, s0 + seg);
   Aff f{0.0, 1.0};
   for (int i = s0; i < s1; ++i) {
@@ -424,7 +424,7 @@ template <int SEG>
 __device__ __forceinline__ void warp_row_thomas_reg(double* x, int m, const double* __restrict__ w,
                                                     const double* __restrict__ inv_d) {
   const int lane = threadIdx.x & 31;
-  const int seg = (m + 31) >> 5;
+  const int seg = ((m + 31) >> 5) | 1;  // odd: lanes' segments start in distinct shared-memory banks
   const int s0 = min(m, lane * seg), len = min(m, s0 + seg) - s0;
   double v[SEG];
 #pragma unroll
@@ -1248,7 +1248,10 @@ void launch_row(double* G, const F3Geom& g, const double* w, const double* id, c
   const int64_t rows = g.m0 * g.m1;
   const int threads = 256;
   const size_t smem = size_t(2 + threads / 32) * m * 8;
-  const int nc = (m + 31) / 32;
+  // lanes solve segments of an ODD number of values (warp_row_thomas_reg): an
+  // even segment length puts the lanes' strided shared-memory accesses on a
+  // few banks (m2 = 251: 47 -> 13 us at 51 x 251 rows)
+  const int nc = ((m + 31) / 32) | 1;
   const int64_t blocks = std::min<int64_t>((rows + 7) / 8, int64_t(kNumSMs) * kRowCtas(nc));
 #define ROW_(NC)                                                                                           \
   do {                                                                                                     \
@@ -1257,7 +1260,6 @@ void launch_row(double* G, const F3Geom& g, const double* w, const double* id, c
                 pdl_launch(k_f3_row<NC>, dim3(unsigned(blocks)), dim3(threads), smem, ex.s, !ex.prof, G, rows, m, w, id)); \
   } while (0)
   if (nc <= 1) ROW_(1);
-  else if (nc <= 2) ROW_(2);
   else if (nc <= 3) ROW_(3);
   else if (nc <= 5) ROW_(5);
   else if (nc <= 9) ROW_(9);

@@ -1436,7 +1436,7 @@ __global__ void __launch_bounds__(256) k_axis_solve_rows(double* __restrict__ y,
     if (goff) off[i] = goff[i];
   }
   __syncthreads();
-  const int seg = (m + 31) >> 5;
+  const int seg = ((m + 31) >> 5) | 1;  // odd: lanes' segments start in distinct shared-memory banks
   const int s0 = min(m, lane * seg), s1 = min(m, s0 + seg);
   for (int64_t line = int64_t(blockIdx.x) * nw + warp; line < nlines; line += int64_t(gridDim.x) * nw) {
     double* gl = y + line * m;
