@@ -42,7 +42,6 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
-#include <vector>
 
 #include "fused3d.h"
 
@@ -1269,22 +1268,6 @@ void launch_row(double* G, const F3Geom& g, const double* w, const double* id, c
 #undef ROW_
 }
 
-// Tables of the band pass (below, "band pass").
-struct BandTabs {
-  const double* lw;   // [m1] band-local forward factor (0 at a band's first row)
-  const double* lid;  // [m1] band-local 1 / d
-  const double* sv;   // [m1] spike of the upper interface (0 in the first band)
-  const double* su;   // [m1] spike of the lower interface (0 in the last band)
-  const double* ic;   // [3 (nb - 1)] per interface: uL, vF, 1 / (1 - uL vF)
-  int nb, base, rem;  // the first rem bands have base + 1 rows, the others base
-  int m2;
-};
-__host__ __device__ inline int band_start(const BandTabs& t, int b) { return b * t.base + min(b, t.rem); }
-__host__ __device__ inline int band_of(const BandTabs& t, int i1) {
-  const int big = t.rem * (t.base + 1);
-  return i1 < big ? i1 / (t.base + 1) : t.rem + (i1 - big) / t.base;
-}
-
 // ------------------------------------------------------------ column pass
 // Thomas along axis 0 or 1 of the coarse fp64 volume G (m0 x m1 x m2).
 // 16 consecutive columns per block; each column is split into S segments
@@ -1294,11 +1277,10 @@ __host__ __device__ inline int band_of(const BandTabs& t, int i1) {
 // from its true carry.  With `coarse` set the result is applied:
 // coarse += sign * z (apply_correction, transform.hpp:435-477); otherwise it
 // is written back to G.
-template <typename T, int LS, bool APPLY, int MAXT, bool BAND = false>
+template <typename T, int LS, bool APPLY, int MAXT>
 __global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : (MAXT == kColThreads12 ? 3 : 1))
     k_f3_col(double* __restrict__ G, T* __restrict__ coarse, double sign, int64_t ncols, int m, int64_t stride,
-             int64_t outer_stride, int64_t inner, const double* __restrict__ w, const double* __restrict__ inv_d,
-             const double2* __restrict__ P, const BandTabs bt) {
+             int64_t outer_stride, int64_t inner, const double* __restrict__ w, const double* __restrict__ inv_d) {
   extern __shared__ double sc[];
   const int lane = threadIdx.x, S = 2 * blockDim.y;
   const int c16 = lane & 15, s = 2 * threadIdx.y + (lane >> 4);
@@ -1326,19 +1308,6 @@ __global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : (MAXT == kColT
     for (int k = 0; k < LS; ++k) {
       v[k] = (valid && k < len) ? (APPLY ? __ldcs(gp) : *gp) : 0.0;
       gp += stride;
-    }
-    if (BAND && valid) {  // axis-0 pass after the band pass: add the two spike terms of the axis-1 solve
-      const int i1 = int(col / bt.m2), i2 = int(col - int64_t(i1) * bt.m2);
-      const double sv = bt.sv[i1], su = bt.su[i1];
-      const double2* pp = P + (int64_t(s0) * bt.nb + band_of(bt, i1)) * bt.m2 + i2;
-      const int64_t pstep = int64_t(bt.nb) * bt.m2;
-#pragma unroll
-      for (int k = 0; k < LS; ++k)
-        if (k < len) {
-          const double2 p = __ldg(pp);
-          v[k] = fma(-su, p.y, fma(-sv, p.x, v[k]));
-          pp += pstep;
-        }
     }
   }
   __syncthreads();
@@ -1456,24 +1425,9 @@ bool pick_tile(F3Geom& g, size_t optin, size_t per_sm) {
   return best > 0.0;
 }
 
-BandTabs band_tabs_of(const F3Geom& g) {
-  BandTabs t;
-  const int m1 = int(g.m1);
-  t.lw = g.band_tab;
-  t.lid = g.band_tab + m1;
-  t.sv = g.band_tab + 2 * m1;
-  t.su = g.band_tab + 3 * m1;
-  t.ic = g.band_tab + 4 * m1;
-  t.nb = g.band_nb;
-  t.base = m1 / g.band_nb;
-  t.rem = m1 % g.band_nb;
-  t.m2 = int(g.m2);
-  return t;
-}
-
 template <typename T>
 void launch_col(double* G, T* coarse, double sign, const F3Geom& g, int axis, const double* w, const double* id,
-                const Exec& ex, const double2* P = nullptr) {
+                const Exec& ex) {
   int64_t stride, outer_stride, inner, ncols;
   int m;
   if (axis == 1) {
@@ -1499,16 +1453,9 @@ void launch_col(double* G, T* coarse, double sign, const F3Geom& g, int axis, co
     const int SY = (m + 2 * LS - 1) / (2 * LS);                                                          \
     MGRX_LAUNCH(ex, tag, pdl_launch(k_f3_col<T, LS, AP, MT>, dim3(blocks), dim3(32, SY),                      \
                                     size_t(2 * m + 2 * 2 * SY * 16) * 8, ex.s, !ex.prof, G, coarse, sign, ncols, m,       \
-                                    stride, outer_stride, inner, w, id, static_cast<const double2*>(nullptr),  \
-                                    BandTabs{}));                                                               \
+                                    stride, outer_stride, inner, w, id));                                       \
   }
-  if (P) {  // axis-0 pass after the band pass (m0 <= 264, apply)
-    const BandTabs bt = band_tabs_of(g);
-    const int SY = (m + 2 * 12 - 1) / (2 * 12);
-    MGRX_LAUNCH(ex, tag, pdl_launch(k_f3_col<T, 12, true, kColThreads12, true>, dim3(blocks), dim3(32, SY),
-                                    size_t(2 * m + 2 * 2 * SY * 16) * 8, ex.s, !ex.prof, G, coarse, sign, ncols, m,
-                                    stride, outer_stride, inner, w, id, P, bt));
-  } else if (m <= 264) {
+  if (m <= 264) {
     if (coarse) MGRX_COLL(12, true, kColThreads12) else MGRX_COLL(12, false, kColThreads12)
   } else if (m <= 320) {
     if (coarse) MGRX_COL(true, kColThreads) else MGRX_COL(false, kColThreads)
@@ -1517,196 +1464,6 @@ void launch_col(double* G, T* coarse, double sign, const F3Geom& g, int axis, co
   }
 #undef MGRX_COL
 #undef MGRX_COLL
-}
-
-// -------------------------------------------------------------- band pass
-// The axis-2 and axis-1 solves of G in ONE read + write of G (instead of the
-// row pass and the axis-1 column pass, a read + write each).  Axis 1 is cut
-// into nb bands of >= 32 rows; a CTA holds one band of one plane in shared
-// memory, solves its rows along axis 2 (the row pass's warp solve) and then
-// every column of the band along axis 1 with the band's OWN tridiagonal block
-// (the coupling to the neighbouring bands dropped).  The exact solution
-// differs from this local one by two "spikes" per band (the SPIKE
-// partitioning of a tridiagonal solve):
-//   x_r = xloc_r - sv_r * x(last row of the band above) - su_r * x(first row of the band below),
-// sv = T_b^-1 (e_first / 3), su = T_b^-1 (e_last / 3).  The spikes of this
-// diagonally dominant matrix decay by 2 - sqrt(3) = 0.268 per row, i.e. below
-// 2e-18 across a band of >= 32 rows, so each interface's two unknowns
-// decouple from the other interfaces to far below fp64 rounding:
-//   xL = (xloc_L - uL xloc_F) / (1 - uL vF),  xF = xloc_F - vF xL
-// (k_f3_iface, a few rows per plane), and the spike terms are added where the
-// axis-0 pass loads G (k_f3_col<BAND>): exact algebra, rounding-level
-// differences, like the segmented solves.
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-constexpr int kBandMaxRows = 64;
-
-template <int NC>
-__global__ void __launch_bounds__(32 * NC, NC <= 5 ? 4 : 3)
-    k_f3_band(double* __restrict__ G, int m1, int m2, const BandTabs bt, const double* __restrict__ w2,
-              const double* __restrict__ id2) {
-  extern __shared__ double bs[];
-  double* tw = bs;
-  double* tid = tw + m2;
-  double* lw = tid + m2;
-  double* lid = lw + kBandMaxRows;
-  double* X = lid + kBandMaxRows;
-  const int nb = bt.nb;
-  // bands from the last plane down (the plane pass wrote the high planes last)
-  const int blk = int(gridDim.x) - 1 - int(blockIdx.x);
-  const int plane = blk / nb, b = blk - plane * nb;
-  const int s = band_start(bt, b), nr = bt.base + (b < bt.rem ? 1 : 0);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int i = threadIdx.x; i < m2; i += blockDim.x) {
-    tw[i] = w2[i];
-    tid[i] = id2[i];
-  }
-  if (threadIdx.x < nr) {
-    lw[threadIdx.x] = bt.lw[s + threadIdx.x];
-    lid[threadIdx.x] = bt.lid[s + threadIdx.x];
-  }
-  pdl_wait();
-  double* Gp = G + (int64_t(plane) * m1 + s) * m2;
-  for (int r = warp; r < nr; r += nw) {
-    const double* src = Gp + int64_t(r) * m2 + lane;
-    double* dst = X + r * m2 + lane;
-#pragma unroll
-    for (int k = 0; k < NC; ++k)
-      if (lane + 32 * k < m2) cp_async8(dst + 32 * k, src + 32 * k);
-  }
-  cp_async_wait_all();
-  __syncthreads();  // tables + every lane's copies of the warp's rows
-  for (int r = warp; r < nr; r += nw) warp_row_thomas_reg<NC>(X + r * m2, m2, tw, tid);
-  __syncthreads();
-  if (int(threadIdx.x) < m2) {  // axis 1, this band's block only: one thread per column
-    double* x = X + threadIdx.x;
-    double y = x[0];
-#pragma unroll 4
-    for (int r = 1; r < nr; ++r) {
-      y = x[r * m2] - lw[r] * y;
-      x[r * m2] = y;
-    }
-    double z = y * lid[nr - 1];
-    x[(nr - 1) * m2] = z;
-#pragma unroll 4
-    for (int r = nr - 2; r >= 0; --r) {
-      z = (x[r * m2] - kOff * z) * lid[r];
-      x[r * m2] = z;
-    }
-  }
-  __syncthreads();
-  pdl_trigger();
-  const uint64_t pkeep = pol_keep();
-  for (int r = warp; r < nr; r += nw) {
-    double* dst = Gp + int64_t(r) * m2 + lane;
-    const double* src = X + r * m2 + lane;
-#pragma unroll
-    for (int k = 0; k < NC; ++k)
-      if (lane + 32 * k < m2) st_pol(dst + 32 * k, src[32 * k], pkeep);
-  }
-}
-
-// Interface values of the band pass: P[i0][b][i2] = (true x of the last row of
-// band b - 1, true x of the first row of band b + 1), zeros at the ends.
-__global__ void __launch_bounds__(256) k_f3_iface(const double* __restrict__ G, double2* __restrict__ P, int m0, int m1,
-                                                  const BandTabs bt) {
-  const int m2 = bt.m2, ni = bt.nb - 1;
-  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  pdl_wait();
-  if (idx >= int64_t(m0) * ni * m2) return;
-  const int i2 = int(idx % m2);
-  const int j = int((idx / m2) % ni);
-  const int64_t i0 = idx / (int64_t(m2) * ni);
-  const int e = band_start(bt, j + 1);
-  const double xl = G[(i0 * m1 + e - 1) * m2 + i2], xf = G[(i0 * m1 + e) * m2 + i2];
-  const double uL = bt.ic[3 * j], vF = bt.ic[3 * j + 1], inv = bt.ic[3 * j + 2];
-  const double XL = (xl - uL * xf) * inv;
-  const double XF = xf - vF * XL;
-  double2* Pp = P + (i0 * bt.nb) * m2 + i2;
-  Pp[int64_t(j + 1) * m2].x = XL;
-  Pp[int64_t(j) * m2].y = XF;
-  if (j == 0) Pp[0].x = 0.0;
-  if (j == ni - 1) Pp[int64_t(ni) * m2].y = 0.0;
-}
-
-// The band pass + the interface values (into P).
-static cudaError_t launch_band(double* G, double2* P, const F3Geom& g, const ThomasLevel& th, const Exec& ex) {
-  const BandTabs bt = band_tabs_of(g);
-  const int m1 = int(g.m1), m2 = int(g.m2), m0 = int(g.m0);
-  const int maxrows = bt.base + (bt.rem ? 1 : 0);
-  const size_t smem = size_t(2 * m2 + 2 * kBandMaxRows + maxrows * m2) * 8;
-  const unsigned grid = unsigned(m0 * bt.nb);
-  cudaError_t e;
-  if (m2 <= 160) {
-    e = cudaFuncSetAttribute(k_f3_band<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    MGRX_LAUNCH(ex, "f3_band", pdl_launch(k_f3_band<5>, dim3(grid), dim3(160), smem, ex.s, !ex.prof, G, m1, m2, bt,
-                                          th.w[2], th.inv_d[2]));
-  } else {
-    e = cudaFuncSetAttribute(k_f3_band<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    MGRX_LAUNCH(ex, "f3_band", pdl_launch(k_f3_band<9>, dim3(grid), dim3(288), smem, ex.s, !ex.prof, G, m1, m2, bt,
-                                          th.w[2], th.inv_d[2]));
-  }
-  const int64_t n = int64_t(m0) * (bt.nb - 1) * m2;
-  MGRX_LAUNCH(ex, "f3_iface", pdl_launch(k_f3_iface, dim3(unsigned((n + 255) / 256)), dim3(256), size_t(0), ex.s,
-                                         !ex.prof, static_cast<const double*>(G), P, m0, m1, bt));
-  return cudaGetLastError();
-}
-
-// Host tables of the band pass for an axis of m unknowns cut into nb bands
-// (the mass matrix of ThomasAux::build, transform.hpp:29-43: diagonal 2/3 at
-// both ends, 4/3 inside, off-diagonal 1/3): per row the band-local Thomas
-// factors and the two spikes, per interface uL, vF, 1 / (1 - uL vF).
-static std::vector<double> band_host_tables(int m, int nb) {
-  std::vector<double> t(size_t(4 * m + 3 * (nb - 1)), 0.0);
-  double *lw = t.data(), *lid = lw + m, *sv = lid + m, *su = sv + m, *ic = su + m;
-  const int base = m / nb, rem = m % nb;
-  auto start = [&](int b) { return b * base + std::min(b, rem); };
-  for (int b = 0; b < nb; ++b) {
-    const int s = start(b), n = start(b + 1) - s;
-    double dd = 0.0;
-    for (int r = 0; r < n; ++r) {
-      const double diag = (s + r == 0 || s + r == m - 1) ? kDiagB : kDiagI;
-      if (r == 0) {
-        lw[s] = 0.0;
-        dd = diag;
-      } else {
-        const double wi = kOff / dd;
-        lw[s + r] = wi;
-        dd = diag - wi * kOff;
-      }
-      lid[s + r] = 1.0 / dd;
-    }
-    auto solve = [&](std::vector<double>& x) {  // the kernel's band-local Thomas
-      for (int r = 1; r < n; ++r) x[r] -= lw[s + r] * x[r - 1];
-      x[n - 1] *= lid[s + n - 1];
-      for (int r = n - 2; r >= 0; --r) x[r] = (x[r] - kOff * x[r + 1]) * lid[s + r];
-    };
-    if (b > 0) {
-      std::vector<double> x(n, 0.0);
-      x[0] = kOff;
-      solve(x);
-      for (int r = 0; r < n; ++r) sv[s + r] = x[r];
-    }
-    if (b + 1 < nb) {
-      std::vector<double> x(n, 0.0);
-      x[n - 1] = kOff;
-      solve(x);
-      for (int r = 0; r < n; ++r) su[s + r] = x[r];
-    }
-  }
-  for (int j = 0; j + 1 < nb; ++j) {
-    const int e = start(j + 1);
-    const double uL = su[e - 1], vF = sv[e];
-    ic[3 * j] = uL;
-    ic[3 * j + 1] = vF;
-    ic[3 * j + 2] = 1.0 / (1.0 - uL * vF);
-  }
-  return t;
 }
 
 // Axis-2 then axis-1 solves of G: the row pass and the axis-1 column pass.
@@ -1783,24 +1540,6 @@ Fused3DPlan fused3d_plan(const LevelGeom& lg, int esize) {
   g.grid = g.units;  // one CTA per unit; the hardware scheduler balances
   fp.enabled = true;
   fp.scratch_bytes = size_t(g.m0) * g.m1 * g.m2 * 8 + 256;
-  // band pass (axis-2 + axis-1 solves in one read + write of G) on levels
-  // whose axis-1 lines cut into >= 4 bands of >= 32 rows and whose rows fit
-  // a 9-warp CTA; MGRX_NO_BAND keeps the separate row / column passes
-  static const bool no_band = std::getenv("MGRX_NO_BAND") != nullptr;
-  if (!no_band && g.m1 >= 128 && g.m1 <= 264 && g.m0 <= 264 && g.m2 >= 97 && g.m2 <= 288) {
-    const int nb = int(g.m1 / 32);
-    const std::vector<double> tabs = band_host_tables(int(g.m1), nb);
-    double* d = nullptr;
-    if (cudaMalloc(&d, tabs.size() * sizeof(double)) == cudaSuccess &&
-        cudaMemcpy(d, tabs.data(), tabs.size() * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess) {
-      g.band_nb = nb;
-      g.band_tab = d;  // lives as long as the plan cache (a few KB per level)
-      g.band_off = (fp.scratch_bytes + 255) / 256 * 256;
-      fp.scratch_bytes = g.band_off + size_t(g.m0) * nb * g.m2 * 16 + 256;
-    } else {
-      cudaGetLastError();
-    }
-  }
   return fp;
 }
 
@@ -1933,15 +1672,8 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
     e = cudaEventRecord(ex.after_plane, ex.s);
     if (e != cudaSuccess) return e;
   }
-  if (g.band_nb) {
-    double2* P = reinterpret_cast<double2*>(static_cast<char*>(scratch) + g.band_off);
-    e = launch_band(G, P, g, th, ex);
-    if (e != cudaSuccess) return e;
-    launch_col<T>(G, coarse, 1.0, g, 0, th.w[0], th.inv_d[0], ex, P);
-  } else {
-    row_col1(G, g, th, ex);
-    launch_col<T>(G, coarse, 1.0, g, 0, th.w[0], th.inv_d[0], ex);
-  }
+  row_col1(G, g, th, ex);
+  launch_col<T>(G, coarse, 1.0, g, 0, th.w[0], th.inv_d[0], ex);
   return cudaGetLastError();
 }
 
@@ -1972,12 +1704,7 @@ cudaError_t fused3d_recompose_correction(const T* shell, void* scratch, const Fu
     MGRX_LAUNCH(ex, "f3_rec_plane", pdl_launch(k_f3_rec_plane<T, 4, kPlaneMaxThreads, 3>, dim3(gd.grid),
                                                dim3(gd.threads), plane_smem3r<T>(gd), ex.s, !ex.prof, shell, G, gd));
   }
-  if (g.band_nb) {
-    e = launch_band(G, reinterpret_cast<double2*>(static_cast<char*>(scratch) + g.band_off), g, th, ex);
-    if (e != cudaSuccess) return e;
-  } else {
-    row_col1(G, g, th, ex);
-  }
+  row_col1(G, g, th, ex);
   return cudaGetLastError();
 }
 
@@ -1987,8 +1714,7 @@ cudaError_t fused3d_recompose_finish(const T* shell, T* coarse, T* fine, void* s
                                      const ThomasLevel& th, const Exec& ex) {
   const F3Geom& g = fp.g;
   double* G = static_cast<double*>(scratch);
-  launch_col<T>(G, coarse, -1.0, g, 0, th.w[0], th.inv_d[0], ex,
-                g.band_nb ? reinterpret_cast<const double2*>(static_cast<char*>(scratch) + g.band_off) : nullptr);
+  launch_col<T>(G, coarse, -1.0, g, 0, th.w[0], th.inv_d[0], ex);
   cudaError_t e = launch_interp<T>(shell, coarse, fine, g, ex);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

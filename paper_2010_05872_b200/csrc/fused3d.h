@@ -31,11 +31,6 @@ struct F3Geom {
   // (the even planes' region and the odd planes' region of a rank are two
   // separate runs of the level-centric buffer); 0 = one global buffer
   int64_t odd_shift = 0;
-  // band pass (fused3d.cu, "band pass"): the axis-2 and axis-1 solves of G in
-  // one read + write; 0 = separate row and column passes
-  int band_nb = 0;                   // bands along axis 1 (0: off)
-  const double* band_tab = nullptr;  // device tables of the band pass (lw, lid, sv, su: m1 each; then 3 per interface)
-  size_t band_off = 0;               // byte offset of the interface values P inside the level's scratch
 };
 
 struct Fused3DPlan {
