@@ -1085,9 +1085,8 @@ static void decompose_quantize_impl(mgrx_gpu_ctx* c, Plan& p, const T* d_field, 
     if (used) {
       cudaStream_t sd = c->side[0];
       cuda_check(cudaStreamWaitEvent(sd, c->lvl_done[L], 0), "cudaStreamWaitEvent");
-      static const int resident = std::getenv("MGRX_QOV_CTAS") ? std::atoi(std::getenv("MGRX_QOV_CTAS")) : 0;
       cuda_check(quantize_labels_range<T>(d_coeffs, d_labels, qt.counts, qt.flags, ql, split, qt.nch,
-                                          exec_on(c, sd, L), resident),
+                                          exec_on(c, sd, L)),
                  "quantize finest shell");
       cuda_check(cudaEventRecord(c->lvl_done[0], sd), "cudaEventRecord");
       cuda_check(cudaStreamWaitEvent(c->stream, c->lvl_done[0], 0), "cudaStreamWaitEvent");

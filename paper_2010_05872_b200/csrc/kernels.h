@@ -85,8 +85,7 @@ cudaError_t quantize_pass2(const T* c, const uint32_t* chunk_counts, const uint6
 int64_t quant_chunk_of(const QuantLevels& ql, int64_t pos);
 template <typename T>
 cudaError_t quantize_labels_range(const T* c, int32_t* labels, uint32_t* chunk_counts, int* flags,
-                                  const QuantLevels& ql, int64_t chunk_begin, int64_t chunk_end, const Exec& ex,
-                                  int resident_ctas = 0);  // > 0: that many CTAs loop over the chunks
+                                  const QuantLevels& ql, int64_t chunk_begin, int64_t chunk_end, const Exec& ex);
 cudaError_t quantize_scan(const uint32_t* chunk_counts, uint64_t* offsets, const QuantLevels& ql, const Exec& ex);
 template <typename T>
 cudaError_t dequantize_range(const int32_t* labels, const uint64_t* opos, const T* oval, uint64_t n_out, T* c,

@@ -153,23 +153,6 @@ __global__ void __launch_bounds__(kQBlock, 4) k_quant_labels(const T* __restrict
   quant_chunk<T>(c, labels, chunk_counts, flags, ql, chunk_begin + int64_t(blockIdx.x), warp_sums);
 }
 
-// The same over chunks chunk_begin + blockIdx.x, + gridDim.x, ... : a small
-// resident grid that trickles through the finest shell beside the
-// decomposition's remaining passes (decompose_quantize) instead of flooding
-// every SM.
-template <typename T>
-__global__ void __launch_bounds__(kQBlock, 4) k_quant_labels_loop(const T* __restrict__ c,
-                                                                  int32_t* __restrict__ labels,
-                                                                  uint32_t* __restrict__ chunk_counts,
-                                                                  int* __restrict__ flags, const QuantLevels ql,
-                                                                  const int64_t chunk_begin, const int64_t chunk_end) {
-  __shared__ int warp_sums[kQBlock / 32];
-  for (int64_t ch = chunk_begin + int64_t(blockIdx.x); ch < chunk_end; ch += gridDim.x) {
-    quant_chunk<T>(c, labels, chunk_counts, flags, ql, ch, warp_sums);
-    __syncthreads();  // warp_sums is reused
-  }
-}
-
 // Exclusive scan of the chunk counts in one CTA; offsets[nchunks] = total.
 // The counts are staged in (dynamic) shared memory with one round of
 // coalesced loads per tile of up to kScanMax; thread t scans its contiguous
@@ -361,16 +344,10 @@ int64_t quant_chunk_of(const QuantLevels& ql, int64_t pos) { return (pos - ql.ba
 // as that shell is final).
 template <typename T>
 cudaError_t quantize_labels_range(const T* c, int32_t* labels, uint32_t* chunk_counts, int* flags,
-                                  const QuantLevels& ql, int64_t chunk_begin, int64_t chunk_end, const Exec& ex,
-                                  int resident_ctas) {
-  if (chunk_end > chunk_begin) {
-    if (resident_ctas > 0 && chunk_end - chunk_begin > resident_ctas)
-      MGRX_LAUNCH(ex, "quant_labels", k_quant_labels_loop<T><<<unsigned(resident_ctas), kQBlock, 0, ex.s>>>(
-                                          c, labels, chunk_counts, flags, ql, chunk_begin, chunk_end));
-    else
-      MGRX_LAUNCH(ex, "quant_labels", k_quant_labels<T><<<unsigned(chunk_end - chunk_begin), kQBlock, 0, ex.s>>>(
-                                          c, labels, chunk_counts, flags, ql, chunk_begin));
-  }
+                                  const QuantLevels& ql, int64_t chunk_begin, int64_t chunk_end, const Exec& ex) {
+  if (chunk_end > chunk_begin)
+    MGRX_LAUNCH(ex, "quant_labels", k_quant_labels<T><<<unsigned(chunk_end - chunk_begin), kQBlock, 0, ex.s>>>(
+                                        c, labels, chunk_counts, flags, ql, chunk_begin));
   return cudaGetLastError();
 }
 
@@ -442,7 +419,7 @@ cudaError_t dequantize_range(const int32_t* labels, const uint64_t* opos, const 
   template cudaError_t dequantize_run<T>(const int32_t*, const uint64_t*, const T*, uint64_t, T*,            \
                                          const QuantLevels&, const Exec&);                                  \
   template cudaError_t quantize_labels_range<T>(const T*, int32_t*, uint32_t*, int*, const QuantLevels&,     \
-                                                int64_t, int64_t, const Exec&, int);                           \
+                                                int64_t, int64_t, const Exec&);                                \
   template cudaError_t dequantize_range<T>(const int32_t*, const uint64_t*, const T*, uint64_t, T*,          \
                                            const QuantLevels&, int64_t, int64_t, const Exec&);
 MGRX_INST(float)

@@ -5,4 +5,4 @@ mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/g_tests.log
 timeout 300 python bench.py --steps 10 --warmup 3 > gpurun_out/g_bench.log 2>&1
-for p in 0 1; do MGRX_P2=$p timeout 300 python tools/tools_levels.py > gpurun_out/g_levels_p2_$p.log 2>&1; done
+timeout 300 python tools/tools_levels.py > gpurun_out/g_levels.log 2>&1
