@@ -136,6 +136,33 @@ void thomas_aux(int64_t m, double* w, double* inv_d) {
   }
 }
 
+// End-correction tables of the Toeplitz solves (fused3d.cu "Toeplitz
+// solves"): with the constant factors w' = kTw, 1/d' = kTid the matrix
+// T' = L' U' equals the correction matrix T except T'(0,0) = d' (T: 2/3) and
+// T'(m-1,m-1) = w'/3 + d' (T: 2/3), so T = T' - a e_0 e_0^T - b e_l e_l^T and
+// x = z + z_0 Gt + z_{m-1} Ht with z = T'^-1 f, Gt = a g / (1 - a g_0),
+// Ht = b h / (1 - b h_{m-1}), g = T'^-1 e_0, h = T'^-1 e_{m-1} (the two ends
+// decouple for m >= kToepMinM).  out: Gt[0..32) from the first row on,
+// Ht[0..32) from the last row backwards.  Extended precision on the host.
+void toeplitz_end_tables(int64_t m, double* out) {
+  typedef long double ld;
+  const ld w = ld(kTw), id = ld(kTid), d = 1.0L / id, o = ld(kOff);
+  const ld a = d - ld(kDiagB), b = w * o + d - ld(kDiagB);
+  const int64_t n = std::max<int64_t>(m, 2);
+  std::vector<ld> y(n), g(n), h(n);
+  y[0] = 1.0L;
+  for (int64_t i = 1; i < n; ++i) y[i] = -w * y[i - 1];
+  g[n - 1] = y[n - 1] * id;
+  for (int64_t i = n - 2; i >= 0; --i) g[i] = (y[i] - o * g[i + 1]) * id;
+  h[n - 1] = id;
+  for (int64_t i = n - 2; i >= 0; --i) h[i] = -o * id * h[i + 1];
+  const ld ca = a / (1.0L - a * g[0]), cb = b / (1.0L - b * h[n - 1]);
+  for (int k = 0; k < kToepEnds; ++k) {
+    out[k] = k < n ? double(ca * g[k]) : 0.0;
+    out[kToepEnds + k] = k < n ? double(cb * h[n - 1 - k]) : 0.0;
+  }
+}
+
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 // ------------------------------------------------------------------ plan
@@ -345,8 +372,9 @@ Plan* get_plan(mgrx_gpu_ctx* c, int dtype, int nd, const uint64_t* dims, int lev
     for (int a = 0; a < nd; ++a) {
       const int64_t m = h.dims[l - 1][a];
       starts.push_back(host.size());
-      host.resize(host.size() + 2 * size_t(m));
+      host.resize(host.size() + 2 * size_t(m) + 2 * kToepEnds);  // w | inv_d | Toeplitz end corrections
       thomas_aux(m, host.data() + starts.back(), host.data() + starts.back() + m);
+      toeplitz_end_tables(m, host.data() + starts.back() + 2 * m);
     }
   }
   if (!host.empty()) {

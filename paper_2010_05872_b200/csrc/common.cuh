@@ -19,6 +19,13 @@ constexpr int kNumSMs = 148;
 constexpr double kOff = 1.0 / 3.0;
 constexpr double kDiagB = 2.0 / 3.0;
 constexpr double kDiagI = 4.0 / 3.0;
+// Toeplitz form of the correction solves (fused3d.cu "Toeplitz solves"): the
+// limit of the ThomasAux factors, w = 2 - sqrt(3) (w^2 - 4 w + 1 = 0) and
+// 1 / d with d = 4/3 - w / 3.
+constexpr double kTw = 2.0 - 1.7320508075688772;
+constexpr double kTid = 1.0 / (kDiagI - kTw * kOff);
+constexpr int kToepEnds = 32;   // end-correction entries per side
+constexpr int kToepMinM = 40;   // shortest line solved this way (the two ends decouple below 1e-22)
 constexpr double kW12 = 1.0 / 12.0;
 constexpr double kW5_12 = 5.0 / 12.0;
 constexpr double kW5_6 = 5.0 / 6.0;

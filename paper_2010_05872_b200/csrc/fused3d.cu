@@ -474,6 +474,106 @@ __device__ __forceinline__ void warp_row_thomas_reg(double* x, int m, const doub
   __syncwarp();
 }
 
+// ------------------------------------------------------- Toeplitz solves
+// The correction matrix tridiag(1/3; 2/3, 4/3 ... 4/3, 2/3; 1/3) is Toeplitz
+// except for its two corner entries, and the ThomasAux factors converge to
+// the constants w = 2 - sqrt(3), 1/d = 1/(4/3 - w/3) within ~16 rows.  Solve
+// with the CONSTANT factors (the matrix T' = L' U' equals T except
+// T'(0,0) = d and T'(m-1,m-1) = 4/3) and correct the two ends
+// (Sherman-Morrison): x = z + z_0 Gt + z_{m-1} Ht, z = T'^-1 f, where Gt / Ht
+// (host tables, api.cu:toeplitz_end_tables) decay by w per row from their end
+// — 32 entries each reach 2e-18 — and the ends decouple for m >= 40.  Exact
+// algebra, rounding-level differences from batched_solve
+// (transform.hpp:116-130), like the segmented solves; no factor tables are
+// read in the recurrences and every segment's affine map has the same
+// multiplier, so the scans move one value instead of two.
+template <int N>
+struct PowTab {
+  double v[N + 1];
+  constexpr PowTab(double x) : v() {
+    v[0] = 1.0;
+    for (int i = 1; i <= N; ++i) v[i] = v[i - 1] * x;
+  }
+};
+constexpr double kTc = kOff * kTid;  // back-substitution multiplier
+
+// Row x[0..m) in shared memory by one warp: lane = SEG consecutive values
+// (zero past the end), carries by a shuffle scan of one value per lane.
+template <int SEG>
+__device__ __forceinline__ void warp_row_toep(double* x, int m, const double* __restrict__ gt,
+                                              const double* __restrict__ ht) {
+  constexpr PowTab<SEG> PF(-kTw), PB(-kTc);
+  const int lane = threadIdx.x & 31;
+  const int s0 = lane * SEG;
+  double v[SEG];
+#pragma unroll
+  for (int k = 0; k < SEG; ++k) v[k] = (s0 + k < m) ? x[s0 + k] : 0.0;
+  // forward y_i = f_i - w y_{i-1} from a zero carry
+  double a = 0.0;
+#pragma unroll
+  for (int k = 0; k < SEG; ++k) {
+    a = v[k] - kTw * a;
+    v[k] = a;
+  }
+  {
+    double b = PF.v[SEG];  // (-w)^SEG, squared at every doubling step
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const double o = __shfl_up_sync(0xffffffffu, a, off);
+      if (lane >= off) a = a + b * o;
+      b = b * b;
+    }
+  }
+  double c = __shfl_up_sync(0xffffffffu, a, 1);
+  if (lane == 0) c = 0.0;
+#pragma unroll
+  for (int k = 0; k < SEG; ++k) v[k] = (s0 + k < m) ? v[k] + PF.v[k + 1] * c : 0.0;  // zero past the end again
+  // back substitution z_i = (y_i - z_{i+1} / 3) / d from a zero carry
+  double g = 0.0;
+#pragma unroll
+  for (int k = SEG - 1; k >= 0; --k) {
+    g = (v[k] - kOff * g) * kTid;
+    v[k] = g;
+  }
+  {
+    double b = PB.v[SEG];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const double o = __shfl_down_sync(0xffffffffu, g, off);
+      if (lane + off < 32) g = g + b * o;
+      b = b * b;
+    }
+  }
+  double z = __shfl_down_sync(0xffffffffu, g, 1);
+  if (lane == 31) z = 0.0;
+#pragma unroll
+  for (int k = 0; k < SEG; ++k) v[k] = v[k] + PB.v[SEG - k] * z;
+  // end corrections
+  const int last = m - 1;
+  double zl = 0.0;
+#pragma unroll
+  for (int k = 0; k < SEG; ++k)
+    if (s0 + k == last) zl = v[k];
+  const double z0 = __shfl_sync(0xffffffffu, v[0], 0);
+  const double zm = __shfl_sync(0xffffffffu, zl, last / SEG);
+  if (s0 < kToepEnds) {
+#pragma unroll
+    for (int k = 0; k < SEG; ++k)
+      if (s0 + k < kToepEnds) v[k] = v[k] + z0 * gt[s0 + k];
+  }
+  if (s0 + SEG > m - kToepEnds) {
+#pragma unroll
+    for (int k = 0; k < SEG; ++k) {
+      const int rev = last - (s0 + k);
+      if (rev >= 0 && rev < kToepEnds) v[k] = v[k] + zm * ht[rev];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < SEG; ++k)
+    if (s0 + k < m) x[s0 + k] = v[k];
+  __syncwarp();
+}
+
 // L0 (axis-0 load-vector restriction) on registers: the coarse planes
 // k-1, k, k+1 around fine plane p (k = p/2) accumulate the plane's
 // restricted rows Q in stencil order (load_entry, transform.hpp:84-96);
@@ -1201,7 +1301,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kPlaneMaxThreads ? 3 : 1)
 // pass is bound by HBM latency x bytes in flight, not by the solve).
 __host__ __device__ constexpr int kRowCtas(int nc) { return nc <= 5 ? 4 : (nc <= 9 ? 3 : (nc <= 17 ? 2 : 1)); }
 
-template <int NC>
+template <int NC, bool TOEP = false>
 __global__ void __launch_bounds__(256, kRowCtas(NC)) k_f3_row(double* __restrict__ G, int64_t rows, int m,
                                                 const double* __restrict__ w, const double* __restrict__ inv_d) {
   extern __shared__ double rs[];
@@ -1209,9 +1309,13 @@ __global__ void __launch_bounds__(256, kRowCtas(NC)) k_f3_row(double* __restrict
   double* tid = rs + m;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   double* buf = tid + m + warp * m;
-  for (int i = threadIdx.x; i < m; i += blockDim.x) {
-    tw[i] = w[i];
-    tid[i] = inv_d[i];
+  if (TOEP) {  // only the end-correction tables (they follow inv_d: api.cu get_plan)
+    for (int i = threadIdx.x; i < 2 * kToepEnds; i += blockDim.x) tw[i] = inv_d[m + i];
+  } else {
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      tw[i] = w[i];
+      tid[i] = inv_d[i];
+    }
   }
   __syncthreads();
   pdl_wait();
@@ -1234,7 +1338,8 @@ __global__ void __launch_bounds__(256, kRowCtas(NC)) k_f3_row(double* __restrict
       if (lane + 32 * k < m) buf[lane + 32 * k] = t[k];
     __syncwarp();
     if (r + step < rows) load(r + step);
-    warp_row_thomas_reg<NC>(buf, m, tw, tid);
+    if (TOEP) warp_row_toep<NC>(buf, m, tw, tw + kToepEnds);
+    else warp_row_thomas_reg<NC>(buf, m, tw, tid);
     double* gr = G + (rows - 1 - r) * m;
 #pragma unroll
     for (int k = 0; k < NC; ++k)
@@ -1243,7 +1348,13 @@ __global__ void __launch_bounds__(256, kRowCtas(NC)) k_f3_row(double* __restrict
   }
 }
 
-void launch_row(double* G, const F3Geom& g, const double* w, const double* id, const Exec& ex) {
+// MGRX_NO_TOEP keeps the table-driven Thomas solves (A/B switch)
+bool toep_enabled() {
+  static const bool off = std::getenv("MGRX_NO_TOEP") != nullptr;
+  return !off;
+}
+
+void launch_row(double* G, const F3Geom& g, const double* w, const double* id, const Exec& ex, bool toep = false) {
   const int m = int(g.m2);
   const int64_t rows = g.m0 * g.m1;
   const int threads = 256;
@@ -1255,9 +1366,15 @@ void launch_row(double* G, const F3Geom& g, const double* w, const double* id, c
   const int64_t blocks = std::min<int64_t>((rows + 7) / 8, int64_t(kNumSMs) * kRowCtas(nc));
 #define ROW_(NC)                                                                                           \
   do {                                                                                                     \
-    cudaFuncSetAttribute(k_f3_row<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));            \
-    MGRX_LAUNCH(ex, "f3_row",                                                                              \
-                pdl_launch(k_f3_row<NC>, dim3(unsigned(blocks)), dim3(threads), smem, ex.s, !ex.prof, G, rows, m, w, id)); \
+    if (toep && m >= kToepMinM) {                                                                          \
+      cudaFuncSetAttribute(k_f3_row<NC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));    \
+      MGRX_LAUNCH(ex, "f3_row", pdl_launch(k_f3_row<NC, true>, dim3(unsigned(blocks)), dim3(threads), smem, ex.s, \
+                                           !ex.prof, G, rows, m, w, id));                                  \
+    } else {                                                                                               \
+      cudaFuncSetAttribute(k_f3_row<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));          \
+      MGRX_LAUNCH(ex, "f3_row", pdl_launch(k_f3_row<NC>, dim3(unsigned(blocks)), dim3(threads), smem, ex.s, \
+                                           !ex.prof, G, rows, m, w, id));                                  \
+    }                                                                                                      \
   } while (0)
   if (nc <= 1) ROW_(1);
   else if (nc <= 3) ROW_(3);
@@ -1376,6 +1493,114 @@ __global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : (MAXT == kColT
   }
 }
 
+// The column pass in Toeplitz form (see "Toeplitz solves"): segments of
+// exactly LS values (zero past the end), no factor tables in the recurrences,
+// one folded value per segment; the two end corrections need the column's
+// z_0 and z_{m-1}, passed through shared memory.
+template <typename T, int LS, bool APPLY, int MAXT>
+__global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : (MAXT == kColThreads12 ? 3 : 1))
+    k_f3_col_toep(double* __restrict__ G, T* __restrict__ coarse, double sign, int64_t ncols, int m, int64_t stride,
+                  int64_t outer_stride, int64_t inner, const double* __restrict__ gh) {
+  constexpr PowTab<LS> PF(-kTw), PB(-kTc);
+  extern __shared__ double sc[];
+  const int lane = threadIdx.x, S = 2 * blockDim.y;
+  const int c16 = lane & 15, s = 2 * threadIdx.y + (lane >> 4);
+  double* gt = sc;               // [kToepEnds]
+  double* ht = sc + kToepEnds;   // [kToepEnds]
+  double* A = ht + kToepEnds;    // [S][16]
+  double* E = A + S * 16;        // [2][16]: z_0 and z_{m-1} of the 16 columns
+  for (int i = threadIdx.y * 32 + lane; i < 2 * kToepEnds; i += blockDim.y * 32) sc[i] = gh[i];
+  const int64_t col = int64_t(gridDim.x - 1 - blockIdx.x) * 16 + c16;
+  const bool valid = col < ncols;
+  const int64_t base = valid ? (col / inner) * outer_stride + (col % inner) : 0;
+  const int s0 = s * LS;
+  const int len = max(0, min(m, s0 + LS) - s0);
+  double v[LS];
+  pdl_wait();
+  {
+    const double* gp = G + base + int64_t(s0) * stride;
+#pragma unroll
+    for (int k = 0; k < LS; ++k) {
+      v[k] = (valid && k < len) ? (APPLY ? __ldcs(gp) : *gp) : 0.0;
+      gp += stride;
+    }
+  }
+  // forward from a zero carry; v[k] keeps the zero-carry values
+  double a = 0.0;
+#pragma unroll
+  for (int k = 0; k < LS; ++k) {
+    a = v[k] - kTw * a;
+    v[k] = a;
+  }
+  A[s * 16 + c16] = a;
+  __syncthreads();
+  double y = 0.0;
+  for (int q = 0; q < s; ++q) y = A[q * 16 + c16] + PF.v[LS] * y;
+#pragma unroll
+  for (int k = 0; k < LS; ++k) v[k] = (k < len) ? v[k] + PF.v[k + 1] * y : 0.0;
+  // back substitution from a zero carry
+  double g = 0.0;
+#pragma unroll
+  for (int k = LS - 1; k >= 0; --k) {
+    g = (v[k] - kOff * g) * kTid;
+    v[k] = g;
+  }
+  __syncthreads();  // the forward folds have read A
+  A[s * 16 + c16] = g;
+  __syncthreads();
+  double z = 0.0;
+  for (int q = S - 1; q > s; --q) z = A[q * 16 + c16] + PB.v[LS] * z;
+#pragma unroll
+  for (int k = 0; k < LS; ++k) v[k] = v[k] + PB.v[LS - k] * z;
+  // end corrections: x = z + z_0 Gt + z_{m-1} Ht
+  const int last = m - 1;
+  if (s == 0) E[c16] = v[0];
+  if (s == last / LS) {
+    double zl = 0.0;
+#pragma unroll
+    for (int k = 0; k < LS; ++k)
+      if (s0 + k == last) zl = v[k];
+    E[16 + c16] = zl;
+  }
+  __syncthreads();
+  if (s0 < kToepEnds) {
+    const double z0 = E[c16];
+#pragma unroll
+    for (int k = 0; k < LS; ++k)
+      if (s0 + k < kToepEnds) v[k] = v[k] + z0 * gt[s0 + k];
+  }
+  if (s0 + LS > m - kToepEnds) {
+    const double zm = E[16 + c16];
+#pragma unroll
+    for (int k = 0; k < LS; ++k) {
+      const int rev = last - (s0 + k);
+      if (rev >= 0 && rev < kToepEnds) v[k] = v[k] + zm * ht[rev];
+    }
+  }
+  pdl_trigger();
+  if (!valid) return;
+  if (APPLY) {  // coarse values loaded only now, four at a time: fewer live registers
+    T* c = coarse + base + int64_t(s0) * stride;
+#pragma unroll
+    for (int k0 = 0; k0 < LS; k0 += 4) {
+      T cv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cv[u] = (k0 + u < LS && k0 + u < len) ? c[int64_t(k0 + u) * stride] : T(0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k0 + u < LS && k0 + u < len) c[int64_t(k0 + u) * stride] = to_t<T>(double(cv[u]) + sign * v[k0 + u]);
+    }
+  } else {
+    double* gp = G + base + int64_t(s0) * stride;
+    const uint64_t pol = pol_keep();
+#pragma unroll
+    for (int k = 0; k < LS; ++k) {
+      if (k < len) st_pol(gp, v[k], pol);
+      gp += stride;
+    }
+  }
+}
+
 // ------------------------------------------------------------ host side
 
 template <typename T, int TI1>
@@ -1427,7 +1652,7 @@ bool pick_tile(F3Geom& g, size_t optin, size_t per_sm) {
 
 template <typename T>
 void launch_col(double* G, T* coarse, double sign, const F3Geom& g, int axis, const double* w, const double* id,
-                const Exec& ex) {
+                const Exec& ex, bool toep = false) {
   int64_t stride, outer_stride, inner, ncols;
   int m;
   if (axis == 1) {
@@ -1455,7 +1680,22 @@ void launch_col(double* G, T* coarse, double sign, const F3Geom& g, int axis, co
                                     size_t(2 * m + 2 * 2 * SY * 16) * 8, ex.s, !ex.prof, G, coarse, sign, ncols, m,       \
                                     stride, outer_stride, inner, w, id));                                       \
   }
-  if (m <= 264) {
+#define MGRX_COLT(LS, AP, MT)                                                                            \
+  {                                                                                                       \
+    const int SY = (m + 2 * LS - 1) / (2 * LS);                                                          \
+    MGRX_LAUNCH(ex, tag, pdl_launch(k_f3_col_toep<T, LS, AP, MT>, dim3(blocks), dim3(32, SY),             \
+                                    size_t(2 * kToepEnds + 2 * SY * 16 + 32) * 8, ex.s, !ex.prof, G, coarse, sign, \
+                                    ncols, m, stride, outer_stride, inner, id + m));                      \
+  }
+  if (toep && m >= kToepMinM) {  // the end-correction tables follow inv_d (api.cu get_plan)
+    if (m <= 264) {
+      if (coarse) MGRX_COLT(12, true, kColThreads12) else MGRX_COLT(12, false, kColThreads12)
+    } else if (m <= 320) {
+      if (coarse) MGRX_COLT(16, true, kColThreads) else MGRX_COLT(16, false, kColThreads)
+    } else {
+      if (coarse) MGRX_COLT(16, true, 2 * kColThreads) else MGRX_COLT(16, false, 2 * kColThreads)
+    }
+  } else if (m <= 264) {
     if (coarse) MGRX_COLL(12, true, kColThreads12) else MGRX_COLL(12, false, kColThreads12)
   } else if (m <= 320) {
     if (coarse) MGRX_COL(true, kColThreads) else MGRX_COL(false, kColThreads)
@@ -1464,12 +1704,13 @@ void launch_col(double* G, T* coarse, double sign, const F3Geom& g, int axis, co
   }
 #undef MGRX_COL
 #undef MGRX_COLL
+#undef MGRX_COLT
 }
 
 // Axis-2 then axis-1 solves of G: the row pass and the axis-1 column pass.
 static void row_col1(double* G, const F3Geom& g, const ThomasLevel& th, const Exec& ex) {
-  launch_row(G, g, th.w[2], th.inv_d[2], ex);
-  launch_col<float>(G, static_cast<float*>(nullptr), 0.0, g, 1, th.w[1], th.inv_d[1], ex);
+  launch_row(G, g, th.w[2], th.inv_d[2], ex, toep_enabled());
+  launch_col<float>(G, static_cast<float*>(nullptr), 0.0, g, 1, th.w[1], th.inv_d[1], ex, toep_enabled());
 }
 
 }  // namespace
@@ -1673,7 +1914,7 @@ cudaError_t fused3d_decompose_level(const T* blk, T* shell, T* coarse, void* scr
     if (e != cudaSuccess) return e;
   }
   row_col1(G, g, th, ex);
-  launch_col<T>(G, coarse, 1.0, g, 0, th.w[0], th.inv_d[0], ex);
+  launch_col<T>(G, coarse, 1.0, g, 0, th.w[0], th.inv_d[0], ex, toep_enabled());
   return cudaGetLastError();
 }
 
@@ -1714,7 +1955,7 @@ cudaError_t fused3d_recompose_finish(const T* shell, T* coarse, T* fine, void* s
                                      const ThomasLevel& th, const Exec& ex) {
   const F3Geom& g = fp.g;
   double* G = static_cast<double*>(scratch);
-  launch_col<T>(G, coarse, -1.0, g, 0, th.w[0], th.inv_d[0], ex);
+  launch_col<T>(G, coarse, -1.0, g, 0, th.w[0], th.inv_d[0], ex, toep_enabled());
   cudaError_t e = launch_interp<T>(shell, coarse, fine, g, ex);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
@@ -1818,8 +2059,8 @@ cudaError_t fused3d_slab_inplane(double* G, const Fused3DPlan& fp, const ThomasL
   F3Geom gs = fp.g;
   gs.m0 = k1 - k0;
   double* Gs = G + k0 * fp.g.m1 * fp.g.m2;
-  launch_row(Gs, gs, th.w[2], th.inv_d[2], ex);
-  launch_col<float>(Gs, static_cast<float*>(nullptr), 0.0, gs, 1, th.w[1], th.inv_d[1], ex);
+  launch_row(Gs, gs, th.w[2], th.inv_d[2], ex, toep_enabled());
+  launch_col<float>(Gs, static_cast<float*>(nullptr), 0.0, gs, 1, th.w[1], th.inv_d[1], ex, toep_enabled());
   return cudaGetLastError();
 }
 
@@ -1865,7 +2106,7 @@ cudaError_t fused3d_slab_axis0(double* Gt, int64_t width, const Fused3DPlan& fp,
   F3Geom gs = fp.g;
   gs.m1 = 1;
   gs.m2 = width;
-  launch_col<float>(Gt, static_cast<float*>(nullptr), 0.0, gs, 0, th.w[0], th.inv_d[0], ex);
+  launch_col<float>(Gt, static_cast<float*>(nullptr), 0.0, gs, 0, th.w[0], th.inv_d[0], ex, toep_enabled());
   return cudaGetLastError();
 }
 
