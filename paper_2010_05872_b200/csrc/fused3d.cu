@@ -1348,9 +1348,68 @@ __global__ void __launch_bounds__(256, kRowCtas(NC)) k_f3_row(double* __restrict
   }
 }
 
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Row pass in Toeplitz form with a deeper prefetch: every warp owns a ring of
+// kRowRing row buffers filled by cp.async (8-byte copies: rows are only
+// 8-byte aligned), two rows in flight while one is solved; no registers are
+// spent on the prefetch.
+constexpr int kRowRing = 3;
+template <int NC>
+__global__ void __launch_bounds__(256, kRowCtas(NC)) k_f3_row_ring(double* __restrict__ G, int64_t rows, int m,
+                                                                    const double* __restrict__ gh) {
+  extern __shared__ double rs[];
+  double* gt = rs;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double* ring = rs + 2 * kToepEnds + size_t(warp) * kRowRing * m;
+  for (int i = threadIdx.x; i < 2 * kToepEnds; i += blockDim.x) gt[i] = gh[i];
+  __syncthreads();
+  pdl_wait();
+  const int64_t step = int64_t(gridDim.x) * nw;
+  const int64_t r0 = int64_t(blockIdx.x) * nw + warp;
+  const uint64_t pkeep = pol_keep();
+  // rows are walked from the last one down (the producer wrote the high planes last)
+  auto issue = [&](int64_t rr, int slot) {
+    if (rr < rows) {
+      const double* gr = G + (rows - 1 - rr) * m + lane;
+      double* dst = ring + slot * m + lane;
+#pragma unroll
+      for (int k = 0; k < NC; ++k)
+        if (lane + 32 * k < m) cp_async8(dst + 32 * k, gr + 32 * k);
+    }
+    cp_async_commit();  // a group per step, empty past the end
+  };
+  issue(r0, 0);
+  issue(r0 + step, 1);
+  int slot = 0;
+  for (int64_t r = r0; r < rows; r += step) {
+    issue(r + 2 * step, (slot + 2) % kRowRing);
+    cp_async_wait<2>();
+    __syncwarp();
+    double* buf = ring + slot * m;
+    warp_row_toep<NC>(buf, m, gt, gt + kToepEnds);
+    double* gr = G + (rows - 1 - r) * m;
+#pragma unroll
+    for (int k = 0; k < NC; ++k)
+      if (lane + 32 * k < m) st_pol(gr + lane + 32 * k, buf[lane + 32 * k], pkeep);
+    __syncwarp();
+    slot = (slot + 1) % kRowRing;
+  }
+}
+
 // MGRX_NO_TOEP keeps the table-driven Thomas solves (A/B switch)
 bool toep_enabled() {
   static const bool off = std::getenv("MGRX_NO_TOEP") != nullptr;
+  return !off;
+}
+
+bool ring_enabled() {
+  static const bool off = std::getenv("MGRX_NO_ROW_RING") != nullptr;
   return !off;
 }
 
@@ -1366,7 +1425,12 @@ void launch_row(double* G, const F3Geom& g, const double* w, const double* id, c
   const int64_t blocks = std::min<int64_t>((rows + 7) / 8, int64_t(kNumSMs) * kRowCtas(nc));
 #define ROW_(NC)                                                                                           \
   do {                                                                                                     \
-    if (toep && m >= kToepMinM) {                                                                          \
+    if (toep && m >= kToepMinM && ring_enabled()) {                                                        \
+      const size_t rsm = size_t(2 * kToepEnds + (threads / 32) * kRowRing * m) * 8;                        \
+      cudaFuncSetAttribute(k_f3_row_ring<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rsm));      \
+      MGRX_LAUNCH(ex, "f3_row", pdl_launch(k_f3_row_ring<NC>, dim3(unsigned(blocks)), dim3(threads), rsm, ex.s, \
+                                           !ex.prof, G, rows, m, id + m));                                 \
+    } else if (toep && m >= kToepMinM) {                                                                   \
       cudaFuncSetAttribute(k_f3_row<NC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));    \
       MGRX_LAUNCH(ex, "f3_row", pdl_launch(k_f3_row<NC, true>, dim3(unsigned(blocks)), dim3(threads), smem, ex.s, \
                                            !ex.prof, G, rows, m, w, id));                                  \
