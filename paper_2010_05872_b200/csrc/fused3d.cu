@@ -2139,12 +2139,12 @@ cudaError_t f3_axis_solve(double* y, int64_t outer, int64_t m, int64_t inner, co
     g.m0 = outer;
     g.m1 = 1;
     g.m2 = m;
-    launch_row(y, g, w, id, ex);
+    launch_row(y, g, w, id, ex, toep_enabled());
   } else {
     g.m0 = outer;
     g.m1 = m;
     g.m2 = inner;
-    launch_col<float>(y, static_cast<float*>(nullptr), 0.0, g, 1, w, id, ex);
+    launch_col<float>(y, static_cast<float*>(nullptr), 0.0, g, 1, w, id, ex, toep_enabled());
   }
   return cudaGetLastError();
 }
@@ -2159,7 +2159,7 @@ cudaError_t f3_axis0_solve(double* y, int64_t m0, int64_t inner, const double* w
   g.m0 = m0;
   g.m1 = 1;
   g.m2 = inner;
-  launch_col<float>(y, static_cast<float*>(nullptr), 0.0, g, 0, w, id, ex);
+  launch_col<float>(y, static_cast<float*>(nullptr), 0.0, g, 0, w, id, ex, toep_enabled());
   return cudaGetLastError();
 }
 

@@ -75,6 +75,8 @@ cudaError_t fused3d_slab_interp(const T* shell, const T* coarse, T* fine, const 
                                 const Exec& ex);
 
 // Thomas along the middle axis of [outer][m][inner] (rows when inner == 1).
+// w / id: the uniform ThomasAux tables of a plan (api.cu get_plan): id[m ..
+// m + 64) holds the end-correction tables of the Toeplitz form, used for m >= 40.
 cudaError_t f3_axis_solve(double* y, int64_t outer, int64_t m, int64_t inner, const double* w, const double* id,
                           const Exec& ex);
 // Axis-0 Thomas of the columns of a [m0][inner] fp64 array (the segmented
