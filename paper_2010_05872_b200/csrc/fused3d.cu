@@ -574,6 +574,79 @@ __device__ __forceinline__ void warp_row_toep(double* x, int m, const double* __
   __syncwarp();
 }
 
+// The same row solve on a RIGHT-ALIGNED buffer of 32 SEG values: element i of
+// the row sits at position i + P0, P0 = 32 SEG - m, and the positions before
+// it hold zeros.  The last element is then the last value of lane 31, so the
+// back substitution starts from a zero carry without a test, and leading zeros
+// are harmless in both recurrences (forward: they stay zero; backward: what
+// they become is never stored): no per-value bounds tests or selects.  The
+// end corrections read z_0 / z_{m-1} back from the buffer and lane l fixes
+// elements l and m - 1 - l (gl = Gt[l], hl = Ht[l]).  Needs m >= 32.
+template <int SEG>
+struct ScanPow {  // B^(2^j), j = 0..4, for B = x^SEG
+  double v[5];
+  constexpr ScanPow(double x) : v() {
+    double b = 1.0;
+    for (int i = 0; i < SEG; ++i) b *= x;
+    for (int j = 0; j < 5; ++j) {
+      v[j] = b;
+      if (j < 4) b *= b;
+    }
+  }
+};
+
+template <int SEG>
+__device__ __forceinline__ void warp_row_toep_ra(double* x, int m, double gl, double hl) {
+  constexpr PowTab<SEG> PF(-kTw), PB(-kTc);
+  constexpr ScanPow<SEG> SF(-kTw), SB(-kTc);
+  const int lane = threadIdx.x & 31;
+  const int s0 = lane * SEG;
+  const int P0 = 32 * SEG - m;
+  double v[SEG];
+#pragma unroll
+  for (int k = 0; k < SEG; ++k) v[k] = x[s0 + k];
+  double a = 0.0;
+#pragma unroll
+  for (int k = 0; k < SEG; ++k) {
+    a = v[k] - kTw * a;
+    v[k] = a;
+  }
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    const double o = __shfl_up_sync(0xffffffffu, a, 1 << j);
+    if (lane >= (1 << j)) a = a + SF.v[j] * o;
+  }
+  double c = __shfl_up_sync(0xffffffffu, a, 1);
+  if (lane == 0) c = 0.0;
+#pragma unroll
+  for (int k = 0; k < SEG; ++k) v[k] = v[k] + PF.v[k + 1] * c;
+  double g = 0.0;
+#pragma unroll
+  for (int k = SEG - 1; k >= 0; --k) {
+    g = (v[k] - kOff * g) * kTid;
+    v[k] = g;
+  }
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    const double o = __shfl_down_sync(0xffffffffu, g, 1 << j);
+    if (lane + (1 << j) < 32) g = g + SB.v[j] * o;
+  }
+  double z = __shfl_down_sync(0xffffffffu, g, 1);
+  if (lane == 31) z = 0.0;
+#pragma unroll
+  for (int k = 0; k < SEG; ++k) {
+    v[k] = v[k] + PB.v[SEG - k] * z;
+    if (s0 + k >= P0) x[s0 + k] = v[k];
+  }
+  __syncwarp();
+  const double z0 = x[P0], zm = x[32 * SEG - 1];
+  __syncwarp();
+  x[P0 + lane] = x[P0 + lane] + z0 * gl;
+  __syncwarp();
+  x[32 * SEG - 1 - lane] = x[32 * SEG - 1 - lane] + zm * hl;
+  __syncwarp();
+}
+
 // L0 (axis-0 load-vector restriction) on registers: the coarse planes
 // k-1, k, k+1 around fine plane p (k = p/2) accumulate the plane's
 // restricted rows Q in stencil order (load_entry, transform.hpp:84-96);
@@ -1364,11 +1437,14 @@ template <int NC>
 __global__ void __launch_bounds__(256, kRowCtas(NC)) k_f3_row_ring(double* __restrict__ G, int64_t rows, int m,
                                                                     const double* __restrict__ gh) {
   extern __shared__ double rs[];
-  double* gt = rs;
+  constexpr int W = 32 * NC;  // buffer width: the row right-aligned, zeros before it (warp_row_toep_ra)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  double* ring = rs + 2 * kToepEnds + size_t(warp) * kRowRing * m;
-  for (int i = threadIdx.x; i < 2 * kToepEnds; i += blockDim.x) gt[i] = gh[i];
-  __syncthreads();
+  double* ring = rs + size_t(warp) * kRowRing * W;
+  const int P0 = W - m;
+  for (int i = lane; i < kRowRing * W; i += 32)
+    if (i % W < P0) ring[i] = 0.0;
+  const double gl = gh[lane], hl = gh[kToepEnds + lane];
+  __syncwarp();
   pdl_wait();
   const int64_t step = int64_t(gridDim.x) * nw;
   const int64_t r0 = int64_t(blockIdx.x) * nw + warp;
@@ -1377,7 +1453,7 @@ __global__ void __launch_bounds__(256, kRowCtas(NC)) k_f3_row_ring(double* __res
   auto issue = [&](int64_t rr, int slot) {
     if (rr < rows) {
       const double* gr = G + (rows - 1 - rr) * m + lane;
-      double* dst = ring + slot * m + lane;
+      double* dst = ring + slot * W + P0 + lane;
 #pragma unroll
       for (int k = 0; k < NC; ++k)
         if (lane + 32 * k < m) cp_async8(dst + 32 * k, gr + 32 * k);
@@ -1388,17 +1464,18 @@ __global__ void __launch_bounds__(256, kRowCtas(NC)) k_f3_row_ring(double* __res
   issue(r0 + step, 1);
   int slot = 0;
   for (int64_t r = r0; r < rows; r += step) {
-    issue(r + 2 * step, (slot + 2) % kRowRing);
+    issue(r + 2 * step, slot >= 1 ? slot - 1 : kRowRing - 1);  // (slot + 2) % 3
     cp_async_wait<2>();
     __syncwarp();
-    double* buf = ring + slot * m;
-    warp_row_toep<NC>(buf, m, gt, gt + kToepEnds);
-    double* gr = G + (rows - 1 - r) * m;
+    double* buf = ring + slot * W;
+    warp_row_toep_ra<NC>(buf, m, gl, hl);
+    double* gr = G + (rows - 1 - r) * m + lane;
+    const double* src = buf + P0 + lane;
 #pragma unroll
     for (int k = 0; k < NC; ++k)
-      if (lane + 32 * k < m) st_pol(gr + lane + 32 * k, buf[lane + 32 * k], pkeep);
+      if (lane + 32 * k < m) st_pol(gr + 32 * k, src[32 * k], pkeep);
     __syncwarp();
-    slot = (slot + 1) % kRowRing;
+    slot = slot == kRowRing - 1 ? 0 : slot + 1;
   }
 }
 
@@ -1426,7 +1503,7 @@ void launch_row(double* G, const F3Geom& g, const double* w, const double* id, c
 #define ROW_(NC)                                                                                           \
   do {                                                                                                     \
     if (toep && m >= kToepMinM && ring_enabled()) {                                                        \
-      const size_t rsm = size_t(2 * kToepEnds + (threads / 32) * kRowRing * m) * 8;                        \
+      const size_t rsm = size_t((threads / 32) * kRowRing * 32 * NC) * 8;                                  \
       cudaFuncSetAttribute(k_f3_row_ring<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rsm));      \
       MGRX_LAUNCH(ex, "f3_row", pdl_launch(k_f3_row_ring<NC>, dim3(unsigned(blocks)), dim3(threads), rsm, ex.s, \
                                            !ex.prof, G, rows, m, id + m));                                 \
