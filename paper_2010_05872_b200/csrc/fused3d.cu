@@ -17,9 +17,13 @@
 //                            fp64 component in registers; a finished coarse
 //                            plane's rows go to the fp64 volume G (optionally
 //                            also check_finite of every value it reads).
-//              f3_row        Thomas along axis 2 on G, in place (a warp per row).
-//              f3_col (axis 1)  Thomas along axis 1 on G, in place.
-//              f3_col (axis 0)  Thomas along axis 0 + coarse += z.
+//              f3_row        solve along axis 2 on G, in place (a warp per row).
+//              f3_col (axis 1)  solve along axis 1 on G, in place.
+//              f3_col (axis 0)  solve along axis 0 + coarse += z.
+//                            (lines of >= 40 unknowns in Toeplitz form —
+//                            constant Thomas factors + end corrections, see
+//                            "Toeplitz solves" — k_f3_row_ring, k_f3_col_toep;
+//                            shorter lines with the ThomasAux tables)
 //   recompose  f3_rec_plane  same load-vector accumulation, reading the
 //                            component from the shell;
 //              f3_row, f3_col x2  as above, coarse -= z;

@@ -277,6 +277,40 @@ def test_fused_path_against_oracle(torch, mg, ws_auto, dtype):
             assert float(np.max(np.abs(rt.astype(np.float64) - x))) <= (1e-9 if dtype == "f64" else 1e-4) * rg
 
 
+TOEPLITZ_SHAPES = [(79, 79, 79),     # 40 unknowns on every axis: the shortest lines solved in Toeplitz form
+                   (77, 81, 83),     # 39 (factor tables), 41, 42
+                   (33, 40, 575),    # rows of 288 = 32 * 9: no leading zeros in the right-aligned row buffer
+                   (20, 35, 191),    # rows of 96 = 32 * 3
+                   (130, 36, 127),   # 65 planes, rows of 64 in a 96-wide buffer
+                   (12, 20, 1919)]   # rows of 960, 33 values per lane
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_toeplitz_solves_against_oracle(torch, mg, ws_auto, dtype):
+    """The Toeplitz form of the correction solves (constant Thomas factors +
+    end corrections, fused3d.cu) at its thresholds: line lengths 39 / 40 / 41,
+    row buffers with and without leading zeros, the widest rows.  fp64 within
+    1e-13 of the range (the bar is 1e-12; the solves differ from
+    batched_solve, transform.hpp:116-130, only in rounding)."""
+    from oracle.oracle import Oracle
+
+    o = Oracle()
+    rng = np.random.default_rng(17)
+    npdt = np.float64 if dtype == "f64" else np.float32
+    tol = 1e-13 if dtype == "f64" else 1e-5
+    for shape in TOEPLITZ_SHAPES:
+        x = rng.uniform(-10, 10, shape).astype(npdt)
+        rg = float(x.max() - x.min())
+        h = mg.GridHierarchy.create(shape)
+        want = o.decompose(x, 0)
+        mc = mg.decompose(to_dev(torch, x), h, 0, ws_auto)
+        err = float(np.max(np.abs(mc.buffer.cpu().numpy().astype(np.float64) - want)))
+        assert err <= tol * rg, (shape, dtype, err / rg)
+        back = mg.recompose(mg.MultilevelCoefficients(to_dev(torch, want), h, 0), ws_auto).cpu().numpy()
+        err = float(np.max(np.abs(back.astype(np.float64) - o.recompose(want, shape, 0))))
+        assert err <= tol * rg, (shape, dtype, "rec", err / rg)
+
+
 def test_graph_capture_matches_eager(torch, mg):
     """decompose + recompose captured in a CUDA graph (the recompose forks
     its level corrections onto the context's side streams and joins them)
