@@ -1428,6 +1428,9 @@ __global__ void __launch_bounds__(256, kRowCtas(NC)) k_f3_row(double* __restrict
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -1654,6 +1657,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : (MAXT == kColT
   double* ht = sc + kToepEnds;   // [kToepEnds]
   double* A = ht + kToepEnds;    // [S][16]
   double* E = A + S * 16;        // [2][16]: z_0 and z_{m-1} of the 16 columns
+  T* cbuf = reinterpret_cast<T*>(E + 32);  // APPLY: [S * LS][16] the coarse values, prefetched under the solve
   for (int i = threadIdx.y * 32 + lane; i < 2 * kToepEnds; i += blockDim.y * 32) sc[i] = gh[i];
   const int64_t col = int64_t(gridDim.x - 1 - blockIdx.x) * 16 + c16;
   const bool valid = col < ncols;
@@ -1669,6 +1673,19 @@ __global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : (MAXT == kColT
       v[k] = (valid && k < len) ? (APPLY ? __ldcs(gp) : *gp) : 0.0;
       gp += stride;
     }
+  }
+  if (APPLY) {  // this thread's coarse values into its own slots of cbuf (4- or 8-byte cp.async)
+    const T* c = coarse + base + int64_t(s0) * stride;
+    T* mine = cbuf + s0 * 16 + c16;
+#pragma unroll
+    for (int k = 0; k < LS; ++k) {
+      if (valid && k < len) {
+        if (sizeof(T) == 4) cp_async4(mine + k * 16, c);
+        else cp_async8(mine + k * 16, c);
+      }
+      c += stride;
+    }
+    cp_async_commit();
   }
   // forward from a zero carry; v[k] keeps the zero-carry values
   double a = 0.0;
@@ -1724,16 +1741,14 @@ __global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : (MAXT == kColT
   }
   pdl_trigger();
   if (!valid) return;
-  if (APPLY) {  // coarse values loaded only now, four at a time: fewer live registers
+  if (APPLY) {  // the coarse values were prefetched into this thread's slots of cbuf
+    cp_async_wait<0>();
     T* c = coarse + base + int64_t(s0) * stride;
+    const T* mine = cbuf + s0 * 16 + c16;
 #pragma unroll
-    for (int k0 = 0; k0 < LS; k0 += 4) {
-      T cv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) cv[u] = (k0 + u < LS && k0 + u < len) ? c[int64_t(k0 + u) * stride] : T(0);
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (k0 + u < LS && k0 + u < len) c[int64_t(k0 + u) * stride] = to_t<T>(double(cv[u]) + sign * v[k0 + u]);
+    for (int k = 0; k < LS; ++k) {
+      if (k < len) *c = to_t<T>(double(mine[k * 16]) + sign * v[k]);
+      c += stride;
     }
   } else {
     double* gp = G + base + int64_t(s0) * stride;
@@ -1828,9 +1843,11 @@ void launch_col(double* G, T* coarse, double sign, const F3Geom& g, int axis, co
 #define MGRX_COLT(LS, AP, MT)                                                                            \
   {                                                                                                       \
     const int SY = (m + 2 * LS - 1) / (2 * LS);                                                          \
-    MGRX_LAUNCH(ex, tag, pdl_launch(k_f3_col_toep<T, LS, AP, MT>, dim3(blocks), dim3(32, SY),             \
-                                    size_t(2 * kToepEnds + 2 * SY * 16 + 32) * 8, ex.s, !ex.prof, G, coarse, sign, \
-                                    ncols, m, stride, outer_stride, inner, id + m));                      \
+    const size_t csm = size_t(2 * kToepEnds + 2 * SY * 16 + 32) * 8 +                                     \
+                       (AP ? size_t(2 * SY * LS * 16) * sizeof(T) : size_t(0)); /* + the prefetched coarse values */ \
+    cudaFuncSetAttribute(k_f3_col_toep<T, LS, AP, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csm)); \
+    MGRX_LAUNCH(ex, tag, pdl_launch(k_f3_col_toep<T, LS, AP, MT>, dim3(blocks), dim3(32, SY), csm, ex.s, !ex.prof, \
+                                    G, coarse, sign, ncols, m, stride, outer_stride, inner, id + m));     \
   }
   if (toep && m >= kToepMinM) {  // the end-correction tables follow inv_d (api.cu get_plan)
     if (m <= 264) {
