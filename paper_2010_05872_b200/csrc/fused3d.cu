@@ -1510,7 +1510,11 @@ void launch_row(double* G, const F3Geom& g, const double* w, const double* id, c
 #define ROW_(NC)                                                                                           \
   do {                                                                                                     \
     if (toep && m >= kToepMinM && ring_enabled()) {                                                        \
-      const size_t rsm = size_t((threads / 32) * kRowRing * 32 * NC) * 8;                                  \
+      /* at least so much shared memory that one block more than kRowCtas(NC) cannot be resident: the  \
+         grid is kRowCtas blocks per SM, and a register allocation that lets a 4th block in measured   \
+         48 -> 58 us (uneven blocks per SM) */                                                           \
+      const size_t rsm = std::max(size_t((threads / 32) * kRowRing * 32 * NC) * 8,                         \
+                                  size_t(228 * 1024) / (kRowCtas(NC) + 1) + 1024);                         \
       cudaFuncSetAttribute(k_f3_row_ring<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rsm));      \
       MGRX_LAUNCH(ex, "f3_row", pdl_launch(k_f3_row_ring<NC>, dim3(unsigned(blocks)), dim3(threads), rsm, ex.s, \
                                            !ex.prof, G, rows, m, id + m));                                 \
@@ -1658,7 +1662,9 @@ __global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : (MAXT == kColT
   double* A = ht + kToepEnds;    // [S][16]
   double* E = A + S * 16;        // [2][16]: z_0 and z_{m-1} of the 16 columns
   T* cbuf = reinterpret_cast<T*>(E + 32);  // APPLY: [S * LS][16] the coarse values, prefetched under the solve
-  for (int i = threadIdx.y * 32 + lane; i < 2 * kToepEnds; i += blockDim.y * 32) sc[i] = gh[i];
+  // the end-correction tables: loaded now, stored after this thread's G loads are in flight
+  const int gi = threadIdx.y * 32 + lane;
+  const double ghv = gi < 2 * kToepEnds ? gh[gi] : 0.0;
   const int64_t col = int64_t(gridDim.x - 1 - blockIdx.x) * 16 + c16;
   const bool valid = col < ncols;
   const int64_t base = valid ? (col / inner) * outer_stride + (col % inner) : 0;
@@ -1674,6 +1680,7 @@ __global__ void __launch_bounds__(MAXT, MAXT == kColThreads ? 3 : (MAXT == kColT
       gp += stride;
     }
   }
+  if (gi < 2 * kToepEnds) sc[gi] = ghv;
   if (APPLY) {  // this thread's coarse values into its own slots of cbuf (4- or 8-byte cp.async)
     const T* c = coarse + base + int64_t(s0) * stride;
     T* mine = cbuf + s0 * 16 + c16;
